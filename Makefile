@@ -1,0 +1,44 @@
+# Build of the B200 hot path (sm_100a only) and of the C++ drop-in API.
+#
+#   make            -> paper_2303_05098_b200/lib/libsparseoracle_b200.so   (CUDA kernels + C-ABI)
+#                      paper_2303_05098_b200/lib/libsparseoracle.so        (C++ API, sparseoracle::)
+#   make oracle     -> oracle/_build/liboracle.so, oracle/_ref/libsparseoracle_ref.so (test only)
+
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2303_05098_b200
+LIBDIR   := $(PKG)/lib
+CSRC     := $(PKG)/csrc
+CU_SRCS  := $(wildcard $(CSRC)/*.cu)
+CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(LIBDIR)/obj/%.o,$(CU_SRCS))
+CU_HDRS  := $(wildcard $(CSRC)/*.cuh) include/sparseoracle_b200.h
+NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr \
+            -Xptxas -warn-spills
+CPP_SRCS := $(wildcard $(PKG)/cpp/*.cpp)
+CPP_OBJS := $(patsubst $(PKG)/cpp/%.cpp,$(LIBDIR)/obj/cpp_%.o,$(CPP_SRCS))
+CPP_HDRS := $(wildcard include/sparseoracle/*.hpp) include/sparseoracle_b200.h
+
+all: $(LIBDIR)/libsparseoracle_b200.so $(if $(CPP_SRCS),$(LIBDIR)/libsparseoracle.so)
+
+$(LIBDIR)/obj/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p $(LIBDIR)/obj
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIBDIR)/libsparseoracle_b200.so: $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
+
+$(LIBDIR)/obj/cpp_%.o: $(PKG)/cpp/%.cpp $(CPP_HDRS)
+	@mkdir -p $(LIBDIR)/obj
+	$(CXX) -std=c++20 -O2 -fPIC -Iinclude -c $< -o $@
+
+$(LIBDIR)/libsparseoracle.so: $(CPP_OBJS) $(LIBDIR)/libsparseoracle_b200.so
+	$(CXX) -shared -o $@ $(CPP_OBJS) -L$(LIBDIR) -lsparseoracle_b200 -Wl,-rpath,'$$ORIGIN'
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(LIBDIR)
+
+.PHONY: all oracle clean

@@ -1,0 +1,215 @@
+/* sparseoracle_b200.h -- C-ABI of the B200 (sm_100a) hot path.
+ *
+ * This is the boundary the reference's C++ API (proj/include/sparseoracle/
+ * *.hpp) is re-implemented on top of: the C++ drop-in in
+ * paper_2303_05098_b200/cpp/ calls only these entry points, and so do the
+ * Python parity tests (ctypes) and bench.py.  Plain pointers and sizes, no
+ * torch types, no C++ exceptions across the boundary: every call returns an
+ * so_status and leaves a thread-local message in so_last_error().
+ *
+ * Each entry point names the reference interface it replaces
+ * (file:line under /root/reference/proj).
+ *
+ * Device layout (HBM), see DESIGN.md §3:
+ *   COO  row int32[z], col int32[z], val f64[z]          (canonical: row-major sorted)
+ *   CSR  row_ptr int64[n+1], col int32[z], val f64[z]     (+ row-block partition int32)
+ *   DIA  offsets int64[D], values f64[D*n] diagonal-major (same as host)
+ *   ELL  col int32[K*n], val f64[K*n] COLUMN-major (host view is row-major i*K+k)
+ *   HYB  ELL part + COO part;   HDC  DIA part + CSR part
+ * Row/column counts must be < 2^31 (int32 device indices); nnz is 64-bit.
+ */
+#ifndef SPARSEORACLE_B200_H
+#define SPARSEORACLE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The C++ shim rethrows each as the matching
+ * sparseoracle::Error subclass (errors.hpp:8-71). */
+typedef enum so_status {
+    SO_OK = 0,
+    SO_INVALID_INPUT = 1,          /* errors.hpp:13  InvalidInput        */
+    SO_PADDING_OVERFLOW = 2,       /* errors.hpp:19  PaddingOverflow     */
+    SO_DIMENSION_MISMATCH = 3,     /* errors.hpp:23  DimensionMismatch   */
+    SO_EMPTY_MATRIX = 4,           /* errors.hpp:27  EmptyMatrix         */
+    SO_MALFORMED_MODEL = 5,        /* errors.hpp:32  MalformedModel      */
+    SO_INDEX_OUT_OF_RANGE = 6,     /* errors.hpp:53  IndexOutOfRange     */
+    SO_ALL_FORMATS_INFEASIBLE = 7, /* errors.hpp:69  AllFormatsInfeasible*/
+    SO_CUDA_ERROR = 8,
+    SO_OUT_OF_MEMORY = 9,
+    SO_ERROR = 10
+} so_status;
+
+/* formats.hpp:17-24 -- stable ids (model files, CSVs) */
+typedef enum so_format {
+    SO_COO = 0,
+    SO_CSR = 1,
+    SO_DIA = 2,
+    SO_ELL = 3,
+    SO_HYB = 4,
+    SO_HDC = 5
+} so_format;
+
+/* formats.hpp:124-139 ConversionConfig */
+typedef struct so_conversion_config {
+    int64_t kh_override;       /* 0 selects ceil(nnz / nrows)            */
+    double true_diag_ratio;    /* default 0.2                            */
+    double max_padding_factor; /* default 10.0                           */
+    int64_t max_padded_entries;/* >0 overrides the factor                */
+} so_conversion_config;
+
+/* features.hpp:12-23 FeatureVector (field order = struct order) */
+typedef struct so_feature_vector {
+    int64_t nrows, ncols, nnz;
+    double avg_nnz_per_row, density;
+    int64_t max_nnz_per_row, min_nnz_per_row;
+    double nnz_row_spread;
+    int64_t ndiags, ntrue_diags;
+} so_feature_vector;
+
+/* features.hpp:27-32 FeatureScanStats */
+typedef struct so_scan_stats {
+    int64_t entry_visits, structure_reads;
+} so_scan_stats;
+
+/* Shape of a device matrix (every field the host containers expose). */
+typedef struct so_matrix_info {
+    int32_t format;
+    int32_t device;
+    int64_t nrows, ncols, nnz;     /* nnz = DynamicMatrix::nnz() (formats.cpp:397-409) */
+    int64_t coo_nnz;               /* COO, HYB coo part                       */
+    int64_t csr_nnz;               /* CSR, HDC csr part                       */
+    int64_t ndiags;                /* DIA, HDC dia part                       */
+    int64_t dia_stored_nnz;
+    int64_t ell_width;             /* ELL, HYB ell part (entries_per_row)     */
+    int64_t ell_stored_nnz;
+    int64_t kh;                    /* HYB configured K_H                      */
+    int64_t true_diag_threshold;   /* HDC                                     */
+} so_matrix_info;
+
+/* Host arrays in the REFERENCE host layout (int64 indices, ELL row-major).
+ * Unused slots may be NULL.  Sizes follow so_matrix_info. */
+typedef struct so_host_arrays {
+    int64_t* coo_row; int64_t* coo_col; double* coo_val;
+    int64_t* csr_row_ptr; int64_t* csr_col; double* csr_val;
+    int64_t* dia_offsets; double* dia_values;
+    int64_t* ell_col; double* ell_val;
+} so_host_arrays;
+
+/* formats.hpp:55, model.hpp:40-53 TuneOutcome subset */
+typedef struct so_tune_outcome {
+    int32_t chosen;        /* FormatId                                 */
+    int32_t source;        /* TunerKind: 1 decision_tree, 2 random_forest */
+    int32_t switched;      /* chosen != active format                  */
+    int32_t fallback_csr;  /* predicted format infeasible              */
+    double feature_time_seconds; /* T_FE  (device time, cudaEvent)     */
+    double predict_time_seconds; /* T_PRED (device time, cudaEvent)    */
+    so_feature_vector features;  /* what the model saw                 */
+} so_tune_outcome;
+
+typedef struct so_matrix so_matrix; /* opaque, device-resident */
+typedef struct so_forest so_forest; /* opaque, device-resident */
+
+/* ---- context ----------------------------------------------------------- */
+const char* so_last_error(void);
+const char* so_version(void);
+so_status so_set_device(int device);          /* device for new objects */
+so_status so_device_sync(void);
+/* Opaque cudaStream_t used by every host-facing call on the current device. */
+void* so_default_stream(void);
+
+/* ---- containers: upload / download / info  (formats.hpp:37-122) --------- */
+/* Host arrays are copied H2D; int64 indices are range-checked and narrowed on
+ * the device.  No canonical check here (from_coo does it). */
+so_status so_matrix_upload_coo(int64_t nrows, int64_t ncols, int64_t nnz,
+                               const int64_t* row, const int64_t* col,
+                               const double* val, so_matrix** out);
+so_status so_matrix_upload_csr(int64_t nrows, int64_t ncols, int64_t nnz,
+                               const int64_t* row_ptr, const int64_t* col,
+                               const double* val, so_matrix** out);
+so_status so_matrix_upload_dia(int64_t nrows, int64_t ncols, int64_t ndiags,
+                               const int64_t* offsets, const double* values,
+                               int64_t stored_nnz, so_matrix** out);
+so_status so_matrix_upload_ell(int64_t nrows, int64_t ncols, int64_t width,
+                               const int64_t* col_rowmajor,
+                               const double* val_rowmajor, int64_t stored_nnz,
+                               so_matrix** out);
+so_status so_matrix_upload_hyb(int64_t nrows, int64_t ncols, int64_t width,
+                               const int64_t* ell_col, const double* ell_val,
+                               int64_t ell_stored_nnz, int64_t coo_nnz,
+                               const int64_t* coo_row, const int64_t* coo_col,
+                               const double* coo_val, int64_t kh,
+                               so_matrix** out);
+so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags,
+                               const int64_t* offsets, const double* values,
+                               int64_t dia_stored_nnz, int64_t csr_nnz,
+                               const int64_t* row_ptr, const int64_t* col,
+                               const double* val, int64_t threshold,
+                               so_matrix** out);
+void so_matrix_free(so_matrix* m);
+so_status so_matrix_info_get(const so_matrix* m, so_matrix_info* out);
+/* D2H into caller buffers sized per so_matrix_info (ELL transposed back to
+ * row-major, indices widened to int64). */
+so_status so_matrix_download(const so_matrix* m, const so_host_arrays* out);
+
+/* ---- conversions  (formats.cpp:411-467) ---------------------------------- */
+/* from_coo: canonical check (InvalidInput), then the target's size phase,
+ * the PaddingOverflow cap check BEFORE any dense allocation, then fill. */
+so_status so_from_coo(const so_matrix* coo, int32_t target,
+                      const so_conversion_config* cfg, so_matrix** out);
+/* switch_format semantics: from_coo(to_coo(src), target) (formats.cpp:463-467),
+ * done entirely on the device.  Same-format returns a deep copy. */
+so_status so_convert(const so_matrix* src, int32_t target,
+                     const so_conversion_config* cfg, so_matrix** out);
+/* to_coo (formats.cpp:432-461): drop DIA zero cells / ELL sentinels, sort. */
+so_status so_to_coo(const so_matrix* src, so_matrix** out);
+/* format_feasible (tuners.cpp:26-45), host arithmetic on a feature vector. */
+int32_t so_format_feasible(int32_t target, const so_feature_vector* f,
+                           const so_conversion_config* cfg);
+
+/* ---- SpMV  (spmv.hpp:20-32, spmv.cpp:191-246) ------------------------------ */
+/* Device pointers, stream-ordered, no sync.  x has ncols, y has nrows slots. */
+so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev,
+                         void* stream);
+/* spmv(m, x): host vectors, H2D x + kernel(s) + D2H y, synchronous. */
+so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y);
+/* time_spmv: x uploaded once, 1 untimed warm-up, then `reps` multiplies each
+ * timed with a cudaEvent pair on the launching stream.  total = sum. */
+so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen,
+                       int64_t reps, double* per_rep_seconds,
+                       double* total_seconds);
+/* Algorithmic (compulsory) HBM bytes of one multiply, DESIGN.md §4. */
+int64_t so_spmv_bytes(const so_matrix* m);
+
+/* ---- features  (features.hpp:33-42, features.cpp:82-153) ------------------- */
+so_status so_extract_features(const so_matrix* m, double true_diag_ratio,
+                              so_feature_vector* out, so_scan_stats* stats);
+
+/* ---- model  (model.hpp:18-53, model.cpp:202-228) --------------------------- */
+/* kind 0 = tree (predict uses trees.front(), tuners.cpp:103-105), 1 = forest.
+ * Flat nodes: tree t owns [node_off[t], node_off[t+1]); child indices are
+ * tree-local.  feature == -1 marks a leaf. */
+so_status so_forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off,
+                           const int32_t* feature, const double* threshold,
+                           const int32_t* left, const int32_t* right,
+                           const int32_t* cls, so_forest** out);
+void so_forest_free(so_forest* f);
+/* predict on a host feature vector (one device launch). */
+so_status so_predict(const so_forest* f, const so_feature_vector* x, int32_t* out);
+/* Batched predict: rows is [n][10] in features_to_row order. */
+so_status so_predict_rows(const so_forest* f, int64_t n, const double* rows,
+                          int32_t* out);
+
+/* ---- tuner  (tuners.hpp:57-63, tuners.cpp:92-114) ------------------------- */
+/* tune_ml: features -> predict -> feasibility/CSR fallback fully on the device;
+ * one small D2H of the outcome.  Never runs SpMV, never mutates m. */
+so_status so_tune_ml(const so_matrix* m, const so_forest* f, double true_diag_ratio,
+                     const so_conversion_config* cfg, so_tune_outcome* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEORACLE_B200_H */

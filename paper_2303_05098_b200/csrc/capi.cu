@@ -1,0 +1,683 @@
+// extern "C" boundary (include/sparseoracle_b200.h): argument validation with
+// the reference's error types/messages, H2D/D2H staging between the
+// reference's host layout (int64 indices, row-major ELL) and the device
+// layout, and the per-device context.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "features.cuh"
+#include "forest.cuh"
+
+namespace sob {
+
+// model.cu
+so_forest* forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off, const int32_t* feature,
+                         const double* threshold, const int32_t* left, const int32_t* right, const int32_t* cls,
+                         cudaStream_t s);
+void predict_rows(const so_forest& f, const double* rows_dev, int64_t n, int32_t* out_dev, cudaStream_t s);
+void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,
+                          so_tune_outcome* out_dev, cudaStream_t s);
+
+namespace {
+thread_local std::string g_err;
+std::mutex g_mu;
+Context g_ctx[64];
+bool g_ready[64];
+thread_local int g_dev = -1;
+}  // namespace
+
+void set_error(const std::string& m) { g_err = m; }
+
+Context& ctx(int d) {
+    if (d < 0 || d >= 64) fail(SO_INVALID_INPUT, "bad device ordinal");
+    std::lock_guard<std::mutex> lk(g_mu);
+    Context& c = g_ctx[d];
+    if (!g_ready[d]) {
+        SOB_CUDA(cudaSetDevice(d));
+        c.device = d;
+        SOB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        SOB_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, d));
+        int l2 = 0;
+        SOB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, d));
+        c.l2_bytes = l2;
+        // keep freed pool memory cached: conversions and scratch are stream-
+        // ordered allocations, reuse must not go back to the driver
+        cudaMemPool_t pool;
+        SOB_CUDA(cudaDeviceGetDefaultMemPool(&pool, d));
+        uint64_t thresh = UINT64_MAX;
+        SOB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+        g_ready[d] = true;
+    }
+    return c;
+}
+
+Context& current_ctx() {
+    if (g_dev < 0) {
+        int d = 0;
+        SOB_CUDA(cudaGetDevice(&d));
+        g_dev = d;
+    }
+    SOB_CUDA(cudaSetDevice(g_dev));
+    return ctx(g_dev);
+}
+
+namespace {
+
+// ------------------------------------------------------------ staging kernels
+
+__global__ void narrow_idx(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t n, int64_t hi,
+                           int allow_sentinel, int* __restrict__ bad) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t v = in[i];
+    const bool ok = (v >= 0 && v < hi) || (allow_sentinel && v == -1);
+    if (!ok) atomicExch(bad, 1);
+    out[i] = int32_t(v);
+}
+
+__global__ void widen_idx(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
+}
+
+// row-major [n][K] (int64 / f64) <-> column-major [K][n] (int32 / f64)
+__global__ void ell_to_colmajor(const int64_t* __restrict__ col_rm, const double* __restrict__ val_rm, int64_t n,
+                                int64_t K, int64_t ncols, int32_t* __restrict__ col_cm, double* __restrict__ val_cm,
+                                int* __restrict__ bad) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // row-major index
+    if (idx >= n * K) return;
+    const int64_t i = idx / K, k = idx - i * K;
+    const int64_t c = col_rm[idx];
+    if (!((c >= 0 && c < ncols) || c == -1)) atomicExch(bad, 1);
+    col_cm[k * n + i] = int32_t(c);
+    val_cm[k * n + i] = val_rm[idx];
+}
+
+__global__ void ell_to_rowmajor(const int32_t* __restrict__ col_cm, const double* __restrict__ val_cm, int64_t n,
+                                int64_t K, int64_t* __restrict__ col_rm, double* __restrict__ val_rm) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // column-major index
+    if (idx >= n * K) return;
+    const int64_t k = idx / n, i = idx - k * n;
+    col_rm[i * K + k] = col_cm[idx];
+    val_rm[i * K + k] = val_cm[idx];
+}
+
+__global__ void check_row_ptr(const int64_t* __restrict__ rp, int64_t n, int64_t nnz, int* __restrict__ bad) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == 0 && rp[0] != 0) atomicExch(bad, 1);
+    if (i == n && rp[n] != nnz) atomicExch(bad, 1);
+    if (i < n && rp[i + 1] < rp[i]) atomicExch(bad, 1);
+}
+
+__global__ void ell_short_rows(const int32_t* __restrict__ col_cm, int64_t n, int64_t K,
+                               unsigned long long* __restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool s = i < n && K > 0 && col_cm[(K - 1) * n + i] == -1;
+    const unsigned b = __ballot_sync(0xffffffffu, s);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
+}
+
+unsigned grid1(int64_t n) { return unsigned(ceil_div(n > 0 ? n : 1, 256)); }
+
+void check_dims(int64_t nrows, int64_t ncols) {
+    if (nrows < 0 || ncols < 0) fail(SO_INVALID_INPUT, "negative dimension");
+    if (nrows >= (int64_t(1) << 31) || ncols >= (int64_t(1) << 31) || nrows + ncols >= (int64_t(1) << 31))
+        fail(SO_INVALID_INPUT, "device layout needs nrows + ncols < 2^31");
+}
+
+template <typename T>
+void h2d(DBuf<T>& buf, const T* src, int64_t n, cudaStream_t s) {
+    buf.alloc(n, s);
+    if (n > 0) {
+        if (!src) fail(SO_INVALID_INPUT, "null host array");
+        SOB_CUDA(cudaMemcpyAsync(buf.get(), src, sizeof(T) * size_t(n), cudaMemcpyHostToDevice, s));
+    }
+}
+
+template <typename T>
+void d2h(T* dst, const DBuf<T>& buf, int64_t n, cudaStream_t s) {
+    if (n > 0 && dst) SOB_CUDA(cudaMemcpyAsync(dst, buf.get(), sizeof(T) * size_t(n), cudaMemcpyDeviceToHost, s));
+}
+
+struct BadFlag {
+    DBuf<int> f;
+    cudaStream_t s;
+    explicit BadFlag(cudaStream_t st) : f(1, st), s(st) { SOB_CUDA(cudaMemsetAsync(f.get(), 0, sizeof(int), s)); }
+    int* get() { return f.get(); }
+    void raise_if(so_status st, const char* msg) {
+        if (d2h_scalar(f.get(), s)) fail(st, msg);
+    }
+};
+
+void upload_idx(DBuf<int32_t>& out, const int64_t* src, int64_t n, int64_t hi, bool sentinel, BadFlag& bad,
+                cudaStream_t s) {
+    DBuf<int64_t> stage;
+    h2d(stage, src, n, s);
+    out.alloc(n, s);
+    if (n > 0) {
+        narrow_idx<<<grid1(n), 256, 0, s>>>(stage.get(), out.get(), n, hi, sentinel ? 1 : 0, bad.get());
+        SOB_LAUNCH("narrow_idx");
+    }
+}
+
+void download_idx(int64_t* dst, const DBuf<int32_t>& src, int64_t n, cudaStream_t s) {
+    if (n <= 0 || !dst) return;
+    DBuf<int64_t> stage(n, s);
+    widen_idx<<<grid1(n), 256, 0, s>>>(src.get(), stage.get(), n);
+    SOB_LAUNCH("widen_idx");
+    d2h(dst, stage, n, s);
+    SOB_CUDA(cudaStreamSynchronize(s));
+}
+
+void upload_csr_part(CsrPart& c, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rp, const int64_t* col,
+                     const double* val, cudaStream_t s) {
+    BadFlag bad(s);
+    c.nnz = nnz;
+    h2d(c.row_ptr, rp, nrows + 1, s);
+    check_row_ptr<<<grid1(nrows + 1), 256, 0, s>>>(c.row_ptr.get(), nrows, nnz, bad.get());
+    SOB_LAUNCH("check_row_ptr");
+    upload_idx(c.col, col, nnz, ncols, false, bad, s);
+    h2d(c.val, val, nnz, s);
+    bad.raise_if(SO_INVALID_INPUT, "CSR arrays inconsistent (row_ptr or column index out of range)");
+    build_row_blocks(c, nrows, s);
+}
+
+void upload_dia_part(DiaPart& d, int64_t nrows, int64_t ncols, int64_t ndiags, const int64_t* offsets,
+                     const double* values, int64_t stored, cudaStream_t s) {
+    for (int64_t k = 0; k < ndiags; ++k) {
+        if (offsets[k] < -(nrows - 1) || offsets[k] > ncols - 1)
+            fail(SO_INVALID_INPUT, "DIA offset outside [-(nrows-1), ncols-1]");
+        if (k > 0 && offsets[k] <= offsets[k - 1]) fail(SO_INVALID_INPUT, "DIA offsets must be strictly increasing");
+    }
+    d.ndiags = ndiags;
+    d.stored_nnz = stored;
+    h2d(d.offsets, offsets, ndiags, s);
+    h2d(d.values, values, ndiags * nrows, s);
+}
+
+void upload_ell_part(EllPart& e, int64_t nrows, int64_t ncols, int64_t width, const int64_t* col, const double* val,
+                     int64_t stored, cudaStream_t s) {
+    BadFlag bad(s);
+    e.width = width;
+    e.stored_nnz = stored;
+    DBuf<int64_t> scol;
+    DBuf<double> sval;
+    h2d(scol, col, nrows * width, s);
+    h2d(sval, val, nrows * width, s);
+    e.col.alloc(nrows * width, s);
+    e.val.alloc(nrows * width, s);
+    if (nrows * width > 0) {
+        ell_to_colmajor<<<grid1(nrows * width), 256, 0, s>>>(scol.get(), sval.get(), nrows, width, ncols, e.col.get(),
+                                                             e.val.get(), bad.get());
+        SOB_LAUNCH("ell_to_colmajor");
+    }
+    bad.raise_if(SO_INVALID_INPUT, "ELL column index out of range");
+}
+
+void upload_coo_part(CooPart& c, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row, const int64_t* col,
+                     const double* val, cudaStream_t s) {
+    BadFlag bad(s);
+    c.nnz = nnz;
+    upload_idx(c.row, row, nnz, nrows, false, bad, s);
+    upload_idx(c.col, col, nnz, ncols, false, bad, s);
+    h2d(c.val, val, nnz, s);
+    bad.raise_if(SO_INVALID_INPUT, "COO index out of range");
+}
+
+so_matrix* new_host_matrix(int32_t fmt, int64_t nrows, int64_t ncols) {
+    check_dims(nrows, ncols);
+    Context& c = current_ctx();
+    auto* m = new so_matrix();
+    m->device = c.device;
+    m->format = fmt;
+    m->nrows = nrows;
+    m->ncols = ncols;
+    return m;
+}
+
+cudaStream_t on_device(const so_matrix* m) {
+    if (!m) fail(SO_INVALID_INPUT, "null matrix");
+    SOB_CUDA(cudaSetDevice(m->device));
+    g_dev = m->device;
+    return ctx(m->device).stream;
+}
+
+template <typename F>
+so_status make(so_matrix** out, F&& f) {
+    return guard([&] {
+        if (!out) fail(SO_INVALID_INPUT, "null out pointer");
+        *out = nullptr;
+        std::unique_ptr<so_matrix> m(f());
+        SOB_CUDA(cudaStreamSynchronize(ctx(m->device).stream));
+        *out = m.release();
+    });
+}
+
+so_conversion_config cfg_or_default(const so_conversion_config* c) {
+    if (c) return *c;
+    return so_conversion_config{0, 0.2, 10.0, 0};
+}
+
+void check_ratio(const so_matrix& m, double ratio) {  // features.cpp:86-91
+    if (m.nrows < 1 || m.ncols < 1) fail(SO_EMPTY_MATRIX, "extract_features: matrix has a zero dimension");
+    if (!(ratio > 0.0) || ratio > 1.0) fail(SO_INVALID_INPUT, "extract_features: true_diag_ratio must be in (0, 1]");
+}
+
+void check_x(const so_matrix& m, int64_t xlen) {  // spmv.cpp:12-19
+    if (xlen != m.ncols)
+        fail(SO_DIMENSION_MISMATCH, "spmv: vector length " + std::to_string(xlen) + " does not match ncols " +
+                                        std::to_string(m.ncols));
+}
+
+}  // namespace
+}  // namespace sob
+
+using namespace sob;
+
+extern "C" {
+
+const char* so_last_error(void) { return g_err.c_str(); }
+const char* so_version(void) { return "sparseoracle-b200 0.1 (sm_100a)"; }
+
+so_status so_set_device(int device) {
+    return guard([&] {
+        SOB_CUDA(cudaSetDevice(device));
+        g_dev = device;
+        ctx(device);
+    });
+}
+
+so_status so_device_sync(void) {
+    return guard([&] { SOB_CUDA(cudaStreamSynchronize(current_ctx().stream)); });
+}
+
+void* so_default_stream(void) {
+    try {
+        return reinterpret_cast<void*>(current_ctx().stream);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+// ---------------------------------------------------------------- uploads
+
+so_status so_matrix_upload_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row, const int64_t* col,
+                               const double* val, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_COO, nrows, ncols));
+        upload_coo_part(m->coo, nrows, ncols, nnz, row, col, val, ctx(m->device).stream);
+        return m.release();
+    });
+}
+
+so_status so_matrix_upload_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr, const int64_t* col,
+                               const double* val, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_CSR, nrows, ncols));
+        upload_csr_part(m->csr, nrows, ncols, nnz, row_ptr, col, val, ctx(m->device).stream);
+        return m.release();
+    });
+}
+
+so_status so_matrix_upload_dia(int64_t nrows, int64_t ncols, int64_t ndiags, const int64_t* offsets,
+                               const double* values, int64_t stored_nnz, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_DIA, nrows, ncols));
+        upload_dia_part(m->dia, nrows, ncols, ndiags, offsets, values, stored_nnz, ctx(m->device).stream);
+        return m.release();
+    });
+}
+
+so_status so_matrix_upload_ell(int64_t nrows, int64_t ncols, int64_t width, const int64_t* col, const double* val,
+                               int64_t stored_nnz, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_ELL, nrows, ncols));
+        upload_ell_part(m->ell, nrows, ncols, width, col, val, stored_nnz, ctx(m->device).stream);
+        return m.release();
+    });
+}
+
+so_status so_matrix_upload_hyb(int64_t nrows, int64_t ncols, int64_t width, const int64_t* ell_col,
+                               const double* ell_val, int64_t ell_stored_nnz, int64_t coo_nnz, const int64_t* coo_row,
+                               const int64_t* coo_col, const double* coo_val, int64_t kh, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_HYB, nrows, ncols));
+        cudaStream_t s = ctx(m->device).stream;
+        upload_ell_part(m->ell, nrows, ncols, width, ell_col, ell_val, ell_stored_nnz, s);
+        upload_coo_part(m->coo, nrows, ncols, coo_nnz, coo_row, coo_col, coo_val, s);
+        m->kh = kh;
+        return m.release();
+    });
+}
+
+so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags, const int64_t* offsets,
+                               const double* values, int64_t dia_stored_nnz, int64_t csr_nnz, const int64_t* row_ptr,
+                               const int64_t* col, const double* val, int64_t threshold, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_HDC, nrows, ncols));
+        cudaStream_t s = ctx(m->device).stream;
+        upload_dia_part(m->dia, nrows, ncols, ndiags, offsets, values, dia_stored_nnz, s);
+        upload_csr_part(m->csr, nrows, ncols, csr_nnz, row_ptr, col, val, s);
+        m->threshold = threshold;
+        return m.release();
+    });
+}
+
+void so_matrix_free(so_matrix* m) {
+    if (!m) return;
+    try {
+        cudaSetDevice(m->device);
+    } catch (...) {
+    }
+    delete m;
+}
+
+so_status so_matrix_info_get(const so_matrix* m, so_matrix_info* out) {
+    return guard([&] {
+        if (!m || !out) fail(SO_INVALID_INPUT, "null argument");
+        out->format = m->format;
+        out->device = m->device;
+        out->nrows = m->nrows;
+        out->ncols = m->ncols;
+        out->nnz = m->nnz();
+        out->coo_nnz = m->coo.nnz;
+        out->csr_nnz = m->csr.nnz;
+        out->ndiags = m->dia.ndiags;
+        out->dia_stored_nnz = m->dia.stored_nnz;
+        out->ell_width = m->ell.width;
+        out->ell_stored_nnz = m->ell.stored_nnz;
+        out->kh = m->kh;
+        out->true_diag_threshold = m->threshold;
+    });
+}
+
+so_status so_matrix_download(const so_matrix* m, const so_host_arrays* a) {
+    return guard([&] {
+        if (!a) fail(SO_INVALID_INPUT, "null host arrays");
+        cudaStream_t s = on_device(m);
+        const int64_t n = m->nrows;
+        const bool coo = m->format == SO_COO || m->format == SO_HYB;
+        const bool csr = m->format == SO_CSR || m->format == SO_HDC;
+        const bool dia = m->format == SO_DIA || m->format == SO_HDC;
+        const bool ell = m->format == SO_ELL || m->format == SO_HYB;
+        if (coo) {
+            download_idx(a->coo_row, m->coo.row, m->coo.nnz, s);
+            download_idx(a->coo_col, m->coo.col, m->coo.nnz, s);
+            d2h(a->coo_val, m->coo.val, m->coo.nnz, s);
+        }
+        if (csr) {
+            d2h(a->csr_row_ptr, m->csr.row_ptr, n + 1, s);
+            download_idx(a->csr_col, m->csr.col, m->csr.nnz, s);
+            d2h(a->csr_val, m->csr.val, m->csr.nnz, s);
+        }
+        if (dia) {
+            d2h(a->dia_offsets, m->dia.offsets, m->dia.ndiags, s);
+            d2h(a->dia_values, m->dia.values, m->dia.ndiags * n, s);
+        }
+        if (ell) {
+            const int64_t tot = n * m->ell.width;
+            if (tot > 0 && (a->ell_col || a->ell_val)) {
+                DBuf<int64_t> c(tot, s);
+                DBuf<double> v(tot, s);
+                ell_to_rowmajor<<<grid1(tot), 256, 0, s>>>(m->ell.col.get(), m->ell.val.get(), n, m->ell.width, c.get(),
+                                                           v.get());
+                SOB_LAUNCH("ell_to_rowmajor");
+                d2h(a->ell_col, c, tot, s);
+                d2h(a->ell_val, v, tot, s);
+                SOB_CUDA(cudaStreamSynchronize(s));
+            }
+        }
+        SOB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// ------------------------------------------------------------ conversions
+
+so_status so_from_coo(const so_matrix* coo, int32_t target, const so_conversion_config* cfg, so_matrix** out) {
+    return make(out, [&]() -> so_matrix* {
+        cudaStream_t s = on_device(coo);
+        if (coo->format != SO_COO) fail(SO_INVALID_INPUT, "from_coo: source is not a COO matrix");
+        if (target < 0 || target > 5)
+            fail(SO_INVALID_INPUT, "format id " + std::to_string(target) + " outside 0..5");
+        if (!coo_is_canonical(*coo, s)) fail(SO_INVALID_INPUT, "from_coo: source matrix is not canonical COO");
+        if (target == SO_COO) return clone_matrix(*coo, s);
+        std::unique_ptr<so_matrix> csr(coo_to_csr_device(*coo, s));
+        if (target == SO_CSR) return csr.release();
+        so_matrix* r = csr_to_format(*csr, target, cfg_or_default(cfg), s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+        return r;
+    });
+}
+
+so_status so_convert(const so_matrix* src, int32_t target, const so_conversion_config* cfg, so_matrix** out) {
+    return make(out, [&]() -> so_matrix* {
+        cudaStream_t s = on_device(src);
+        if (target < 0 || target > 5)
+            fail(SO_INVALID_INPUT, "format id " + std::to_string(target) + " outside 0..5");
+        if (src->format == target) return clone_matrix(*src, s);
+        std::unique_ptr<so_matrix> csr(any_to_csr(*src, s));
+        if (target == SO_CSR) return csr.release();
+        so_matrix* r = csr_to_format(*csr, target, cfg_or_default(cfg), s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+        return r;
+    });
+}
+
+so_status so_to_coo(const so_matrix* src, so_matrix** out) {
+    return make(out, [&]() -> so_matrix* {
+        cudaStream_t s = on_device(src);
+        if (src->format == SO_COO) return clone_matrix(*src, s);  // formats.cpp:436-437
+        std::unique_ptr<so_matrix> csr(any_to_csr(*src, s));
+        so_matrix* r = csr_to_coo(*csr, s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+        return r;
+    });
+}
+
+int32_t so_format_feasible(int32_t target, const so_feature_vector* f, const so_conversion_config* cfgp) {
+    const so_conversion_config cfg = cfg_or_default(cfgp);
+    const int64_t cap = padded_entry_cap(cfg, f->nnz);  // tuners.cpp:26-45
+    switch (target) {
+        case SO_COO:
+        case SO_CSR:
+            return 1;
+        case SO_DIA:
+            return f->ndiags * f->nrows <= cap;
+        case SO_ELL:
+            return f->max_nnz_per_row * f->nrows <= cap;
+        case SO_HYB: {
+            const int64_t kh = effective_kh(cfg, f->nnz, f->nrows);
+            return std::min(kh, f->max_nnz_per_row) * f->nrows <= cap;
+        }
+        case SO_HDC:
+            return f->ntrue_diags * f->nrows <= cap;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------ SpMV
+
+so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev, void* stream) {
+    return guard([&] {
+        on_device(m);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx(m->device).stream;
+        spmv_device(*m, x_dev, y_dev, s);
+    });
+}
+
+so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) {
+    return guard([&] {
+        cudaStream_t s = on_device(m);
+        check_x(*m, xlen);
+        DBuf<double> dx, dy(m->nrows, s);
+        h2d(dx, x, xlen, s);
+        spmv_device(*m, dx.get(), dy.get(), s);
+        d2h(y, dy, m->nrows, s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen, int64_t reps, double* per_rep,
+                       double* total) {
+    return guard([&] {
+        if (reps < 1) fail(SO_INVALID_INPUT, "time_spmv: repetitions must be >= 1");  // spmv.cpp:223-225
+        cudaStream_t s = on_device(m);
+        check_x(*m, xlen);
+        DBuf<double> dx, dy(m->nrows, s);
+        h2d(dx, x, xlen, s);
+        spmv_device(*m, dx.get(), dy.get(), s);  // warm-up, untimed (spmv.cpp:231)
+        std::vector<cudaEvent_t> ev(size_t(reps) + 1);
+        for (auto& e : ev) SOB_CUDA(cudaEventCreate(&e));
+        SOB_CUDA(cudaEventRecord(ev[0], s));
+        for (int64_t r = 0; r < reps; ++r) {
+            spmv_device(*m, dx.get(), dy.get(), s);
+            SOB_CUDA(cudaEventRecord(ev[size_t(r) + 1], s));
+        }
+        SOB_CUDA(cudaStreamSynchronize(s));
+        double sum = 0.0;
+        for (int64_t r = 0; r < reps; ++r) {
+            float ms = 0.f;
+            SOB_CUDA(cudaEventElapsedTime(&ms, ev[size_t(r)], ev[size_t(r) + 1]));
+            per_rep[r] = double(ms) * 1e-3;
+            sum += per_rep[r];
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        *total = sum;
+    });
+}
+
+int64_t so_spmv_bytes(const so_matrix* m) {
+    int64_t bytes = -1;
+    guard([&] {
+        cudaStream_t s = on_device(m);
+        const int64_t n = m->nrows, nc = m->ncols;
+        int64_t b = 8 * nc + 8 * n;  // x read once, y written once
+        auto dia_bytes = [&]() {
+            std::vector<int64_t> off(size_t(m->dia.ndiags));
+            d2h(off.data(), m->dia.offsets, m->dia.ndiags, s);
+            SOB_CUDA(cudaStreamSynchronize(s));
+            int64_t cells = 0;
+            for (int64_t o : off) {
+                const int64_t lo = std::max<int64_t>(0, -o), hi = std::min(n, nc - o);
+                if (hi > lo) cells += hi - lo;
+            }
+            return 8 * cells + 8 * m->dia.ndiags;
+        };
+        auto ell_bytes = [&]() {
+            DBuf<unsigned long long> c(1, s);
+            SOB_CUDA(cudaMemsetAsync(c.get(), 0, sizeof(unsigned long long), s));
+            if (n > 0) {
+                ell_short_rows<<<grid1(n), 256, 0, s>>>(m->ell.col.get(), n, m->ell.width, c.get());
+                SOB_LAUNCH("ell_short_rows");
+            }
+            const int64_t shortr = int64_t(d2h_scalar(c.get(), s));
+            return m->ell.stored_nnz * 12 + 4 * shortr;
+        };
+        switch (m->format) {
+            case SO_COO: b += m->coo.nnz * 16; break;
+            case SO_CSR: b += m->csr.nnz * 12 + (n + 1) * 8; break;
+            case SO_DIA: b += dia_bytes(); break;
+            case SO_ELL: b += ell_bytes(); break;
+            case SO_HYB: b += ell_bytes() + m->coo.nnz * 16; break;
+            case SO_HDC: b += dia_bytes() + m->csr.nnz * 12 + (n + 1) * 8; break;
+        }
+        bytes = b;
+    });
+    return bytes;
+}
+
+// -------------------------------------------------------------- features
+
+so_status so_extract_features(const so_matrix* m, double ratio, so_feature_vector* out, so_scan_stats* stats) {
+    return guard([&] {
+        cudaStream_t s = on_device(m);
+        check_ratio(*m, ratio);
+        DBuf<FeatState> st(1, s);
+        enqueue_features(*m, ratio, st.get(), s);
+        FeatState h;
+        SOB_CUDA(cudaMemcpyAsync(&h, st.get(), sizeof(FeatState), cudaMemcpyDeviceToHost, s));
+        SOB_CUDA(cudaStreamSynchronize(s));
+        if (out) *out = h.out;
+        if (stats) {
+            stats->entry_visits = int64_t(h.visits);
+            stats->structure_reads = int64_t(h.structure);
+        }
+    });
+}
+
+// ----------------------------------------------------------------- model
+
+so_status so_forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off, const int32_t* feature,
+                           const double* threshold, const int32_t* left, const int32_t* right, const int32_t* cls,
+                           so_forest** out) {
+    return guard([&] {
+        *out = nullptr;
+        *out = forest_upload(kind, n_trees, node_off, feature, threshold, left, right, cls, current_ctx().stream);
+    });
+}
+
+void so_forest_free(so_forest* f) { delete f; }
+
+so_status so_predict_rows(const so_forest* f, int64_t n, const double* rows, int32_t* out) {
+    return guard([&] {
+        if (!f) fail(SO_INVALID_INPUT, "null forest");
+        SOB_CUDA(cudaSetDevice(f->device));
+        cudaStream_t s = ctx(f->device).stream;
+        DBuf<double> dr;
+        h2d(dr, rows, n * 10, s);
+        DBuf<int32_t> dout(n, s);
+        predict_rows(*f, dr.get(), n, dout.get(), s);
+        d2h(out, dout, n, s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+so_status so_predict(const so_forest* f, const so_feature_vector* x, int32_t* out) {
+    double row[10] = {double(x->nrows),          double(x->ncols),          double(x->nnz),
+                      x->avg_nnz_per_row,        x->density,                double(x->max_nnz_per_row),
+                      double(x->min_nnz_per_row), x->nnz_row_spread,        double(x->ndiags),
+                      double(x->ntrue_diags)};
+    return so_predict_rows(f, 1, row, out);
+}
+
+so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const so_conversion_config* cfgp,
+                     so_tune_outcome* out) {
+    return guard([&] {
+        if (!f || !out) fail(SO_INVALID_INPUT, "null argument");
+        cudaStream_t s = on_device(m);
+        if (f->device != m->device) fail(SO_INVALID_INPUT, "forest and matrix live on different devices");
+        check_ratio(*m, ratio);
+        so_conversion_config cfg = cfg_or_default(cfgp);
+        cfg.true_diag_ratio = ratio;  // TunerConfig::effective_conversion (tuners.hpp:21-25)
+        DBuf<FeatState> st(1, s);
+        DBuf<so_tune_outcome> dout(1, s);
+        cudaEvent_t e0, e1, e2;
+        SOB_CUDA(cudaEventCreate(&e0));
+        SOB_CUDA(cudaEventCreate(&e1));
+        SOB_CUDA(cudaEventCreate(&e2));
+        SOB_CUDA(cudaEventRecord(e0, s));
+        enqueue_features(*m, ratio, st.get(), s);
+        SOB_CUDA(cudaEventRecord(e1, s));
+        enqueue_tune_predict(*f, st.get(), cfg, m->format, dout.get(), s);
+        SOB_CUDA(cudaEventRecord(e2, s));
+        so_tune_outcome h;
+        SOB_CUDA(cudaMemcpyAsync(&h, dout.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        SOB_CUDA(cudaStreamSynchronize(s));
+        float fe = 0.f, pr = 0.f;
+        SOB_CUDA(cudaEventElapsedTime(&fe, e0, e1));
+        SOB_CUDA(cudaEventElapsedTime(&pr, e1, e2));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        h.feature_time_seconds = double(fe) * 1e-3;
+        h.predict_time_seconds = double(pr) * 1e-3;
+        *out = h;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,789 @@
+// Device conversions, CSR -> {COO, DIA, ELL, HYB, HDC} and back.
+//
+// The reference converts through canonical COO on the host (formats.cpp:
+// 411-467).  Here the canonical source is the device CSR (identical content:
+// to_coo(CSR) is canonical), and every conversion is two-phase: a size pass
+// on the device, the PaddingOverflow cap check on the host BEFORE the dense
+// allocation (formats.cpp:81-84, 111-112), then a fill pass.  Host-visible
+// arrays are bit-identical to the reference's (tests/test_gpu_formats.py).
+#include <cmath>
+#include <limits>
+#include <memory>
+
+#include "hist.cuh"
+#include "matrix.cuh"
+
+namespace sob {
+
+// ---------------------------------------------------------------- host rules
+
+int64_t checked_mul(int64_t a, int64_t b) {  // formats.cpp:14-20
+    if (a == 0 || b == 0) return 0;
+    if (a > std::numeric_limits<int64_t>::max() / b) return std::numeric_limits<int64_t>::max();
+    return a * b;
+}
+
+int64_t padded_entry_cap(const so_conversion_config& c, int64_t nnz) {  // formats.cpp:348-355
+    if (c.max_padded_entries > 0) return c.max_padded_entries;
+    const double cap = c.max_padding_factor * double(nnz);
+    if (cap >= double(std::numeric_limits<int64_t>::max())) return std::numeric_limits<int64_t>::max();
+    return int64_t(cap);
+}
+
+int64_t effective_kh(const so_conversion_config& c, int64_t nnz, int64_t nrows) {  // :357-361
+    if (c.kh_override > 0) return c.kh_override;
+    if (nrows <= 0 || nnz <= 0) return 0;
+    return (nnz + nrows - 1) / nrows;
+}
+
+int64_t true_diag_threshold(double ratio, int64_t nrows, int64_t ncols) {  // :363-367
+    const double len = double(nrows < ncols ? nrows : ncols);
+    return int64_t(std::ceil(ratio * len));
+}
+
+static void check_cap(int64_t allocation, int64_t cap, const char* what) {  // formats.cpp:36-43
+    if (allocation > cap)
+        fail(SO_PADDING_OVERFLOW, std::string(what) + " allocation of " + std::to_string(allocation) +
+                                      " entries exceeds padding cap " + std::to_string(cap));
+}
+
+namespace {
+
+constexpr int kB = 256;
+
+// ------------------------------------------------------- generic entry sweep
+// CTA-per-row-block sweep over the entries of a CSR (grid-stride over blocks).
+// op(row, k) is called for every entry; rows are found by binary search in the
+// block's row_ptr slice staged in shared memory.  Loop trip counts are
+// block-uniform so ops may use warp-synchronous primitives (valid=false lanes).
+template <class Op>
+__global__ void __launch_bounds__(kB) csr_sweep(const int32_t* __restrict__ blk, int64_t nblk,
+                                                 const int64_t* __restrict__ rp, Op op) {
+    __shared__ int64_t srp[kRowsPerBlock + 1];
+    op.begin();
+    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const int r0 = blk[b], nr = blk[b + 1] - r0;
+        __syncthreads();
+        for (int j = threadIdx.x; j <= nr; j += kB) srp[j] = rp[r0 + j];
+        __syncthreads();
+        const int64_t k0 = srp[0], k1 = srp[nr];
+        for (int64_t base = k0; base < k1; base += kB) {
+            const int64_t k = base + threadIdx.x;
+            const bool valid = k < k1;
+            const int r = valid ? r0 + row_in_block(srp, nr, k) : -1;
+            op(r, k, valid);
+        }
+    }
+    op.end();
+}
+
+struct OpBase {
+    __device__ void begin() {}
+    __device__ void end() {}
+};
+
+template <class Op>
+void sweep(const so_matrix& csr, Op op, cudaStream_t s, int per_sm = 4) {
+    if (csr.csr.nblk == 0) return;
+    csr_sweep<Op><<<grid_for(csr.csr.nblk * kB, kB, per_sm), kB, 0, s>>>(csr.csr.blk.get(), csr.csr.nblk,
+                                                                         csr.csr.row_ptr.get(), op);
+    SOB_LAUNCH("csr_sweep");
+}
+
+// ---------------------------------------------------------- row-block build
+
+__global__ void row_block_flags(const int64_t* __restrict__ rp, int64_t n, int32_t* __restrict__ flag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t len = rp[i + 1] - rp[i];
+    bool start = (i == 0) || (i % kRowsPerBlock == 0) || len > kWindow;
+    if (i > 0) {
+        const int64_t plen = rp[i] - rp[i - 1];
+        start = start || plen > kWindow || (rp[i] / kWindow) != (rp[i - 1] / kWindow);
+    }
+    flag[i] = start ? 1 : 0;
+}
+
+__global__ void row_block_scatter(const int32_t* __restrict__ flag, const int64_t* __restrict__ pos,
+                                  int64_t n, int32_t* __restrict__ blk) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) blk[pos[i]] = int32_t(i);
+    if (i == n) blk[pos[n]] = int32_t(n);
+}
+
+// ------------------------------------------------------------ COO -> CSR
+
+__global__ void coo_canonical_check(const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                                    int64_t z, int* __restrict__ bad) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x + 1;
+    if (k >= z) return;
+    const int32_t r0 = row[k - 1], r1 = row[k];
+    if (!(r0 < r1 || (r0 == r1 && col[k - 1] < col[k]))) atomicExch(bad, 1);
+}
+
+// row_ptr from a row-sorted row array: every row_ptr slot written exactly once.
+__global__ void coo_row_ptr(const int32_t* __restrict__ row, int64_t z, int64_t n, int64_t* __restrict__ rp) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k > z) return;
+    const int64_t lo = k == 0 ? 0 : int64_t(row[k - 1]) + 1;
+    const int64_t hi = k == z ? n : int64_t(row[k]);
+    for (int64_t r = lo; r <= hi; ++r) rp[r] = k;
+}
+
+// --------------------------------------------------------------- reductions
+
+__global__ void row_len_max(const int64_t* __restrict__ rp, int64_t n, int64_t cap_at,
+                            unsigned long long* __restrict__ out) {
+    int64_t m = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t len = rp[i + 1] - rp[i];
+        if (cap_at >= 0 && len > cap_at) len = cap_at;
+        m = len > m ? len : m;
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+}
+
+// ------------------------------------------------------------------- DIA
+// formats.cpp:64-96: seen[key] -> ascending offsets -> cap -> fill.
+
+struct MarkKeys : OpBase {
+    const int32_t* col;
+    int64_t nrows;
+    const int32_t* bins;  // optional: HDC qualification (count >= thr)
+    int64_t thr;
+    int32_t* flag;
+    __device__ void operator()(int r, int64_t k, bool valid) const {
+        if (!valid) return;
+        const int64_t key = int64_t(col[k]) - r + nrows - 1;
+        if (bins && bins[key] < thr) return;
+        flag[key] = 1;
+    }
+};
+
+__global__ void keys_to_offsets(const int32_t* __restrict__ flag, const int64_t* __restrict__ pos,
+                                int64_t nkeys, int64_t nrows, int64_t* __restrict__ offsets) {
+    const int64_t key = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (key < nkeys && flag[key]) offsets[pos[key]] = key - (nrows - 1);
+}
+
+struct FillDia : OpBase {
+    const int32_t* col;
+    const double* val;
+    int64_t nrows;
+    const int64_t* pos;  // key -> diagonal slot
+    const int32_t* bins;
+    int64_t thr;
+    double* values;
+    unsigned long long* stored;
+    __device__ void operator()(int r, int64_t k, bool valid) const {
+        bool nz = false;
+        if (valid) {
+            const int64_t key = int64_t(col[k]) - r + nrows - 1;
+            if (!bins || bins[key] >= thr) {
+                const double v = val[k];
+                values[pos[key] * nrows + r] = v;
+                nz = v != 0.0;  // formats.cpp:93 -- stored_nnz counts nonzero cells
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, nz);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(stored, (unsigned long long)__popc(b));
+    }
+};
+
+// -------------------------------------------------------------- ELL / HYB
+
+// Slot-major fill: thread per (slot, row); writes every padded slot exactly
+// once (column-major, coalesced), real entries first, then sentinel -1 / 0.0.
+__global__ void ell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                         const double* __restrict__ val, int64_t nrows, int64_t width,
+                         int32_t* __restrict__ ecol, double* __restrict__ eval) {
+    const int64_t total = nrows * width;
+    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = idx / nrows, r = idx - j * nrows;
+        const int64_t a = rp[r], len = rp[r + 1] - a;
+        if (j < len) {
+            ecol[idx] = col[a + j];
+            eval[idx] = val[a + j];
+        } else {
+            ecol[idx] = -1;
+            eval[idx] = 0.0;
+        }
+    }
+}
+
+__global__ void hyb_surplus(const int64_t* __restrict__ rp, int64_t n, int64_t kh, int64_t* __restrict__ cnt) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t len = rp[i + 1] - rp[i];
+    cnt[i] = len > kh ? len - kh : 0;
+}
+
+struct FillHybCoo : OpBase {
+    const int64_t* rp;
+    const int32_t* col;
+    const double* val;
+    int64_t kh;
+    const int64_t* coo_off;
+    int32_t *crow, *ccol;
+    double* cval;
+    __device__ void operator()(int r, int64_t k, bool valid) const {
+        if (!valid) return;
+        const int64_t j = k - rp[r];
+        if (j < kh) return;
+        const int64_t p = coo_off[r] + (j - kh);
+        crow[p] = r;
+        ccol[p] = col[k];
+        cval[p] = val[k];
+    }
+};
+
+// ------------------------------------------------------------------- HDC
+
+struct DiagHist : OpBase {
+    const int32_t* col;
+    int64_t nrows;
+    int32_t* bins;
+    SmemHash* h;
+    __device__ void begin() {
+        __shared__ SmemHash sh;
+        h = &sh;
+        hash_init(sh);
+        __syncthreads();
+    }
+    __device__ void operator()(int r, int64_t k, bool valid) {
+        const int32_t key = valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1;
+        hash_add(*h, bins, key);
+    }
+    __device__ void end() {
+        __syncthreads();
+        hash_flush(*h, bins);
+    }
+};
+
+// Per-row count of entries that stay in the CSR part (diag count < thr).
+__global__ void hdc_rest_counts(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const int32_t* __restrict__ bins, int64_t nrows, int64_t thr,
+                                int64_t* __restrict__ cnt) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t c = 0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) c += bins[int64_t(col[k]) - i + nrows - 1] < thr;
+    cnt[i] = c;
+}
+
+// Stable per-row compaction of the CSR-part entries.
+__global__ void hdc_rest_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, const int32_t* __restrict__ bins,
+                              int64_t nrows, int64_t thr, const int64_t* __restrict__ orp,
+                              int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t p = orp[i];
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+        if (bins[int64_t(col[k]) - i + nrows - 1] < thr) {
+            ocol[p] = col[k];
+            oval[p] = val[k];
+            ++p;
+        }
+    }
+}
+
+// ------------------------------------------------------------ to CSR (any)
+
+struct RowOfEntry : OpBase {
+    int32_t* row;
+    __device__ void operator()(int r, int64_t k, bool valid) const {
+        if (valid) row[k] = r;
+    }
+};
+
+__global__ void dia_row_counts(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ off,
+                               const double* __restrict__ vals, int64_t* __restrict__ cnt, bool accumulate) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t c = 0;
+    for (int d = 0; d < ndiags; ++d) {
+        const int64_t j = i + off[d];
+        if (j >= 0 && j < ncols && vals[int64_t(d) * nrows + i] != 0.0) ++c;
+    }
+    cnt[i] = accumulate ? cnt[i] + c : c;
+}
+
+__global__ void ell_row_counts(int64_t nrows, int64_t width, const int32_t* __restrict__ ecol,
+                               int64_t* __restrict__ cnt) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t c = 0;
+    while (c < width && ecol[c * nrows + i] != -1) ++c;
+    cnt[i] = c;
+}
+
+__global__ void csr_row_counts(const int64_t* __restrict__ rp, int64_t nrows, int64_t* __restrict__ cnt,
+                               bool accumulate) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    const int64_t c = rp[i + 1] - rp[i];
+    cnt[i] = accumulate ? cnt[i] + c : c;
+}
+
+__global__ void coo_row_counts_atomic(const int32_t* __restrict__ row, int64_t z,
+                                      unsigned long long* __restrict__ cnt) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= z) return;
+    atomicAdd(cnt + row[k], 1ull);
+}
+
+// Entries of DIA cells (nonzero, in range) of row i, appended at rp[i]+fill[i].
+__global__ void dia_to_rows(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ off,
+                            const double* __restrict__ vals, const int64_t* __restrict__ rp,
+                            int64_t* __restrict__ fill, int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t p = rp[i] + fill[i];
+    for (int d = 0; d < ndiags; ++d) {
+        const int64_t j = i + off[d];
+        if (j < 0 || j >= ncols) continue;
+        const double v = vals[int64_t(d) * nrows + i];
+        if (v != 0.0) {  // formats.cpp:225: holes and padding are skipped
+            ocol[p] = int32_t(j);
+            oval[p] = v;
+            ++p;
+        }
+    }
+    fill[i] = p - rp[i];
+}
+
+__global__ void ell_to_rows(int64_t nrows, int64_t width, const int32_t* __restrict__ ecol,
+                            const double* __restrict__ evals, const int64_t* __restrict__ rp,
+                            int64_t* __restrict__ fill, int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t p = rp[i] + fill[i];
+    for (int64_t k = 0; k < width; ++k) {
+        const int32_t c = ecol[k * nrows + i];
+        if (c == -1) break;  // formats.cpp:234
+        ocol[p] = c;
+        oval[p] = evals[k * nrows + i];
+        ++p;
+    }
+    fill[i] = p - rp[i];
+}
+
+__global__ void csr_to_rows(int64_t nrows, const int64_t* __restrict__ srp, const int32_t* __restrict__ scol,
+                            const double* __restrict__ sval, const int64_t* __restrict__ rp,
+                            int64_t* __restrict__ fill, int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t p = rp[i] + fill[i];
+    for (int64_t k = srp[i]; k < srp[i + 1]; ++k) {
+        ocol[p] = scol[k];
+        oval[p] = sval[k];
+        ++p;
+    }
+    fill[i] = p - rp[i];
+}
+
+__global__ void coo_to_rows(int64_t z, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, const int64_t* __restrict__ rp,
+                            unsigned long long* __restrict__ fill, int32_t* __restrict__ ocol,
+                            double* __restrict__ oval) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= z) return;
+    const int32_t r = row[k];
+    const int64_t p = rp[r] + int64_t(atomicAdd(fill + r, 1ull));
+    ocol[p] = col[k];
+    oval[p] = val[k];
+}
+
+// Per-row sortedness check + insertion sort of unsorted rows (to_coo's
+// std::sort, formats.cpp:247-265).  Valid containers are already sorted;
+// this only runs on rows assembled from several parts (HDC, HYB) or on
+// user-mutated host arrays.
+__global__ void sort_rows(const int64_t* __restrict__ rp, int64_t nrows, int32_t* __restrict__ col,
+                          double* __restrict__ val) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    const int64_t a = rp[i], e = rp[i + 1];
+    bool sorted = true;
+    for (int64_t k = a + 1; k < e && sorted; ++k) sorted = col[k - 1] <= col[k];
+    if (sorted) return;
+    for (int64_t k = a + 1; k < e; ++k) {
+        const int32_t c = col[k];
+        const double v = val[k];
+        int64_t j = k - 1;
+        while (j >= a && col[j] > c) {
+            col[j + 1] = col[j];
+            val[j + 1] = val[j];
+            --j;
+        }
+        col[j + 1] = c;
+        val[j + 1] = v;
+    }
+}
+
+// ------------------------------------------------------------ helpers
+
+so_matrix* new_matrix(const so_matrix& like, int32_t fmt) {
+    auto* m = new so_matrix();
+    m->device = like.device;
+    m->format = fmt;
+    m->nrows = like.nrows;
+    m->ncols = like.ncols;
+    return m;
+}
+
+unsigned long long reduce_max_len(const so_matrix& csr, int64_t cap_at, cudaStream_t s) {
+    DBuf<unsigned long long> out(1, s);
+    SOB_CUDA(cudaMemsetAsync(out.get(), 0, sizeof(unsigned long long), s));
+    if (csr.nrows > 0) {
+        row_len_max<<<grid_for(csr.nrows, 256), 256, 0, s>>>(csr.csr.row_ptr.get(), csr.nrows, cap_at, out.get());
+        SOB_LAUNCH("row_len_max");
+    }
+    return d2h_scalar(out.get(), s);
+}
+
+// Distinct flagged keys -> ascending offsets.  Returns ndiags; pos holds the
+// key -> slot map (exclusive scan of flags).
+int64_t compact_keys(const DBuf<int32_t>& flag, int64_t nkeys, int64_t nrows, DBuf<int64_t>& pos,
+                     DBuf<int64_t>& offsets, int64_t cap, cudaStream_t s) {
+    pos.alloc(nkeys + 1, s);
+    exclusive_scan_i32_to_i64(flag.get(), pos.get(), nkeys, s);
+    const int64_t nd = d2h_scalar(pos.get() + nkeys, s);
+    check_cap(checked_mul(nd, nrows), cap, "DIA");  // formats.cpp:81-82, before allocation
+    offsets.alloc(nd, s);
+    if (nd > 0) {
+        keys_to_offsets<<<unsigned(ceil_div(nkeys, 256)), 256, 0, s>>>(flag.get(), pos.get(), nkeys, nrows,
+                                                                       offsets.get());
+        SOB_LAUNCH("keys_to_offsets");
+    }
+    return nd;
+}
+
+void build_dia_part(const so_matrix& csr, const int32_t* bins, int64_t thr, DiaPart& dia, int64_t cap,
+                    cudaStream_t s) {
+    const int64_t n = csr.nrows;
+    const int64_t nkeys = (n > 0 && csr.ncols > 0) ? n + csr.ncols - 1 : 0;
+    DBuf<int32_t> flag(nkeys, s);
+    if (nkeys) SOB_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t) * size_t(nkeys), s));
+    MarkKeys mk;
+    mk.col = csr.csr.col.get();
+    mk.nrows = n;
+    mk.bins = bins;
+    mk.thr = thr;
+    mk.flag = flag.get();
+    sweep(csr, mk, s);
+    DBuf<int64_t> pos;
+    dia.ndiags = compact_keys(flag, nkeys, n, pos, dia.offsets, cap, s);
+    dia.values.alloc(dia.ndiags * n, s);
+    if (dia.values.n) SOB_CUDA(cudaMemsetAsync(dia.values.get(), 0, dia.values.bytes(), s));
+    DBuf<unsigned long long> stored(1, s);
+    SOB_CUDA(cudaMemsetAsync(stored.get(), 0, sizeof(unsigned long long), s));
+    FillDia fd;
+    fd.col = csr.csr.col.get();
+    fd.val = csr.csr.val.get();
+    fd.nrows = n;
+    fd.pos = pos.get();
+    fd.bins = bins;
+    fd.thr = thr;
+    fd.values = dia.values.get();
+    fd.stored = stored.get();
+    if (dia.ndiags > 0) sweep(csr, fd, s);
+    dia.stored_nnz = int64_t(d2h_scalar(stored.get(), s));
+}
+
+void fill_ell_part(const so_matrix& csr, int64_t width, EllPart& ell, cudaStream_t s) {
+    const int64_t n = csr.nrows;
+    ell.width = width;
+    ell.col.alloc(width * n, s);
+    ell.val.alloc(width * n, s);
+    if (width * n > 0) {
+        ell_fill<<<grid_for(width * n, 256), 256, 0, s>>>(csr.csr.row_ptr.get(), csr.csr.col.get(),
+                                                          csr.csr.val.get(), n, width, ell.col.get(),
+                                                          ell.val.get());
+        SOB_LAUNCH("ell_fill");
+    }
+}
+
+}  // namespace
+
+// ======================================================== public (internal)
+
+void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
+    if (n <= 0) {
+        csr.nblk = 0;
+        csr.blk.alloc(1, s);
+        SOB_CUDA(cudaMemsetAsync(csr.blk.get(), 0, sizeof(int32_t), s));
+        return;
+    }
+    DBuf<int32_t> flag(n, s);
+    DBuf<int64_t> pos(n + 1, s);
+    row_block_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, flag.get());
+    SOB_LAUNCH("row_block_flags");
+    exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
+    csr.nblk = d2h_scalar(pos.get() + n, s);
+    csr.blk.alloc(csr.nblk + 1, s);
+    row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), n, csr.blk.get());
+    SOB_LAUNCH("row_block_scatter");
+}
+
+bool coo_is_canonical(const so_matrix& coo, cudaStream_t s) {  // formats.cpp:324-340
+    if (coo.coo.nnz <= 1) return true;
+    DBuf<int> bad(1, s);
+    SOB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    coo_canonical_check<<<unsigned(ceil_div(coo.coo.nnz - 1, 256)), 256, 0, s>>>(
+        coo.coo.row.get(), coo.coo.col.get(), coo.coo.nnz, bad.get());
+    SOB_LAUNCH("coo_canonical_check");
+    return d2h_scalar(bad.get(), s) == 0;
+}
+
+so_matrix* coo_to_csr_device(const so_matrix& coo, cudaStream_t s) {  // formats.cpp:45-60
+    auto* m = new_matrix(coo, SO_CSR);
+    const int64_t z = coo.coo.nnz, n = coo.nrows;
+    CsrPart& c = m->csr;
+    c.nnz = z;
+    c.row_ptr.alloc(n + 1, s);
+    c.col.alloc(z, s);
+    c.val.alloc(z, s);
+    if (z) {
+        SOB_CUDA(cudaMemcpyAsync(c.col.get(), coo.coo.col.get(), c.col.bytes(), cudaMemcpyDeviceToDevice, s));
+        SOB_CUDA(cudaMemcpyAsync(c.val.get(), coo.coo.val.get(), c.val.bytes(), cudaMemcpyDeviceToDevice, s));
+    }
+    coo_row_ptr<<<unsigned(ceil_div(z + 1, 256)), 256, 0, s>>>(coo.coo.row.get(), z, n, c.row_ptr.get());
+    SOB_LAUNCH("coo_row_ptr");
+    build_row_blocks(c, n, s);
+    return m;
+}
+
+so_matrix* csr_to_coo(const so_matrix& csr, cudaStream_t s) {
+    auto* m = new_matrix(csr, SO_COO);
+    const int64_t z = csr.csr.nnz;
+    CooPart& c = m->coo;
+    c.nnz = z;
+    c.row.alloc(z, s);
+    c.col.alloc(z, s);
+    c.val.alloc(z, s);
+    if (z) {
+        SOB_CUDA(cudaMemcpyAsync(c.col.get(), csr.csr.col.get(), c.col.bytes(), cudaMemcpyDeviceToDevice, s));
+        SOB_CUDA(cudaMemcpyAsync(c.val.get(), csr.csr.val.get(), c.val.bytes(), cudaMemcpyDeviceToDevice, s));
+        RowOfEntry op;
+        op.row = c.row.get();
+        sweep(csr, op, s);
+    }
+    return m;
+}
+
+so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
+    auto* m = new_matrix(src, src.format);
+    auto cp = [&](auto& dst, const auto& from) {
+        dst.alloc(from.n, s);
+        if (from.n) SOB_CUDA(cudaMemcpyAsync(dst.get(), from.get(), from.bytes(), cudaMemcpyDeviceToDevice, s));
+    };
+    m->coo.nnz = src.coo.nnz;
+    cp(m->coo.row, src.coo.row);
+    cp(m->coo.col, src.coo.col);
+    cp(m->coo.val, src.coo.val);
+    m->csr.nnz = src.csr.nnz;
+    m->csr.nblk = src.csr.nblk;
+    cp(m->csr.row_ptr, src.csr.row_ptr);
+    cp(m->csr.col, src.csr.col);
+    cp(m->csr.val, src.csr.val);
+    cp(m->csr.blk, src.csr.blk);
+    m->dia.ndiags = src.dia.ndiags;
+    m->dia.stored_nnz = src.dia.stored_nnz;
+    cp(m->dia.offsets, src.dia.offsets);
+    cp(m->dia.values, src.dia.values);
+    m->ell.width = src.ell.width;
+    m->ell.stored_nnz = src.ell.stored_nnz;
+    cp(m->ell.col, src.ell.col);
+    cp(m->ell.val, src.ell.val);
+    m->kh = src.kh;
+    m->threshold = src.threshold;
+    return m;
+}
+
+so_matrix* csr_to_format(const so_matrix& csr, int32_t target, const so_conversion_config& cfg, cudaStream_t s) {
+    const int64_t n = csr.nrows, z = csr.csr.nnz;
+    const int64_t cap = padded_entry_cap(cfg, z);  // formats.cpp:414
+    switch (target) {
+        case SO_COO:
+            return csr_to_coo(csr, s);
+        case SO_CSR:
+            return clone_matrix(csr, s);
+        case SO_DIA: {  // formats.cpp:98-105
+            std::unique_ptr<so_matrix> m(new_matrix(csr, SO_DIA));
+            build_dia_part(csr, nullptr, 0, m->dia, cap, s);
+            return m.release();
+        }
+        case SO_ELL: {  // formats.cpp:132-138
+            const int64_t width = int64_t(reduce_max_len(csr, -1, s));
+            check_cap(checked_mul(width, n), cap, "ELL");
+            std::unique_ptr<so_matrix> m(new_matrix(csr, SO_ELL));
+            fill_ell_part(csr, width, m->ell, s);
+            m->ell.stored_nnz = z;
+            return m.release();
+        }
+        case SO_HYB: {  // formats.cpp:140-172
+            const int64_t kh = effective_kh(cfg, z, n);
+            const int64_t width = int64_t(reduce_max_len(csr, kh, s));
+            check_cap(checked_mul(width, n), cap, "ELL");
+            std::unique_ptr<so_matrix> m(new_matrix(csr, SO_HYB));
+            m->kh = kh;
+            fill_ell_part(csr, width, m->ell, s);
+            DBuf<int64_t> cnt(n, s), off(n + 1, s);
+            if (n) {
+                hyb_surplus<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.csr.row_ptr.get(), n, kh, cnt.get());
+                SOB_LAUNCH("hyb_surplus");
+            }
+            exclusive_scan_i64(cnt.get(), off.get(), n, s);
+            const int64_t zc = d2h_scalar(off.get() + n, s);
+            m->ell.stored_nnz = z - zc;
+            CooPart& c = m->coo;
+            c.nnz = zc;
+            c.row.alloc(zc, s);
+            c.col.alloc(zc, s);
+            c.val.alloc(zc, s);
+            if (zc) {
+                FillHybCoo op;
+                op.rp = csr.csr.row_ptr.get();
+                op.col = csr.csr.col.get();
+                op.val = csr.csr.val.get();
+                op.kh = kh;
+                op.coo_off = off.get();
+                op.crow = c.row.get();
+                op.ccol = c.col.get();
+                op.cval = c.val.get();
+                sweep(csr, op, s);
+            }
+            return m.release();
+        }
+        case SO_HDC: {  // formats.cpp:174-205
+            const int64_t thr = true_diag_threshold(cfg.true_diag_ratio, n, csr.ncols);
+            std::unique_ptr<so_matrix> m(new_matrix(csr, SO_HDC));
+            m->threshold = thr;
+            const int64_t nbins = n + csr.ncols;
+            DBuf<int32_t> bins(nbins, s);
+            if (nbins) SOB_CUDA(cudaMemsetAsync(bins.get(), 0, bins.bytes(), s));
+            DiagHist dh;
+            dh.col = csr.csr.col.get();
+            dh.nrows = n;
+            dh.bins = bins.get();
+            sweep(csr, dh, s, 2);
+            // entries on diagonals with count >= thr go to the DIA part
+            build_dia_part(csr, bins.get(), thr, m->dia, cap, s);
+            CsrPart& c = m->csr;
+            DBuf<int64_t> cnt(n, s);
+            c.row_ptr.alloc(n + 1, s);
+            if (n) {
+                hdc_rest_counts<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.csr.row_ptr.get(), csr.csr.col.get(),
+                                                                           bins.get(), n, thr, cnt.get());
+                SOB_LAUNCH("hdc_rest_counts");
+            }
+            exclusive_scan_i64(cnt.get(), c.row_ptr.get(), n, s);
+            c.nnz = d2h_scalar(c.row_ptr.get() + n, s);
+            c.col.alloc(c.nnz, s);
+            c.val.alloc(c.nnz, s);
+            if (c.nnz) {
+                hdc_rest_fill<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(
+                    csr.csr.row_ptr.get(), csr.csr.col.get(), csr.csr.val.get(), bins.get(), n, thr,
+                    c.row_ptr.get(), c.col.get(), c.val.get());
+                SOB_LAUNCH("hdc_rest_fill");
+            }
+            build_row_blocks(c, n, s);
+            return m.release();
+        }
+    }
+    fail(SO_INVALID_INPUT, "unknown target format");
+}
+
+// to_coo semantics (formats.cpp:432-461) delivered as a canonical-order CSR.
+so_matrix* any_to_csr(const so_matrix& m, cudaStream_t s) {
+    const int64_t n = m.nrows;
+    if (m.format == SO_COO) {
+        // to_coo(COO) returns the payload unchanged; from_coo then demands
+        // canonical input (formats.cpp:22-26).
+        if (!coo_is_canonical(m, s)) fail(SO_INVALID_INPUT, "from_coo: source matrix is not canonical COO");
+        return coo_to_csr_device(m, s);
+    }
+    std::unique_ptr<so_matrix> out(new_matrix(m, SO_CSR));
+    CsrPart& c = out->csr;
+    DBuf<int64_t> cnt(n, s);
+    auto grid = unsigned(ceil_div(n, 256));
+    const bool need_sort = true;  // cheap when rows are already sorted
+    if (n > 0) {
+        switch (m.format) {
+            case SO_CSR:
+                csr_row_counts<<<grid, 256, 0, s>>>(m.csr.row_ptr.get(), n, cnt.get(), false);
+                break;
+            case SO_DIA:
+                dia_row_counts<<<grid, 256, 0, s>>>(n, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                                    m.dia.values.get(), cnt.get(), false);
+                break;
+            case SO_ELL:
+            case SO_HYB:
+                ell_row_counts<<<grid, 256, 0, s>>>(n, m.ell.width, m.ell.col.get(), cnt.get());
+                if (m.format == SO_HYB && m.coo.nnz) {
+                    SOB_LAUNCH("ell_row_counts");
+                    coo_row_counts_atomic<<<unsigned(ceil_div(m.coo.nnz, 256)), 256, 0, s>>>(
+                        m.coo.row.get(), m.coo.nnz, reinterpret_cast<unsigned long long*>(cnt.get()));
+                }
+                break;
+            case SO_HDC:
+                dia_row_counts<<<grid, 256, 0, s>>>(n, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                                    m.dia.values.get(), cnt.get(), false);
+                SOB_LAUNCH("dia_row_counts");
+                csr_row_counts<<<grid, 256, 0, s>>>(m.csr.row_ptr.get(), n, cnt.get(), true);
+                break;
+        }
+        SOB_LAUNCH("row counts");
+    }
+    c.row_ptr.alloc(n + 1, s);
+    exclusive_scan_i64(cnt.get(), c.row_ptr.get(), n, s);
+    c.nnz = d2h_scalar(c.row_ptr.get() + n, s);
+    c.col.alloc(c.nnz, s);
+    c.val.alloc(c.nnz, s);
+    if (c.nnz > 0) {
+        DBuf<int64_t> fill(n, s);
+        SOB_CUDA(cudaMemsetAsync(fill.get(), 0, fill.bytes(), s));
+        switch (m.format) {
+            case SO_CSR:
+                csr_to_rows<<<grid, 256, 0, s>>>(n, m.csr.row_ptr.get(), m.csr.col.get(), m.csr.val.get(),
+                                                 c.row_ptr.get(), fill.get(), c.col.get(), c.val.get());
+                break;
+            case SO_DIA:
+                dia_to_rows<<<grid, 256, 0, s>>>(n, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                                 m.dia.values.get(), c.row_ptr.get(), fill.get(), c.col.get(),
+                                                 c.val.get());
+                break;
+            case SO_ELL:
+            case SO_HYB:
+                ell_to_rows<<<grid, 256, 0, s>>>(n, m.ell.width, m.ell.col.get(), m.ell.val.get(),
+                                                 c.row_ptr.get(), fill.get(), c.col.get(), c.val.get());
+                if (m.format == SO_HYB && m.coo.nnz) {
+                    SOB_LAUNCH("ell_to_rows");
+                    coo_to_rows<<<unsigned(ceil_div(m.coo.nnz, 256)), 256, 0, s>>>(
+                        m.coo.nnz, m.coo.row.get(), m.coo.col.get(), m.coo.val.get(), c.row_ptr.get(),
+                        reinterpret_cast<unsigned long long*>(fill.get()), c.col.get(), c.val.get());
+                }
+                break;
+            case SO_HDC:
+                dia_to_rows<<<grid, 256, 0, s>>>(n, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                                 m.dia.values.get(), c.row_ptr.get(), fill.get(), c.col.get(),
+                                                 c.val.get());
+                SOB_LAUNCH("dia_to_rows");
+                csr_to_rows<<<grid, 256, 0, s>>>(n, m.csr.row_ptr.get(), m.csr.col.get(), m.csr.val.get(),
+                                                 c.row_ptr.get(), fill.get(), c.col.get(), c.val.get());
+                break;
+        }
+        SOB_LAUNCH("to rows");
+        if (need_sort) {
+            sort_rows<<<grid, 256, 0, s>>>(c.row_ptr.get(), n, c.col.get(), c.val.get());
+            SOB_LAUNCH("sort_rows");
+        }
+    }
+    build_row_blocks(c, n, s);
+    return out.release();
+}
+
+}  // namespace sob

@@ -1,0 +1,661 @@
+// The ten structural features (features.cpp:82-153) on the device.
+//
+// Pass 1 (one kernel per stored part, no conversion): per-row counts and the
+// diagonal histogram, with shared-memory privatised bins (hist.cuh).  DIA
+// parts count per diagonal directly (no dense bins).
+// Pass 2: row statistics + per-chunk sums of squared deviations; N_D / N_TD
+// over the bins.
+// Pass 3: nnz_row_spread.  The reference sums (c_i - avg)^2 SEQUENTIALLY in
+// row order (features.cpp:139-144); a parallel reduction lands closer to the
+// exact value and misses the 1e-12 parity target by up to 1.7e-9.
+// The "binade replay" below reproduces the sequential rounding bit-exactly:
+// while the running sum S stays inside one binade [2^e, 2^(e+1)), fl(S+t)
+// adds round(t / ulp) ulps, so a run of additions is an integer sum -- except
+// at exact ties, where round-half-even depends on the parity of S.  Each
+// element is therefore a function parity -> (ulp increment, parity); these
+// compose associatively, so chunks are summarised in parallel and a single
+// warp walks the chunk summaries, verifying every binade assumption exactly
+// and recursing (32-way) into any chunk where S changes binade.  The result
+// is the reference's double, not an approximation of it.
+#include <cfloat>
+
+#include "features.cuh"
+#include "hist.cuh"
+
+namespace sob {
+
+namespace {
+
+constexpr int kB = 256;
+constexpr int kSpreadChunk = 2048;  // rows per spread chunk (8 per thread)
+constexpr int kMaxSmemDiag = 4096;
+
+// ------------------------------------------------------------ pass 1: scans
+
+template <bool ACCUM_RC>
+__global__ void __launch_bounds__(kB)
+    feat_csr(const int32_t* __restrict__ blk, int64_t nblk, const int64_t* __restrict__ rp,
+             const int32_t* __restrict__ col, int64_t nrows, int32_t* __restrict__ rc,
+             int32_t* __restrict__ bins, FeatState* __restrict__ st) {
+    __shared__ int64_t srp[kRowsPerBlock + 1];
+    __shared__ SmemHash h;
+    hash_init(h);
+    unsigned long long visits = 0;
+    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const int r0 = blk[b], nr = blk[b + 1] - r0;
+        __syncthreads();
+        for (int j = threadIdx.x; j <= nr; j += kB) srp[j] = rp[r0 + j];
+        __syncthreads();
+        for (int j = threadIdx.x; j < nr; j += kB) {
+            const int len = int(srp[j + 1] - srp[j]);
+            rc[r0 + j] = ACCUM_RC ? rc[r0 + j] + len : len;
+        }
+        const int64_t k0 = srp[0], k1 = srp[nr];
+        visits += k1 - k0;
+        for (int64_t base = k0; base < k1; base += kB) {
+            const int64_t k = base + threadIdx.x;
+            int32_t key = -1;
+            if (k < k1) {
+                const int r = r0 + row_in_block(srp, nr, k);
+                key = int32_t(int64_t(col[k]) - r + nrows - 1);
+            }
+            hash_add(h, bins, key);
+        }
+    }
+    __syncthreads();
+    hash_flush(h, bins);
+    if (threadIdx.x == 0 && visits) atomicAdd(&st->visits, visits);
+}
+
+__global__ void __launch_bounds__(kB)
+    feat_coo(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+             int32_t* __restrict__ rc, int32_t* __restrict__ bins, FeatState* __restrict__ st) {
+    __shared__ SmemHash h;
+    hash_init(h);
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31u;
+    for (int64_t base = int64_t(blockIdx.x) * kB; base < z; base += int64_t(gridDim.x) * kB) {
+        const int64_t k = base + threadIdx.x;
+        const bool valid = k < z;
+        const int32_t r = valid ? row[k] : -2 - int32_t(lane);
+        // warp-aggregated row counts (canonical rows are sorted => long runs)
+        const unsigned peers = __match_any_sync(0xffffffffu, r);
+        if (valid && int(lane) == __ffs(peers) - 1) atomicAdd(rc + r, __popc(peers));
+        hash_add(h, bins, valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1);
+    }
+    __syncthreads();
+    hash_flush(h, bins);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&st->visits, (unsigned long long)z);
+}
+
+__global__ void __launch_bounds__(kB)
+    feat_ell(int64_t nrows, int width, const int32_t* __restrict__ ecol, int32_t* __restrict__ rc,
+             int32_t* __restrict__ bins, FeatState* __restrict__ st) {
+    __shared__ SmemHash h;
+    hash_init(h);
+    __syncthreads();
+    unsigned long long visits = 0, structure = 0;
+    for (int64_t base = int64_t(blockIdx.x) * kB; base < nrows; base += int64_t(gridDim.x) * kB) {
+        const int64_t i = base + threadIdx.x;
+        bool done = i >= nrows;
+        int cnt = 0;
+        for (int k = 0; k < width; ++k) {
+            if (!__any_sync(0xffffffffu, !done)) break;
+            int32_t key = -1;
+            if (!done) {
+                const int32_t c = ecol[int64_t(k) * nrows + i];
+                if (c == -1) {  // features.cpp:71-74: one sentinel probe per padded row
+                    done = true;
+                    ++structure;
+                } else {
+                    ++cnt;
+                    key = int32_t(int64_t(c) - i + nrows - 1);
+                }
+            }
+            hash_add(h, bins, key);
+        }
+        if (i < nrows) rc[i] = cnt;
+        visits += cnt;
+    }
+    visits = warp_sum(visits);
+    structure = warp_sum(structure);
+    if ((threadIdx.x & 31) == 0) {
+        if (visits) atomicAdd(&st->visits, visits);
+        if (structure) atomicAdd(&st->structure, structure);
+    }
+    __syncthreads();
+    hash_flush(h, bins);
+}
+
+// DIA: one thread per row, diagonals ascending; per-diagonal entry counts are
+// reduced warp -> shared -> one global atomic per diagonal per CTA.
+__global__ void __launch_bounds__(kB)
+    feat_dia(int64_t nrows, int64_t ncols, int nd, const int64_t* __restrict__ off,
+             const double* __restrict__ vals, int32_t* __restrict__ rc,
+             unsigned long long* __restrict__ dcount, FeatState* __restrict__ st) {
+    __shared__ unsigned long long sdc[kMaxSmemDiag];
+    const int nsm = nd < kMaxSmemDiag ? nd : kMaxSmemDiag;
+    for (int d = threadIdx.x; d < nsm; d += kB) sdc[d] = 0;
+    __syncthreads();
+    unsigned long long visits = 0, structure = 0;
+    for (int64_t base = int64_t(blockIdx.x) * kB; base < nrows; base += int64_t(gridDim.x) * kB) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < nrows;
+        int cnt = 0;
+        for (int d = 0; d < nd; ++d) {
+            const int64_t j = i + off[d];
+            const bool inr = valid && j >= 0 && j < ncols;
+            const bool nz = inr && vals[int64_t(d) * nrows + i] != 0.0;  // features.cpp:57
+            cnt += nz;
+            structure += inr && !nz;
+            const unsigned b = __ballot_sync(0xffffffffu, nz);
+            if ((threadIdx.x & 31) == 0 && b) {
+                if (d < kMaxSmemDiag)
+                    atomicAdd(&sdc[d], (unsigned long long)__popc(b));
+                else
+                    atomicAdd(&dcount[d], (unsigned long long)__popc(b));
+            }
+        }
+        if (valid) rc[i] = cnt;
+        visits += cnt;
+    }
+    visits = warp_sum(visits);
+    structure = warp_sum(structure);
+    if ((threadIdx.x & 31) == 0) {
+        if (visits) atomicAdd(&st->visits, visits);
+        if (structure) atomicAdd(&st->structure, structure);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < nsm; d += kB)
+        if (sdc[d]) atomicAdd(&dcount[d], sdc[d]);
+}
+
+// HDC: fold the DIA part's per-diagonal counts into the dense bins.
+__global__ void dcount_to_bins(const unsigned long long* __restrict__ dcount, const int64_t* __restrict__ off,
+                               int nd, int64_t nrows, int32_t* __restrict__ bins) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d < nd && dcount[d]) atomicAdd(bins + (off[d] + nrows - 1), int32_t(dcount[d]));
+}
+
+// ------------------------------------------------------ pass 2: statistics
+
+__device__ __forceinline__ double sq_dev(int32_t c, double avg) {
+    const double dev = __dsub_rn(double(c), avg);  // features.cpp:140
+    return __dmul_rn(dev, dev);
+}
+
+__global__ void __launch_bounds__(kB)
+    feat_rows(const int32_t* __restrict__ rc, int64_t nrows, FeatState* __restrict__ st,
+              double* __restrict__ csum) {
+    const double avg = double(st->visits) / double(nrows);
+    const int64_t base = int64_t(blockIdx.x) * kSpreadChunk;
+    int mx = 0, mn = INT32_MAX;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < kSpreadChunk / kB; ++j) {
+        const int64_t i = base + j * kB + threadIdx.x;
+        if (i < nrows) {
+            const int32_t c = rc[i];
+            mx = c > mx ? c : mx;
+            mn = c < mn ? c : mn;
+            s += sq_dev(c, avg);
+        }
+    }
+    mx = warp_max(mx);
+    mn = warp_min(mn);
+    s = warp_sum(s);
+    __shared__ double ss[kB / 32];
+    __shared__ int smx[kB / 32], smn[kB / 32];
+    if ((threadIdx.x & 31) == 0) {
+        ss[threadIdx.x >> 5] = s;
+        smx[threadIdx.x >> 5] = mx;
+        smn[threadIdx.x >> 5] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kB / 32; ++w) {
+            t += ss[w];
+            mx = smx[w] > mx ? smx[w] : mx;
+            mn = smn[w] < mn ? smn[w] : mn;
+        }
+        csum[blockIdx.x] = t;
+        atomicMax(&st->max_row, mx);
+        atomicMin(&st->min_row, mn);
+    }
+}
+
+// counts >= 1 -> N_D, counts >= thr -> N_TD (features.cpp:146-151)
+template <typename T>
+__global__ void feat_bins(const T* __restrict__ bins, int64_t nbins, int64_t thr, FeatState* __restrict__ st) {
+    unsigned long long nd = 0, ntd = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nbins; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = int64_t(bins[i]);
+        nd += c >= 1;
+        ntd += c >= thr;
+    }
+    nd = warp_sum(nd);
+    ntd = warp_sum(ntd);
+    if ((threadIdx.x & 31) == 0) {
+        if (nd) atomicAdd(&st->nd, nd);
+        if (ntd) atomicAdd(&st->ntd, ntd);
+    }
+}
+
+// ------------------------------------------------ pass 3: binade replay
+
+// f: parity -> (ulp increment, parity).  p bit0 = out parity for in 0,
+// bit1 = out parity for in 1.
+struct Mono {
+    long long a0, a1;
+    int p;
+};
+
+__device__ __forceinline__ Mono mono_id() { return Mono{0, 0, 2}; }
+
+__device__ __forceinline__ Mono mono_cat(const Mono& m, const Mono& n) {  // m first, then n
+    const int r0 = m.p & 1, r1 = (m.p >> 1) & 1;
+    Mono o;
+    o.a0 = m.a0 + (r0 ? n.a1 : n.a0);
+    o.a1 = m.a1 + (r1 ? n.a1 : n.a0);
+    const int q0 = r0 ? (n.p >> 1) & 1 : n.p & 1;
+    const int q1 = r1 ? (n.p >> 1) & 1 : n.p & 1;
+    o.p = q0 | (q1 << 1);
+    return o;
+}
+
+constexpr double kTwo53 = 9007199254740992.0;
+
+// Element t added at binade e (ulp 2^(e-52)).  Returns false when t alone
+// reaches the next binade (q >= 2^53).
+__device__ __forceinline__ bool mono_elem(double t, int e, Mono& out) {
+    if (t == 0.0) {
+        out = mono_id();
+        return true;
+    }
+    const double q = ldexp(t, 52 - e);  // exact (power-of-two scaling)
+    if (!(q < kTwo53)) return false;
+    const double fl = floor(q);
+    const double fr = q - fl;  // exact
+    const long long k = (long long)fl;
+    if (fr < 0.5) {
+        out = Mono{k, k, int(k & 1) | (int((k + 1) & 1) << 1)};
+    } else if (fr > 0.5) {
+        const long long k1 = k + 1;
+        out = Mono{k1, k1, int(k1 & 1) | (int((k1 + 1) & 1) << 1)};
+    } else {  // tie: round half to even, depends on the parity of S
+        out = Mono{k + (k & 1), k + ((k + 1) & 1), 0};
+    }
+    return true;
+}
+
+__device__ __forceinline__ Mono shfl_mono_down(const Mono& m, int o) {
+    return Mono{__shfl_down_sync(0xffffffffu, m.a0, o), __shfl_down_sync(0xffffffffu, m.a1, o),
+                __shfl_down_sync(0xffffffffu, m.p, o)};
+}
+__device__ __forceinline__ Mono shfl_mono_up(const Mono& m, int o) {
+    return Mono{__shfl_up_sync(0xffffffffu, m.a0, o), __shfl_up_sync(0xffffffffu, m.a1, o),
+                __shfl_up_sync(0xffffffffu, m.p, o)};
+}
+// ordered warp reduction: lane 0 ends with M_0 . M_1 . ... . M_31
+__device__ __forceinline__ Mono warp_reduce_mono(Mono m, bool& ok) {
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const Mono other = shfl_mono_down(m, o);
+        const bool ook = __shfl_down_sync(0xffffffffu, ok, o);
+        if ((lane & (2 * o - 1)) == 0) {
+            m = mono_cat(m, other);
+            ok = ok && ook;
+        }
+    }
+    return m;
+}
+
+// ordered inclusive scan across the warp
+__device__ __forceinline__ Mono warp_scan_mono(Mono m, bool& ok) {
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const Mono up = shfl_mono_up(m, o);
+        const bool uok = __shfl_up_sync(0xffffffffu, ok, o);
+        if (lane >= unsigned(o)) {
+            m = mono_cat(up, m);
+            ok = ok && uok;
+        }
+    }
+    return m;
+}
+
+enum : int { kMonoSafe = 1, kMonoIdent = 2 };
+
+struct MonoRec {
+    long long a0, a1;
+    int p;
+    int e;
+    int flags;
+    int pad;
+};
+
+// exclusive prefix of the chunk sums (approximate S at chunk starts)
+__global__ void __launch_bounds__(512) spread_prefix(const double* __restrict__ csum, int64_t nch,
+                                                       double* __restrict__ P) {
+    __shared__ double wt[33];
+    double carry = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t base = 0; base < nch; base += 512) {
+        const int64_t i = base + threadIdx.x;
+        const double v = i < nch ? csum[i] : 0.0;
+        double inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double w = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += w;
+        }
+        if (lane == 31) wt[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const double w = lane < 16 ? wt[lane] : 0.0;
+            double wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double u = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += u;
+            }
+            if (lane < 16) wt[lane] = wi - w;
+            if (lane == 15) wt[32] = wi;
+        }
+        __syncthreads();
+        if (i < nch) P[i] = carry + wt[warp] + inc - v;
+        carry += wt[32];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) P[nch] = carry;
+}
+
+// Chunk summaries at the binade the approximate prefix puts the chunk in.
+__global__ void __launch_bounds__(kB)
+    spread_mono(const int32_t* __restrict__ rc, int64_t nrows, const FeatState* __restrict__ st,
+                const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec) {
+    const int64_t c = blockIdx.x;
+    __shared__ Mono wm[kB / 32];
+    __shared__ bool wok[kB / 32];
+    if (csum[c] == 0.0) {  // every t == 0: identity at any binade
+        if (threadIdx.x == 0) rec[c] = MonoRec{0, 0, 2, 0, kMonoIdent, 0};
+        return;
+    }
+    const double lo = P[c], hi = P[c + 1];
+    const double d = 1e-6;
+    const bool safe = lo > 0.0 && ilogb(lo * (1.0 - d)) == ilogb(hi * (1.0 + d));
+    if (!safe) {
+        if (threadIdx.x == 0) rec[c] = MonoRec{0, 0, 2, 0, 0, 0};
+        return;
+    }
+    const int e = ilogb(lo);
+    const double avg = double(st->visits) / double(nrows);
+    Mono m = mono_id();
+    bool ok = true;
+    const int64_t base = c * kSpreadChunk + int64_t(threadIdx.x) * (kSpreadChunk / kB);
+#pragma unroll
+    for (int j = 0; j < kSpreadChunk / kB; ++j) {
+        const int64_t i = base + j;
+        if (i < nrows) {
+            Mono el;
+            ok = ok && mono_elem(sq_dev(rc[i], avg), e, el);
+            if (ok) m = mono_cat(m, el);
+        }
+    }
+    m = warp_reduce_mono(m, ok);
+    if ((threadIdx.x & 31) == 0) {
+        wm[threadIdx.x >> 5] = m;
+        wok[threadIdx.x >> 5] = ok;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Mono t = mono_id();
+        bool tok = true;
+        for (int w = 0; w < kB / 32; ++w) {
+            t = mono_cat(t, wm[w]);
+            tok = tok && wok[w];
+        }
+        rec[c] = MonoRec{t.a0, t.a1, t.p, e, tok ? kMonoSafe : 0, 0};
+    }
+}
+
+// Exact sequential semantics over rows [lo, hi), warp-cooperative (all 32
+// lanes call with the same arguments; returns the same S in every lane).
+__device__ double advance_exact(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
+    const unsigned lane = threadIdx.x & 31u;
+    int64_t stack[12];
+    int sp = 0;
+    int64_t cur_hi = hi;
+    while (true) {
+        if (lo >= cur_hi) {
+            if (sp == 0) break;
+            cur_hi = stack[--sp];
+            continue;
+        }
+        if (S == 0.0) {
+            // 0 + t == t exactly: jump to the first nonzero t
+            int64_t found = -1;
+            for (int64_t b = lo; b < cur_hi && found < 0; b += 32) {
+                const int64_t i = b + lane;
+                const bool nz = i < cur_hi && sq_dev(rc[i], avg) != 0.0;
+                const unsigned bal = __ballot_sync(0xffffffffu, nz);
+                if (bal) found = b + (__ffs(bal) - 1);
+            }
+            if (found < 0) {
+                lo = cur_hi;
+                continue;
+            }
+            S = sq_dev(rc[found], avg);
+            lo = found + 1;
+            continue;
+        }
+        const int64_t len = cur_hi - lo;
+        const int64_t piece = (len + 31) / 32;
+        const int e = ilogb(S);
+        const long long m = (long long)ldexp(S, 52 - e);
+        const int64_t a = lo + int64_t(lane) * piece;
+        const int64_t b = a + piece < cur_hi ? a + piece : cur_hi;
+        Mono mm = mono_id();
+        bool ok = true;
+        for (int64_t i = a; i < b && ok; ++i) {
+            Mono el;
+            ok = mono_elem(sq_dev(rc[i], avg), e, el);
+            if (ok) mm = mono_cat(mm, el);
+        }
+        Mono pre = warp_scan_mono(mm, ok);
+        const long long mi = m + ((m & 1) ? pre.a1 : pre.a0);
+        const bool good = ok && double(mi) < kTwo53;
+        const unsigned bad = __ballot_sync(0xffffffffu, !good);
+        const int j = bad ? __ffs(bad) - 1 : 32;
+        if (j > 0) {
+            const long long mj = __shfl_sync(0xffffffffu, mi, j - 1);
+            S = ldexp(double(mj), e - 52);
+        }
+        if (j == 32) {
+            lo = cur_hi;
+            continue;
+        }
+        lo = lo + int64_t(j) * piece;
+        if (piece == 1) {  // the single step that changes binade: plain IEEE add
+            S = __dadd_rn(S, sq_dev(rc[lo], avg));
+            lo += 1;
+            continue;
+        }
+        const int64_t piece_hi = lo + piece < cur_hi ? lo + piece : cur_hi;
+        stack[sp++] = cur_hi;
+        cur_hi = piece_hi;
+    }
+    return S;
+}
+
+// One warp walks the chunk summaries in order, 32 at a time; then finalizes
+// the FeatureVector (features.cpp:121-152).
+__global__ void __launch_bounds__(32)
+    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch,
+                const MonoRec* __restrict__ rec, FeatState* __restrict__ st) {
+    const unsigned lane = threadIdx.x;
+    const double avg = double(st->visits) / double(nrows);
+    double S = 0.0;
+    int64_t c = 0;
+    while (c < nch) {
+        const int64_t ci = c + lane;
+        MonoRec r = ci < nch ? rec[ci] : MonoRec{0, 0, 2, 0, kMonoIdent, 0};
+        const int eS = S > 0.0 ? ilogb(S) : INT32_MIN;
+        const bool usable = ci < nch && ((r.flags & kMonoIdent) || ((r.flags & kMonoSafe) && r.e == eS));
+        const unsigned badm = __ballot_sync(0xffffffffu, !usable);
+        int j = badm ? __ffs(badm) - 1 : 32;
+        const int64_t remaining = nch - c;
+        if (j > remaining) j = int(remaining);
+        if (j > 0) {
+            Mono mm = (int(lane) < j) ? Mono{r.a0, r.a1, r.p} : mono_id();
+            bool ok = true;
+            Mono pre = warp_scan_mono(mm, ok);
+            if (S == 0.0) {  // only identity chunks can be usable at S == 0
+                c += j;
+                continue;
+            }
+            const long long m = (long long)ldexp(S, 52 - eS);
+            const long long mi = m + ((m & 1) ? pre.a1 : pre.a0);
+            const bool good = double(mi) < kTwo53 || int(lane) >= j;
+            const unsigned bad = __ballot_sync(0xffffffffu, !good);
+            const int f = bad ? __ffs(bad) - 1 : j;  // first chunk whose prefix leaves the binade
+            if (f > 0) {
+                const long long mf = __shfl_sync(0xffffffffu, mi, f - 1);
+                S = ldexp(double(mf), eS - 52);
+            }
+            c += f;
+            if (f == j) continue;
+        }
+        // chunk c needs the exact slow path
+        const int64_t lo = c * kSpreadChunk;
+        const int64_t hi = lo + kSpreadChunk < nrows ? lo + kSpreadChunk : nrows;
+        S = advance_exact(S, lo, hi, rc, avg);
+        c += 1;
+    }
+    if (lane == 0) {
+        st->S = S;
+        so_feature_vector& f = st->out;
+        const int64_t z = int64_t(st->visits);
+        f.nrows = nrows;
+        f.ncols = ncols;
+        f.nnz = z;
+        f.avg_nnz_per_row = avg;
+        f.density = double(z) / (double(nrows) * double(ncols));
+        f.max_nnz_per_row = st->max_row;
+        f.min_nnz_per_row = st->min_row;
+        f.nnz_row_spread = S / double(nrows);
+        f.ndiags = int64_t(st->nd);
+        f.ntrue_diags = int64_t(st->ntd);
+    }
+}
+
+__global__ void feat_init(FeatState* st) {
+    st->visits = 0;
+    st->structure = 0;
+    st->max_row = 0;
+    st->min_row = INT32_MAX;
+    st->nd = 0;
+    st->ntd = 0;
+    st->S = 0.0;
+}
+
+}  // namespace
+
+void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s) {
+    const int64_t n = m.nrows, nc = m.ncols;
+    const int64_t thr = true_diag_threshold(ratio, n, nc);  // features.cpp:146-147
+    feat_init<<<1, 1, 0, s>>>(st);
+    SOB_LAUNCH("feat_init");
+
+    DBuf<int32_t> rc(n, s);
+    const bool dense_bins = m.format != SO_DIA;
+    const int64_t nbins = n + nc;
+    DBuf<int32_t> bins(dense_bins ? nbins : 0, s);
+    if (dense_bins) SOB_CUDA(cudaMemsetAsync(bins.get(), 0, bins.bytes(), s));
+    DBuf<unsigned long long> dcount;
+    const bool has_dia = m.format == SO_DIA || m.format == SO_HDC;
+    if (has_dia) {
+        dcount.alloc(m.dia.ndiags, s);
+        if (m.dia.ndiags) SOB_CUDA(cudaMemsetAsync(dcount.get(), 0, dcount.bytes(), s));
+    }
+    const int grid_rows = grid_for(n, kB, 4);
+
+    auto scan_csr = [&](bool accum) {
+        if (m.csr.nblk == 0) return;
+        const int g = grid_for(m.csr.nblk * kB, kB, 4);
+        if (accum)
+            feat_csr<true><<<g, kB, 0, s>>>(m.csr.blk.get(), m.csr.nblk, m.csr.row_ptr.get(), m.csr.col.get(), n,
+                                            rc.get(), bins.get(), st);
+        else
+            feat_csr<false><<<g, kB, 0, s>>>(m.csr.blk.get(), m.csr.nblk, m.csr.row_ptr.get(), m.csr.col.get(), n,
+                                             rc.get(), bins.get(), st);
+        SOB_LAUNCH("feat_csr");
+    };
+    auto scan_dia = [&]() {
+        feat_dia<<<grid_rows, kB, 0, s>>>(n, nc, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(),
+                                          rc.get(), dcount.get(), st);
+        SOB_LAUNCH("feat_dia");
+    };
+    auto scan_ell = [&]() {
+        feat_ell<<<grid_rows, kB, 0, s>>>(n, int(m.ell.width), m.ell.col.get(), rc.get(), bins.get(), st);
+        SOB_LAUNCH("feat_ell");
+    };
+    auto scan_coo = [&]() {
+        if (m.coo.nnz == 0) return;
+        feat_coo<<<grid_for(m.coo.nnz, kB, 4), kB, 0, s>>>(m.coo.nnz, n, m.coo.row.get(), m.coo.col.get(),
+                                                            rc.get(), bins.get(), st);
+        SOB_LAUNCH("feat_coo");
+    };
+
+    switch (m.format) {
+        case SO_COO:
+            SOB_CUDA(cudaMemsetAsync(rc.get(), 0, rc.bytes(), s));
+            scan_coo();
+            break;
+        case SO_CSR:
+            scan_csr(false);
+            break;
+        case SO_DIA:
+            scan_dia();
+            break;
+        case SO_ELL:
+            scan_ell();
+            break;
+        case SO_HYB:
+            scan_ell();
+            scan_coo();
+            break;
+        case SO_HDC:
+            scan_dia();
+            if (m.dia.ndiags) {
+                dcount_to_bins<<<unsigned(ceil_div(m.dia.ndiags, 256)), 256, 0, s>>>(
+                    dcount.get(), m.dia.offsets.get(), int(m.dia.ndiags), n, bins.get());
+                SOB_LAUNCH("dcount_to_bins");
+            }
+            scan_csr(true);
+            break;
+    }
+
+    const int64_t nch = ceil_div(n, kSpreadChunk);
+    DBuf<double> csum(nch, s), P(nch + 1, s);
+    DBuf<MonoRec> rec(nch, s);
+    feat_rows<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, st, csum.get());
+    SOB_LAUNCH("feat_rows");
+    if (dense_bins) {
+        feat_bins<int32_t><<<grid_for(nbins, 256), 256, 0, s>>>(bins.get(), nbins, thr, st);
+    } else if (m.dia.ndiags) {
+        feat_bins<unsigned long long><<<grid_for(m.dia.ndiags, 256), 256, 0, s>>>(dcount.get(), m.dia.ndiags, thr, st);
+    }
+    SOB_LAUNCH("feat_bins");
+    spread_prefix<<<1, 512, 0, s>>>(csum.get(), nch, P.get());
+    SOB_LAUNCH("spread_prefix");
+    spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, st, csum.get(), P.get(), rec.get());
+    SOB_LAUNCH("spread_mono");
+    spread_walk<<<1, 32, 0, s>>>(rc.get(), n, nc, nch, rec.get(), st);
+    SOB_LAUNCH("spread_walk");
+}
+
+}  // namespace sob

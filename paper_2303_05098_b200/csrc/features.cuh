@@ -1,0 +1,23 @@
+// Device-side feature state shared by features.cu (producer) and model.cu
+// (tune_ml consumer: predict + feasibility read it without a host round trip).
+#pragma once
+
+#include "matrix.cuh"
+
+namespace sob {
+
+struct FeatState {
+    unsigned long long visits;     // entry visits = NNZ (features.cpp:22-26)
+    unsigned long long structure;  // structure reads (DIA holes, ELL sentinels)
+    int max_row;
+    int min_row;
+    unsigned long long nd, ntd;    // N_D, N_TD
+    double S;                      // exact sequential sum of squared deviations
+    so_feature_vector out;         // finalized vector
+};
+
+// Enqueue the whole feature pipeline on stream s; the finalized vector lands in
+// st->out (device).  Scratch is stream-ordered and released on return.
+void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s);
+
+}  // namespace sob

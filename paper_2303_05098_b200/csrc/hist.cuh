@@ -1,0 +1,79 @@
+// Diagonal histogram with shared-memory privatisation.
+//
+// Banded/stencil matrices send every entry into a handful of diagonal bins
+// (27 for configs 2 and 5), so direct global atomics would serialise on the
+// L2 atomic units.  Each persistent CTA keeps an open-addressing hash of
+// (key -> count) in shared memory; lanes holding the same key are first
+// merged with __match_any_sync, leaders insert into the hash, and the hash is
+// flushed with one global atomic per distinct key per CTA.  Keys that do not
+// find a slot within kProbe probes (scattered matrices) go straight to the
+// global bins, where they are spread over many addresses anyway.
+#pragma once
+
+#include "common.cuh"
+
+namespace sob {
+
+constexpr int kHashSlots = 2048;  // power of two
+constexpr int kProbe = 8;
+constexpr int32_t kEmptyKey = -1;
+
+struct SmemHash {
+    int32_t keys[kHashSlots];
+    int32_t cnts[kHashSlots];
+};
+
+__device__ __forceinline__ void hash_init(SmemHash& h) {
+    for (int i = threadIdx.x; i < kHashSlots; i += blockDim.x) {
+        h.keys[i] = kEmptyKey;
+        h.cnts[i] = 0;
+    }
+}
+
+// key >= 0 valid; key < 0 means "no entry for this lane".  Every lane of the
+// warp must call this (warp-synchronous).
+__device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbins, int32_t key) {
+    const unsigned lane = threadIdx.x & 31u;
+    // distinct dummy keys for idle lanes so they never merge with real ones
+    const int32_t k = key >= 0 ? key : -2 - int32_t(lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (key < 0) return;
+    const int leader = __ffs(peers) - 1;
+    if (int(lane) != leader) return;
+    const int32_t add = __popc(peers);
+    unsigned slot = unsigned(key) & (kHashSlots - 1);
+#pragma unroll 1
+    for (int p = 0; p < kProbe; ++p) {
+        int32_t old = h.keys[slot];
+        if (old == kEmptyKey) old = atomicCAS(&h.keys[slot], kEmptyKey, key);
+        if (old == kEmptyKey || old == key) {
+            atomicAdd(&h.cnts[slot], add);
+            return;
+        }
+        slot = (slot + 1) & (kHashSlots - 1);
+    }
+    atomicAdd(gbins + key, add);
+}
+
+__device__ __forceinline__ void hash_flush(SmemHash& h, int32_t* __restrict__ gbins) {
+    for (int i = threadIdx.x; i < kHashSlots; i += blockDim.x) {
+        const int32_t k = h.keys[i];
+        if (k != kEmptyKey && h.cnts[i] != 0) atomicAdd(gbins + k, h.cnts[i]);
+    }
+}
+
+// Row of entry k inside a row-block whose row_ptr slice [r0, r0+nr] is staged
+// in shared memory: the last row whose start is <= k.
+__device__ __forceinline__ int row_in_block(const int64_t* srp, int nr, int64_t k) {
+    int lo = 0, hi = nr;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (srp[mid] <= k)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+}  // namespace sob

@@ -1,0 +1,92 @@
+// Device-resident sparse containers (the HBM layout of DESIGN.md §3) and the
+// internal entry points shared by the .cu translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace sob {
+
+// CSR row-block partition (the "analysis" done once per matrix):
+// CTA b of the streaming CSR kernel owns rows [blk[b], blk[b+1]).  A block
+// holds the rows whose first entry falls into one kWindow-wide nnz window
+// (<= 2*kWindow entries, staged in shared memory), at most kRowsPerBlock rows,
+// or exactly one row longer than kWindow ("long row" block).
+constexpr int kWindow = 2048;
+constexpr int kRowsPerBlock = 1024;
+constexpr int kStreamBlock = 256;
+
+struct CooPart {
+    int64_t nnz = 0;
+    DBuf<int32_t> row, col;
+    DBuf<double> val;
+};
+struct CsrPart {
+    int64_t nnz = 0;
+    DBuf<int64_t> row_ptr;
+    DBuf<int32_t> col;
+    DBuf<double> val;
+    DBuf<int32_t> blk;  // row-block partition, nblk+1 entries
+    int64_t nblk = 0;
+};
+struct DiaPart {
+    int64_t ndiags = 0;
+    DBuf<int64_t> offsets;
+    DBuf<double> values;  // [d * nrows + i]
+    int64_t stored_nnz = 0;
+};
+struct EllPart {
+    int64_t width = 0;
+    DBuf<int32_t> col;  // column-major [k * nrows + i], sentinel -1
+    DBuf<double> val;
+    int64_t stored_nnz = 0;
+};
+
+}  // namespace sob
+
+struct so_matrix {
+    int device = 0;
+    int32_t format = SO_COO;
+    int64_t nrows = 0, ncols = 0;
+    sob::CooPart coo;  // COO, HYB coo part
+    sob::CsrPart csr;  // CSR, HDC csr part
+    sob::DiaPart dia;  // DIA, HDC dia part
+    sob::EllPart ell;  // ELL, HYB ell part
+    int64_t kh = 0;
+    int64_t threshold = 0;
+
+    int64_t nnz() const {
+        switch (format) {
+            case SO_COO: return coo.nnz;
+            case SO_CSR: return csr.nnz;
+            case SO_DIA: return dia.stored_nnz;
+            case SO_ELL: return ell.stored_nnz;
+            case SO_HYB: return ell.stored_nnz + coo.nnz;
+            case SO_HDC: return dia.stored_nnz + csr.nnz;
+        }
+        return 0;
+    }
+};
+
+namespace sob {
+
+// --- conversions (convert.cu) ---
+void build_row_blocks(CsrPart& csr, int64_t nrows, cudaStream_t s);
+so_matrix* coo_to_csr_device(const so_matrix& coo, cudaStream_t s);  // canonical input
+so_matrix* csr_to_format(const so_matrix& csr, int32_t target, const so_conversion_config& cfg,
+                         cudaStream_t s);
+so_matrix* any_to_csr(const so_matrix& m, cudaStream_t s);  // to_coo semantics, CSR layout
+so_matrix* csr_to_coo(const so_matrix& csr, cudaStream_t s);
+so_matrix* clone_matrix(const so_matrix& m, cudaStream_t s);
+bool coo_is_canonical(const so_matrix& coo, cudaStream_t s);
+
+// --- spmv (spmv.cu) ---
+void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s);
+int64_t spmv_bytes(const so_matrix& m);
+
+// --- host-side cap rules (formats.cpp:348-367), shared by convert + tune ---
+int64_t padded_entry_cap(const so_conversion_config& c, int64_t nnz);
+int64_t effective_kh(const so_conversion_config& c, int64_t nnz, int64_t nrows);
+int64_t true_diag_threshold(double ratio, int64_t nrows, int64_t ncols);
+int64_t checked_mul(int64_t a, int64_t b);
+
+}  // namespace sob

@@ -1,0 +1,225 @@
+// Decision-tree / random-forest inference on the device (model.cpp:202-228)
+// and the fused ML tuner (tuners.cpp:92-114): features -> predict ->
+// format_feasible -> CSR fallback, with no host round trip until the final
+// 8-int outcome.
+#include <string>
+#include <vector>
+
+#include "features.cuh"
+
+#include "forest.cuh"
+
+namespace sob {
+
+namespace {
+
+constexpr int kPB = 256;
+
+struct ForestView {
+    int kind, n_trees;
+    const int32_t *feature, *left, *right, *cls;
+    const double* threshold;
+    const int64_t* root;
+};
+
+ForestView view(const so_forest& f) {
+    return ForestView{f.f.kind,           f.f.n_trees,      f.f.feature.get(),   f.f.left.get(),
+                      f.f.right.get(),    f.f.cls.get(),    f.f.threshold.get(), f.f.root.get()};
+}
+
+// features_to_row (features.cpp:155-166)
+__device__ __forceinline__ void to_row(const so_feature_vector& f, double* row) {
+    row[0] = double(f.nrows);
+    row[1] = double(f.ncols);
+    row[2] = double(f.nnz);
+    row[3] = f.avg_nnz_per_row;
+    row[4] = f.density;
+    row[5] = double(f.max_nnz_per_row);
+    row[6] = double(f.min_nnz_per_row);
+    row[7] = f.nnz_row_spread;
+    row[8] = double(f.ndiags);
+    row[9] = double(f.ntrue_diags);
+}
+
+// Root-to-leaf walk: x[feature] <= threshold goes left (model.cpp:202-213).
+__device__ __forceinline__ int walk(const ForestView& f, int t, const double* row) {
+    int64_t node = f.root[t];
+    int feat = f.feature[node];
+    while (feat != -1) {
+        node = row[feat] <= f.threshold[node] ? f.left[node] : f.right[node];
+        feat = f.feature[node];
+    }
+    return f.cls[node];
+}
+
+// One CTA per feature row: thread per tree, integer votes in shared memory,
+// argmax with strict '>' so ties go to the lowest FormatId (model.cpp:215-228).
+__device__ int predict_block(const ForestView& f, const double* row, int trees) {
+    __shared__ int votes[8];
+    if (threadIdx.x < 8) votes[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < trees; t += blockDim.x) atomicAdd(&votes[walk(f, t, row)], 1);
+    __syncthreads();
+    int best = 0;
+    for (int c = 1; c < 6; ++c)
+        if (votes[c] > votes[best]) best = c;
+    __syncthreads();
+    return best;
+}
+
+__global__ void __launch_bounds__(kPB) predict_rows_kernel(ForestView f, const double* __restrict__ rows, int64_t n,
+                                                           int32_t* __restrict__ out) {
+    __shared__ double row[10];
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        if (threadIdx.x < 10) row[threadIdx.x] = rows[r * 10 + threadIdx.x];
+        __syncthreads();
+        const int best = predict_block(f, row, f.n_trees);  // predict_forest votes over every tree
+        if (threadIdx.x == 0) out[r] = best;
+        __syncthreads();
+    }
+}
+
+struct CapCfg {
+    int64_t kh_override;
+    double max_padding_factor;
+    int64_t max_padded_entries;
+};
+
+__device__ int64_t d_padded_entry_cap(const CapCfg& c, int64_t nnz) {  // formats.cpp:348-355
+    if (c.max_padded_entries > 0) return c.max_padded_entries;
+    const double cap = c.max_padding_factor * double(nnz);
+    if (cap >= 9223372036854775807.0) return INT64_MAX;
+    return int64_t(cap);
+}
+
+// tuners.cpp:26-45 (row_to_features already applied: integer fields)
+__device__ bool d_feasible(int target, const so_feature_vector& f, const CapCfg& c) {
+    const int64_t cap = d_padded_entry_cap(c, f.nnz);
+    switch (target) {
+        case SO_COO:
+        case SO_CSR:
+            return true;
+        case SO_DIA:
+            return f.ndiags * f.nrows <= cap;
+        case SO_ELL:
+            return f.max_nnz_per_row * f.nrows <= cap;
+        case SO_HYB: {
+            int64_t kh = c.kh_override > 0 ? c.kh_override
+                         : (f.nrows <= 0 || f.nnz <= 0) ? 0
+                                                         : (f.nnz + f.nrows - 1) / f.nrows;
+            const int64_t w = kh < f.max_nnz_per_row ? kh : f.max_nnz_per_row;
+            return w * f.nrows <= cap;
+        }
+        case SO_HDC:
+            return f.ntrue_diags * f.nrows <= cap;
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(kPB) tune_predict_kernel(ForestView f, const FeatState* __restrict__ st, CapCfg cfg,
+                                                           int active, so_tune_outcome* __restrict__ out) {
+    __shared__ double row[10];
+    if (threadIdx.x == 0) to_row(st->out, row);
+    __syncthreads();
+    // kind tree evaluates trees.front() only (tuners.cpp:103-105)
+    int chosen = predict_block(f, row, f.kind == 0 ? 1 : f.n_trees);
+    if (threadIdx.x == 0) {
+        // the model saw row_to_features(features_to_row(f)); feasibility uses
+        // the integer fields, identical for counts < 2^53
+        const so_feature_vector& fv = st->out;
+        int fallback = 0;
+        if (!d_feasible(chosen, fv, cfg)) {
+            chosen = SO_CSR;
+            fallback = 1;
+        }
+        out->chosen = chosen;
+        out->source = f.kind == 0 ? 1 : 2;
+        out->switched = chosen != active;
+        out->fallback_csr = fallback;
+        out->features = fv;
+    }
+}
+
+}  // namespace
+
+so_forest* forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off, const int32_t* feature,
+                         const double* threshold, const int32_t* left, const int32_t* right, const int32_t* cls,
+                         cudaStream_t s) {
+    if (n_trees < 1) fail(SO_INVALID_INPUT, "forest has no trees");
+    const int64_t nn = node_off[n_trees];
+    std::vector<int32_t> gl(nn), gr(nn), fe(nn), cl(nn);
+    std::vector<int64_t> root(n_trees);
+    for (int t = 0; t < n_trees; ++t) {
+        const int64_t b = node_off[t], e = node_off[t + 1];
+        if (e <= b) fail(SO_INVALID_INPUT, "tree with no nodes");
+        root[t] = b;
+        for (int64_t i = b; i < e; ++i) {
+            fe[i] = feature[i];
+            cl[i] = cls[i];
+            if (feature[i] == -1) {
+                gl[i] = gr[i] = -1;
+                if (cls[i] < 0 || cls[i] > 5) fail(SO_MALFORMED_MODEL, "leaf class outside 0..5");
+            } else {
+                if (feature[i] < 0 || feature[i] > 9) fail(SO_MALFORMED_MODEL, "feature index outside 0..9");
+                if (left[i] < 0 || left[i] >= e - b || right[i] < 0 || right[i] >= e - b)
+                    fail(SO_MALFORMED_MODEL, "dangling child reference");
+                gl[i] = int32_t(b + left[i]);
+                gr[i] = int32_t(b + right[i]);
+            }
+        }
+    }
+    // every node reachable exactly once from the root (model.cpp:151-176):
+    // rules out cycles before anything walks the tree on the device
+    for (int t = 0; t < n_trees; ++t) {
+        const int64_t b = node_off[t], e = node_off[t + 1];
+        std::vector<char> seen(size_t(e - b), 0);
+        std::vector<int64_t> stack{0};
+        seen[0] = 1;
+        int64_t visited = 0;
+        while (!stack.empty()) {
+            const int64_t id = stack.back();
+            stack.pop_back();
+            ++visited;
+            if (feature[b + id] == -1) continue;
+            for (int64_t ch : {int64_t(left[b + id]), int64_t(right[b + id])}) {
+                if (seen[size_t(ch)]) fail(SO_MALFORMED_MODEL, "node " + std::to_string(ch) + " referenced more than once");
+                seen[size_t(ch)] = 1;
+                stack.push_back(ch);
+            }
+        }
+        if (visited != e - b) fail(SO_MALFORMED_MODEL, "unreachable nodes in tree");
+    }
+    auto* f = new so_forest();
+    SOB_CUDA(cudaGetDevice(&f->device));
+    ForestDev& d = f->f;
+    d.kind = kind;
+    d.n_trees = n_trees;
+    d.n_nodes = nn;
+    auto up = [&](auto& buf, const auto* src, int64_t n) {
+        buf.alloc(n, s);
+        SOB_CUDA(cudaMemcpyAsync(buf.get(), src, sizeof(*src) * size_t(n), cudaMemcpyHostToDevice, s));
+    };
+    up(d.feature, fe.data(), nn);
+    up(d.left, gl.data(), nn);
+    up(d.right, gr.data(), nn);
+    up(d.cls, cl.data(), nn);
+    up(d.threshold, threshold, nn);
+    up(d.root, root.data(), n_trees);
+    SOB_CUDA(cudaStreamSynchronize(s));  // host staging vectors go out of scope
+    return f;
+}
+
+void predict_rows(const so_forest& f, const double* rows_dev, int64_t n, int32_t* out_dev, cudaStream_t s) {
+    if (n <= 0) return;
+    predict_rows_kernel<<<grid_for(n * kPB, kPB, 8), kPB, 0, s>>>(view(f), rows_dev, n, out_dev);
+    SOB_LAUNCH("predict_rows_kernel");
+}
+
+void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,
+                          so_tune_outcome* out_dev, cudaStream_t s) {
+    CapCfg c{cfg.kh_override, cfg.max_padding_factor, cfg.max_padded_entries};
+    tune_predict_kernel<<<1, kPB, 0, s>>>(view(f), st, c, active, out_dev);
+    SOB_LAUNCH("tune_predict_kernel");
+}
+
+}  // namespace sob

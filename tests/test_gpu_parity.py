@@ -1,0 +1,368 @@
+"""GPU parity: the sm_100a path through the C-ABI versus the oracle.
+
+Mirrors the reference's own suites (proj/tests/test_formats.cpp,
+test_spmv.cpp, test_features.cpp, test_model.cpp, test_tuners.cpp, criteria
+1/2/3/7/8 of acceptance.cpp) on the same seeded generators.  Bars:
+  * converted arrays, integer features, labels: bit-exact;
+  * spread/avg/density: bit-exact (binade replay), contract 1e-12 relative;
+  * SpMV: bit-exact for CSR/DIA/ELL/HDC rows (reference per-row order),
+    <= 1e-12 relative per row under max(1,|y|) for COO/HYB (oracles.hpp:166-174).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SPMV_TOL = 1e-12  # test_spmv.cpp:59, north star
+EXACT_FORMATS = (1, 2, 3, 5)  # CSR, DIA, ELL, HDC
+
+
+def to_dev(so, coo):
+    return so.DeviceMatrix.coo(coo["nrows"], coo["ncols"], coo["row"], coo["col"], coo["val"])
+
+
+def max_rel(got, want):
+    if got.size == 0:
+        return 0.0
+    return float(np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))))
+
+
+def cmp_host(a, b, path=""):
+    if isinstance(a, dict):
+        for k in a:
+            if k != "format":
+                cmp_host(a[k], b[k], path + "/" + k)
+    elif isinstance(a, np.ndarray):
+        assert a.dtype == b.dtype, path
+        assert np.array_equal(a, b), path
+    else:
+        assert a == b, (path, a, b)
+
+
+def worked(O):
+    return O.from_triplets(3, 3, [0, 0, 1, 2, 2], [0, 2, 1, 0, 2], [1.0, 2.0, 3.0, 4.0, 5.0])
+
+
+# ----------------------------------------------------------------- formats
+
+def test_worked_example_every_target(so, O):
+    a = worked(O)
+    d = to_dev(so, a)
+    for f in range(6):
+        m = d.from_coo(f)
+        assert m.format == f
+        cmp_host(m.download(), O.oc_convert(a, f))
+        assert np.array_equal(m.to_coo().download()["val"], a["val"])
+        assert m.spmv(np.ones(3)).tolist() == [3.0, 3.0, 9.0]  # test_spmv.cpp:10-18
+
+
+def test_from_coo_rejects_non_canonical(so):
+    bad = so.DeviceMatrix.coo(2, 2, [1, 0], [0, 0], [1.0, 2.0])
+    with pytest.raises(so.InvalidInput):
+        bad.from_coo(so.CSR)
+    with pytest.raises(so.InvalidInput):
+        bad.convert(so.DIA)
+
+
+def test_empty_and_1x1(so, O):  # test_formats.cpp:76-96
+    empty = O.coo_dict(4, 4, [], [], [])
+    tiny = O.coo_dict(1, 1, [0], [0], [7.0])
+    for f in range(6):
+        m = to_dev(so, empty).from_coo(f)
+        assert m.nnz() == 0
+        assert m.to_coo().download()["val"].size == 0
+        assert m.spmv([5, 6, 7, 8]).tolist() == [0, 0, 0, 0]
+        t = to_dev(so, tiny).from_coo(f)
+        assert t.nnz() == 1
+        cmp_host(t.to_coo().download(), tiny)
+
+
+def test_caps_raise_before_allocation(so, O):  # test_formats.cpp:118-141
+    n = 100
+    r, c, v = [], [], []
+    for i in range(n):
+        for j in (i - 1, i, i + 1):
+            if 0 <= j < n:
+                r.append(i), c.append(j), v.append(1.0 + (i + j) % 7)
+    band = O.from_triplets(n, n, r, c, v)
+    with pytest.raises(so.PaddingOverflow):
+        to_dev(so, band).from_coo(so.ELL, so.ConversionConfig(max_padded_entries=10))
+    csr = to_dev(so, band).from_coo(so.CSR)
+    with pytest.raises(so.PaddingOverflow):
+        csr.convert(so.ELL, so.ConversionConfig(max_padded_entries=10))
+    r = [k % 8 for k in range(40)]
+    c = [(k * 7 + k % 8) % 64 for k in range(40)]
+    sc = O.from_triplets(64, 64, r, c, [1.0] * 40)
+    with pytest.raises(so.PaddingOverflow):
+        to_dev(so, sc).from_coo(so.DIA)
+
+
+def test_hyb_kh_override(so, O):  # test_formats.cpp:98-107
+    m = to_dev(so, worked(O)).from_coo(so.CSR).convert(so.HYB, so.ConversionConfig(kh_override=1))
+    h = m.download()
+    assert h["ell"]["stored_nnz"] == 3 and h["coo"]["val"].size == 2 and h["kh"] == 1
+    cmp_host(m.to_coo().download(), worked(O))
+
+
+def test_explicit_zeros(so, O):  # test_formats.cpp:143-152
+    m = O.from_triplets(2, 2, [0, 0, 1], [0, 1, 0], [0.0, 2.0, 3.0])
+    for f in (0, 1, 3, 4):
+        cmp_host(to_dev(so, m).from_coo(f).to_coo().download(), m)
+    d = to_dev(so, m).from_coo(so.DIA)
+    assert d.nnz() == 2
+
+
+@pytest.mark.parametrize("seed,trials", [(2024, 200), (1000, 200)])
+def test_random_conversions_spmv_features(so, O, seed, trials):
+    """test_formats.cpp:154-245 + test_spmv.cpp:43-62 + test_features.cpp:90-108
+    + acceptance criteria 1-3, against the oracle on the same seeded matrices."""
+    rng, vrng = O.Rng(seed), O.Rng(seed + 1)
+    feasible = 0
+    for t in range(trials):
+        coo = rng.random_coo()
+        x = vrng.random_vector(coo["ncols"])
+        d = to_dev(so, coo)
+        ratio = 0.2 if t % 2 == 0 else 0.05 + 0.9 * (t % 7) / 7
+        for f in range(6):
+            try:
+                want = O.oc_convert(coo, f)
+            except O.PaddingOverflowOracle:
+                with pytest.raises(so.PaddingOverflow):
+                    d.from_coo(f)
+                continue
+            feasible += 1
+            m = d.from_coo(f)
+            got = m.download()
+            cmp_host(got, want, f"trial {t} fmt {f}")
+            cmp_host(m.to_coo().download(), coo, f"roundtrip {t} {f}")
+            assert m.nnz() == coo["val"].size
+            y = m.spmv(x)
+            y_ref = O.oc_spmv(want, x)
+            if f in EXACT_FORMATS:
+                assert np.array_equal(y, y_ref), (t, f)
+            else:
+                assert max_rel(y, y_ref) <= SPMV_TOL, (t, f)
+            fv, st = m.extract_features(ratio, with_stats=True)
+            fo, so_ = O.oc_features(want, ratio)
+            assert np.array_equal(np.array(fv.to_row()), fo), (t, f, fv.to_row(), fo)
+            assert (st.entry_visits, st.structure_reads) == so_, (t, f)
+            assert st.entry_visits <= 2 * coo["val"].size  # test_features.cpp:110-127
+    assert feasible > 400
+
+
+def test_switch_format_all_pairs(so, O):
+    rng = O.Rng(31)
+    for _ in range(25):
+        coo = rng.random_coo(40)
+        d = to_dev(so, coo)
+        for src in range(6):
+            try:
+                ms = d.from_coo(src)
+            except so.PaddingOverflow:
+                continue
+            for dst in range(6):
+                try:
+                    want = O.oc_convert(coo, dst)
+                except O.PaddingOverflowOracle:
+                    with pytest.raises(so.PaddingOverflow):
+                        ms.convert(dst)
+                    continue
+                cmp_host(ms.convert(dst).download(), want, f"{src}->{dst}")
+
+
+def test_upload_download_identity(so, O):
+    rng = O.Rng(77)
+    for _ in range(20):
+        coo = rng.random_coo(30)
+        for f in range(6):
+            try:
+                want = O.oc_convert(coo, f)
+            except O.PaddingOverflowOracle:
+                continue
+            cmp_host(so.DeviceMatrix.from_host(want).download(), want)
+
+
+# -------------------------------------------------------------------- SpMV
+
+def test_spmv_errors_and_timing(so, O):
+    m = to_dev(so, worked(O)).from_coo(so.CSR)
+    with pytest.raises(so.DimensionMismatch):
+        m.spmv([1.0, 1.0])
+    with pytest.raises(so.InvalidInput):
+        m.time_spmv(np.ones(3), 0)
+    per, tot = m.time_spmv(np.ones(3), 1)  # test_spmv.cpp:152-159
+    assert per.size == 1 and per[0] == tot and tot > 0
+    per, tot = m.time_spmv(np.ones(3), 1000)
+    assert per.size == 1000 and tot > 0 and abs(per.sum() - tot) <= 1e-9 * tot
+
+
+def test_ell_padding_poison(so, O):  # test_spmv.cpp:139-150
+    e = O.oc_convert(worked(O), O.ELL)
+    before = so.DeviceMatrix.from_host(e).spmv(np.ones(3))
+    e["val"][e["col"] == -1] = 1e9
+    assert np.array_equal(so.DeviceMatrix.from_host(e).spmv(np.ones(3)), before)
+
+
+def test_linearity(so, O):  # test_spmv.cpp:64-87
+    rng = O.Rng(11)
+    for _ in range(40):
+        coo = rng.random_coo(32)
+        m = to_dev(so, coo).from_coo(so.CSR)
+        x, z = rng.random_vector(coo["ncols"]), rng.random_vector(coo["ncols"])
+        a, b = rng.uniform_real(-2, 2), rng.uniform_real(-2, 2)
+        assert max_rel(m.spmv(a * x + b * z), a * m.spmv(x) + b * m.spmv(z)) <= 1e-10
+
+
+# ---------------------------------------------------------------- features
+
+def test_features_known_answers(so, O):  # test_features.cpp:27-72
+    f = to_dev(so, worked(O)).extract_features(0.5)
+    assert f.to_row()[:3] == [3, 3, 5] and f.max_nnz_per_row == 2 and f.min_nnz_per_row == 1
+    assert abs(f.nnz_row_spread - 2 / 9) <= 1e-12 and f.ndiags == 3 and f.ntrue_diags == 1
+    for n in (1, 3, 17):
+        ident = O.from_triplets(n, n, range(n), range(n), [1.0] * n)
+        g = to_dev(so, ident).extract_features(0.2)
+        assert (g.nnz, g.avg_nnz_per_row, g.nnz_row_spread, g.ndiags, g.ntrue_diags) == (n, 1.0, 0.0, 1, 1)
+    row = O.from_triplets(4, 4, [0] * 4, range(4), [1.0] * 4)
+    h = to_dev(so, row).extract_features(0.5)
+    assert (h.max_nnz_per_row, h.min_nnz_per_row, h.ndiags, h.ntrue_diags) == (4, 0, 4, 0)
+
+
+def test_features_errors(so, O):  # test_features.cpp:74-88
+    with pytest.raises(so.EmptyMatrix):
+        so.DeviceMatrix.coo(0, 5, [], [], []).extract_features(0.2)
+    for bad in (0.0, 1.5):
+        with pytest.raises(so.InvalidInput):
+            to_dev(so, worked(O)).extract_features(bad)
+
+
+# ------------------------------------------------------------------- model
+
+def flat(trees, kind=1):
+    off, fe, th, le, ri, cl = [0], [], [], [], [], []
+    for t in trees:
+        for (f, thr, l, r, c) in t:
+            fe.append(f), th.append(thr), le.append(l), ri.append(r), cl.append(c)
+        off.append(off[-1] + len(t))
+    import paper_2303_05098_b200 as P
+    return P.FlatForest(kind, np.array(off, np.int64), np.array(fe, np.int32), np.array(th),
+                        np.array(le, np.int32), np.array(ri, np.int32), np.array(cl, np.int32))
+
+
+STUMP = [(2, 4.0, 1, 2, -1), (-1, 0.0, -1, -1, 1), (-1, 0.0, -1, -1, 0)]
+COO_LEAF = [(-1, 0.0, -1, -1, 0)]
+CSR_LEAF = [(-1, 0.0, -1, -1, 1)]
+
+
+def test_predict_known_answers(so):  # test_model.cpp:72-118
+    stump = so.DeviceForest(flat([STUMP], kind=0))
+    for nnz, want in ((5, 0), (4, 1), (3, 1)):
+        assert stump.predict(so.FeatureVector.from_row([8, 8, nnz] + [0] * 7)) == want
+    assert so.DeviceForest(flat([CSR_LEAF, CSR_LEAF, COO_LEAF])).predict(so.FeatureVector()) == 1
+    assert so.DeviceForest(flat([COO_LEAF, CSR_LEAF])).predict(so.FeatureVector()) == 0
+
+
+def test_predict_random_forest_vs_oracle(so, O):  # test_model.cpp:120-158
+    rng = O.Rng(5150)
+    trees = []
+    for _ in range(10):
+        feat = int(rng.uniform_index(10))
+        thr = rng.uniform_real(0, 100)
+        lc, rc = int(rng.uniform_index(6)), int(rng.uniform_index(6))
+        trees.append([(feat, thr, 1, 2, -1), (-1, 0.0, -1, -1, lc), (-1, 0.0, -1, -1, rc)])
+    ff = flat(trees)
+    df = so.DeviceForest(ff)
+    rows = np.array([[rng.uniform_real(0, 100) for _ in range(10)] for _ in range(200)])
+    got = df.predict_rows(rows)
+    want = [O.oc_predict_forest(ff, r) for r in rows]
+    assert got.tolist() == want
+
+
+def test_malformed_forest_rejected(so):
+    with pytest.raises(so.MalformedModel):  # dangling child
+        so.DeviceForest(flat([[(2, 4.0, 1, 5, -1), (-1, 0, -1, -1, 1), (-1, 0, -1, -1, 0)]]))
+    with pytest.raises(so.MalformedModel):  # cycle (test_model.cpp:279-284)
+        so.DeviceForest(flat([[(2, 4.0, 1, 1, -1), (2, 8.0, 0, 0, -1)]]))
+
+
+# ------------------------------------------------------------------- tuner
+
+def test_tune_ml_stump_and_fallback(so, O):  # test_tuners.cpp:142-184
+    stump = so.DeviceForest(flat([STUMP], kind=0))
+    o = so.tune_ml(to_dev(so, worked(O)), stump)
+    assert o.chosen == 0 and o.source == 1 and o.switched == 0
+    assert o.feature_time_seconds > 0 and o.predict_time_seconds > 0
+    full_row = O.from_triplets(40, 40, [0] * 40, range(40), [1.0] * 40)
+    ell_model = so.DeviceForest(flat([[(-1, 0.0, -1, -1, 3)]], kind=0))
+    o = so.tune_ml(to_dev(so, full_row), ell_model)
+    assert o.fallback_csr == 1 and o.chosen == 1 and o.switched == 1
+
+
+def test_tune_ml_composes_features_and_predict(so, O):  # test_tuners.cpp:155-167
+    rng = O.Rng(43)
+    stump_ff = flat([STUMP], kind=0)
+    stump = so.DeviceForest(stump_ff)
+    for _ in range(100):
+        coo = rng.random_coo(32)
+        m = to_dev(so, coo).from_coo(so.CSR)
+        o = so.tune_ml(m, stump)
+        fo, _ = O.oc_features(O.oc_convert(coo, O.CSR), 0.2)
+        assert o.chosen == O.oc_predict_forest(stump_ff, fo)
+        assert o.features.to_row() == fo.tolist()
+
+
+def test_format_feasible_mirrors_conversion(so, O):  # test_tuners.cpp:297-317
+    rng = O.Rng(59)
+    for _ in range(100):
+        coo = rng.random_coo(48)
+        d = to_dev(so, coo)
+        f = d.extract_features(0.2)
+        for t in range(6):
+            try:
+                d.from_coo(t)
+                actual = True
+            except so.PaddingOverflow:
+                actual = False
+            assert so.format_feasible(t, f) == actual
+
+
+# ------------------------------------------- structured, realistic sizes
+
+def _structured(so, O, csr, ratio=0.2, formats=range(6)):
+    rows = csr.coo_rows()
+    coo = O.coo_dict(csr.nrows, csr.ncols, rows, csr.col, csr.val)
+    d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+    x = np.random.default_rng(9).uniform(-1, 1, csr.ncols)
+    want_feats, _ = O.oc_features(O.oc_convert(coo, O.CSR), ratio)
+    for f in formats:
+        try:
+            want = O.oc_convert(coo, f)
+        except O.PaddingOverflowOracle:
+            with pytest.raises(so.PaddingOverflow):
+                d.convert(f)
+            continue
+        m = d.convert(f)
+        cmp_host(m.download(), want, f"fmt {f}")
+        y, y_ref = m.spmv(x), O.oc_spmv(want, x)
+        if f in EXACT_FORMATS and np.diff(csr.row_ptr).max(initial=0) <= 2048:
+            assert np.array_equal(y, y_ref), f
+        else:
+            assert max_rel(y, y_ref) <= SPMV_TOL, f
+        fv = m.extract_features(ratio)
+        assert np.array_equal(np.array(fv.to_row()), want_feats), (f, fv.to_row(), want_feats)
+
+
+def test_config1_laplacian_full_size(so, O):
+    from paper_2303_05098_b200 import synth
+    _structured(so, O, synth.laplacian_2d(1000, seed=1))
+
+
+def test_banded_and_stencil(so, O):
+    from paper_2303_05098_b200 import synth
+    _structured(so, O, synth.banded(300_000, 13, seed=2))
+    _structured(so, O, synth.stencil_3d(40, 27, seed=5))
+
+
+def test_rmat_skewed(so, O):
+    from paper_2303_05098_b200 import synth
+    _structured(so, O, synth.rmat(16, 16, seed=42))
