@@ -209,8 +209,11 @@ def main():
     csr = build_workload(args.workload)
     base = P.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
 
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-legacy) stream: kernels and timing events share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
     x = torch.ones(csr.ncols, dtype=torch.float64, device="cuda")
     y = torch.empty(csr.nrows, dtype=torch.float64, device="cuda")
     l2 = torch.cuda.get_device_properties(local).L2_cache_size

@@ -160,12 +160,12 @@ __device__ __forceinline__ T warp_inclusive_sum(T v) {
 // Streaming loads: bypass L1 allocation for read-once matrix arrays.
 __device__ __forceinline__ double ld_stream(const double* p) {
     double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
 __device__ __forceinline__ int ld_stream(const int* p) {
     int v;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 

@@ -105,10 +105,17 @@ __global__ void row_block_flags(const int64_t* __restrict__ rp, int64_t n, int32
 }
 
 __global__ void row_block_scatter(const int32_t* __restrict__ flag, const int64_t* __restrict__ pos,
-                                  int64_t n, int32_t* __restrict__ blk) {
+                                  const int64_t* __restrict__ rp, int64_t n, int32_t* __restrict__ blk,
+                                  int64_t* __restrict__ blk_k) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n && flag[i]) blk[pos[i]] = int32_t(i);
-    if (i == n) blk[pos[n]] = int32_t(n);
+    if (i < n && flag[i]) {
+        blk[pos[i]] = int32_t(i);
+        blk_k[pos[i]] = rp[i];
+    }
+    if (i == n) {
+        blk[pos[n]] = int32_t(n);
+        blk_k[pos[n]] = rp[n];
+    }
 }
 
 // ------------------------------------------------------------ COO -> CSR
@@ -514,7 +521,9 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     if (n <= 0) {
         csr.nblk = 0;
         csr.blk.alloc(1, s);
+        csr.blk_k.alloc(1, s);
         SOB_CUDA(cudaMemsetAsync(csr.blk.get(), 0, sizeof(int32_t), s));
+        SOB_CUDA(cudaMemsetAsync(csr.blk_k.get(), 0, sizeof(int64_t), s));
         return;
     }
     DBuf<int32_t> flag(n, s);
@@ -524,7 +533,9 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
     csr.nblk = d2h_scalar(pos.get() + n, s);
     csr.blk.alloc(csr.nblk + 1, s);
-    row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), n, csr.blk.get());
+    csr.blk_k.alloc(csr.nblk + 1, s);
+    row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), csr.row_ptr.get(), n,
+                                                                     csr.blk.get(), csr.blk_k.get());
     SOB_LAUNCH("row_block_scatter");
 }
 
@@ -590,6 +601,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.col, src.csr.col);
     cp(m->csr.val, src.csr.val);
     cp(m->csr.blk, src.csr.blk);
+    cp(m->csr.blk_k, src.csr.blk_k);
     m->dia.ndiags = src.dia.ndiags;
     m->dia.stored_nnz = src.dia.stored_nnz;
     cp(m->dia.offsets, src.dia.offsets);

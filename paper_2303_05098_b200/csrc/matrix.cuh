@@ -25,7 +25,8 @@ struct CsrPart {
     DBuf<int64_t> row_ptr;
     DBuf<int32_t> col;
     DBuf<double> val;
-    DBuf<int32_t> blk;  // row-block partition, nblk+1 entries
+    DBuf<int32_t> blk;    // row-block partition, nblk+1 entries
+    DBuf<int64_t> blk_k;  // first entry of each row block (= row_ptr[blk[b]])
     int64_t nblk = 0;
 };
 struct DiaPart {

@@ -33,18 +33,55 @@ __device__ double block_sum_det(double v, double* scratch) {
 }
 
 // DIA contribution of one row, diagonals ascending (spmv.cpp:45-56 restated
-// per row: y[i] += diag[i] * x[i + off] for every in-range diagonal).
+// per row: y[i] += diag[i] * x[i + off] for every in-range diagonal).  Eight
+// diagonals are fetched before any is accumulated so each thread keeps eight
+// coalesced HBM loads in flight; in-range holes multiply as 0 * x exactly as
+// the reference does.
+constexpr int kDiaSmem = 512;
+
+// offsets come from shared memory (staged per CTA) when ndiags <= kDiaSmem,
+// else straight from global memory (GLOBAL_OFF)
+template <bool GLOBAL_OFF>
 __device__ __forceinline__ double dia_row(int64_t i, int64_t nrows, int64_t ncols, int ndiags,
+                                          const int64_t* __restrict__ soff,
                                           const int64_t* __restrict__ offsets,
                                           const double* __restrict__ vals,
                                           const double* __restrict__ x) {
+    constexpr int U = 8;
+    const int64_t* off = GLOBAL_OFF ? offsets : soff;
     double acc = 0.0;
-#pragma unroll 4
-    for (int d = 0; d < ndiags; ++d) {
-        const int64_t c = i + __ldg(offsets + d);
-        if (c >= 0 && c < ncols) acc = fadd(acc, fmul(ld_stream(vals + int64_t(d) * nrows + i), __ldg(x + c)));
+    int d0 = 0;
+    for (; d0 + U <= ndiags; d0 += U) {
+        double v[U], xv[U];
+        bool ok[U];
+        // unpredicated loads (cells outside the column range exist in the
+        // diagonal-major array, x index is clamped) so all 2U loads issue
+        // back to back; only in-range diagonals are accumulated
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int d = d0 + u;
+            const int64_t c = i + off[d];
+            ok[u] = c >= 0 && c < ncols;
+            const int64_t cc = c < 0 ? 0 : (c >= ncols ? ncols - 1 : c);
+            v[u] = ld_stream(vals + int64_t(d) * nrows + i);
+            xv[u] = __ldg(x + cc);
+        }
+        // x + (-0.0) == x exactly for every x (round-to-nearest), so skipped
+        // diagonals add -0.0: an unconditional chain keeps the loads hoisted
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = fadd(acc, ok[u] ? fmul(v[u], xv[u]) : -0.0);
+    }
+    for (; d0 < ndiags; ++d0) {
+        const int64_t c = i + off[d0];
+        if (c >= 0 && c < ncols) acc = fadd(acc, fmul(ld_stream(vals + int64_t(d0) * nrows + i), __ldg(x + c)));
     }
     return acc;
+}
+
+__device__ __forceinline__ void stage_offsets(int64_t* soff, const int64_t* __restrict__ offsets, int ndiags) {
+    const int m = ndiags < kDiaSmem ? ndiags : kDiaSmem;
+    for (int d = threadIdx.x; d < m; d += blockDim.x) soff[d] = offsets[d];
+    __syncthreads();
 }
 
 // ---------------------------------------------------------------- CSR -------
@@ -55,17 +92,27 @@ __device__ __forceinline__ double dia_row(int64_t i, int64_t nrows, int64_t ncol
 // fuses the HDC DIA part in front of the CSR part (spmv.cpp:101-106).
 template <bool WITH_DIA>
 __global__ void __launch_bounds__(kStreamBlock)
-    csr_stream_kernel(const int32_t* __restrict__ blk, const int64_t* __restrict__ rp,
+    csr_stream_kernel(const int32_t* __restrict__ blk, const int64_t* __restrict__ blk_k,
+                      const int64_t* __restrict__ rp,
                       const int32_t* __restrict__ col, const double* __restrict__ val,
                       const double* __restrict__ x, double* __restrict__ y, int64_t nrows,
                       int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                       const double* __restrict__ dvals) {
     extern __shared__ double prod[];  // 2 * kWindow
+    __shared__ int64_t soff[WITH_DIA ? kDiaSmem : 1];
+    if (WITH_DIA) stage_offsets(soff, offsets, ndiags);
     const int r0 = blk[blockIdx.x], r1 = blk[blockIdx.x + 1];
-    const int64_t k0 = rp[r0], k1 = rp[r1];
+    const int64_t k0 = blk_k[blockIdx.x], k1 = blk_k[blockIdx.x + 1];
     const int64_t nk = k1 - k0;
+    // prefetch this thread's first row bounds for phase 2
+    const int rme = r0 + int(threadIdx.x);
+    int64_t pa = 0, pe = 0;
+    if (rme < r1) {
+        pa = rp[rme];
+        pe = rp[rme + 1];
+    }
     if (nk <= 2 * kWindow) {
-        constexpr int U = 4;
+        constexpr int U = 8;
         const int n = int(nk);
         for (int j0 = 0; j0 < n; j0 += kStreamBlock * U) {
             int c[U];
@@ -85,11 +132,11 @@ __global__ void __launch_bounds__(kStreamBlock)
             }
         }
         __syncthreads();
-        for (int r = r0 + int(threadIdx.x); r < r1; r += kStreamBlock) {
-            const int a = int(rp[r] - k0), e = int(rp[r + 1] - k0);
+        for (int r = rme; r < r1; r += kStreamBlock) {
+            const int a = int((r == rme ? pa : rp[r]) - k0), e = int((r == rme ? pe : rp[r + 1]) - k0);
             double s = 0.0;
             for (int j = a; j < e; ++j) s = fadd(s, prod[j]);
-            if (WITH_DIA) s = fadd(dia_row(r, nrows, ncols, ndiags, offsets, dvals, x), s);
+            if (WITH_DIA) s = fadd((ndiags <= kDiaSmem ? dia_row<false>(r, nrows, ncols, ndiags, soff, offsets, dvals, x) : dia_row<true>(r, nrows, ncols, ndiags, soff, offsets, dvals, x)), s);
             y[r] = s;
         }
     } else {
@@ -99,7 +146,7 @@ __global__ void __launch_bounds__(kStreamBlock)
             s = fadd(s, fmul(ld_stream(val + k), __ldg(x + ld_stream(col + k))));
         double t = block_sum_det<kStreamBlock>(s, prod);
         if (threadIdx.x == 0) {
-            if (WITH_DIA) t = fadd(dia_row(r0, nrows, ncols, ndiags, offsets, dvals, x), t);
+            if (WITH_DIA) t = fadd((ndiags <= kDiaSmem ? dia_row<false>(r0, nrows, ncols, ndiags, soff, offsets, dvals, x) : dia_row<true>(r0, nrows, ncols, ndiags, soff, offsets, dvals, x)), t);
             y[r0] = t;
         }
     }
@@ -108,13 +155,16 @@ __global__ void __launch_bounds__(kStreamBlock)
 // ---------------------------------------------------------------- DIA -------
 // One thread per row, diagonals ascending: consecutive threads read
 // consecutive cells of each diagonal (diagonal-major layout => coalesced).
-__global__ void __launch_bounds__(256)
+template <bool GLOBAL_OFF>
+__global__ void __launch_bounds__(256, 8)
     dia_kernel(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                const double* __restrict__ vals, const double* __restrict__ x,
                double* __restrict__ y) {
+    __shared__ int64_t soff[GLOBAL_OFF ? 1 : kDiaSmem];
+    if (!GLOBAL_OFF) stage_offsets(soff, offsets, ndiags);
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nrows) return;
-    y[i] = dia_row(i, nrows, ncols, ndiags, offsets, vals, x);
+    y[i] = dia_row<GLOBAL_OFF>(i, nrows, ncols, ndiags, soff, offsets, vals, x);
 }
 
 // ---------------------------------------------------------------- ELL -------
@@ -223,82 +273,101 @@ __device__ SegPair block_excl_seg_scan(SegPair in, SegPair* wsc) {
     return res;
 }
 
+// shared-memory slot of chunk item e: one pad slot per kCooItems keeps the
+// per-thread sequential reads (items t*8 .. t*8+7) bank-conflict free
+__device__ __forceinline__ int coo_slot(int e) { return e + (e >> 3); }
+
 template <bool ACCUM>
-__global__ void __launch_bounds__(kCooBlock)
+__global__ void __launch_bounds__(kCooBlock, 6)
     coo_chunk_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row,
                      const int32_t* __restrict__ col, const double* __restrict__ val,
                      const double* __restrict__ x, double* __restrict__ y,
                      CooChunkRec* __restrict__ rec) {
-    __shared__ double sp[kCooChunk];
-    __shared__ int32_t sr[kCooChunk];
+    __shared__ double sp[kCooChunk + kCooChunk / kCooItems];
+    __shared__ int32_t sr[kCooChunk + kCooChunk / kCooItems];
     __shared__ SegPair wsc[kCooBlock / 32 + 1];
     const int64_t base = int64_t(blockIdx.x) * kCooChunk;
     const int cnt = int(z - base < kCooChunk ? z - base : int64_t(kCooChunk));
+    const int prev_row = base > 0 ? row[base - 1] : -1;
+    const int next_row = base + cnt < z ? row[base + cnt] : -1;
 #pragma unroll
     for (int j = 0; j < kCooItems; ++j) {
         const int e = j * kCooBlock + int(threadIdx.x);
         if (e < cnt) {
             const int64_t k = base + e;
-            sr[e] = ld_stream(row + k);
-            sp[e] = fmul(ld_stream(val + k), __ldg(x + ld_stream(col + k)));
+            sr[coo_slot(e)] = ld_stream(row + k);
+            sp[coo_slot(e)] = fmul(ld_stream(val + k), __ldg(x + ld_stream(col + k)));
         }
     }
-    const int prev_row = base > 0 ? row[base - 1] : -1;
-    const int next_row = base + cnt < z ? row[base + cnt] : -1;
     __syncthreads();
 
-    auto is_head = [&](int e) -> bool { return e == 0 ? sr[0] != prev_row : sr[e] != sr[e - 1]; };
+    // this thread's kCooItems consecutive entries, in registers
     const int first = int(threadIdx.x) * kCooItems;
-    const int last = min(first + kCooItems, cnt) - 1;
-    const bool has_items = first < cnt;
+    const int nmine = cnt - first < 0 ? 0 : (cnt - first > kCooItems ? kCooItems : cnt - first);
+    int rr[kCooItems];
+    double pp[kCooItems];
+#pragma unroll
+    for (int j = 0; j < kCooItems; ++j) {
+        rr[j] = j < nmine ? sr[coo_slot(first + j)] : -1;
+        pp[j] = j < nmine ? sp[coo_slot(first + j)] : 0.0;
+    }
+    const int r_before = nmine == 0 ? -1 : (first == 0 ? prev_row : sr[coo_slot(first - 1)]);
+    const int r_after = nmine == 0 ? -1 : (first + nmine < cnt ? sr[coo_slot(first + nmine)] : next_row);
+    const int chunk_first_row = sr[0];
 
-    // pass 1: this thread's tail piece
+    // pass 1: this thread's tail piece (sum of its last segment)
     SegPair mine{false, 0.0};
-    if (has_items) {
-        for (int e = first; e <= last; ++e) {
-            if (is_head(e)) {
+#pragma unroll
+    for (int j = 0; j < kCooItems; ++j) {
+        if (j < nmine) {
+            const bool head = rr[j] != (j == 0 ? r_before : rr[j - 1]);
+            if (head) {
                 mine.f = true;
-                mine.v = ACCUM ? y[sr[e]] : 0.0;
+                mine.v = ACCUM ? y[rr[j]] : 0.0;
             }
-            mine.v = fadd(mine.v, sp[e]);
+            mine.v = fadd(mine.v, pp[j]);
         }
     }
     const SegPair carry = block_excl_seg_scan(mine, wsc);
-    if (!has_items) return;
+    if (nmine == 0) return;
 
     // pass 2: finish segments
-    const bool first_cont = sr[0] == prev_row;
-    bool orphan = !carry.f && !is_head(first);  // piece of a segment begun before this chunk
-    double s = is_head(first) ? (ACCUM ? y[sr[first]] : 0.0) : carry.v;
-    for (int e = first; e <= last; ++e) {
-        const bool head = is_head(e);
-        if (e > first && head) {
-            s = ACCUM ? y[sr[e]] : 0.0;
-            orphan = false;
-        }
-        if (!ACCUM && head) {  // rows strictly between consecutive entries are empty
-            const int p = e == 0 ? prev_row : sr[e - 1];
-            for (int r = p + 1; r < sr[e]; ++r) y[r] = 0.0;
-        }
-        s = fadd(s, sp[e]);
-        const bool ends = (e + 1 < cnt) ? sr[e + 1] != sr[e] : next_row != sr[e];
-        if (ends) {
-            if (orphan)
+    const bool first_cont = chunk_first_row == prev_row;
+    const bool head0 = rr[0] != r_before;
+    bool orphan = !carry.f && !head0;  // piece of a segment begun before this chunk
+    double s = head0 ? (ACCUM ? y[rr[0]] : 0.0) : carry.v;
+#pragma unroll
+    for (int j = 0; j < kCooItems; ++j) {
+        if (j < nmine) {
+            const int prv = j == 0 ? r_before : rr[j - 1];
+            const bool head = rr[j] != prv;
+            if (j > 0 && head) {
+                s = ACCUM ? y[rr[j]] : 0.0;
+                orphan = false;
+            }
+            if (!ACCUM && head)  // rows strictly between consecutive entries are empty
+                for (int r = prv + 1; r < rr[j]; ++r) y[r] = 0.0;
+            s = fadd(s, pp[j]);
+            const int nxt = j + 1 < nmine ? rr[j + 1] : r_after;
+            const bool ends = nxt != rr[j];
+            const bool chunk_last = first + j == cnt - 1;
+            if (ends) {
+                if (orphan)
+                    rec[blockIdx.x].first_sum = s;
+                else
+                    y[rr[j]] = s;
+            } else if (chunk_last && orphan) {  // continues into the next chunk
                 rec[blockIdx.x].first_sum = s;
-            else
-                y[sr[e]] = s;
-        } else if (e == cnt - 1) {  // continues into the next chunk
-            if (orphan) rec[blockIdx.x].first_sum = s;
-        }
-        if (e == cnt - 1) {
-            const bool open = !ends;
-            int32_t f = (first_cont ? kFirstCont : 0) | (open ? kLastOpen : 0) |
-                        ((open && orphan) ? kSingle : 0);
-            rec[blockIdx.x].flags = f;
-            rec[blockIdx.x].last_row = sr[e];
-            rec[blockIdx.x].last_sum = s;
-            if (!ACCUM && base + cnt == z)  // trailing empty rows
-                for (int64_t r = int64_t(sr[e]) + 1; r < nrows; ++r) y[r] = 0.0;
+            }
+            if (chunk_last) {
+                const bool open = !ends;
+                rec[blockIdx.x].flags = (first_cont ? kFirstCont : 0) | (open ? kLastOpen : 0) |
+                                        ((open && orphan) ? kSingle : 0);
+                rec[blockIdx.x].last_row = rr[j];
+                rec[blockIdx.x].last_sum = s;
+                if (!ACCUM && base + cnt == z)  // trailing empty rows
+                    for (int64_t r = int64_t(rr[j]) + 1; r < nrows; ++r) y[r] = 0.0;
+            }
         }
     }
 }
@@ -334,19 +403,23 @@ void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, doubl
     const size_t smem = sizeof(double) * 2 * kWindow;
     if (with_dia) {
         csr_stream_kernel<true><<<unsigned(c.nblk), kStreamBlock, smem, s>>>(
-            c.blk.get(), c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
+            c.blk.get(), c.blk_k.get(), c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
             int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get());
     } else {
         csr_stream_kernel<false><<<unsigned(c.nblk), kStreamBlock, smem, s>>>(
-            c.blk.get(), c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
+            c.blk.get(), c.blk_k.get(), c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
             nullptr, nullptr);
     }
     SOB_LAUNCH("csr_stream_kernel");
 }
 
 void launch_dia(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
-    dia_kernel<<<unsigned(ceil_div(m.nrows, 256)), 256, 0, s>>>(
-        m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(), x, y);
+    if (m.dia.ndiags <= kDiaSmem)
+        dia_kernel<false><<<unsigned(ceil_div(m.nrows, 256)), 256, 0, s>>>(
+            m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(), x, y);
+    else
+        dia_kernel<true><<<unsigned(ceil_div(m.nrows, 256)), 256, 0, s>>>(
+            m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(), x, y);
     SOB_LAUNCH("dia_kernel");
 }
 
@@ -383,7 +456,11 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
             if (m.coo.nnz > 0) launch_coo<true>(m.coo, m.nrows, x, y, s);
             break;
         case SO_HDC:
-            launch_csr_stream(m, true, x, y, s);
+            // one kernel per non-empty part; both parts -> fused per-row kernel
+            if (m.csr.nnz == 0)
+                launch_dia(m, x, y, s);
+            else
+                launch_csr_stream(m, m.dia.ndiags > 0, x, y, s);
             break;
         default:
             fail(SO_INVALID_INPUT, "unknown format");
