@@ -92,6 +92,8 @@ void sweep(const so_matrix& csr, Op op, cudaStream_t s, int per_sm = 4) {
 
 // ---------------------------------------------------------- row-block build
 
+__device__ __forceinline__ int64_t ceil_div_d(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 __global__ void row_block_flags(const int64_t* __restrict__ rp, int64_t n, int32_t* __restrict__ flag) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -115,6 +117,42 @@ __global__ void row_block_scatter(const int32_t* __restrict__ flag, const int64_
     if (i == n) {
         blk[pos[n]] = int32_t(n);
         blk_k[pos[n]] = rp[n];
+    }
+}
+
+__global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_t limit, int32_t* __restrict__ flag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = (rp[i + 1] - rp[i]) > limit ? 1 : 0;
+}
+
+// warp groups: split at 32-row boundaries, window changes and around long rows
+__global__ void group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t win, int32_t* __restrict__ flag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t len = rp[i + 1] - rp[i];
+    // rows longer than win stand alone => every group holds <= 2*win entries
+    bool start = (i % 32 == 0) || len > win;
+    if (i > 0) start = start || (rp[i] - rp[i - 1]) > win || (rp[i] / win) != (rp[i - 1] / win);
+    flag[i] = start ? 1 : 0;
+}
+
+__global__ void long_row_list(const int64_t* __restrict__ rp, const int32_t* __restrict__ flag,
+                              const int64_t* __restrict__ pos, int64_t n, int32_t* __restrict__ lrow,
+                              int64_t* __restrict__ npc) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n || !flag[i]) return;
+    lrow[pos[i]] = int32_t(i);
+    npc[pos[i]] = ceil_div_d(rp[i + 1] - rp[i], kPiece);
+}
+
+__global__ void long_row_pieces(const int64_t* __restrict__ rp, const int32_t* __restrict__ lrow,
+                                const int64_t* __restrict__ lpiece, int64_t nlong, int64_t* __restrict__ pk) {
+    const int64_t l = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (l >= nlong) return;
+    const int64_t a = rp[lrow[l]], e = rp[lrow[l] + 1];
+    for (int64_t p = lpiece[l], k = a; p < lpiece[l + 1]; ++p, k += kPiece) {
+        pk[2 * p] = k;
+        pk[2 * p + 1] = k + kPiece < e ? k + kPiece : e;
     }
 }
 
@@ -520,6 +558,9 @@ void fill_ell_part(const so_matrix& csr, int64_t width, EllPart& ell, cudaStream
 void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     if (n <= 0) {
         csr.nblk = 0;
+        csr.ngrp = 0;
+        csr.nlong = 0;
+        csr.npieces = 0;
         csr.blk.alloc(1, s);
         csr.blk_k.alloc(1, s);
         SOB_CUDA(cudaMemsetAsync(csr.blk.get(), 0, sizeof(int32_t), s));
@@ -537,6 +578,39 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), csr.row_ptr.get(), n,
                                                                      csr.blk.get(), csr.blk_k.get());
     SOB_LAUNCH("row_block_scatter");
+    // SpMV warp groups; the window follows the mean row length
+    const int64_t nnz_total = d2h_scalar(csr.row_ptr.get() + n, s);
+    csr.grp_window = (nnz_total <= 8 * n) ? kGroupWindowShort : kGroupWindowLong;
+    group_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, csr.grp_window, flag.get());
+    SOB_LAUNCH("group_flags");
+    exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
+    csr.ngrp = d2h_scalar(pos.get() + n, s);
+    csr.grp.alloc(csr.ngrp + 1, s);
+    csr.grp_k.alloc(csr.ngrp + 1, s);
+    row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), csr.row_ptr.get(), n,
+                                                                     csr.grp.get(), csr.grp_k.get());
+    SOB_LAUNCH("row_block_scatter");
+    // long rows -> kPiece-entry pieces (SpMV splits them over many CTAs)
+    long_row_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, 2 * int64_t(csr.grp_window),
+                                                              flag.get());
+    SOB_LAUNCH("long_row_flags");
+    exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
+    csr.nlong = d2h_scalar(pos.get() + n, s);
+    csr.npieces = 0;
+    if (csr.nlong > 0) {
+        csr.long_row.alloc(csr.nlong, s);
+        DBuf<int64_t> npc(csr.nlong, s);
+        long_row_list<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), flag.get(), pos.get(), n,
+                                                                 csr.long_row.get(), npc.get());
+        SOB_LAUNCH("long_row_list");
+        csr.long_piece.alloc(csr.nlong + 1, s);
+        exclusive_scan_i64(npc.get(), csr.long_piece.get(), csr.nlong, s);
+        csr.npieces = d2h_scalar(csr.long_piece.get() + csr.nlong, s);
+        csr.piece_k.alloc(2 * csr.npieces, s);
+        long_row_pieces<<<unsigned(ceil_div(csr.nlong, 128)), 128, 0, s>>>(
+            csr.row_ptr.get(), csr.long_row.get(), csr.long_piece.get(), csr.nlong, csr.piece_k.get());
+        SOB_LAUNCH("long_row_pieces");
+    }
 }
 
 bool coo_is_canonical(const so_matrix& coo, cudaStream_t s) {  // formats.cpp:324-340
@@ -602,6 +676,15 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.val, src.csr.val);
     cp(m->csr.blk, src.csr.blk);
     cp(m->csr.blk_k, src.csr.blk_k);
+    m->csr.ngrp = src.csr.ngrp;
+    m->csr.grp_window = src.csr.grp_window;
+    cp(m->csr.grp, src.csr.grp);
+    cp(m->csr.grp_k, src.csr.grp_k);
+    m->csr.nlong = src.csr.nlong;
+    m->csr.npieces = src.csr.npieces;
+    cp(m->csr.long_row, src.csr.long_row);
+    cp(m->csr.long_piece, src.csr.long_piece);
+    cp(m->csr.piece_k, src.csr.piece_k);
     m->dia.ndiags = src.dia.ndiags;
     m->dia.stored_nnz = src.dia.stored_nnz;
     cp(m->dia.offsets, src.dia.offsets);

@@ -11,7 +11,13 @@ namespace sob {
 // holds the rows whose first entry falls into one kWindow-wide nnz window
 // (<= 2*kWindow entries, staged in shared memory), at most kRowsPerBlock rows,
 // or exactly one row longer than kWindow ("long row" block).
-constexpr int kWindow = 2048;
+constexpr int kWindow = 1024;
+constexpr int kPiece = 2048;  // entries per CTA for rows longer than 2*grp_window
+// SpMV warp groups: <= 32 rows whose first entries fall into one window of
+// grp_window entries (so <= 2*grp_window entries); short-row matrices use the
+// small window (8 entries per lane), others the large one (16 per lane).
+constexpr int kGroupWindowShort = 128;
+constexpr int kGroupWindowLong = 256;
 constexpr int kRowsPerBlock = 1024;
 constexpr int kStreamBlock = 256;
 
@@ -28,6 +34,16 @@ struct CsrPart {
     DBuf<int32_t> blk;    // row-block partition, nblk+1 entries
     DBuf<int64_t> blk_k;  // first entry of each row block (= row_ptr[blk[b]])
     int64_t nblk = 0;
+    // SpMV warp-group partition
+    int64_t ngrp = 0;
+    int grp_window = kGroupWindowLong;
+    DBuf<int32_t> grp;     // [ngrp+1]
+    DBuf<int64_t> grp_k;   // [ngrp+1]
+    // rows longer than 2*grp_window, split into kPiece-entry pieces for SpMV
+    int64_t nlong = 0, npieces = 0;
+    DBuf<int32_t> long_row;     // [nlong]
+    DBuf<int64_t> long_piece;   // [nlong+1] first piece of each long row
+    DBuf<int64_t> piece_k;      // [2*npieces] entry range [start, end) of each piece
 };
 struct DiaPart {
     int64_t ndiags = 0;

@@ -9,6 +9,8 @@
 // rows split across threads (CSR rows longer than kWindow, COO/HYB-COO
 // segments spanning thread or chunk boundaries) are combined in a fixed
 // tree order: deterministic, within the 1e-12 relative contract.
+#include <algorithm>
+
 #include "matrix.cuh"
 
 namespace sob {
@@ -85,71 +87,152 @@ __device__ __forceinline__ void stage_offsets(int64_t* soff, const int64_t* __re
 }
 
 // ---------------------------------------------------------------- CSR -------
-// Streaming CSR ("CSR-stream"): CTA b owns rows [blk[b], blk[b+1]).  Phase 1
-// streams the block's contiguous val/col range with coalesced loads, gathers
-// x and stages the rounded products in shared memory; phase 2 gives each row
-// to one thread which sums its products in the reference order.  WITH_DIA
-// fuses the HDC DIA part in front of the CSR part (spmv.cpp:101-106).
-template <bool WITH_DIA>
-__global__ void __launch_bounds__(kStreamBlock)
-    csr_stream_kernel(const int32_t* __restrict__ blk, const int64_t* __restrict__ blk_k,
-                      const int64_t* __restrict__ rp,
-                      const int32_t* __restrict__ col, const double* __restrict__ val,
-                      const double* __restrict__ x, double* __restrict__ y, int64_t nrows,
-                      int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
-                      const double* __restrict__ dvals) {
-    extern __shared__ double prod[];  // 2 * kWindow
+// Streaming CSR ("CSR-stream"), persistent and software-pipelined.  Window w
+// owns rows [blk[w], blk[w+1]) whose entries [blk_k[w], blk_k[w+1]) (at most
+// 2*kWindow) are contiguous.  Phase 1 gathers x for the window's col/val
+// (already in registers) and stages the rounded products in shared memory;
+// then the col/val (and row_ptr) loads of the CTA's NEXT window are issued so
+// they are in flight while phase 2 gives each row to one thread that sums its
+// products in the reference order (bit-exact).  WITH_DIA fuses the HDC DIA
+// part in front of the CSR part (spmv.cpp:101-106).  Windows holding a single
+// row longer than 2*kWindow are skipped here: csr_long_pieces + csr_long_fixup
+// split them over many CTAs.
+// Warp-level CSR stream.  Group g = rows [grp[g], grp[g+1]) (<= 32 rows,
+// entries [grp_k[g], grp_k[g+1]) <= 32*IT) is owned by one warp: coalesced
+// col/val loads (IT per lane), x gather, rounded products into warp-private
+// shared memory, then lane i sums row grp[g]+i sequentially (reference order,
+// bit-exact).  The next group's loads are issued before the sums, so each
+// warp keeps 2*IT loads in flight with no CTA-wide barrier anywhere.
+template <int IT, bool WITH_DIA>
+__global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
+    csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
+                    const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                    int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
+                    const double* __restrict__ dvals) {
+    __shared__ double sp[8][32 * IT];
     __shared__ int64_t soff[WITH_DIA ? kDiaSmem : 1];
     if (WITH_DIA) stage_offsets(soff, offsets, ndiags);
-    const int r0 = blk[blockIdx.x], r1 = blk[blockIdx.x + 1];
-    const int64_t k0 = blk_k[blockIdx.x], k1 = blk_k[blockIdx.x + 1];
-    const int64_t nk = k1 - k0;
-    // prefetch this thread's first row bounds for phase 2
-    const int rme = r0 + int(threadIdx.x);
-    int64_t pa = 0, pe = 0;
-    if (rme < r1) {
-        pa = rp[rme];
-        pe = rp[rme + 1];
-    }
-    if (nk <= 2 * kWindow) {
-        constexpr int U = 8;
-        const int n = int(nk);
-        for (int j0 = 0; j0 < n; j0 += kStreamBlock * U) {
-            int c[U];
-            double v[U];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* prod = sp[wid];
+    int64_t g = int64_t(blockIdx.x) * 8 + wid;
+    const int64_t stride = int64_t(gridDim.x) * 8;
+    if (g >= ngrp) return;
+    int r0 = grp[g], r1 = grp[g + 1];
+    int64_t k0 = grp_k[g], k1 = grp_k[g + 1];
+    int c[IT];
+    double v[IT];
+    bool longrow = k1 - k0 > 32 * IT;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int j = j0 + u * kStreamBlock + int(threadIdx.x);
-                if (j < n) {
-                    c[u] = ld_stream(col + k0 + j);
-                    v[u] = ld_stream(val + k0 + j);
+    for (int u = 0; u < IT; ++u) {
+        const int64_t k = k0 + u * 32 + lane;
+        if (!longrow && k < k1) {
+            c[u] = ld_stream(col + k);
+            v[u] = ld_stream(val + k);
+        }
+    }
+    int64_t pa = 0, pe = 0;
+    if (r0 + lane < r1) {
+        pa = rp[r0 + lane];
+        pe = rp[r0 + lane + 1];
+    }
+    while (true) {
+        const int64_t gn = g + stride;
+        int nr0 = 0, nr1 = 0;
+        int64_t nk0 = 0, nk1 = 0;
+        if (gn < ngrp) {
+            nr0 = grp[gn];
+            nr1 = grp[gn + 1];
+            nk0 = grp_k[gn];
+            nk1 = grp_k[gn + 1];
+        }
+        if (!longrow) {
+#pragma unroll
+            for (int u = 0; u < IT; ++u) {
+                const int64_t k = k0 + u * 32 + lane;
+                if (k < k1) prod[u * 32 + lane] = fmul(v[u], __ldg(x + c[u]));
+            }
+        }
+        __syncwarp();
+        const bool nlong = nk1 - nk0 > 32 * IT;
+        int64_t npa = 0, npe = 0;
+        if (gn < ngrp) {
+#pragma unroll
+            for (int u = 0; u < IT; ++u) {
+                const int64_t k = nk0 + u * 32 + lane;
+                if (!nlong && k < nk1) {
+                    c[u] = ld_stream(col + k);
+                    v[u] = ld_stream(val + k);
                 }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int j = j0 + u * kStreamBlock + int(threadIdx.x);
-                if (j < n) prod[j] = fmul(v[u], __ldg(x + c[u]));
+            if (nr0 + lane < nr1) {
+                npa = rp[nr0 + lane];
+                npe = rp[nr0 + lane + 1];
             }
         }
-        __syncthreads();
-        for (int r = rme; r < r1; r += kStreamBlock) {
-            const int a = int((r == rme ? pa : rp[r]) - k0), e = int((r == rme ? pe : rp[r + 1]) - k0);
+        if (!longrow && r0 + lane < r1) {
+            const int r = r0 + lane;
             double s = 0.0;
-            for (int j = a; j < e; ++j) s = fadd(s, prod[j]);
-            if (WITH_DIA) s = fadd((ndiags <= kDiaSmem ? dia_row<false>(r, nrows, ncols, ndiags, soff, offsets, dvals, x) : dia_row<true>(r, nrows, ncols, ndiags, soff, offsets, dvals, x)), s);
+            for (int64_t j = pa - k0; j < pe - k0; ++j) s = fadd(s, prod[j]);
+            if (WITH_DIA)
+                s = fadd(ndiags <= kDiaSmem ? dia_row<false>(r, nrows, ncols, ndiags, soff, offsets, dvals, x)
+                                            : dia_row<true>(r, nrows, ncols, ndiags, soff, offsets, dvals, x),
+                         s);
             y[r] = s;
         }
-    } else {
-        // one row longer than kWindow: strided partial sums + fixed tree
-        double s = 0.0;
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += kStreamBlock)
-            s = fadd(s, fmul(ld_stream(val + k), __ldg(x + ld_stream(col + k))));
-        double t = block_sum_det<kStreamBlock>(s, prod);
-        if (threadIdx.x == 0) {
-            if (WITH_DIA) t = fadd((ndiags <= kDiaSmem ? dia_row<false>(r0, nrows, ncols, ndiags, soff, offsets, dvals, x) : dia_row<true>(r0, nrows, ncols, ndiags, soff, offsets, dvals, x)), t);
-            y[r0] = t;
-        }
+        __syncwarp();
+        if (gn >= ngrp) break;
+        g = gn;
+        r0 = nr0;
+        r1 = nr1;
+        k0 = nk0;
+        k1 = nk1;
+        pa = npa;
+        pe = npe;
+        longrow = nlong;
     }
+}
+
+// Rows longer than 2*grp_window: piece p covers entries [pk[2p], pk[2p+1]) of row
+// prow[p] (<= kPiece entries, 8 independent loads per thread), reduced with a
+// fixed tree into part[p]; csr_long_fixup then adds the pieces of each row in
+// piece order (deterministic, within the 1e-12 contract).
+__global__ void __launch_bounds__(kStreamBlock)
+    csr_long_pieces(const int64_t* __restrict__ pk, const int32_t* __restrict__ col,
+                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ part) {
+    __shared__ double scratch[kStreamBlock / 32];
+    const int64_t k0 = pk[2 * blockIdx.x], k1 = pk[2 * blockIdx.x + 1];
+    constexpr int U = kPiece / kStreamBlock;
+    int c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + u * kStreamBlock + threadIdx.x;
+        c[u] = k < k1 ? ld_stream(col + k) : 0;
+        v[u] = k < k1 ? ld_stream(val + k) : 0.0;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + u * kStreamBlock + threadIdx.x;
+        if (k < k1) s = fadd(s, fmul(v[u], __ldg(x + c[u])));
+    }
+    const double t = block_sum_det<kStreamBlock>(s, scratch);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+template <bool WITH_DIA>
+__global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, const int64_t* __restrict__ lpiece,
+                               const double* __restrict__ part, double* __restrict__ y, int64_t nrows, int64_t ncols,
+                               int ndiags, const int64_t* __restrict__ offsets, const double* __restrict__ dvals,
+                               const double* __restrict__ x) {
+    const int64_t l = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (l >= nlong) return;
+    double t = 0.0;
+    for (int64_t p = lpiece[l]; p < lpiece[l + 1]; ++p) t = fadd(t, part[p]);
+    const int r = lrow[l];
+    if (WITH_DIA) t = fadd(dia_row<true>(r, nrows, ncols, ndiags, nullptr, offsets, dvals, x), t);
+    y[r] = t;
 }
 
 // ---------------------------------------------------------------- DIA -------
@@ -398,19 +481,44 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
     SOB_LAUNCH("coo_fixup");
 }
 
+template <int IT>
+void launch_csr_warp(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
+    const CsrPart& c = m.csr;
+    const int per_sm = IT > 8 ? 3 : 4;
+    const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
+    if (with_dia)
+        csr_warp_kernel<IT, true><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
+                                                       c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
+                                                       int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get());
+    else
+        csr_warp_kernel<IT, false><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
+                                                        c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
+                                                        nullptr, nullptr);
+    SOB_LAUNCH("csr_warp_kernel");
+}
+
 void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
-    const size_t smem = sizeof(double) * 2 * kWindow;
-    if (with_dia) {
-        csr_stream_kernel<true><<<unsigned(c.nblk), kStreamBlock, smem, s>>>(
-            c.blk.get(), c.blk_k.get(), c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
-            int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get());
-    } else {
-        csr_stream_kernel<false><<<unsigned(c.nblk), kStreamBlock, smem, s>>>(
-            c.blk.get(), c.blk_k.get(), c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
-            nullptr, nullptr);
+    if (c.ngrp == 0) return;
+    if (c.grp_window == kGroupWindowShort)
+        launch_csr_warp<2 * kGroupWindowShort / 32>(m, with_dia, x, y, s);
+    else
+        launch_csr_warp<2 * kGroupWindowLong / 32>(m, with_dia, x, y, s);
+    if (c.nlong > 0) {
+        const int nd = with_dia ? int(m.dia.ndiags) : 0;
+        DBuf<double> part(c.npieces, s);
+        csr_long_pieces<<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(), c.val.get(), x,
+                                                                     part.get());
+        SOB_LAUNCH("csr_long_pieces");
+        const unsigned g = unsigned(ceil_div(c.nlong, 128));
+        if (with_dia)
+            csr_long_fixup<true><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y,
+                                                  m.nrows, m.ncols, nd, m.dia.offsets.get(), m.dia.values.get(), x);
+        else
+            csr_long_fixup<false><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y,
+                                                   m.nrows, m.ncols, 0, nullptr, nullptr, x);
+        SOB_LAUNCH("csr_long_fixup");
     }
-    SOB_LAUNCH("csr_stream_kernel");
 }
 
 void launch_dia(const so_matrix& m, const double* x, double* y, cudaStream_t s) {

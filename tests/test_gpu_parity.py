@@ -366,3 +366,23 @@ def test_banded_and_stencil(so, O):
 def test_rmat_skewed(so, O):
     from paper_2303_05098_b200 import synth
     _structured(so, O, synth.rmat(16, 16, seed=42))
+
+
+def test_hdc_with_long_rows(so, O):
+    """HDC with a populated DIA part AND CSR rows longer than 2*kWindow
+    (exercises the split-row pieces + fused DIA fix-up)."""
+    from paper_2303_05098_b200 import synth
+    band = synth.banded(20_000, 3, seed=3)
+    rows, cols, vals = [band.coo_rows()], [band.col], [band.val]
+    rng = np.random.default_rng(4)
+    for r in (5, 777, 19_999):  # three dense rows
+        c = np.setdiff1d(rng.choice(20_000, 9000, replace=False), np.arange(r - 3, r + 4))
+        rows.append(np.full(c.size, r)), cols.append(c), vals.append(rng.uniform(0.5, 2, c.size))
+    coo = O.from_triplets(20_000, 20_000, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
+    d = to_dev(so, coo)
+    x = np.random.default_rng(5).uniform(-1, 1, 20_000)
+    for f in (1, 5, 0, 4):
+        want = O.oc_convert(coo, f)
+        m = d.from_coo(f)
+        cmp_host(m.download(), want, f"fmt {f}")
+        assert max_rel(m.spmv(x), O.oc_spmv(want, x)) <= SPMV_TOL, f
