@@ -42,3 +42,18 @@ clean:
 	rm -rf $(LIBDIR)
 
 .PHONY: all oracle clean
+
+# The reference's own hot-path unit suites (proj/tests/test_{formats,spmv,
+# features,model,tuners}.cpp, compiled in place, unmodified) linked against
+# the B200 C++ API -> build/reftests/ (test infrastructure; needs /root/reference).
+REF_TESTS := formats spmv features model tuners
+REF_PROJ  ?= /root/reference/proj
+reftests: $(LIBDIR)/libsparseoracle.so
+	@mkdir -p build/reftests
+	@if [ -d $(REF_PROJ)/tests ]; then for t in $(REF_TESTS); do \
+	  $(CXX) -std=c++20 -O1 -Iinclude -Itests/support/doctest_shim -I$(REF_PROJ)/tests \
+	    $(REF_PROJ)/tests/test_$$t.cpp -o build/reftests/test_$$t \
+	    -L$(LIBDIR) -lsparseoracle -lsparseoracle_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' || exit 1; \
+	done; else echo "reftests: $(REF_PROJ)/tests absent, keeping prebuilt binaries"; fi
+
+.PHONY: reftests

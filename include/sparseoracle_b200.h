@@ -149,6 +149,15 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags,
                                const int64_t* row_ptr, const int64_t* col,
                                const double* val, int64_t threshold,
                                so_matrix** out);
+/* CSR already in device memory (e.g. produced by a device generator or another
+ * library): row_ptr int64[n+1], col int32[nnz], val f64[nnz], all device
+ * pointers on the current device, fully written before the call (the copy
+ * is ordered on the library stream, not the producer's).  Copied (D2D) and
+ * validated; the caller keeps ownership of its buffers. */
+so_status so_matrix_import_csr_device(int64_t nrows, int64_t ncols, int64_t nnz,
+                                      const int64_t* row_ptr_dev,
+                                      const int32_t* col_dev,
+                                      const double* val_dev, so_matrix** out);
 void so_matrix_free(so_matrix* m);
 so_status so_matrix_info_get(const so_matrix* m, so_matrix_info* out);
 /* D2H into caller buffers sized per so_matrix_info (ELL transposed back to

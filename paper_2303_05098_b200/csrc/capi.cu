@@ -114,6 +114,11 @@ __global__ void check_row_ptr(const int64_t* __restrict__ rp, int64_t n, int64_t
     if (i < n && rp[i + 1] < rp[i]) atomicExch(bad, 1);
 }
 
+__global__ void check_cols(const int32_t* __restrict__ col, int64_t n, int64_t ncols, int* __restrict__ bad) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && (col[i] < 0 || col[i] >= ncols)) atomicExch(bad, 1);
+}
+
 __global__ void ell_short_rows(const int32_t* __restrict__ col_cm, int64_t n, int64_t K,
                                unsigned long long* __restrict__ out) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -364,6 +369,34 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags, con
         upload_dia_part(m->dia, nrows, ncols, ndiags, offsets, values, dia_stored_nnz, s);
         upload_csr_part(m->csr, nrows, ncols, csr_nnz, row_ptr, col, val, s);
         m->threshold = threshold;
+        return m.release();
+    });
+}
+
+so_status so_matrix_import_csr_device(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr_dev,
+                                      const int32_t* col_dev, const double* val_dev, so_matrix** out) {
+    return make(out, [&] {
+        std::unique_ptr<so_matrix> m(new_host_matrix(SO_CSR, nrows, ncols));
+        cudaStream_t s = ctx(m->device).stream;
+        CsrPart& c = m->csr;
+        c.nnz = nnz;
+        c.row_ptr.alloc(nrows + 1, s);
+        c.col.alloc(nnz, s);
+        c.val.alloc(nnz, s);
+        SOB_CUDA(cudaMemcpyAsync(c.row_ptr.get(), row_ptr_dev, c.row_ptr.bytes(), cudaMemcpyDeviceToDevice, s));
+        if (nnz > 0) {
+            SOB_CUDA(cudaMemcpyAsync(c.col.get(), col_dev, c.col.bytes(), cudaMemcpyDeviceToDevice, s));
+            SOB_CUDA(cudaMemcpyAsync(c.val.get(), val_dev, c.val.bytes(), cudaMemcpyDeviceToDevice, s));
+        }
+        BadFlag bad(s);
+        check_row_ptr<<<grid1(nrows + 1), 256, 0, s>>>(c.row_ptr.get(), nrows, nnz, bad.get());
+        SOB_LAUNCH("check_row_ptr");
+        if (nnz > 0) {
+            check_cols<<<grid1(nnz), 256, 0, s>>>(c.col.get(), nnz, ncols, bad.get());
+            SOB_LAUNCH("check_cols");
+        }
+        bad.raise_if(SO_INVALID_INPUT, "device CSR arrays inconsistent (row_ptr or column index out of range)");
+        build_row_blocks(c, nrows, s);
         return m.release();
     });
 }

@@ -123,6 +123,15 @@ class DeviceMatrix:
         return cls(out)
 
     @classmethod
+    def csr_device(cls, nrows, ncols, nnz, row_ptr_ptr, col_ptr, val_ptr):
+        """Import a CSR that already lives in device memory (int64 row_ptr,
+        int32 col, f64 val device pointers, e.g. torch tensors' data_ptr())."""
+        out = C.c_void_p()
+        _check(A.lib().so_matrix_import_csr_device(nrows, ncols, nnz, C.c_void_p(row_ptr_ptr),
+                                                   C.c_void_p(col_ptr), C.c_void_p(val_ptr), C.byref(out)))
+        return cls(out)
+
+    @classmethod
     def dia(cls, nrows, ncols, offsets, values, stored_nnz):
         offsets, values = _i64(offsets), _f64(values)
         out = C.c_void_p()
