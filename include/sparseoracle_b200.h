@@ -183,6 +183,11 @@ int32_t so_format_feasible(int32_t target, const so_feature_vector* f,
 /* Device pointers, stream-ordered, no sync.  x has ncols, y has nrows slots. */
 so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev,
                          void* stream);
+/* Row range [row_lo, row_hi) of y = A x only (DIA; the row-partitioned
+ * halo iteration computes boundary rows, starts the exchange, then the
+ * interior).  y_dev is indexed by matrix row.  Stream-ordered. */
+so_status so_spmv_device_rows(const so_matrix* m, const double* x_dev, double* y_dev,
+                              int64_t row_lo, int64_t row_hi, void* stream);
 /* spmv(m, x): host vectors, H2D x + kernel(s) + D2H y, synchronous. */
 so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y);
 /* time_spmv: x uploaded once, 1 untimed warm-up, then `reps` multiplies each
@@ -217,6 +222,17 @@ so_status so_predict_rows(const so_forest* f, int64_t n, const double* rows,
  * one small D2H of the outcome.  Never runs SpMV, never mutates m. */
 so_status so_tune_ml(const so_matrix* m, const so_forest* f, double true_diag_ratio,
                      const so_conversion_config* cfg, so_tune_outcome* out);
+
+/* ---- synthetic generators (device; bench / multi-GPU inputs) ------------- */
+/* 27-point stencil on a g^3 grid (row-major z,y,x), restricted to global rows
+ * [row_lo, row_hi) and global columns [col_lo, col_hi), as a DIA matrix of
+ * (row_hi-row_lo) x (col_hi-col_lo) with offsets off + (row_lo - col_lo).
+ * Values are a deterministic hash of (seed, global row, neighbour) in
+ * +-[0.5, 2), so every row slice of the global matrix is consistent
+ * (config 5: row-partitioned iteration). */
+so_status so_gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi,
+                               int64_t col_lo, int64_t col_hi, uint64_t seed,
+                               so_matrix** out);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,8 @@ _SIGS = {
     "so_to_coo": (C.c_int, [vp, P(vp)]),
     "so_format_feasible": (i32, [i32, P(FeatureVector), P(ConversionConfig)]),
     "so_spmv_device": (C.c_int, [vp, vp, vp, vp]),
+    "so_spmv_device_rows": (C.c_int, [vp, vp, vp, i64, i64, vp]),
+    "so_gen_stencil27_dia": (C.c_int, [i64, i64, i64, i64, i64, C.c_uint64, P(vp)]),
     "so_spmv": (C.c_int, [vp, vp, i64, vp]),
     "so_time_spmv": (C.c_int, [vp, vp, i64, i64, vp, P(f64)]),
     "so_spmv_bytes": (i64, [vp]),

@@ -543,6 +543,26 @@ so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev,
     });
 }
 
+so_status so_spmv_device_rows(const so_matrix* m, const double* x_dev, double* y_dev, int64_t row_lo,
+                              int64_t row_hi, void* stream) {
+    return guard([&] {
+        on_device(m);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx(m->device).stream;
+        spmv_device_rows(*m, x_dev, y_dev, row_lo, row_hi, s);
+    });
+}
+
+so_status so_gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_t col_lo, int64_t col_hi,
+                               uint64_t seed, so_matrix** out) {
+    return make(out, [&] {
+        const int64_t n = g * g * g;
+        if (g < 1 || row_lo < 0 || row_hi > n || row_lo > row_hi || col_lo < 0 || col_hi > n || col_lo > col_hi)
+            fail(SO_INVALID_INPUT, "stencil slice outside the g^3 grid");
+        check_dims(row_hi - row_lo, col_hi - col_lo);
+        return gen_stencil27_dia(g, row_lo, row_hi, col_lo, col_hi, seed, current_ctx().stream);
+    });
+}
+
 so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) {
     return guard([&] {
         cudaStream_t s = on_device(m);

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <limits>
 #include <memory>
+#include <vector>
 
 #include "hist.cuh"
 #include "matrix.cuh"
@@ -879,6 +880,74 @@ so_matrix* any_to_csr(const so_matrix& m, cudaStream_t s) {
     }
     build_row_blocks(c, n, s);
     return out.release();
+}
+
+// ------------------------------------------------------------ generators
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// values[d * nloc + il] for the 27-point stencil slice; holes where the
+// neighbour leaves the grid or the column window.
+__global__ void stencil27_fill(int64_t g, int64_t row_lo, int64_t nloc, int64_t col_lo, int64_t col_hi,
+                               uint64_t seed, double* __restrict__ vals, unsigned long long* __restrict__ stored) {
+    int64_t cnt = 0;
+    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < 27 * nloc;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int d = int(idx / nloc);
+        const int64_t il = idx - int64_t(d) * nloc;
+        const int64_t i = row_lo + il;
+        const int dz = d / 9 - 1, dy = (d / 3) % 3 - 1, dx = d % 3 - 1;
+        const int64_t z = i / (g * g), y = (i / g) % g, x = i % g;
+        const int64_t j = i + dz * g * g + dy * g + dx;
+        const bool ok = z + dz >= 0 && z + dz < g && y + dy >= 0 && y + dy < g && x + dx >= 0 && x + dx < g &&
+                        j >= col_lo && j < col_hi;
+        double v = 0.0;
+        if (ok) {
+            const uint64_t h = splitmix(seed ^ splitmix(uint64_t(i) * 27 + uint64_t(d)));
+            const double u = double(h >> 11) * 0x1.0p-53;
+            v = 0.5 + 1.5 * u;
+            if (h & 1) v = -v;
+            ++cnt;
+        }
+        vals[idx] = v;
+    }
+    cnt = warp_sum(cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(stored, (unsigned long long)cnt);
+}
+
+}  // namespace
+
+so_matrix* gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_t col_lo, int64_t col_hi,
+                             uint64_t seed, cudaStream_t s) {
+    auto* m = new so_matrix();
+    SOB_CUDA(cudaGetDevice(&m->device));
+    m->format = SO_DIA;
+    m->nrows = row_hi - row_lo;
+    m->ncols = col_hi - col_lo;
+    DiaPart& d = m->dia;
+    d.ndiags = 27;
+    std::vector<int64_t> off(27);
+    for (int k = 0; k < 27; ++k)  // ascending: dz major, then dy, then dx
+        off[size_t(k)] = (k / 9 - 1) * g * g + ((k / 3) % 3 - 1) * g + (k % 3 - 1) + (row_lo - col_lo);
+    d.offsets.alloc(27, s);
+    SOB_CUDA(cudaMemcpyAsync(d.offsets.get(), off.data(), 27 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    d.values.alloc(27 * m->nrows, s);
+    DBuf<unsigned long long> stored(1, s);
+    SOB_CUDA(cudaMemsetAsync(stored.get(), 0, sizeof(unsigned long long), s));
+    if (m->nrows > 0) {
+        stencil27_fill<<<grid_for(27 * m->nrows, 256), 256, 0, s>>>(g, row_lo, m->nrows, col_lo, col_hi, seed,
+                                                                     d.values.get(), stored.get());
+        SOB_LAUNCH("stencil27_fill");
+    }
+    d.stored_nnz = int64_t(d2h_scalar(stored.get(), s));
+    return m;
 }
 
 }  // namespace sob

@@ -98,6 +98,9 @@ bool coo_is_canonical(const so_matrix& coo, cudaStream_t s);
 
 // --- spmv (spmv.cu) ---
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s);
+void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, cudaStream_t s);
+so_matrix* gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_t col_lo, int64_t col_hi,
+                             uint64_t seed, cudaStream_t s);
 int64_t spmv_bytes(const so_matrix& m);
 
 // --- host-side cap rules (formats.cpp:348-367), shared by convert + tune ---

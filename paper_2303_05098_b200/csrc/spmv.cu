@@ -242,11 +242,11 @@ template <bool GLOBAL_OFF>
 __global__ void __launch_bounds__(256, 8)
     dia_kernel(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                const double* __restrict__ vals, const double* __restrict__ x,
-               double* __restrict__ y) {
+               double* __restrict__ y, int64_t row_lo, int64_t row_hi) {
     __shared__ int64_t soff[GLOBAL_OFF ? 1 : kDiaSmem];
     if (!GLOBAL_OFF) stage_offsets(soff, offsets, ndiags);
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= nrows) return;
+    const int64_t i = row_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= row_hi) return;
     y[i] = dia_row<GLOBAL_OFF>(i, nrows, ncols, ndiags, soff, offsets, vals, x);
 }
 
@@ -521,13 +521,17 @@ void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, doubl
     }
 }
 
-void launch_dia(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
+void launch_dia(const so_matrix& m, const double* x, double* y, cudaStream_t s, int64_t lo = 0,
+                int64_t hi = -1) {
+    if (hi < 0) hi = m.nrows;
+    if (hi <= lo) return;
+    const unsigned grid = unsigned(ceil_div(hi - lo, 256));
     if (m.dia.ndiags <= kDiaSmem)
-        dia_kernel<false><<<unsigned(ceil_div(m.nrows, 256)), 256, 0, s>>>(
-            m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(), x, y);
+        dia_kernel<false><<<grid, 256, 0, s>>>(m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                               m.dia.values.get(), x, y, lo, hi);
     else
-        dia_kernel<true><<<unsigned(ceil_div(m.nrows, 256)), 256, 0, s>>>(
-            m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(), x, y);
+        dia_kernel<true><<<grid, 256, 0, s>>>(m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                              m.dia.values.get(), x, y, lo, hi);
     SOB_LAUNCH("dia_kernel");
 }
 
@@ -539,6 +543,12 @@ void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s) 
 }
 
 }  // namespace
+
+void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, cudaStream_t s) {
+    if (m.format != SO_DIA) fail(SO_INVALID_INPUT, "row-range SpMV is implemented for DIA matrices");
+    if (lo < 0 || hi > m.nrows || lo > hi) fail(SO_INVALID_INPUT, "row range outside the matrix");
+    launch_dia(m, x, y, s, lo, hi);
+}
 
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
     if (m.nrows <= 0) return;

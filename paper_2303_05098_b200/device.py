@@ -281,6 +281,19 @@ class DeviceMatrix:
         _check(A.lib().so_spmv(self._h, C.c_void_p(x_host.ctypes.data), x_host.size,
                                C.c_void_p(y_host.ctypes.data)))
 
+    @classmethod
+    def stencil27(cls, g, row_lo=0, row_hi=None, col_lo=0, col_hi=None, seed=5):
+        """Device-generated 27-point stencil slice (DIA), see so_gen_stencil27_dia."""
+        n = g ** 3
+        out = C.c_void_p()
+        _check(A.lib().so_gen_stencil27_dia(g, row_lo, n if row_hi is None else row_hi, col_lo,
+                                            n if col_hi is None else col_hi, seed, C.byref(out)))
+        return cls(out)
+
+    def spmv_device_rows(self, x_ptr: int, y_ptr: int, row_lo: int, row_hi: int, stream: int | None = None):
+        _check(A.lib().so_spmv_device_rows(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), int(row_lo),
+                                           int(row_hi), C.c_void_p(stream or 0)))
+
     def spmv_device(self, x_ptr: int, y_ptr: int, stream: int | None = None):
         _check(A.lib().so_spmv_device(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
                                       C.c_void_p(stream or 0)))

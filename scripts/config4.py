@@ -62,6 +62,7 @@ def main():
     ap.add_argument("--out", default="profiles/config4.csv")
     ap.add_argument("--model", default=None)
     ap.add_argument("--nmax", type=int, default=5_000_000)
+    ap.add_argument("--only", default=None, help="JSON with test_ids: restrict to the held-out matrices")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -79,6 +80,10 @@ def main():
         forest = P.DeviceForest(F.load_model(a.model))
 
     specs = [synth_dev.corpus_spec(i, nmax=a.nmax) for i in range(a.start, a.start + a.count)]
+    if a.only:
+        import json
+        keep = set(json.load(open(a.only))["test_ids"])
+        specs = [s for s in specs if s["id"] in keep]
     mine = lpt_shard(specs, world, rank)
     rows = []
     t_start = time.perf_counter()
@@ -104,6 +109,7 @@ def main():
         row.update({f"t_{FMT[f]}": tot[f] / a.reps for f in range(6)})
         row["label"] = label
         if forest is not None:
+            P.tune_ml(base, forest)  # warm-up (forest already resident)
             outs = [P.tune_ml(base, forest) for _ in range(3)]
             o = outs[-1]
             row["chosen"] = int(o.chosen)
