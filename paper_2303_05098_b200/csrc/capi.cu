@@ -493,6 +493,11 @@ so_status so_convert(const so_matrix* src, int32_t target, const so_conversion_c
         if (target < 0 || target > 5)
             fail(SO_INVALID_INPUT, "format id " + std::to_string(target) + " outside 0..5");
         if (src->format == target) return clone_matrix(*src, s);
+        if (src->format == SO_CSR && csr_rows_canonical(*src, s)) {
+            so_matrix* r = csr_to_format(*src, target, cfg_or_default(cfg), s);  // no canonicalizing copy
+            SOB_CUDA(cudaStreamSynchronize(s));
+            return r;
+        }
         std::unique_ptr<so_matrix> csr(any_to_csr(*src, s));
         if (target == SO_CSR) return csr.release();
         so_matrix* r = csr_to_format(*csr, target, cfg_or_default(cfg), s);

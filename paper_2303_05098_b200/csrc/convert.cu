@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kB) csr_sweep(const int32_t* __restrict__ blk,
 
 struct OpBase {
     __device__ void begin() {}
+    __device__ void row(int, bool, int64_t) {}
     __device__ void end() {}
 };
 
@@ -89,6 +90,14 @@ void sweep(const so_matrix& csr, Op op, cudaStream_t s, int per_sm = 4) {
     csr_sweep<Op><<<grid_for(csr.csr.nblk * kB, kB, per_sm), kB, 0, s>>>(csr.csr.blk.get(), csr.csr.nblk,
                                                                          csr.csr.row_ptr.get(), op);
     SOB_LAUNCH("csr_sweep");
+}
+
+template <class Op>
+void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s) {
+    if (csr.nrows <= 0) return;
+    row_sweep<Op><<<grid_for(ceil_div(csr.nrows, 32) * 256 / 8, 256, 8), 256, 0, s>>>(csr.csr.row_ptr.get(),
+                                                                                        csr.nrows, op);
+    SOB_LAUNCH("row_sweep");
 }
 
 // ---------------------------------------------------------- row-block build
@@ -193,19 +202,13 @@ __global__ void row_len_max(const int64_t* __restrict__ rp, int64_t n, int64_t c
 // ------------------------------------------------------------------- DIA
 // formats.cpp:64-96: seen[key] -> ascending offsets -> cap -> fill.
 
-struct MarkKeys : OpBase {
-    const int32_t* col;
-    int64_t nrows;
-    const int32_t* bins;  // optional: HDC qualification (count >= thr)
-    int64_t thr;
-    int32_t* flag;
-    __device__ void operator()(int r, int64_t k, bool valid) const {
-        if (!valid) return;
-        const int64_t key = int64_t(col[k]) - r + nrows - 1;
-        if (bins && bins[key] < thr) return;
-        flag[key] = 1;
-    }
-};
+// flag[key] = a diagonal with >= max(1, thr) entries exists (thr = 0: DIA,
+// thr = ceil(ratio*min(n,m)): HDC's true diagonals)
+__global__ void bins_to_flags(const int32_t* __restrict__ bins, int64_t nkeys, int64_t thr,
+                              int32_t* __restrict__ flag) {
+    const int64_t key = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (key < nkeys) flag[key] = (bins[key] >= 1 && bins[key] >= thr) ? 1 : 0;
+}
 
 __global__ void keys_to_offsets(const int32_t* __restrict__ flag, const int64_t* __restrict__ pos,
                                 int64_t nkeys, int64_t nrows, int64_t* __restrict__ offsets) {
@@ -222,39 +225,38 @@ struct FillDia : OpBase {
     int64_t thr;
     double* values;
     unsigned long long* stored;
-    __device__ void operator()(int r, int64_t k, bool valid) const {
-        bool nz = false;
-        if (valid) {
-            const int64_t key = int64_t(col[k]) - r + nrows - 1;
-            if (!bins || bins[key] >= thr) {
-                const double v = val[k];
-                values[pos[key] * nrows + r] = v;
-                nz = v != 0.0;  // formats.cpp:93 -- stored_nnz counts nonzero cells
-            }
+    unsigned long long count = 0;  // per-thread, flushed once in end()
+    __device__ void operator()(int r, int64_t k, bool valid) {
+        if (!valid) return;
+        const int64_t key = int64_t(__ldg(col + k)) - r + nrows - 1;
+        if (!bins || __ldg(bins + key) >= thr) {
+            const double v = __ldg(val + k);
+            values[__ldg(pos + key) * nrows + r] = v;
+            count += v != 0.0;  // formats.cpp:93 -- stored_nnz counts nonzero cells
         }
-        const unsigned b = __ballot_sync(0xffffffffu, nz);
-        if ((threadIdx.x & 31) == 0 && b) atomicAdd(stored, (unsigned long long)__popc(b));
+    }
+    __device__ void end() {
+        const unsigned long long c = warp_sum(count);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(stored, c);
     }
 };
 
 // -------------------------------------------------------------- ELL / HYB
 
-// Slot-major fill: thread per (slot, row); writes every padded slot exactly
-// once (column-major, coalesced), real entries first, then sentinel -1 / 0.0.
+// Row-major traversal, column-major writes: thread per row walks its slots;
+// consecutive threads write consecutive cells of each slot (coalesced) and
+// read their own contiguous row (L1-resident for a warp).  Every padded slot
+// is written exactly once: real entries first, then sentinel -1 / 0.0.
 __global__ void ell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                          const double* __restrict__ val, int64_t nrows, int64_t width,
                          int32_t* __restrict__ ecol, double* __restrict__ eval) {
-    const int64_t total = nrows * width;
-    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-         idx += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t j = idx / nrows, r = idx - j * nrows;
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows;
+         r += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = rp[r], len = rp[r + 1] - a;
-        if (j < len) {
-            ecol[idx] = col[a + j];
-            eval[idx] = val[a + j];
-        } else {
-            ecol[idx] = -1;
-            eval[idx] = 0.0;
+        for (int64_t j = 0; j < width; ++j) {
+            const bool real = j < len;
+            ecol[j * nrows + r] = real ? col[a + j] : -1;
+            eval[j * nrows + r] = real ? val[a + j] : 0.0;
         }
     }
 }
@@ -507,19 +509,33 @@ int64_t compact_keys(const DBuf<int32_t>& flag, int64_t nkeys, int64_t nrows, DB
     return nd;
 }
 
-void build_dia_part(const so_matrix& csr, const int32_t* bins, int64_t thr, DiaPart& dia, int64_t cap,
+// Diagonal histogram of a CSR into dense bins (shared-memory hash,
+// row-lockstep sweep: banded rows aggregate to one update per warp).
+void diag_histogram(const so_matrix& csr, int32_t* bins, cudaStream_t s) {
+    DiagHist dh;
+    dh.col = csr.csr.col.get();
+    dh.nrows = csr.nrows;
+    dh.bins = bins;
+    row_sweep_launch(csr, dh, s);
+}
+
+void build_dia_part(const so_matrix& csr, const int32_t* bins_in, int64_t thr, DiaPart& dia, int64_t cap,
                     cudaStream_t s) {
     const int64_t n = csr.nrows;
     const int64_t nkeys = (n > 0 && csr.ncols > 0) ? n + csr.ncols - 1 : 0;
+    DBuf<int32_t> own_bins;
+    const int32_t* bins = bins_in;
+    if (!bins && nkeys) {
+        own_bins.alloc(n + csr.ncols, s);
+        SOB_CUDA(cudaMemsetAsync(own_bins.get(), 0, own_bins.bytes(), s));
+        diag_histogram(csr, own_bins.get(), s);
+        bins = own_bins.get();
+    }
     DBuf<int32_t> flag(nkeys, s);
-    if (nkeys) SOB_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t) * size_t(nkeys), s));
-    MarkKeys mk;
-    mk.col = csr.csr.col.get();
-    mk.nrows = n;
-    mk.bins = bins;
-    mk.thr = thr;
-    mk.flag = flag.get();
-    sweep(csr, mk, s);
+    if (nkeys) {
+        bins_to_flags<<<unsigned(ceil_div(nkeys, 256)), 256, 0, s>>>(bins, nkeys, thr, flag.get());
+        SOB_LAUNCH("bins_to_flags");
+    }
     DBuf<int64_t> pos;
     dia.ndiags = compact_keys(flag, nkeys, n, pos, dia.offsets, cap, s);
     dia.values.alloc(dia.ndiags * n, s);
@@ -531,11 +547,11 @@ void build_dia_part(const so_matrix& csr, const int32_t* bins, int64_t thr, DiaP
     fd.val = csr.csr.val.get();
     fd.nrows = n;
     fd.pos = pos.get();
-    fd.bins = bins;
+    fd.bins = bins_in;  // HDC: only entries on true diagonals go to the DIA part
     fd.thr = thr;
     fd.values = dia.values.get();
     fd.stored = stored.get();
-    if (dia.ndiags > 0) sweep(csr, fd, s);
+    if (dia.ndiags > 0) row_sweep_launch(csr, fd, s);
     dia.stored_nnz = int64_t(d2h_scalar(stored.get(), s));
 }
 
@@ -545,7 +561,7 @@ void fill_ell_part(const so_matrix& csr, int64_t width, EllPart& ell, cudaStream
     ell.col.alloc(width * n, s);
     ell.val.alloc(width * n, s);
     if (width * n > 0) {
-        ell_fill<<<grid_for(width * n, 256), 256, 0, s>>>(csr.csr.row_ptr.get(), csr.csr.col.get(),
+        ell_fill<<<grid_for(n, 256), 256, 0, s>>>(csr.csr.row_ptr.get(), csr.csr.col.get(),
                                                           csr.csr.val.get(), n, width, ell.col.get(),
                                                           ell.val.get());
         SOB_LAUNCH("ell_fill");
@@ -638,6 +654,7 @@ so_matrix* coo_to_csr_device(const so_matrix& coo, cudaStream_t s) {  // formats
     }
     coo_row_ptr<<<unsigned(ceil_div(z + 1, 256)), 256, 0, s>>>(coo.coo.row.get(), z, n, c.row_ptr.get());
     SOB_LAUNCH("coo_row_ptr");
+    c.canonical = 1;  // from canonical COO
     build_row_blocks(c, n, s);
     return m;
 }
@@ -677,6 +694,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.val, src.csr.val);
     cp(m->csr.blk, src.csr.blk);
     cp(m->csr.blk_k, src.csr.blk_k);
+    m->csr.canonical = src.csr.canonical;
     m->csr.ngrp = src.csr.ngrp;
     m->csr.grp_window = src.csr.grp_window;
     cp(m->csr.grp, src.csr.grp);
@@ -761,11 +779,7 @@ so_matrix* csr_to_format(const so_matrix& csr, int32_t target, const so_conversi
             const int64_t nbins = n + csr.ncols;
             DBuf<int32_t> bins(nbins, s);
             if (nbins) SOB_CUDA(cudaMemsetAsync(bins.get(), 0, bins.bytes(), s));
-            DiagHist dh;
-            dh.col = csr.csr.col.get();
-            dh.nrows = n;
-            dh.bins = bins.get();
-            sweep(csr, dh, s, 2);
+            diag_histogram(csr, bins.get(), s);
             // entries on diagonals with count >= thr go to the DIA part
             build_dia_part(csr, bins.get(), thr, m->dia, cap, s);
             CsrPart& c = m->csr;
@@ -880,6 +894,36 @@ so_matrix* any_to_csr(const so_matrix& m, cudaStream_t s) {
     }
     build_row_blocks(c, n, s);
     return out.release();
+}
+
+// ------------------------------------------------------------ CSR checks
+
+namespace {
+}  // namespace
+
+struct UnsortedOp : OpBase {
+    const int64_t* rp;
+    const int32_t* col;
+    int* bad;
+    __device__ void operator()(int r, int64_t k, bool valid) const {
+        if (valid && k > __ldg(rp + r) && __ldg(col + k - 1) >= __ldg(col + k)) *bad = 1;
+    }
+};
+
+// strictly increasing columns in every row: the CSR already is to_coo's
+// canonical order and can feed conversions without a copy (cached per matrix)
+bool csr_rows_canonical(const so_matrix& m, cudaStream_t s) {
+    if (m.csr.nnz <= 1) return true;
+    if (m.csr.canonical >= 0) return m.csr.canonical == 1;
+    DBuf<int> bad(1, s);
+    SOB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    UnsortedOp op;
+    op.rp = m.csr.row_ptr.get();
+    op.col = m.csr.col.get();
+    op.bad = bad.get();
+    row_sweep_launch(m, op, s);
+    m.csr.canonical = d2h_scalar(bad.get(), s) == 0 ? 1 : 0;
+    return m.csr.canonical == 1;
 }
 
 // ------------------------------------------------------------ generators

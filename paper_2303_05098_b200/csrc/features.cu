@@ -27,45 +27,45 @@ namespace sob {
 namespace {
 
 constexpr int kB = 256;
-constexpr int kSpreadChunk = 2048;  // rows per spread chunk (8 per thread)
-constexpr int kMaxSmemDiag = 4096;
+constexpr int kSpreadChunk = 8192;  // rows per spread chunk (32 per thread)
+constexpr int kMaxSmemDiag = 1024;
 
 // ------------------------------------------------------------ pass 1: scans
 
+// CSR part: row counts from row_ptr, diagonal keys through the shared-memory
+// hash with the row-lockstep sweep (hist.cuh): for banded rows every lane of a
+// warp holds the same key at each step, so 32 updates merge into one.
 template <bool ACCUM_RC>
-__global__ void __launch_bounds__(kB)
-    feat_csr(const int32_t* __restrict__ blk, int64_t nblk, const int64_t* __restrict__ rp,
-             const int32_t* __restrict__ col, int64_t nrows, int32_t* __restrict__ rc,
-             int32_t* __restrict__ bins, FeatState* __restrict__ st) {
-    __shared__ int64_t srp[kRowsPerBlock + 1];
-    __shared__ SmemHash h;
-    hash_init(h);
-    unsigned long long visits = 0;
-    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
-        const int r0 = blk[b], nr = blk[b + 1] - r0;
+struct FeatCsrOp {
+    const int32_t* col;
+    int64_t nrows;
+    int32_t* rc;
+    int32_t* bins;
+    FeatState* st;
+    SmemHash* h;
+    unsigned long long visits;
+    __device__ void begin() {
+        __shared__ SmemHash sh;
+        h = &sh;
+        hash_init(sh);
+        visits = 0;
         __syncthreads();
-        for (int j = threadIdx.x; j <= nr; j += kB) srp[j] = rp[r0 + j];
-        __syncthreads();
-        for (int j = threadIdx.x; j < nr; j += kB) {
-            const int len = int(srp[j + 1] - srp[j]);
-            rc[r0 + j] = ACCUM_RC ? rc[r0 + j] + len : len;
-        }
-        const int64_t k0 = srp[0], k1 = srp[nr];
-        visits += k1 - k0;
-        for (int64_t base = k0; base < k1; base += kB) {
-            const int64_t k = base + threadIdx.x;
-            int32_t key = -1;
-            if (k < k1) {
-                const int r = r0 + row_in_block(srp, nr, k);
-                key = int32_t(int64_t(col[k]) - r + nrows - 1);
-            }
-            hash_add(h, bins, key);
-        }
     }
-    __syncthreads();
-    hash_flush(h, bins);
-    if (threadIdx.x == 0 && visits) atomicAdd(&st->visits, visits);
-}
+    __device__ void row(int r, bool valid, int64_t len) {
+        if (!valid) return;
+        rc[r] = ACCUM_RC ? rc[r] + int(len) : int(len);
+        visits += len;
+    }
+    __device__ void operator()(int r, int64_t k, bool valid) {
+        hash_add(*h, bins, valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1);
+    }
+    __device__ void end() {
+        const unsigned long long v = warp_sum(visits);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&st->visits, v);
+        __syncthreads();
+        hash_flush(*h, bins);
+    }
+};
 
 __global__ void __launch_bounds__(kB)
     feat_coo(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
@@ -127,33 +127,52 @@ __global__ void __launch_bounds__(kB)
     hash_flush(h, bins);
 }
 
-// DIA: one thread per row, diagonals ascending; per-diagonal entry counts are
-// reduced warp -> shared -> one global atomic per diagonal per CTA.
+// DIA: one thread per row, diagonals ascending; eight diagonals' cells are
+// loaded before any is classified (in-bounds for every valid row, so the
+// loads are unpredicated and issue back to back); per-diagonal entry counts
+// are reduced warp (ballot) -> shared -> one global atomic per diagonal per CTA.
 __global__ void __launch_bounds__(kB)
     feat_dia(int64_t nrows, int64_t ncols, int nd, const int64_t* __restrict__ off,
              const double* __restrict__ vals, int32_t* __restrict__ rc,
              unsigned long long* __restrict__ dcount, FeatState* __restrict__ st) {
     __shared__ unsigned long long sdc[kMaxSmemDiag];
+    __shared__ int64_t soff[kMaxSmemDiag];
     const int nsm = nd < kMaxSmemDiag ? nd : kMaxSmemDiag;
-    for (int d = threadIdx.x; d < nsm; d += kB) sdc[d] = 0;
+    for (int d = threadIdx.x; d < nsm; d += kB) {
+        sdc[d] = 0;
+        soff[d] = off[d];
+    }
     __syncthreads();
     unsigned long long visits = 0, structure = 0;
+    constexpr int U = 8;
     for (int64_t base = int64_t(blockIdx.x) * kB; base < nrows; base += int64_t(gridDim.x) * kB) {
         const int64_t i = base + threadIdx.x;
         const bool valid = i < nrows;
+        const int64_t iv = valid ? i : nrows - 1;
         int cnt = 0;
-        for (int d = 0; d < nd; ++d) {
-            const int64_t j = i + off[d];
-            const bool inr = valid && j >= 0 && j < ncols;
-            const bool nz = inr && vals[int64_t(d) * nrows + i] != 0.0;  // features.cpp:57
-            cnt += nz;
-            structure += inr && !nz;
-            const unsigned b = __ballot_sync(0xffffffffu, nz);
-            if ((threadIdx.x & 31) == 0 && b) {
-                if (d < kMaxSmemDiag)
-                    atomicAdd(&sdc[d], (unsigned long long)__popc(b));
-                else
-                    atomicAdd(&dcount[d], (unsigned long long)__popc(b));
+        for (int d0 = 0; d0 < nd; d0 += U) {
+            double v[U];
+            bool inr[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int d = d0 + u < nd ? d0 + u : nd - 1;
+                const int64_t j = iv + (d < kMaxSmemDiag ? soff[d] : off[d]);
+                inr[u] = valid && d0 + u < nd && j >= 0 && j < ncols;
+                v[u] = vals[int64_t(d) * nrows + iv];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool nz = inr[u] && v[u] != 0.0;  // features.cpp:57
+                cnt += nz;
+                structure += inr[u] && !nz;
+                const unsigned b = __ballot_sync(0xffffffffu, nz);
+                if ((threadIdx.x & 31) == 0 && b) {
+                    const int d = d0 + u;
+                    if (d < kMaxSmemDiag)
+                        atomicAdd(&sdc[d], (unsigned long long)__popc(b));
+                    else
+                        atomicAdd(&dcount[d], (unsigned long long)__popc(b));
+                }
             }
         }
         if (valid) rc[i] = cnt;
@@ -396,13 +415,21 @@ __global__ void __launch_bounds__(kB)
     Mono m = mono_id();
     bool ok = true;
     const int64_t base = c * kSpreadChunk + int64_t(threadIdx.x) * (kSpreadChunk / kB);
+    constexpr int kBatch = 8;
+    for (int j0 = 0; j0 < kSpreadChunk / kB; j0 += kBatch) {
+        int32_t cv[kBatch];
 #pragma unroll
-    for (int j = 0; j < kSpreadChunk / kB; ++j) {
-        const int64_t i = base + j;
-        if (i < nrows) {
-            Mono el;
-            ok = ok && mono_elem(sq_dev(rc[i], avg), e, el);
-            if (ok) m = mono_cat(m, el);
+        for (int u = 0; u < kBatch; ++u) {
+            const int64_t i = base + j0 + u;
+            cv[u] = i < nrows ? rc[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            if (base + j0 + u < nrows) {
+                Mono el;
+                ok = ok && mono_elem(sq_dev(cv[u], avg), e, el);
+                if (ok) m = mono_cat(m, el);
+            }
         }
     }
     m = warp_reduce_mono(m, ok);
@@ -424,7 +451,23 @@ __global__ void __launch_bounds__(kB)
 
 // Exact sequential semantics over rows [lo, hi), warp-cooperative (all 32
 // lanes call with the same arguments; returns the same S in every lane).
+__device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg);
+
+// Binade changes cluster where S is still small (the first rows of a chunk),
+// and every change costs one pass over the rest of the current range, so the
+// range is consumed in windows that start small and double after each pass.
 __device__ double advance_exact(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
+    int64_t w = 256;
+    while (lo < hi) {
+        const int64_t whi = lo + w < hi ? lo + w : hi;
+        S = advance_range(S, lo, whi, rc, avg);
+        lo = whi;
+        w *= 2;
+    }
+    return S;
+}
+
+__device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
     const unsigned lane = threadIdx.x & 31u;
     int64_t stack[12];
     int sp = 0;
@@ -460,10 +503,18 @@ __device__ double advance_exact(double S, int64_t lo, int64_t hi, const int32_t*
         const int64_t b = a + piece < cur_hi ? a + piece : cur_hi;
         Mono mm = mono_id();
         bool ok = true;
-        for (int64_t i = a; i < b && ok; ++i) {
-            Mono el;
-            ok = mono_elem(sq_dev(rc[i], avg), e, el);
-            if (ok) mm = mono_cat(mm, el);
+        for (int64_t i0 = a; i0 < b; i0 += 8) {
+            int32_t cv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cv[u] = i0 + u < b ? rc[i0 + u] : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (i0 + u < b && ok) {
+                    Mono el;
+                    ok = mono_elem(sq_dev(cv[u], avg), e, el);
+                    if (ok) mm = mono_cat(mm, el);
+                }
+            }
         }
         Mono pre = warp_scan_mono(mm, ok);
         const long long mi = m + ((m & 1) ? pre.a1 : pre.a0);
@@ -500,9 +551,14 @@ __global__ void __launch_bounds__(32)
     const double avg = double(st->visits) / double(nrows);
     double S = 0.0;
     int64_t c = 0;
+    int64_t pre_c = 0;  // group whose records sit in `nxt`
+    MonoRec nxt = lane < nch ? rec[lane] : MonoRec{0, 0, 2, 0, kMonoIdent, 0};
     while (c < nch) {
         const int64_t ci = c + lane;
-        MonoRec r = ci < nch ? rec[ci] : MonoRec{0, 0, 2, 0, kMonoIdent, 0};
+        MonoRec r = (pre_c == c) ? nxt : (ci < nch ? rec[ci] : MonoRec{0, 0, 2, 0, kMonoIdent, 0});
+        // prefetch the most likely next group (all 32 consumed) while this one is applied
+        pre_c = c + 32;
+        nxt = pre_c + lane < nch ? rec[pre_c + lane] : MonoRec{0, 0, 2, 0, kMonoIdent, 0};
         const int eS = S > 0.0 ? ilogb(S) : INT32_MIN;
         const bool usable = ci < nch && ((r.flags & kMonoIdent) || ((r.flags & kMonoSafe) && r.e == eS));
         const unsigned badm = __ballot_sync(0xffffffffu, !usable);
@@ -584,14 +640,15 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     const int grid_rows = grid_for(n, kB, 4);
 
     auto scan_csr = [&](bool accum) {
-        if (m.csr.nblk == 0) return;
-        const int g = grid_for(m.csr.nblk * kB, kB, 4);
-        if (accum)
-            feat_csr<true><<<g, kB, 0, s>>>(m.csr.blk.get(), m.csr.nblk, m.csr.row_ptr.get(), m.csr.col.get(), n,
-                                            rc.get(), bins.get(), st);
-        else
-            feat_csr<false><<<g, kB, 0, s>>>(m.csr.blk.get(), m.csr.nblk, m.csr.row_ptr.get(), m.csr.col.get(), n,
-                                             rc.get(), bins.get(), st);
+        if (n == 0) return;
+        const int g = grid_for(ceil_div(n, 32) * 256 / 8, 256, 8);
+        if (accum) {
+            FeatCsrOp<true> op{m.csr.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            row_sweep<FeatCsrOp<true>><<<g, 256, 0, s>>>(m.csr.row_ptr.get(), n, op);
+        } else {
+            FeatCsrOp<false> op{m.csr.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            row_sweep<FeatCsrOp<false>><<<g, 256, 0, s>>>(m.csr.row_ptr.get(), n, op);
+        }
         SOB_LAUNCH("feat_csr");
     };
     auto scan_dia = [&]() {

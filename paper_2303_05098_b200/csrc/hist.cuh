@@ -76,4 +76,42 @@ __device__ __forceinline__ int row_in_block(const int64_t* srp, int nr, int64_t 
     return lo;
 }
 
+// ------------------------------------------------------------ row sweep
+// Row-lockstep traversal of a CSR: lane = row, slot j in lockstep across the
+// warp, so banded / stencil rows present the SAME diagonal key in every lane
+// at every step and warp aggregation (hash_add's __match_any_sync) collapses
+// 32 updates into one.  Rows longer than kLockstepMax finish cooperatively:
+// the whole warp strides over the rest of the row.  Every op call is made by
+// all 32 lanes (valid=false for idle lanes), so ops may be warp-synchronous.
+// Op interface: begin(), row(r, valid, len) once per row, (r, k, valid) per
+// entry slot, end().
+constexpr int kLockstepMax = 64;
+
+template <class Op>
+__global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp, int64_t nrows, Op op) {
+    op.begin();
+    const int lane = int(threadIdx.x & 31u);
+    const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / 32);
+    for (int64_t wb = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; wb < nrows;
+         wb += nwarps * 32) {
+        const int64_t r = wb + lane;
+        const bool has = r < nrows;
+        const int64_t a = has ? rp[r] : 0;
+        const int64_t len = has ? rp[r + 1] - a : 0;
+        op.row(int(r), has, len);
+        const int64_t maxlen = warp_max(len < kLockstepMax ? len : int64_t(kLockstepMax));
+        for (int64_t j = 0; j < maxlen; ++j) op(int(r), a + j, has && j < len);
+        unsigned longm = __ballot_sync(0xffffffffu, len > kLockstepMax);
+        while (longm) {
+            const int src = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t la = __shfl_sync(0xffffffffu, a, src);
+            const int64_t ll = __shfl_sync(0xffffffffu, len, src);
+            const int lr = __shfl_sync(0xffffffffu, int(r), src);
+            for (int64_t j0 = kLockstepMax; j0 < ll; j0 += 32) op(lr, la + j0 + lane, j0 + lane < ll);
+        }
+    }
+    op.end();
+}
+
 }  // namespace sob

@@ -34,6 +34,7 @@ struct CsrPart {
     DBuf<int32_t> blk;    // row-block partition, nblk+1 entries
     DBuf<int64_t> blk_k;  // first entry of each row block (= row_ptr[blk[b]])
     int64_t nblk = 0;
+    mutable int canonical = -1;  // rows strictly increasing: -1 unknown, 0 no, 1 yes
     // SpMV warp-group partition
     int64_t ngrp = 0;
     int grp_window = kGroupWindowLong;
@@ -95,6 +96,7 @@ so_matrix* any_to_csr(const so_matrix& m, cudaStream_t s);  // to_coo semantics,
 so_matrix* csr_to_coo(const so_matrix& csr, cudaStream_t s);
 so_matrix* clone_matrix(const so_matrix& m, cudaStream_t s);
 bool coo_is_canonical(const so_matrix& coo, cudaStream_t s);
+bool csr_rows_canonical(const so_matrix& csr, cudaStream_t s);
 
 // --- spmv (spmv.cu) ---
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s);

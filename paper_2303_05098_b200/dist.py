@@ -57,6 +57,8 @@ class Slice:
 def partition(n: int, h: int, rank: int, world: int) -> Slice:
     r0 = n * rank // world
     r1 = n * (rank + 1) // world
+    if world > 1 and h > n // world:
+        raise ValueError("halo wider than a rank's row slice: use fewer ranks")
     return Slice(n, h, rank, world, r0, r1, max(0, r0 - h), min(n, r1 + h))
 
 

@@ -1,0 +1,126 @@
+"""CPU (gloo, world_size 2 and 3): the row-partition / halo-exchange host
+logic of the config-5 iteration (paper_2303_05098_b200/dist.py) reproduces
+the single-rank iterate BIT-FOR-BIT.  The multiply here is a numpy restatement
+of the per-row DIA order; on the GPU path the same `iterate` drives the
+sm_100a row-range DIA kernel and NCCL point-to-point (scripts/config5.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2303_05098_b200 import dist as D
+
+G = 6
+N = G ** 3
+H = G * G + G + 1
+OFFS = [(k // 9 - 1) * G * G + ((k // 3) % 3 - 1) * G + (k % 3 - 1) for k in range(27)]
+
+
+def value(i, d):
+    z, y, x = i // (G * G), (i // G) % G, i % G
+    dz, dy, dx = d // 9 - 1, (d // 3) % 3 - 1, d % 3 - 1
+    if not (0 <= z + dz < G and 0 <= y + dy < G and 0 <= x + dx < G):
+        return 0.0
+    return 0.5 + ((i * 27 + d) * 2654435761 % 1000) / 1000.0 * (1 if (i + d) % 2 else -1)
+
+
+def make_local(s):
+    vals = np.array([[value(s.r0 + il, d) for il in range(s.nloc)] for d in range(27)])
+    return vals, D.local_offsets(OFFS, s)
+
+
+def spmv_rows_factory(s, vals, offs):
+    def spmv_rows(xw, yw, lo, hi):
+        for il in range(lo, hi):
+            acc = 0.0
+            for d in range(27):  # diagonals ascending, in-range only (spmv.cpp:45-56)
+                c = il + offs[d]
+                if 0 <= c < s.nwin:
+                    acc = acc + vals[d, il] * xw[c]
+            yw[s.own_lo + il] = acc
+    return spmv_rows
+
+
+def x0(i):
+    return 1.0 + (i % 7) / 8.0
+
+
+def run_single(iters):
+    s = D.partition(N, H, 0, 1)
+    vals, offs = make_local(s)
+    xa = np.array([x0(s.w0 + k) for k in range(s.nwin)])
+    xb = np.zeros_like(xa)
+    return D.iterate(s, xa, xb, iters, spmv_rows_factory(s, vals, offs), lambda buf, plan: None)
+
+
+def worker(rank, world, port, iters, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    s = D.partition(N, H, rank, world)
+    vals, offs = make_local(s)
+    xa = np.array([x0(s.w0 + k) for k in range(s.nwin)])
+    xb = np.zeros_like(xa)
+
+    def exchange(buf, plan):
+        reqs, recvs = [], []
+        for peer, (sa, sb), (ra, rb) in plan:
+            reqs.append(dist.isend(torch.from_numpy(buf[sa:sb].copy()), peer))
+            t = torch.empty(rb - ra, dtype=torch.float64)
+            reqs.append(dist.irecv(t, peer))
+            recvs.append((t, ra, rb))
+
+        def wait():
+            for r in reqs:
+                r.wait()
+            for t, ra, rb in recvs:
+                buf[ra:rb] = t.numpy()
+        return wait
+
+    out = D.iterate(s, xa, xb, iters, spmv_rows_factory(s, vals, offs), exchange)
+    q.put((rank, s.r0, out[s.own_lo:s.own_hi].copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def free_port():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_iteration_is_bitwise_equal(world):
+    iters = 4
+    want = run_single(iters)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, iters, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = np.concatenate([p[2] for p in sorted(parts)])
+    assert got.shape == want.shape
+    assert np.array_equal(got, want)
+
+
+def test_partition_geometry():
+    n, h = 1000, 37
+    slices = [D.partition(n, h, r, 4) for r in range(4)]
+    assert slices[0].r0 == 0 and slices[-1].r1 == n
+    assert all(a.r1 == b.r0 for a, b in zip(slices, slices[1:]))
+    for s in slices:
+        lo, hi = s.interior()
+        # interior rows never read the halo
+        assert all(0 <= r + s.own_lo - h and r + s.own_lo + h < s.nwin or s.world == 1
+                   for r in range(lo, hi) if s.rank not in (0, s.world - 1))
+        for peer, (sa, sb), (ra, rb) in D.halo_plan(s):
+            assert sb - sa == min(h, s.nloc)
+            assert s.own_lo <= sa and sb <= s.own_hi
+            assert (ra, rb) in [(0, s.own_lo), (s.own_hi, s.nwin)]

@@ -386,3 +386,46 @@ def test_hdc_with_long_rows(so, O):
         m = d.from_coo(f)
         cmp_host(m.download(), want, f"fmt {f}")
         assert max_rel(m.spmv(x), O.oc_spmv(want, x)) <= SPMV_TOL, f
+
+
+def test_stencil27_generator_and_row_slices(so, O):
+    """Device 27-pt stencil (config 5 shape): the full DIA matrix matches the
+    oracle's SpMV bit-for-bit, and 3 row slices with x windows (the
+    row-partitioned iteration of paper_2303_05098_b200/dist.py, exchange done
+    by device copies on one GPU) reproduce the full iterate bit-for-bit."""
+    import torch
+    from paper_2303_05098_b200 import dist as D
+
+    g = 14
+    n = g ** 3
+    h = g * g + g + 1
+    full = so.DeviceMatrix.stencil27(g, seed=7)
+    host = full.download()
+    x = np.random.default_rng(3).uniform(-1, 1, n)
+    assert np.array_equal(full.spmv(x), O.oc_spmv(host, x))
+    assert host["values"].shape[0] == 27 * n and full.nnz() == (3 * g - 2) ** 3
+
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    def run(world, iters=3):
+        sl = [D.partition(n, h, r, world) for r in range(world)]
+        mats = [so.DeviceMatrix.stencil27(g, s.r0, s.r1, s.w0, s.w1, seed=7) for s in sl]
+        xs = [[torch.tensor(1.0 + (np.arange(s.w0, s.w1) % 7) / 8.0, device="cuda"),
+               torch.zeros(s.nwin, dtype=torch.float64, device="cuda")] for s in sl]
+        for _ in range(iters):
+            for s, m, (xc, xn) in zip(sl, mats, xs):
+                m.spmv_device_rows(xc.data_ptr(), xn.data_ptr() + 8 * s.own_lo, 0, s.nloc, stream.cuda_stream)
+            for r, s in enumerate(sl):  # halo exchange by device copies
+                for peer, (sa, sb), (ra, rb) in D.halo_plan(s):
+                    ps = sl[peer]
+                    # what `peer` sends to r lands in r's (ra, rb)
+                    src = [p for p in D.halo_plan(ps) if p[0] == r][0][1]
+                    xs[r][1][ra:rb] = xs[peer][1][src[0]:src[1]]
+            xs = [[xn, xc] for xc, xn in xs]
+        torch.cuda.synchronize()
+        return np.concatenate([xs[r][0][s.own_lo:s.own_hi].cpu().numpy() for r, s in enumerate(sl)])
+
+    one = run(1)
+    assert np.array_equal(run(3), one)
+    assert np.array_equal(run(4), one)
