@@ -22,6 +22,32 @@ void predict_rows(const so_forest& f, const double* rows_dev, int64_t n, int32_t
 void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,
                           so_tune_outcome* out_dev, cudaStream_t s);
 
+struct TunePlan {
+    uint64_t forest_uid = 0;
+    so_conversion_config cfg{};
+    FeatState* st = nullptr;
+    so_tune_outcome* out = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::unique_ptr<FeatWorkspace> ws;
+    bool matches(uint64_t uid, const so_conversion_config& c) const {
+        return uid == forest_uid && c.kh_override == cfg.kh_override && c.true_diag_ratio == cfg.true_diag_ratio &&
+               c.max_padding_factor == cfg.max_padding_factor && c.max_padded_entries == cfg.max_padded_entries;
+    }
+};
+
+void destroy_tune_plan(TunePlan* p) {
+    if (!p) return;
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->st) cudaFree(p->st);
+    if (p->out) cudaFree(p->out);
+    if (p->e0) cudaEventDestroy(p->e0);
+    if (p->e1) cudaEventDestroy(p->e1);
+    if (p->e2) cudaEventDestroy(p->e2);
+    p->ws.reset();
+    delete p;
+}
+
 namespace {
 thread_local std::string g_err;
 std::mutex g_mu;
@@ -703,6 +729,11 @@ so_status so_predict(const so_forest* f, const so_feature_vector* x, int32_t* ou
     return so_predict_rows(f, 1, row, out);
 }
 
+// tune_ml with the feature pipeline (about ten kernels + stream-ordered
+// scratch allocations) captured once per (matrix, forest, ratio, caps) as a
+// CUDA graph and replayed with a single launch, so small matrices pay one
+// launch instead of ten; the predict/feasibility kernel follows on the same
+// stream.  The outcome lands in a persistent device buffer (one small D2H).
 so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const so_conversion_config* cfgp,
                      so_tune_outcome* out) {
     return guard([&] {
@@ -712,26 +743,46 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
         check_ratio(*m, ratio);
         so_conversion_config cfg = cfg_or_default(cfgp);
         cfg.true_diag_ratio = ratio;  // TunerConfig::effective_conversion (tuners.hpp:21-25)
-        DBuf<FeatState> st(1, s);
-        DBuf<so_tune_outcome> dout(1, s);
-        cudaEvent_t e0, e1, e2;
-        SOB_CUDA(cudaEventCreate(&e0));
-        SOB_CUDA(cudaEventCreate(&e1));
-        SOB_CUDA(cudaEventCreate(&e2));
-        SOB_CUDA(cudaEventRecord(e0, s));
-        enqueue_features(*m, ratio, st.get(), s);
-        SOB_CUDA(cudaEventRecord(e1, s));
-        enqueue_tune_predict(*f, st.get(), cfg, m->format, dout.get(), s);
-        SOB_CUDA(cudaEventRecord(e2, s));
+        TunePlan* plan = m->tune_plan.get();
+        if (!plan || !plan->matches(f->uid, cfg)) {
+            m->tune_plan.reset();
+            std::unique_ptr<TunePlan, TunePlanDeleter> np(new TunePlan());
+            np->forest_uid = f->uid;
+            np->cfg = cfg;
+            SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np->st), sizeof(FeatState), s));
+            SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np->out), sizeof(so_tune_outcome), s));
+            SOB_CUDA(cudaEventCreate(&np->e0));
+            SOB_CUDA(cudaEventCreate(&np->e1));
+            SOB_CUDA(cudaEventCreate(&np->e2));
+            np->ws.reset(new FeatWorkspace(*m, s));
+            SOB_CUDA(cudaStreamSynchronize(s));
+            cudaGraph_t g = nullptr;
+            SOB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_features(*m, ratio, np->st, s, np->ws.get());
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            SOB_CUDA(cudaStreamEndCapture(s, &g));
+            SOB_CUDA(cudaGraphInstantiate(&np->exec, g, 0));
+            cudaGraphDestroy(g);
+            plan = np.get();
+            m->tune_plan = std::move(np);
+        }
+        // events bracket the graph (T_FE) and the predict kernel (T_PRED)
+        SOB_CUDA(cudaEventRecord(plan->e0, s));
+        SOB_CUDA(cudaGraphLaunch(plan->exec, s));
+        SOB_CUDA(cudaEventRecord(plan->e1, s));
+        enqueue_tune_predict(*f, plan->st, cfg, m->format, plan->out, s);
+        SOB_CUDA(cudaEventRecord(plan->e2, s));
         so_tune_outcome h;
-        SOB_CUDA(cudaMemcpyAsync(&h, dout.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        SOB_CUDA(cudaMemcpyAsync(&h, plan->out, sizeof(h), cudaMemcpyDeviceToHost, s));
         SOB_CUDA(cudaStreamSynchronize(s));
         float fe = 0.f, pr = 0.f;
-        SOB_CUDA(cudaEventElapsedTime(&fe, e0, e1));
-        SOB_CUDA(cudaEventElapsedTime(&pr, e1, e2));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaEventDestroy(e2);
+        SOB_CUDA(cudaEventElapsedTime(&fe, plan->e0, plan->e1));
+        SOB_CUDA(cudaEventElapsedTime(&pr, plan->e1, plan->e2));
         h.feature_time_seconds = double(fe) * 1e-3;
         h.predict_time_seconds = double(pr) * 1e-3;
         *out = h;

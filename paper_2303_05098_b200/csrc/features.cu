@@ -18,6 +18,7 @@
 // and recursing (32-way) into any chunk where S changes binade.  The result
 // is the reference's double, not an approximation of it.
 #include <cfloat>
+#include <memory>
 
 #include "features.cuh"
 #include "hist.cuh"
@@ -27,7 +28,14 @@ namespace sob {
 namespace {
 
 constexpr int kB = 256;
-constexpr int kSpreadChunk = 8192;  // rows per spread chunk (32 per thread)
+// rows per spread chunk: a power of two in [1024, 8192] giving ~512 chunks,
+// so big matrices keep the chunk walk short and small ones keep the exact
+// slow path over their first chunk cheap
+inline int64_t spread_chunk(int64_t n) {
+    int64_t c = 1024;
+    while (c < 8192 && c * 512 < n) c *= 2;
+    return c;
+}
 constexpr int kMaxSmemDiag = 1024;
 
 // ------------------------------------------------------------ pass 1: scans
@@ -204,14 +212,14 @@ __device__ __forceinline__ double sq_dev(int32_t c, double avg) {
 }
 
 __global__ void __launch_bounds__(kB)
-    feat_rows(const int32_t* __restrict__ rc, int64_t nrows, FeatState* __restrict__ st,
+    feat_rows(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, FeatState* __restrict__ st,
               double* __restrict__ csum) {
     const double avg = double(st->visits) / double(nrows);
-    const int64_t base = int64_t(blockIdx.x) * kSpreadChunk;
+    const int64_t base = int64_t(blockIdx.x) * chunk;
     int mx = 0, mn = INT32_MAX;
     double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < kSpreadChunk / kB; ++j) {
+#pragma unroll 4
+    for (int j = 0; j < chunk / kB; ++j) {
         const int64_t i = base + j * kB + threadIdx.x;
         if (i < nrows) {
             const int32_t c = rc[i];
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(512) spread_prefix(const double* __restrict__ 
 
 // Chunk summaries at the binade the approximate prefix puts the chunk in.
 __global__ void __launch_bounds__(kB)
-    spread_mono(const int32_t* __restrict__ rc, int64_t nrows, const FeatState* __restrict__ st,
+    spread_mono(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, const FeatState* __restrict__ st,
                 const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec) {
     const int64_t c = blockIdx.x;
     __shared__ Mono wm[kB / 32];
@@ -414,9 +422,10 @@ __global__ void __launch_bounds__(kB)
     const double avg = double(st->visits) / double(nrows);
     Mono m = mono_id();
     bool ok = true;
-    const int64_t base = c * kSpreadChunk + int64_t(threadIdx.x) * (kSpreadChunk / kB);
-    constexpr int kBatch = 8;
-    for (int j0 = 0; j0 < kSpreadChunk / kB; j0 += kBatch) {
+    const int rpt = int(chunk / kB);  // rows per thread
+    const int64_t base = c * chunk + int64_t(threadIdx.x) * rpt;
+    constexpr int kBatch = 4;
+    for (int j0 = 0; j0 < rpt; j0 += kBatch) {
         int32_t cv[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
@@ -456,7 +465,27 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
 // Binade changes cluster where S is still small (the first rows of a chunk),
 // and every change costs one pass over the rest of the current range, so the
 // range is consumed in windows that start small and double after each pass.
+// Plain sequential IEEE additions, 32 rows per step: every lane holds one
+// t_i and all lanes run the same shuffle-fed chain (so S stays warp-uniform).
+__device__ double seq_rows(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
+    const unsigned lane = threadIdx.x & 31u;
+    for (int64_t b = lo; b < hi; b += 32) {
+        const int64_t i = b + lane;
+        const double t = i < hi ? sq_dev(rc[i], avg) : 0.0;
+        const int cnt = int(hi - b < 32 ? hi - b : 32);
+        for (int j = 0; j < cnt; ++j) S = __dadd_rn(S, __shfl_sync(0xffffffffu, t, j));
+    }
+    return S;
+}
+
 __device__ double advance_exact(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
+    if (S == 0.0) {
+        // the head of the matrix: S doubles every few rows, so binade
+        // changes are dense -- cheaper to add the first rows one by one
+        const int64_t h = lo + 256 < hi ? lo + 256 : hi;
+        S = seq_rows(S, lo, h, rc, avg);
+        lo = h;
+    }
     int64_t w = 256;
     while (lo < hi) {
         const int64_t whi = lo + w < hi ? lo + w : hi;
@@ -545,7 +574,7 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
 // One warp walks the chunk summaries in order, 32 at a time; then finalizes
 // the FeatureVector (features.cpp:121-152).
 __global__ void __launch_bounds__(32)
-    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch,
+    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
                 const MonoRec* __restrict__ rec, FeatState* __restrict__ st) {
     const unsigned lane = threadIdx.x;
     const double avg = double(st->visits) / double(nrows);
@@ -586,8 +615,8 @@ __global__ void __launch_bounds__(32)
             if (f == j) continue;
         }
         // chunk c needs the exact slow path
-        const int64_t lo = c * kSpreadChunk;
-        const int64_t hi = lo + kSpreadChunk < nrows ? lo + kSpreadChunk : nrows;
+        const int64_t lo = c * chunk;
+        const int64_t hi = lo + chunk < nrows ? lo + chunk : nrows;
         S = advance_exact(S, lo, hi, rc, avg);
         c += 1;
     }
@@ -620,23 +649,33 @@ __global__ void feat_init(FeatState* st) {
 
 }  // namespace
 
-void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s) {
+FeatWorkspace::FeatWorkspace(const so_matrix& m, cudaStream_t s) {
+    const int64_t n = m.nrows;
+    const int64_t nch = ceil_div(n, spread_chunk(n));
+    rc.alloc(n, s);
+    if (m.format != SO_DIA) bins.alloc(n + m.ncols, s);
+    if (m.format == SO_DIA || m.format == SO_HDC) dcount.alloc(m.dia.ndiags, s);
+    csum.alloc(nch, s);
+    P.alloc(nch + 1, s);
+    rec.alloc(nch * int64_t(sizeof(MonoRec)), s);
+}
+
+void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s, FeatWorkspace* ws_in) {
     const int64_t n = m.nrows, nc = m.ncols;
     const int64_t thr = true_diag_threshold(ratio, n, nc);  // features.cpp:146-147
     feat_init<<<1, 1, 0, s>>>(st);
     SOB_LAUNCH("feat_init");
 
-    DBuf<int32_t> rc(n, s);
+    std::unique_ptr<FeatWorkspace> own;
+    if (!ws_in) own.reset(new FeatWorkspace(m, s));
+    FeatWorkspace& ws = ws_in ? *ws_in : *own;
+    DBuf<int32_t>& rc = ws.rc;
     const bool dense_bins = m.format != SO_DIA;
     const int64_t nbins = n + nc;
-    DBuf<int32_t> bins(dense_bins ? nbins : 0, s);
+    DBuf<int32_t>& bins = ws.bins;
     if (dense_bins) SOB_CUDA(cudaMemsetAsync(bins.get(), 0, bins.bytes(), s));
-    DBuf<unsigned long long> dcount;
-    const bool has_dia = m.format == SO_DIA || m.format == SO_HDC;
-    if (has_dia) {
-        dcount.alloc(m.dia.ndiags, s);
-        if (m.dia.ndiags) SOB_CUDA(cudaMemsetAsync(dcount.get(), 0, dcount.bytes(), s));
-    }
+    DBuf<unsigned long long>& dcount = ws.dcount;
+    if (dcount.n) SOB_CUDA(cudaMemsetAsync(dcount.get(), 0, dcount.bytes(), s));
     const int grid_rows = grid_for(n, kB, 4);
 
     auto scan_csr = [&](bool accum) {
@@ -696,10 +735,12 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
             break;
     }
 
-    const int64_t nch = ceil_div(n, kSpreadChunk);
-    DBuf<double> csum(nch, s), P(nch + 1, s);
-    DBuf<MonoRec> rec(nch, s);
-    feat_rows<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, st, csum.get());
+    const int64_t chunk = spread_chunk(n);
+    const int64_t nch = ceil_div(n, chunk);
+    DBuf<double>& csum = ws.csum;
+    DBuf<double>& P = ws.P;
+    MonoRec* rec = reinterpret_cast<MonoRec*>(ws.rec.get());
+    feat_rows<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get());
     SOB_LAUNCH("feat_rows");
     if (dense_bins) {
         feat_bins<int32_t><<<grid_for(nbins, 256), 256, 0, s>>>(bins.get(), nbins, thr, st);
@@ -709,9 +750,9 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     SOB_LAUNCH("feat_bins");
     spread_prefix<<<1, 512, 0, s>>>(csum.get(), nch, P.get());
     SOB_LAUNCH("spread_prefix");
-    spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, st, csum.get(), P.get(), rec.get());
+    spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get(), P.get(), rec);
     SOB_LAUNCH("spread_mono");
-    spread_walk<<<1, 32, 0, s>>>(rc.get(), n, nc, nch, rec.get(), st);
+    spread_walk<<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, st);
     SOB_LAUNCH("spread_walk");
 }
 

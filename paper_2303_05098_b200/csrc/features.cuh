@@ -16,8 +16,20 @@ struct FeatState {
     so_feature_vector out;         // finalized vector
 };
 
+// Scratch of the feature pipeline for one matrix (reusable across calls, e.g.
+// by the cached tune graph, so the graph holds no allocation nodes).
+struct FeatWorkspace {
+    DBuf<int32_t> rc, bins;
+    DBuf<unsigned long long> dcount;
+    DBuf<double> csum, P;
+    DBuf<unsigned char> rec;
+    FeatWorkspace(const so_matrix& m, cudaStream_t s);
+};
+
 // Enqueue the whole feature pipeline on stream s; the finalized vector lands in
-// st->out (device).  Scratch is stream-ordered and released on return.
-void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s);
+// st->out (device).  Without a workspace, scratch is stream-ordered and
+// released on return.
+void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s,
+                      FeatWorkspace* ws = nullptr);
 
 }  // namespace sob

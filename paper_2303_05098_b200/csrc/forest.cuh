@@ -5,7 +5,19 @@
 
 namespace sob {
 
+// One node in one 32-byte record: a tree walk costs one dependent round trip
+// per level instead of three.
+struct alignas(16) PackedNode {
+    double threshold;
+    int32_t feature;  // -1: leaf
+    int32_t left;     // global node ids
+    int32_t right;
+    int32_t cls;
+    int32_t pad[2];
+};
+
 struct ForestDev {
+    DBuf<PackedNode> nodes;
     int kind = 1;  // 0 tree, 1 forest
     int n_trees = 0;
     int64_t n_nodes = 0;
@@ -18,5 +30,6 @@ struct ForestDev {
 
 struct so_forest {
     int device = 0;
+    uint64_t uid = 0;  // unique per upload (tune plans are keyed by it)
     sob::ForestDev f;
 };

@@ -21,6 +21,7 @@ constexpr int32_t kEmptyKey = -1;
 struct SmemHash {
     int32_t keys[kHashSlots];
     int32_t cnts[kHashSlots];
+    int32_t used;  // distinct keys inserted; past half full, new keys go straight to global
 };
 
 __device__ __forceinline__ void hash_init(SmemHash& h) {
@@ -28,6 +29,7 @@ __device__ __forceinline__ void hash_init(SmemHash& h) {
         h.keys[i] = kEmptyKey;
         h.cnts[i] = 0;
     }
+    if (threadIdx.x == 0) h.used = 0;
 }
 
 // key >= 0 valid; key < 0 means "no entry for this lane".  Every lane of the
@@ -42,13 +44,26 @@ __device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbin
     if (int(lane) != leader) return;
     const int32_t add = __popc(peers);
     unsigned slot = unsigned(key) & (kHashSlots - 1);
+    const bool full = h.used >= kHashSlots / 2;  // scattered keys: the hash only costs probes
 #pragma unroll 1
     for (int p = 0; p < kProbe; ++p) {
         int32_t old = h.keys[slot];
-        if (old == kEmptyKey) old = atomicCAS(&h.keys[slot], kEmptyKey, key);
-        if (old == kEmptyKey || old == key) {
+        if (old == key) {
             atomicAdd(&h.cnts[slot], add);
             return;
+        }
+        if (old == kEmptyKey) {
+            if (full) break;
+            old = atomicCAS(&h.keys[slot], kEmptyKey, key);
+            if (old == kEmptyKey) {
+                atomicAdd(&h.used, 1);
+                atomicAdd(&h.cnts[slot], add);
+                return;
+            }
+            if (old == key) {
+                atomicAdd(&h.cnts[slot], add);
+                return;
+            }
         }
         slot = (slot + 1) & (kHashSlots - 1);
     }

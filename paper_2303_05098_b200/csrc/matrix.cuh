@@ -2,6 +2,8 @@
 // internal entry points shared by the .cu translation units.
 #pragma once
 
+#include <memory>
+
 #include "common.cuh"
 
 namespace sob {
@@ -61,7 +63,16 @@ struct EllPart {
 
 }  // namespace sob
 
+namespace sob {
+struct TunePlan;  // cached CUDA graph of tune_ml (capi.cu)
+void destroy_tune_plan(TunePlan* p);
+struct TunePlanDeleter {
+    void operator()(TunePlan* p) const { destroy_tune_plan(p); }
+};
+}  // namespace sob
+
 struct so_matrix {
+    mutable std::unique_ptr<sob::TunePlan, sob::TunePlanDeleter> tune_plan;
     int device = 0;
     int32_t format = SO_COO;
     int64_t nrows = 0, ncols = 0;

@@ -2,6 +2,7 @@
 // and the fused ML tuner (tuners.cpp:92-114): features -> predict ->
 // format_feasible -> CSR fallback, with no host round trip until the final
 // 8-int outcome.
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -17,15 +18,11 @@ constexpr int kPB = 256;
 
 struct ForestView {
     int kind, n_trees;
-    const int32_t *feature, *left, *right, *cls;
-    const double* threshold;
+    const PackedNode* nodes;
     const int64_t* root;
 };
 
-ForestView view(const so_forest& f) {
-    return ForestView{f.f.kind,           f.f.n_trees,      f.f.feature.get(),   f.f.left.get(),
-                      f.f.right.get(),    f.f.cls.get(),    f.f.threshold.get(), f.f.root.get()};
-}
+ForestView view(const so_forest& f) { return ForestView{f.f.kind, f.f.n_trees, f.f.nodes.get(), f.f.root.get()}; }
 
 // features_to_row (features.cpp:155-166)
 __device__ __forceinline__ void to_row(const so_feature_vector& f, double* row) {
@@ -43,13 +40,9 @@ __device__ __forceinline__ void to_row(const so_feature_vector& f, double* row) 
 
 // Root-to-leaf walk: x[feature] <= threshold goes left (model.cpp:202-213).
 __device__ __forceinline__ int walk(const ForestView& f, int t, const double* row) {
-    int64_t node = f.root[t];
-    int feat = f.feature[node];
-    while (feat != -1) {
-        node = row[feat] <= f.threshold[node] ? f.left[node] : f.right[node];
-        feat = f.feature[node];
-    }
-    return f.cls[node];
+    PackedNode nd = f.nodes[f.root[t]];
+    while (nd.feature != -1) nd = f.nodes[row[nd.feature] <= nd.threshold ? nd.left : nd.right];
+    return nd.cls;
 }
 
 // One CTA per feature row: thread per tree, integer votes in shared memory,
@@ -190,6 +183,8 @@ so_forest* forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off,
         if (visited != e - b) fail(SO_MALFORMED_MODEL, "unreachable nodes in tree");
     }
     auto* f = new so_forest();
+    static std::atomic<uint64_t> next_uid{1};
+    f->uid = next_uid++;
     SOB_CUDA(cudaGetDevice(&f->device));
     ForestDev& d = f->f;
     d.kind = kind;
@@ -205,6 +200,10 @@ so_forest* forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off,
     up(d.cls, cl.data(), nn);
     up(d.threshold, threshold, nn);
     up(d.root, root.data(), n_trees);
+    std::vector<PackedNode> packed(static_cast<size_t>(nn));
+    for (int64_t i = 0; i < nn; ++i)
+        packed[size_t(i)] = PackedNode{threshold[i], fe[size_t(i)], gl[size_t(i)], gr[size_t(i)], cl[size_t(i)], {0, 0}};
+    up(d.nodes, packed.data(), nn);
     SOB_CUDA(cudaStreamSynchronize(s));  // host staging vectors go out of scope
     return f;
 }
