@@ -33,6 +33,9 @@ CONFIGS = {
     "rmat": "R-MAT 2^22 rows, avg degree 16 (configs[2])",
 }
 FMT = ("COO", "CSR", "DIA", "ELL", "HYB", "HDC")
+# dominant kernel per format on the workload (HDC with an empty CSR part runs the DIA kernel)
+KERNEL_OF = {"COO": "coo_chunk_kernel", "CSR": "csr_warp_kernel", "DIA": "dia_kernel", "ELL": "ell_kernel",
+             "HYB": "ell_kernel", "HDC": "dia_kernel"}
 
 
 def parse():
@@ -56,6 +59,16 @@ def build_workload(name):
     if name == "rmat":
         return synth.rmat(22, 16, seed=42)
     raise ValueError(name)
+
+
+def committed_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/traffic.json, written by scripts/ncu_summary.py)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
 
 
 def peaks():
@@ -326,7 +339,8 @@ def main():
                        "nrows": csr.nrows, "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": round(nbytes / sec / 1e9, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(nbytes / sec / 1e9 / peak, 4),
-                         "traffic": None, "peak_kind": peak_kind},
+                         "traffic": committed_traffic(KERNEL_OF[FMT[tuned]]), "algorithmic_bytes": nbytes,
+                         "kernel": KERNEL_OF[FMT[tuned]], "peak_kind": peak_kind},
             "e2e": {"value": round(world * nbytes / e2e_sec / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * csr.ncols, "d2h_bytes_per_step": 8 * csr.nrows},
             "gpu_launches": args.steps * (2 if FMT[tuned] == "HYB" else 1),

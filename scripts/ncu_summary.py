@@ -65,5 +65,29 @@ def full(path):
     return "\n".join(out)
 
 
+def traffic(path, kernel, out_json):
+    """Record DRAM read+write bytes per launch of `kernel` (from a full capture)
+    into profiles/traffic.json for bench.py's roofline.traffic."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = r[0], r[1], r[2]
+
+    def val(name):
+        v = float(vals[hdr.index(name)].replace(",", ""))
+        u = units[hdr.index(name)].lower()
+        return v * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
+
+    b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+    d = json.load(open(out_json)) if os.path.exists(out_json) else {}
+    d[kernel] = int(b)
+    json.dump(d, open(out_json, "w"), indent=1)
+    return f"{kernel}: {b / 1e6:.1f} MB per launch"
+
+
 if __name__ == "__main__":
-    print(launches(sys.argv[2]) if sys.argv[1] == "launches" else full(sys.argv[2]))
+    if sys.argv[1] == "traffic":
+        print(traffic(sys.argv[2], sys.argv[3], sys.argv[4]))
+    else:
+        print(launches(sys.argv[2]) if sys.argv[1] == "launches" else full(sys.argv[2]))
