@@ -149,6 +149,12 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags,
                                const int64_t* row_ptr, const int64_t* col,
                                const double* val, int64_t threshold,
                                so_matrix** out);
+/* CooMatrix::from_triplets (formats.cpp:293-322) on the device: range check
+ * (SO_INDEX_OUT_OF_RANGE), stable radix sort by (row, col), duplicates summed
+ * in input order.  Result: canonical device COO. */
+so_status so_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n,
+                               const int64_t* row, const int64_t* col,
+                               const double* val, so_matrix** out);
 /* CSR already in device memory (e.g. produced by a device generator or another
  * library): row_ptr int64[n+1], col int32[nnz], val f64[nnz], all device
  * pointers on the current device, fully written before the call (the copy

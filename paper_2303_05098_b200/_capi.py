@@ -94,6 +94,7 @@ _SIGS = {
     "so_matrix_upload_ell": (C.c_int, [i64, i64, i64, vp, vp, i64, P(vp)]),
     "so_matrix_upload_hyb": (C.c_int, [i64, i64, i64, vp, vp, i64, i64, vp, vp, vp, i64, P(vp)]),
     "so_matrix_upload_hdc": (C.c_int, [i64, i64, i64, vp, vp, i64, i64, vp, vp, vp, i64, P(vp)]),
+    "so_coo_from_triplets": (C.c_int, [i64, i64, i64, vp, vp, vp, P(vp)]),
     "so_matrix_import_csr_device": (C.c_int, [i64, i64, i64, vp, vp, vp, P(vp)]),
     "so_matrix_free": (None, [vp]),
     "so_matrix_info_get": (C.c_int, [vp, P(MatrixInfo)]),

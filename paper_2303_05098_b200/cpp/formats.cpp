@@ -191,33 +191,26 @@ FormatId format_from_id(int id) {
 
 // ---------------------------------------------------------------- COO
 
-// Host construction of the canonical container (formats.cpp:293-322): range
-// check, lexicographic sort, duplicate sum in sorted order.
+// formats.cpp:293-322 on the device (so_coo_from_triplets): range check,
+// stable radix sort by (row, col), duplicates summed in input order; the
+// canonical result is downloaded into the host container.
 CooMatrix CooMatrix::from_triplets(index_t nrows, index_t ncols, std::vector<Triplet> triplets) {
-    for (const Triplet& t : triplets)
-        if (t.row < 0 || t.row >= nrows || t.col < 0 || t.col >= ncols)
-            throw IndexOutOfRange("triplet (" + std::to_string(t.row) + ", " + std::to_string(t.col) +
-                                  ") outside " + std::to_string(nrows) + "x" + std::to_string(ncols));
-    std::stable_sort(triplets.begin(), triplets.end(), [](const Triplet& a, const Triplet& b) {
-        return a.row < b.row || (a.row == b.row && a.col < b.col);
-    });
-    CooMatrix out;
-    out.nrows = nrows;
-    out.ncols = ncols;
-    out.row_idx.reserve(triplets.size());
-    out.col_idx.reserve(triplets.size());
-    out.values.reserve(triplets.size());
-    for (const Triplet& t : triplets) {
-        const bool dup = !out.values.empty() && out.row_idx.back() == t.row && out.col_idx.back() == t.col;
-        if (dup) {
-            out.values.back() += t.value;
-        } else {
-            out.row_idx.push_back(t.row);
-            out.col_idx.push_back(t.col);
-            out.values.push_back(t.value);
-        }
+    const std::size_t n = triplets.size();
+    std::vector<index_t> r(n), c(n);
+    std::vector<double> v(n);
+    for (std::size_t k = 0; k < n; ++k) {
+        r[k] = triplets[k].row;
+        c[k] = triplets[k].col;
+        v[k] = triplets[k].value;
     }
-    return out;
+    for (std::size_t k = 0; k < n; ++k)  // message of formats.cpp:296-300
+        if (r[k] < 0 || r[k] >= nrows || c[k] < 0 || c[k] >= ncols)
+            throw IndexOutOfRange("triplet (" + std::to_string(r[k]) + ", " + std::to_string(c[k]) + ") outside " +
+                                  std::to_string(nrows) + "x" + std::to_string(ncols));
+    so_matrix* out = nullptr;
+    detail::check(so_coo_from_triplets(nrows, ncols, static_cast<int64_t>(n), r.data(), c.data(), v.data(), &out));
+    detail::DeviceMirror coo(out);
+    return std::get<CooMatrix>(coo.download());
 }
 
 bool CooMatrix::is_canonical() const {  // formats.cpp:324-340

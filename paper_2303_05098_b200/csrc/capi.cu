@@ -399,6 +399,15 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags, con
     });
 }
 
+so_status so_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n, const int64_t* row, const int64_t* col,
+                               const double* val, so_matrix** out) {
+    return make(out, [&] {
+        check_dims(nrows, ncols);
+        if (n > 0 && (!row || !col || !val)) fail(SO_INVALID_INPUT, "null host array");
+        return coo_from_triplets_device(nrows, ncols, n, row, col, val, current_ctx().stream);
+    });
+}
+
 so_status so_matrix_import_csr_device(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr_dev,
                                       const int32_t* col_dev, const double* val_dev, so_matrix** out) {
     return make(out, [&] {
@@ -668,7 +677,8 @@ int64_t so_spmv_bytes(const so_matrix* m) {
             case SO_DIA: b += dia_bytes(); break;
             case SO_ELL: b += ell_bytes(); break;
             case SO_HYB: b += ell_bytes() + m->coo.nnz * 16; break;
-            case SO_HDC: b += dia_bytes() + m->csr.nnz * 12 + (n + 1) * 8; break;
+            // an empty CSR part is never touched (the DIA kernel runs alone)
+            case SO_HDC: b += dia_bytes() + (m->csr.nnz > 0 ? m->csr.nnz * 12 + (n + 1) * 8 : 0); break;
         }
         bytes = b;
     });

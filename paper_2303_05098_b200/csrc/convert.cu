@@ -92,12 +92,21 @@ void sweep(const so_matrix& csr, Op op, cudaStream_t s, int per_sm = 4) {
     SOB_LAUNCH("csr_sweep");
 }
 
+// Row-lockstep sweep of every entry; rows longer than 2*grp_window go
+// through the piece-parallel sweep (no single-warp tail on skewed rows).
 template <class Op>
 void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s) {
     if (csr.nrows <= 0) return;
-    row_sweep<Op><<<grid_for(ceil_div(csr.nrows, 32) * 256 / 8, 256, 8), 256, 0, s>>>(csr.csr.row_ptr.get(),
-                                                                                        csr.nrows, op);
+    const CsrPart& c = csr.csr;
+    const int64_t skip = c.nlong > 0 ? 2 * int64_t(c.grp_window) : INT64_MAX;
+    row_sweep<Op><<<grid_for(ceil_div(csr.nrows, 32) * 256 / 8, 256, 8), 256, 0, s>>>(c.row_ptr.get(), csr.nrows,
+                                                                                        op, skip);
     SOB_LAUNCH("row_sweep");
+    if (c.nlong > 0) {
+        piece_sweep<Op><<<unsigned(c.npieces), 256, 0, s>>>(c.piece_k.get(), c.long_row.get(), c.long_piece.get(),
+                                                            c.nlong, op);
+        SOB_LAUNCH("piece_sweep");
+    }
 }
 
 // ---------------------------------------------------------- row-block build

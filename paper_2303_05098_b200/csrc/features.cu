@@ -411,9 +411,12 @@ __global__ void __launch_bounds__(kB)
         if (threadIdx.x == 0) rec[c] = MonoRec{0, 0, 2, 0, kMonoIdent, 0};
         return;
     }
+    // The binade is only a guess from the approximate prefix: spread_walk
+    // checks it against the exact running sum (r.e == ilogb(S)) and that no
+    // prefix leaves it, so no safety margin is needed here -- a margin would
+    // reject every chunk of a matrix whose S sits just above a power of two.
     const double lo = P[c], hi = P[c + 1];
-    const double d = 1e-6;
-    const bool safe = lo > 0.0 && ilogb(lo * (1.0 - d)) == ilogb(hi * (1.0 + d));
+    const bool safe = lo > 0.0 && ilogb(lo) == ilogb(hi);
     if (!safe) {
         if (threadIdx.x == 0) rec[c] = MonoRec{0, 0, 2, 0, 0, 0};
         return;
@@ -681,14 +684,23 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     auto scan_csr = [&](bool accum) {
         if (n == 0) return;
         const int g = grid_for(ceil_div(n, 32) * 256 / 8, 256, 8);
+        const CsrPart& c = m.csr;
+        // long rows (SpMV pieces) are swept piece-parallel instead of by one warp
+        const int64_t skip = c.nlong > 0 ? 2 * int64_t(c.grp_window) : INT64_MAX;
         if (accum) {
-            FeatCsrOp<true> op{m.csr.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep<FeatCsrOp<true>><<<g, 256, 0, s>>>(m.csr.row_ptr.get(), n, op);
+            FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            row_sweep<FeatCsrOp<true>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip);
         } else {
-            FeatCsrOp<false> op{m.csr.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep<FeatCsrOp<false>><<<g, 256, 0, s>>>(m.csr.row_ptr.get(), n, op);
+            FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            row_sweep<FeatCsrOp<false>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip);
         }
         SOB_LAUNCH("feat_csr");
+        if (c.nlong > 0) {
+            FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            piece_sweep<FeatCsrOp<false>><<<unsigned(c.npieces), 256, 0, s>>>(c.piece_k.get(), c.long_row.get(),
+                                                                              c.long_piece.get(), c.nlong, op);
+            SOB_LAUNCH("feat_csr_pieces");
+        }
     };
     auto scan_dia = [&]() {
         feat_dia<<<grid_rows, kB, 0, s>>>(n, nc, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(),

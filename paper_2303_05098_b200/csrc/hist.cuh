@@ -99,11 +99,13 @@ __device__ __forceinline__ int row_in_block(const int64_t* srp, int nr, int64_t 
 // the whole warp strides over the rest of the row.  Every op call is made by
 // all 32 lanes (valid=false for idle lanes), so ops may be warp-synchronous.
 // Op interface: begin(), row(r, valid, len) once per row, (r, k, valid) per
-// entry slot, end().
+// entry slot, end().  Entries of rows longer than skip_above are not visited
+// (CSR long rows are split into kPiece pieces and swept by piece_sweep).
 constexpr int kLockstepMax = 64;
 
 template <class Op>
-__global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp, int64_t nrows, Op op) {
+__global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp, int64_t nrows, Op op,
+                                                 int64_t skip_above = INT64_MAX) {
     op.begin();
     const int lane = int(threadIdx.x & 31u);
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / 32);
@@ -114,18 +116,41 @@ __global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp,
         const int64_t a = has ? rp[r] : 0;
         const int64_t len = has ? rp[r + 1] - a : 0;
         op.row(int(r), has, len);
-        const int64_t maxlen = warp_max(len < kLockstepMax ? len : int64_t(kLockstepMax));
-        for (int64_t j = 0; j < maxlen; ++j) op(int(r), a + j, has && j < len);
-        unsigned longm = __ballot_sync(0xffffffffu, len > kLockstepMax);
+        // rows above skip_above are left entirely to a piece-parallel kernel
+        const int64_t elen = len > skip_above ? 0 : len;
+        const int64_t maxlen = warp_max(elen < kLockstepMax ? elen : int64_t(kLockstepMax));
+        for (int64_t j = 0; j < maxlen; ++j) op(int(r), a + j, has && j < elen);
+        unsigned longm = __ballot_sync(0xffffffffu, elen > kLockstepMax);
         while (longm) {
             const int src = __ffs(longm) - 1;
             longm &= longm - 1;
             const int64_t la = __shfl_sync(0xffffffffu, a, src);
-            const int64_t ll = __shfl_sync(0xffffffffu, len, src);
+            const int64_t ll = __shfl_sync(0xffffffffu, elen, src);
             const int lr = __shfl_sync(0xffffffffu, int(r), src);
             for (int64_t j0 = kLockstepMax; j0 < ll; j0 += 32) op(lr, la + j0 + lane, j0 + lane < ll);
         }
     }
+    op.end();
+}
+
+// One CTA per long-row piece (CsrPart::piece_k): coalesced entries of a
+// single row, so no row search.  Same op interface (row() is not called).
+template <class Op>
+__global__ void __launch_bounds__(256) piece_sweep(const int64_t* __restrict__ pk, const int32_t* __restrict__ lrow,
+                                                   const int64_t* __restrict__ lpiece, int64_t nlong, Op op) {
+    op.begin();
+    const int64_t k0 = pk[2 * blockIdx.x], k1 = pk[2 * blockIdx.x + 1];
+    // row of this piece: the long row whose piece range holds blockIdx.x
+    int64_t lo = 0, hi = nlong;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (lpiece[mid] <= int64_t(blockIdx.x))
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const int r = lrow[lo];
+    for (int64_t b = k0; b < k1; b += blockDim.x) op(r, b + threadIdx.x, b + threadIdx.x < k1);
     op.end();
 }
 

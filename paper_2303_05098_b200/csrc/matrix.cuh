@@ -107,6 +107,8 @@ so_matrix* any_to_csr(const so_matrix& m, cudaStream_t s);  // to_coo semantics,
 so_matrix* csr_to_coo(const so_matrix& csr, cudaStream_t s);
 so_matrix* clone_matrix(const so_matrix& m, cudaStream_t s);
 bool coo_is_canonical(const so_matrix& coo, cudaStream_t s);
+so_matrix* coo_from_triplets_device(int64_t nrows, int64_t ncols, int64_t n, const int64_t* row_h,
+                                    const int64_t* col_h, const double* val_h, cudaStream_t s);
 bool csr_rows_canonical(const so_matrix& csr, cudaStream_t s);
 
 // --- spmv (spmv.cu) ---

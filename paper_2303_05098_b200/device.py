@@ -115,6 +115,15 @@ class DeviceMatrix:
         return cls(out)
 
     @classmethod
+    def from_triplets(cls, nrows, ncols, row, col, val):
+        """CooMatrix::from_triplets on the device -> canonical COO."""
+        row, col, val = _i64(row), _i64(col), _f64(val)
+        out = C.c_void_p()
+        _check(A.lib().so_coo_from_triplets(nrows, ncols, val.size, _ptr(row), _ptr(col), _ptr(val),
+                                            C.byref(out)))
+        return cls(out)
+
+    @classmethod
     def csr(cls, nrows, ncols, row_ptr, col, val):
         row_ptr, col, val = _i64(row_ptr), _i64(col), _f64(val)
         out = C.c_void_p()

@@ -429,3 +429,53 @@ def test_stencil27_generator_and_row_slices(so, O):
     one = run(1)
     assert np.array_equal(run(3), one)
     assert np.array_equal(run(4), one)
+
+
+def test_device_from_triplets(so, O):
+    """CooMatrix::from_triplets on the device (stable radix sort + duplicate
+    sum in input order) == the oracle's stable sort + sum, bit for bit."""
+    rng = np.random.default_rng(17)
+    for n, m, z in [(1, 1, 3), (7, 5, 40), (300, 200, 5000), (70_000, 90_000, 400_000)]:
+        r = rng.integers(0, n, z)
+        c = rng.integers(0, m, z)
+        v = rng.uniform(-2, 2, z)
+        want = O.from_triplets(n, m, r, c, v)
+        got = so.DeviceMatrix.from_triplets(n, m, r, c, v).download()
+        cmp_host(got, want)
+    with pytest.raises(so.IndexOutOfRange):
+        so.DeviceMatrix.from_triplets(2, 2, [2], [0], [1.0])
+    assert so.DeviceMatrix.from_triplets(4, 4, [], [], []).nnz() == 0
+
+
+def _csr_from_lengths(lens, ncols):
+    lens = np.asarray(lens, dtype=np.int64)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    r = np.arange(lens.size)
+    col = np.empty(rp[-1], dtype=np.int64)
+    off = np.arange(lens.max())
+    for k in np.unique(lens):
+        rows = r[lens == k]
+        col[(rp[rows][:, None] + off[:k]).ravel()] = ((rows[:, None] + off[:k]) % ncols).ravel()
+    # keep every row sorted (wrap-around rows start at a smaller column)
+    for i in np.nonzero(r + lens > ncols)[0]:
+        col[rp[i]:rp[i + 1]] = np.sort(col[rp[i]:rp[i + 1]])
+    return rp, col
+
+
+@pytest.mark.parametrize("head", [3, 5, 2])
+def test_spread_sum_just_above_power_of_two(so, O, head):
+    """nnz_row_spread when the running sum sits just above 2^k for millions
+    of rows (one short/long head row, every other row at ~avg): the chunk
+    binade guesses must be checked exactly, not rejected by a margin
+    (config-4 corpus id 877 took 12 ms before)."""
+    n = 2_500_000
+    lens = np.full(n, 4)
+    lens[0] = head
+    lens[-1] = 2
+    rp, col = _csr_from_lengths(lens, n)
+    val = np.ones(rp[-1])
+    d = so.DeviceMatrix.csr(n, n, rp, col, val)
+    coo = O.coo_dict(n, n, np.repeat(np.arange(n), lens), col, val)
+    want, _ = O.oc_features(O.oc_convert(coo, O.CSR), 0.2)
+    got = np.array(d.extract_features(0.2).to_row())
+    assert np.array_equal(got, want), (got, want)
