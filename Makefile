@@ -14,7 +14,7 @@ CU_SRCS  := $(wildcard $(CSRC)/*.cu)
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(LIBDIR)/obj/%.o,$(CU_SRCS))
 CU_HDRS  := $(wildcard $(CSRC)/*.cuh) include/sparseoracle_b200.h
 NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr \
-            -Xptxas -warn-spills
+            -Xptxas -warn-spills $(EXTRA)
 CPP_SRCS := $(wildcard $(PKG)/cpp/*.cpp)
 CPP_OBJS := $(patsubst $(PKG)/cpp/%.cpp,$(LIBDIR)/obj/cpp_%.o,$(CPP_SRCS))
 CPP_HDRS := $(wildcard include/sparseoracle/*.hpp) include/sparseoracle_b200.h

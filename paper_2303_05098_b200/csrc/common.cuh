@@ -106,7 +106,7 @@ struct DBuf {
     T* get() const { return p; }
 };
 
-inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Grid sizing: a multiple of the SM count (148 on B200) times resident CTAs,
 // capped by the work available.

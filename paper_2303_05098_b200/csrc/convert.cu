@@ -99,8 +99,13 @@ void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s) {
     if (csr.nrows <= 0) return;
     const CsrPart& c = csr.csr;
     const int64_t skip = c.nlong > 0 ? 2 * int64_t(c.grp_window) : INT64_MAX;
+    DBuf<unsigned> ticket;  // dynamic row groups when the row lengths are skewed
+    if (c.nlong > 0) {
+        ticket.alloc(1, s);
+        SOB_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
+    }
     row_sweep<Op><<<grid_for(ceil_div(csr.nrows, 32) * 256 / 8, 256, 8), 256, 0, s>>>(c.row_ptr.get(), csr.nrows,
-                                                                                        op, skip);
+                                                                                        op, skip, ticket.get());
     SOB_LAUNCH("row_sweep");
     if (c.nlong > 0) {
         piece_sweep<Op><<<unsigned(c.npieces), 256, 0, s>>>(c.piece_k.get(), c.long_row.get(), c.long_piece.get(),

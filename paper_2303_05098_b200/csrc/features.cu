@@ -28,12 +28,14 @@ namespace sob {
 namespace {
 
 constexpr int kB = 256;
+constexpr int kMaxSpreadChunk = 8192;
+constexpr int kSubs = 32;  // sub-chunks per spread chunk (one per lane of the walk)
 // rows per spread chunk: a power of two in [1024, 8192] giving ~512 chunks,
 // so big matrices keep the chunk walk short and small ones keep the exact
 // slow path over their first chunk cheap
 inline int64_t spread_chunk(int64_t n) {
     int64_t c = 1024;
-    while (c < 8192 && c * 512 < n) c *= 2;
+    while (c < kMaxSpreadChunk && c * 512 < n) c *= 2;
     return c;
 }
 constexpr int kMaxSmemDiag = 1024;
@@ -400,64 +402,94 @@ __global__ void __launch_bounds__(512) spread_prefix(const double* __restrict__ 
     if (threadIdx.x == 0) P[nch] = carry;
 }
 
-// Chunk summaries at the binade the approximate prefix puts the chunk in.
+__device__ __forceinline__ MonoRec ident_rec() { return MonoRec{0, 0, 2, 0, kMonoIdent, 0}; }
+
+// Two-level summaries.  Every chunk is cut into 32 sub-chunks of chunk/32
+// rows (8 threads each); a sub-chunk is summarised at the binade its
+// approximate prefix (P[c] + sums of the earlier sub-chunks) puts it in, the
+// chunk record is the ordered product of its sub-chunk records when they all
+// share one binade.  spread_walk descends to the sub-chunk records of a
+// chunk it cannot take whole, so the exact row-by-row path only ever runs
+// over the one sub-chunk where the running sum changes binade.
 __global__ void __launch_bounds__(kB)
     spread_mono(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, const FeatState* __restrict__ st,
-                const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec) {
+                const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec,
+                MonoRec* __restrict__ fine) {
     const int64_t c = blockIdx.x;
-    __shared__ Mono wm[kB / 32];
-    __shared__ bool wok[kB / 32];
+    const int t = threadIdx.x, lane = t & 31;
     if (csum[c] == 0.0) {  // every t == 0: identity at any binade
-        if (threadIdx.x == 0) rec[c] = MonoRec{0, 0, 2, 0, kMonoIdent, 0};
+        if (t < kSubs) fine[c * kSubs + t] = ident_rec();
+        if (t == 0) rec[c] = ident_rec();
         return;
     }
-    // The binade is only a guess from the approximate prefix: spread_walk
-    // checks it against the exact running sum (r.e == ilogb(S)) and that no
-    // prefix leaves it, so no safety margin is needed here -- a margin would
-    // reject every chunk of a matrix whose S sits just above a power of two.
-    const double lo = P[c], hi = P[c + 1];
-    const bool safe = lo > 0.0 && ilogb(lo) == ilogb(hi);
-    if (!safe) {
-        if (threadIdx.x == 0) rec[c] = MonoRec{0, 0, 2, 0, 0, 0};
-        return;
-    }
-    const int e = ilogb(lo);
+    __shared__ double sub_sum[kSubs];
+    __shared__ double psub[kSubs + 1];
+    __shared__ MonoRec fr[kSubs];
     const double avg = double(st->visits) / double(nrows);
-    Mono m = mono_id();
-    bool ok = true;
-    const int rpt = int(chunk / kB);  // rows per thread
-    const int64_t base = c * chunk + int64_t(threadIdx.x) * rpt;
-    constexpr int kBatch = 4;
-    for (int j0 = 0; j0 < rpt; j0 += kBatch) {
-        int32_t cv[kBatch];
+    const int rpt = int(chunk / kB);  // rows per thread; 8 threads per sub-chunk
+    const int64_t base = c * chunk + int64_t(t) * rpt;
+    double ps = 0.0;  // approximate (order is irrelevant for the guess)
+    for (int j = 0; j < rpt; ++j)
+        if (base + j < nrows) ps += sq_dev(rc[base + j], avg);
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            const int64_t i = base + j0 + u;
-            cv[u] = i < nrows ? rc[i] : 0;
+    for (int o = 1; o < 8; o <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    if ((lane & 7) == 0) sub_sum[t >> 3] = ps;
+    __syncthreads();
+    if (t < 32) {
+        const double v = sub_sum[lane];
+        double inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double w = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += w;
         }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            if (base + j0 + u < nrows) {
+        psub[lane] = P[c] + (inc - v);
+        if (lane == 31) psub[kSubs] = P[c] + inc;
+    }
+    __syncthreads();
+    const int sj = t >> 3;
+    const double lo = psub[sj], hi = psub[sj + 1];
+    const bool zero = sub_sum[sj] == 0.0;  // sum of non-negative terms: all zero
+    const bool safe = !zero && lo > 0.0 && ilogb(lo) == ilogb(hi);
+    const int e = safe ? ilogb(lo) : 0;
+    Mono m = mono_id();
+    bool ok = safe;
+    if (safe) {
+        for (int j = 0; j < rpt && ok; ++j) {
+            if (base + j < nrows) {
                 Mono el;
-                ok = ok && mono_elem(sq_dev(cv[u], avg), e, el);
+                ok = mono_elem(sq_dev(rc[base + j], avg), e, el);
                 if (ok) m = mono_cat(m, el);
             }
         }
     }
-    m = warp_reduce_mono(m, ok);
-    if ((threadIdx.x & 31) == 0) {
-        wm[threadIdx.x >> 5] = m;
-        wok[threadIdx.x >> 5] = ok;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {  // ordered product over the 8 threads of the sub-chunk
+        const Mono other = shfl_mono_down(m, o);
+        const bool ook = __shfl_down_sync(0xffffffffu, ok, o);
+        if ((lane & (2 * o - 1)) == 0) {
+            m = mono_cat(m, other);
+            ok = ok && ook;
+        }
+    }
+    if ((lane & 7) == 0) {
+        const MonoRec r = zero ? ident_rec() : MonoRec{m.a0, m.a1, m.p, e, ok ? kMonoSafe : 0, 0};
+        fine[c * kSubs + sj] = r;
+        fr[sj] = r;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        Mono t = mono_id();
-        bool tok = true;
-        for (int w = 0; w < kB / 32; ++w) {
-            t = mono_cat(t, wm[w]);
-            tok = tok && wok[w];
+    if (t == 0) {
+        Mono acc = mono_id();
+        int ce = INT32_MIN;
+        bool cok = true;
+        for (int j = 0; j < kSubs && cok; ++j) {
+            const MonoRec& r = fr[j];
+            if (r.flags & kMonoIdent) continue;
+            if (!(r.flags & kMonoSafe) || (ce != INT32_MIN && r.e != ce)) cok = false;
+            ce = r.e;
+            acc = mono_cat(acc, Mono{r.a0, r.a1, r.p});
         }
-        rec[c] = MonoRec{t.a0, t.a1, t.p, e, tok ? kMonoSafe : 0, 0};
+        rec[c] = cok ? MonoRec{acc.a0, acc.a1, acc.p, ce, kMonoSafe, 0} : MonoRec{0, 0, 2, 0, 0, 0};
     }
 }
 
@@ -574,34 +606,33 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
     return S;
 }
 
-// One warp walks the chunk summaries in order, 32 at a time; then finalizes
-// the FeatureVector (features.cpp:121-152).
-__global__ void __launch_bounds__(32)
-    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
-                const MonoRec* __restrict__ rec, FeatState* __restrict__ st) {
-    const unsigned lane = threadIdx.x;
-    const double avg = double(st->visits) / double(nrows);
-    double S = 0.0;
+// Apply records rec[0..nrec) in order to S, 32 at a time (one per lane):
+// every record whose binade matches the exact running sum is folded in with
+// one warp scan, verified to stay inside the binade; a record that cannot be
+// taken whole goes to fallback(S, index).
+template <class Fallback>
+__device__ double walk_records(double S, const MonoRec* __restrict__ rec, int64_t nrec, Fallback fallback) {
+    const unsigned lane = threadIdx.x & 31u;
     int64_t c = 0;
     int64_t pre_c = 0;  // group whose records sit in `nxt`
-    MonoRec nxt = lane < nch ? rec[lane] : MonoRec{0, 0, 2, 0, kMonoIdent, 0};
-    while (c < nch) {
+    MonoRec nxt = lane < nrec ? rec[lane] : ident_rec();
+    while (c < nrec) {
         const int64_t ci = c + lane;
-        MonoRec r = (pre_c == c) ? nxt : (ci < nch ? rec[ci] : MonoRec{0, 0, 2, 0, kMonoIdent, 0});
+        MonoRec r = (pre_c == c) ? nxt : (ci < nrec ? rec[ci] : ident_rec());
         // prefetch the most likely next group (all 32 consumed) while this one is applied
         pre_c = c + 32;
-        nxt = pre_c + lane < nch ? rec[pre_c + lane] : MonoRec{0, 0, 2, 0, kMonoIdent, 0};
+        nxt = pre_c + lane < nrec ? rec[pre_c + lane] : ident_rec();
         const int eS = S > 0.0 ? ilogb(S) : INT32_MIN;
-        const bool usable = ci < nch && ((r.flags & kMonoIdent) || ((r.flags & kMonoSafe) && r.e == eS));
+        const bool usable = ci < nrec && ((r.flags & kMonoIdent) || ((r.flags & kMonoSafe) && r.e == eS));
         const unsigned badm = __ballot_sync(0xffffffffu, !usable);
         int j = badm ? __ffs(badm) - 1 : 32;
-        const int64_t remaining = nch - c;
+        const int64_t remaining = nrec - c;
         if (j > remaining) j = int(remaining);
         if (j > 0) {
             Mono mm = (int(lane) < j) ? Mono{r.a0, r.a1, r.p} : mono_id();
             bool ok = true;
             Mono pre = warp_scan_mono(mm, ok);
-            if (S == 0.0) {  // only identity chunks can be usable at S == 0
+            if (S == 0.0) {  // only identity records can be usable at S == 0
                 c += j;
                 continue;
             }
@@ -609,7 +640,7 @@ __global__ void __launch_bounds__(32)
             const long long mi = m + ((m & 1) ? pre.a1 : pre.a0);
             const bool good = double(mi) < kTwo53 || int(lane) >= j;
             const unsigned bad = __ballot_sync(0xffffffffu, !good);
-            const int f = bad ? __ffs(bad) - 1 : j;  // first chunk whose prefix leaves the binade
+            const int f = bad ? __ffs(bad) - 1 : j;  // first record whose prefix leaves the binade
             if (f > 0) {
                 const long long mf = __shfl_sync(0xffffffffu, mi, f - 1);
                 S = ldexp(double(mf), eS - 52);
@@ -617,12 +648,34 @@ __global__ void __launch_bounds__(32)
             c += f;
             if (f == j) continue;
         }
-        // chunk c needs the exact slow path
-        const int64_t lo = c * chunk;
-        const int64_t hi = lo + chunk < nrows ? lo + chunk : nrows;
-        S = advance_exact(S, lo, hi, rc, avg);
+        S = fallback(S, c);
         c += 1;
     }
+    return S;
+}
+
+// One warp walks the chunk records, descending into the sub-chunk records of
+// a chunk it cannot take whole and to the exact row-by-row path only for the
+// sub-chunk where S changes binade; then finalizes the FeatureVector
+// (features.cpp:121-152).
+__global__ void __launch_bounds__(32)
+    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
+                const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
+    const unsigned lane = threadIdx.x;
+    const double avg = double(st->visits) / double(nrows);
+    const int64_t sub = chunk / kSubs;
+    const double S = walk_records(0.0, rec, nch, [&](double S, int64_t c) {
+        const int64_t r0 = c * chunk;
+        const int64_t nsub = ceil_div(((r0 + chunk < nrows) ? r0 + chunk : nrows) - r0, sub);
+        return walk_records(S, fine + c * kSubs, nsub, [&](double S, int64_t j) {
+#ifdef SOB_SPREAD_DEBUG
+            if (lane == 0)
+                printf("spread exact chunk %lld sub %lld S=%.17g\n", (long long)c, (long long)j, S);
+#endif
+            const int64_t lo = r0 + j * sub;
+            return advance_exact(S, lo, lo + sub < nrows ? lo + sub : nrows, rc, avg);
+        });
+    });
     if (lane == 0) {
         st->S = S;
         so_feature_vector& f = st->out;
@@ -648,6 +701,7 @@ __global__ void feat_init(FeatState* st) {
     st->nd = 0;
     st->ntd = 0;
     st->S = 0.0;
+    st->ticket = 0;
 }
 
 }  // namespace
@@ -660,7 +714,7 @@ FeatWorkspace::FeatWorkspace(const so_matrix& m, cudaStream_t s) {
     if (m.format == SO_DIA || m.format == SO_HDC) dcount.alloc(m.dia.ndiags, s);
     csum.alloc(nch, s);
     P.alloc(nch + 1, s);
-    rec.alloc(nch * int64_t(sizeof(MonoRec)), s);
+    rec.alloc(nch * (1 + kSubs) * int64_t(sizeof(MonoRec)), s);  // chunk + sub-chunk records
 }
 
 void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s, FeatWorkspace* ws_in) {
@@ -687,12 +741,13 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         const CsrPart& c = m.csr;
         // long rows (SpMV pieces) are swept piece-parallel instead of by one warp
         const int64_t skip = c.nlong > 0 ? 2 * int64_t(c.grp_window) : INT64_MAX;
+        unsigned* ticket = c.nlong > 0 ? &st->ticket : nullptr;  // skewed rows: dynamic groups
         if (accum) {
             FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep<FeatCsrOp<true>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip);
+            row_sweep<FeatCsrOp<true>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip, ticket);
         } else {
             FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep<FeatCsrOp<false>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip);
+            row_sweep<FeatCsrOp<false>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip, ticket);
         }
         SOB_LAUNCH("feat_csr");
         if (c.nlong > 0) {
@@ -762,9 +817,10 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     SOB_LAUNCH("feat_bins");
     spread_prefix<<<1, 512, 0, s>>>(csum.get(), nch, P.get());
     SOB_LAUNCH("spread_prefix");
-    spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get(), P.get(), rec);
+    MonoRec* fine = rec + nch;
+    spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get(), P.get(), rec, fine);
     SOB_LAUNCH("spread_mono");
-    spread_walk<<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, st);
+    spread_walk<<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
     SOB_LAUNCH("spread_walk");
 }
 

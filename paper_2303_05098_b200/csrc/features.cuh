@@ -13,6 +13,7 @@ struct FeatState {
     int min_row;
     unsigned long long nd, ntd;    // N_D, N_TD
     double S;                      // exact sequential sum of squared deviations
+    unsigned ticket;               // dynamic row-group counter of the CSR sweep
     so_feature_vector out;         // finalized vector
 };
 

@@ -44,9 +44,13 @@ __device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbin
     if (int(lane) != leader) return;
     const int32_t add = __popc(peers);
     unsigned slot = unsigned(key) & (kHashSlots - 1);
-    const bool full = h.used >= kHashSlots / 2;  // scattered keys: the hash only costs probes
+    // scattered keys (hash half full): only the home slot is checked, so keys
+    // that were hot early still merge in shared memory and the rest go
+    // straight to the global bins without a probe chain
+    const bool full = h.used >= kHashSlots / 2;
+    const int probes = full ? 1 : kProbe;
 #pragma unroll 1
-    for (int p = 0; p < kProbe; ++p) {
+    for (int p = 0; p < probes; ++p) {
         int32_t old = h.keys[slot];
         if (old == key) {
             atomicAdd(&h.cnts[slot], add);
@@ -103,14 +107,23 @@ __device__ __forceinline__ int row_in_block(const int64_t* srp, int nr, int64_t 
 // (CSR long rows are split into kPiece pieces and swept by piece_sweep).
 constexpr int kLockstepMax = 64;
 
+// With a ticket (a zeroed counter), warps claim 32-row groups dynamically --
+// skewed row lengths (power-law) otherwise leave most warps of a CTA waiting
+// at op.end()'s barrier for the one that drew the heavy rows.
+__device__ __forceinline__ int64_t next_group(unsigned* ticket) {
+    unsigned t = 0;
+    if ((threadIdx.x & 31u) == 0) t = atomicAdd(ticket, 1u);
+    return int64_t(__shfl_sync(0xffffffffu, t, 0)) * 32;
+}
+
 template <class Op>
 __global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp, int64_t nrows, Op op,
-                                                 int64_t skip_above = INT64_MAX) {
+                                                 int64_t skip_above = INT64_MAX, unsigned* ticket = nullptr) {
     op.begin();
     const int lane = int(threadIdx.x & 31u);
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / 32);
-    for (int64_t wb = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; wb < nrows;
-         wb += nwarps * 32) {
+    for (int64_t wb = ticket ? next_group(ticket) : (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32;
+         wb < nrows; wb = ticket ? next_group(ticket) : wb + nwarps * 32) {
         const int64_t r = wb + lane;
         const bool has = r < nrows;
         const int64_t a = has ? rp[r] : 0;
