@@ -116,6 +116,8 @@ typedef struct so_forest so_forest; /* opaque, device-resident */
 /* ---- context ----------------------------------------------------------- */
 const char* so_last_error(void);
 const char* so_version(void);
+/* Number of kernels this library has launched in the process (monotone). */
+int64_t so_kernel_launches(void);
 so_status so_set_device(int device);          /* device for new objects */
 so_status so_device_sync(void);
 /* Opaque cudaStream_t used by every host-facing call on the current device. */

@@ -85,6 +85,7 @@ class TuneOutcome(C.Structure):
 _SIGS = {
     "so_last_error": (C.c_char_p, []),
     "so_version": (C.c_char_p, []),
+    "so_kernel_launches": (C.c_int64, []),
     "so_set_device": (C.c_int, [C.c_int]),
     "so_device_sync": (C.c_int, []),
     "so_default_stream": (vp, []),

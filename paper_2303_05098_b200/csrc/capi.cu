@@ -1,3 +1,4 @@
+#include <atomic>
 // extern "C" boundary (include/sparseoracle_b200.h): argument validation with
 // the reference's error types/messages, H2D/D2H staging between the
 // reference's host layout (int64 indices, row-major ELL) and the device
@@ -66,6 +67,8 @@ Context& ctx(int d) {
         SOB_CUDA(cudaSetDevice(d));
         c.device = d;
         SOB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        SOB_CUDA(cudaStreamCreateWithFlags(&c.copy_in, cudaStreamNonBlocking));
+        SOB_CUDA(cudaStreamCreateWithFlags(&c.copy_out, cudaStreamNonBlocking));
         SOB_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, d));
         int l2 = 0;
         SOB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, d));
@@ -306,6 +309,85 @@ void check_x(const so_matrix& m, int64_t xlen) {  // spmv.cpp:12-19
 }
 
 }  // namespace
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace sob
+
+namespace sob {
+namespace {
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Row-chunk pipeline of spmv(m, x) for matrices whose rows only read a known
+// column window (DIA, HDC with an empty CSR part): x is uploaded in the
+// windows the chunks need (copy engine, copy_in), chunk k's rows run on the
+// compute stream as soon as its window has landed, and chunk k's y is read
+// back on copy_out while later chunks upload and compute -- the host<->device
+// transfers of both directions overlap each other and the kernels.  Results
+// are identical to the one-shot path (same kernel per row).
+constexpr int64_t kPipeRows = 1 << 18;
+
+bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
+    const bool dia_only = m.format == SO_DIA || (m.format == SO_HDC && m.csr.nnz == 0);
+    if (!dia_only || m.dia.ndiags == 0 || m.nrows < 2 * kPipeRows) return false;
+    if (!is_pinned(x) || !is_pinned(y)) return false;
+    if (!m.dia_window_known) {
+        std::vector<int64_t> off(size_t(m.dia.ndiags));
+        d2h(off.data(), m.dia.offsets, m.dia.ndiags, s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+        m.dia_omin = *std::min_element(off.begin(), off.end());
+        m.dia_omax = *std::max_element(off.begin(), off.end());
+        m.dia_window_known = true;
+    }
+    Context& c = ctx(m.device);
+    const int64_t n = m.nrows, nc = m.ncols;
+    const int64_t nchunks = std::min<int64_t>(16, ceil_div(n, kPipeRows));
+    const int64_t rows_per = ceil_div(n, nchunks);
+    DBuf<double> dx(nc, s), dy(n, s);
+    thread_local std::vector<cudaEvent_t> ev;
+    while (ev.size() < size_t(2 * nchunks + 1)) {
+        cudaEvent_t e;
+        SOB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+    }
+    // buffers come from the compute stream's pool: the copy streams wait on it
+    SOB_CUDA(cudaEventRecord(ev[0], s));
+    SOB_CUDA(cudaStreamWaitEvent(c.copy_in, ev[0], 0));
+    SOB_CUDA(cudaStreamWaitEvent(c.copy_out, ev[0], 0));
+    int64_t x_hi = 0;
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int64_t a = k * rows_per, b = std::min(n, a + rows_per);
+        if (a >= b) break;
+        const int64_t need = std::min(nc, std::max<int64_t>(0, b + m.dia_omax));
+        const int64_t want = k + 1 == nchunks ? nc : need;
+        if (want > x_hi) {
+            SOB_CUDA(cudaMemcpyAsync(dx.get() + x_hi, x + x_hi, sizeof(double) * size_t(want - x_hi),
+                                     cudaMemcpyHostToDevice, c.copy_in));
+            x_hi = want;
+        }
+        SOB_CUDA(cudaEventRecord(ev[1 + 2 * k], c.copy_in));
+        SOB_CUDA(cudaStreamWaitEvent(s, ev[1 + 2 * k], 0));
+        spmv_device_rows(m, dx.get(), dy.get(), a, b, s);
+        SOB_CUDA(cudaEventRecord(ev[2 + 2 * k], s));
+        SOB_CUDA(cudaStreamWaitEvent(c.copy_out, ev[2 + 2 * k], 0));
+        SOB_CUDA(cudaMemcpyAsync(y + a, dy.get() + a, sizeof(double) * size_t(b - a), cudaMemcpyDeviceToHost,
+                                 c.copy_out));
+    }
+    // the buffers are released on s: order s after the last read-back
+    SOB_CUDA(cudaEventRecord(ev[0], c.copy_out));
+    SOB_CUDA(cudaStreamWaitEvent(s, ev[0], 0));
+    return true;
+}
+
+}  // namespace
 }  // namespace sob
 
 using namespace sob;
@@ -314,6 +396,8 @@ extern "C" {
 
 const char* so_last_error(void) { return g_err.c_str(); }
 const char* so_version(void) { return "sparseoracle-b200 0.1 (sm_100a)"; }
+
+int64_t so_kernel_launches(void) { return sob::g_launches.load(std::memory_order_relaxed); }
 
 so_status so_set_device(int device) {
     return guard([&] {
@@ -607,6 +691,10 @@ so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) 
     return guard([&] {
         cudaStream_t s = on_device(m);
         check_x(*m, xlen);
+        if (m->nrows > 0 && spmv_pipelined(*m, x, y, s)) {
+            SOB_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
         DBuf<double> dx, dy(m->nrows, s);
         h2d(dx, x, xlen, s);
         spmv_device(*m, dx.get(), dy.get(), s);

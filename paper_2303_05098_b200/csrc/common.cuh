@@ -30,7 +30,10 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 
 #define SOB_CUDA(call) ::sob::cuda_check((call), #call)
-#define SOB_LAUNCH(what) ::sob::cuda_check(cudaGetLastError(), what)
+// every kernel launch of the library goes through this check; it also counts
+// launches (so_kernel_launches, used by bench.py's gpu_launches)
+void count_launch();
+#define SOB_LAUNCH(what) (::sob::count_launch(), ::sob::cuda_check(cudaGetLastError(), what))
 
 void set_error(const std::string& m);
 
@@ -56,6 +59,8 @@ so_status guard(F&& f) {
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // copy-engine streams of the pipelined host spmv (capi.cu so_spmv)
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
     int num_sms = 148;
     int64_t l2_bytes = 0;
 };
@@ -167,6 +172,20 @@ __device__ __forceinline__ int ld_stream(const int* p) {
     int v;
     asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
+}
+
+// 256-bit streaming loads (sm_100: LDG.E.ENL2.256): one instruction moves 32
+// contiguous bytes per lane, so a warp covers 1 KB with no L1 allocation.
+// The pointer must be 32-byte aligned.
+__device__ __forceinline__ void ld_stream_v8(const int* p, int (&v)[8]) {
+    asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        : "l"(p));
+}
+__device__ __forceinline__ void ld_stream_v4(const double* p, double* v) {
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+        : "l"(p));
 }
 
 // ----------------------------------------------------------- host helpers ---

@@ -92,13 +92,13 @@ void sweep(const so_matrix& csr, Op op, cudaStream_t s, int per_sm = 4) {
     SOB_LAUNCH("csr_sweep");
 }
 
-// Row-lockstep sweep of every entry; rows longer than 2*grp_window go
+// Row-lockstep sweep of every entry; rows longer than grp_cap go
 // through the piece-parallel sweep (no single-warp tail on skewed rows).
 template <class Op>
 void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s) {
     if (csr.nrows <= 0) return;
     const CsrPart& c = csr.csr;
-    const int64_t skip = c.nlong > 0 ? 2 * int64_t(c.grp_window) : INT64_MAX;
+    const int64_t skip = c.nlong > 0 ? int64_t(c.grp_cap) : INT64_MAX;
     DBuf<unsigned> ticket;  // dynamic row groups when the row lengths are skewed
     if (c.nlong > 0) {
         ticket.alloc(1, s);
@@ -149,15 +149,37 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
     if (i < n) flag[i] = (rp[i + 1] - rp[i]) > limit ? 1 : 0;
 }
 
-// warp groups: split at 32-row boundaries, window changes and around long rows
-__global__ void group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t win, int32_t* __restrict__ flag) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t len = rp[i + 1] - rp[i];
-    // rows longer than win stand alone => every group holds <= 2*win entries
-    bool start = (i % 32 == 0) || len > win;
-    if (i > 0) start = start || (rp[i] - rp[i - 1]) > win || (rp[i] / win) != (rp[i - 1] / win);
-    flag[i] = start ? 1 : 0;
+// SpMV warp groups, greedy: a group is <= 32 consecutive rows holding <= cap
+// entries; a row longer than cap stands alone (and is split into pieces).
+// One thread walks kGroupChunk rows (chunk starts are forced group starts,
+// so the partition is deterministic and parallel) and flags group starts.
+constexpr int kGroupChunk = 512;
+__global__ void group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t cap, int32_t* __restrict__ flag) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t lo = c * kGroupChunk;
+    if (lo >= n) return;
+    const int64_t hi = lo + kGroupChunk < n ? lo + kGroupChunk : n;
+    int64_t i = lo;
+    int64_t next_start = lo;
+    int64_t base = 0;
+    int64_t rpi = rp[lo];
+    for (; i < hi; ++i) {
+        const int64_t rpn = rp[i + 1];
+        if (i == next_start) {
+            flag[i] = 1;
+            base = rpi;
+            next_start = i + 32;
+            if (rpn - rpi > cap) next_start = i + 1;  // long row: alone
+        } else if (rpn - base > cap) {
+            flag[i] = 1;  // row does not fit: starts the next group
+            base = rpi;
+            next_start = i + 32;
+            if (rpn - rpi > cap) next_start = i + 1;
+        } else {
+            flag[i] = 0;
+        }
+        rpi = rpn;
+    }
 }
 
 __global__ void long_row_list(const int64_t* __restrict__ rp, const int32_t* __restrict__ flag,
@@ -609,10 +631,11 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), csr.row_ptr.get(), n,
                                                                      csr.blk.get(), csr.blk_k.get());
     SOB_LAUNCH("row_block_scatter");
-    // SpMV warp groups; the window follows the mean row length
+    // SpMV warp groups; entries per lane follow the mean row length
     const int64_t nnz_total = d2h_scalar(csr.row_ptr.get() + n, s);
-    csr.grp_window = (nnz_total <= 8 * n) ? kGroupWindowShort : kGroupWindowLong;
-    group_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, csr.grp_window, flag.get());
+    csr.grp_cap = 32 * ((nnz_total <= 8 * n) ? kGroupItemsShort : kGroupItemsLong);
+    group_flags<<<unsigned(ceil_div(ceil_div(n, kGroupChunk), 128)), 128, 0, s>>>(csr.row_ptr.get(), n, csr.grp_cap,
+                                                                                 flag.get());
     SOB_LAUNCH("group_flags");
     exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
     csr.ngrp = d2h_scalar(pos.get() + n, s);
@@ -622,7 +645,7 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
                                                                      csr.grp.get(), csr.grp_k.get());
     SOB_LAUNCH("row_block_scatter");
     // long rows -> kPiece-entry pieces (SpMV splits them over many CTAs)
-    long_row_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, 2 * int64_t(csr.grp_window),
+    long_row_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, int64_t(csr.grp_cap),
                                                               flag.get());
     SOB_LAUNCH("long_row_flags");
     exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
@@ -710,7 +733,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.blk_k, src.csr.blk_k);
     m->csr.canonical = src.csr.canonical;
     m->csr.ngrp = src.csr.ngrp;
-    m->csr.grp_window = src.csr.grp_window;
+    m->csr.grp_cap = src.csr.grp_cap;
     cp(m->csr.grp, src.csr.grp);
     cp(m->csr.grp_k, src.csr.grp_k);
     m->csr.nlong = src.csr.nlong;

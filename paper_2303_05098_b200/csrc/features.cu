@@ -740,7 +740,7 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         const int g = grid_for(ceil_div(n, 32) * 256 / 8, 256, 8);
         const CsrPart& c = m.csr;
         // long rows (SpMV pieces) are swept piece-parallel instead of by one warp
-        const int64_t skip = c.nlong > 0 ? 2 * int64_t(c.grp_window) : INT64_MAX;
+        const int64_t skip = c.nlong > 0 ? int64_t(c.grp_cap) : INT64_MAX;
         unsigned* ticket = c.nlong > 0 ? &st->ticket : nullptr;  // skewed rows: dynamic groups
         if (accum) {
             FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};

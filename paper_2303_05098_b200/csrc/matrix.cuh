@@ -14,12 +14,12 @@ namespace sob {
 // (<= 2*kWindow entries, staged in shared memory), at most kRowsPerBlock rows,
 // or exactly one row longer than kWindow ("long row" block).
 constexpr int kWindow = 1024;
-constexpr int kPiece = 2048;  // entries per CTA for rows longer than 2*grp_window
-// SpMV warp groups: <= 32 rows whose first entries fall into one window of
-// grp_window entries (so <= 2*grp_window entries); short-row matrices use the
-// small window (8 entries per lane), others the large one (16 per lane).
-constexpr int kGroupWindowShort = 128;
-constexpr int kGroupWindowLong = 256;
+constexpr int kPiece = 2048;  // entries per CTA for rows longer than grp_cap
+// SpMV warp groups: <= 32 consecutive rows holding <= grp_cap = 32*items
+// entries (greedy); short-row matrices (mean <= 8) load 8 entries per lane,
+// others 12 (scripts/spmv_lab.cu measurements).
+constexpr int kGroupItemsShort = 8;
+constexpr int kGroupItemsLong = 12;
 constexpr int kRowsPerBlock = 1024;
 constexpr int kStreamBlock = 256;
 
@@ -39,10 +39,10 @@ struct CsrPart {
     mutable int canonical = -1;  // rows strictly increasing: -1 unknown, 0 no, 1 yes
     // SpMV warp-group partition
     int64_t ngrp = 0;
-    int grp_window = kGroupWindowLong;
+    int grp_cap = 32 * kGroupItemsLong;
     DBuf<int32_t> grp;     // [ngrp+1]
     DBuf<int64_t> grp_k;   // [ngrp+1]
-    // rows longer than 2*grp_window, split into kPiece-entry pieces for SpMV
+    // rows longer than grp_cap, split into kPiece-entry pieces for SpMV
     int64_t nlong = 0, npieces = 0;
     DBuf<int32_t> long_row;     // [nlong]
     DBuf<int64_t> long_piece;   // [nlong+1] first piece of each long row
@@ -82,6 +82,9 @@ struct so_matrix {
     sob::EllPart ell;  // ELL, HYB ell part
     int64_t kh = 0;
     int64_t threshold = 0;
+    // cached min/max DIA offset (pipelined host spmv), filled on first use
+    mutable bool dia_window_known = false;
+    mutable int64_t dia_omin = 0, dia_omax = 0;
 
     int64_t nnz() const {
         switch (format) {

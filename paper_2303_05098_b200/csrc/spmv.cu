@@ -35,74 +35,69 @@ __device__ double block_sum_det(double v, double* scratch) {
 }
 
 // DIA contribution of one row, diagonals ascending (spmv.cpp:45-56 restated
-// per row: y[i] += diag[i] * x[i + off] for every in-range diagonal).  Eight
-// diagonals are fetched before any is accumulated so each thread keeps eight
-// coalesced HBM loads in flight; in-range holes multiply as 0 * x exactly as
-// the reference does.
+// per row: y[i] += diag[i] * x[i + off] for every in-range diagonal).  Nine
+// diagonals' values and x are fetched before any is accumulated (so each
+// thread keeps 18 loads in flight); the last batch re-reads the last diagonal
+// for its dead slots.  Index math is 32-bit (rows, columns and offsets are
+// < 2^31 on the device); only the diagonal base is 64-bit.
+// In-range holes multiply as 0 * x exactly as the reference does.
 constexpr int kDiaSmem = 512;
+constexpr int kDiaBatch = 9;
 
-// offsets come from shared memory (staged per CTA) when ndiags <= kDiaSmem,
-// else straight from global memory (GLOBAL_OFF)
+// offsets come from shared memory (staged per CTA as int32) when
+// ndiags <= kDiaSmem, else straight from global memory (GLOBAL_OFF)
 template <bool GLOBAL_OFF>
-__device__ __forceinline__ double dia_row(int64_t i, int64_t nrows, int64_t ncols, int ndiags,
-                                          const int64_t* __restrict__ soff,
-                                          const int64_t* __restrict__ offsets,
-                                          const double* __restrict__ vals,
+__device__ __forceinline__ int dia_off(const int* soff, const int64_t* __restrict__ offsets, int d) {
+    return GLOBAL_OFF ? int(offsets[d]) : soff[d];
+}
+
+template <bool GLOBAL_OFF>
+__device__ __forceinline__ double dia_row(int i, int nrows, int ncols, int ndiags, const int* soff,
+                                          const int64_t* __restrict__ offsets, const double* __restrict__ vals,
                                           const double* __restrict__ x) {
-    constexpr int U = 8;
-    const int64_t* off = GLOBAL_OFF ? offsets : soff;
+    constexpr int U = kDiaBatch;
+    const double* vp = vals + i;
     double acc = 0.0;
-    int d0 = 0;
-    for (; d0 + U <= ndiags; d0 += U) {
+    for (int d0 = 0; d0 < ndiags; d0 += U) {
         double v[U], xv[U];
         bool ok[U];
         // unpredicated loads (cells outside the column range exist in the
-        // diagonal-major array, x index is clamped) so all 2U loads issue
+        // diagonal-major array; x index falls back to 0) so all 2U loads issue
         // back to back; only in-range diagonals are accumulated
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int d = d0 + u;
-            const int64_t c = i + off[d];
-            ok[u] = c >= 0 && c < ncols;
-            const int64_t cc = c < 0 ? 0 : (c >= ncols ? ncols - 1 : c);
-            v[u] = ld_stream(vals + int64_t(d) * nrows + i);
-            xv[u] = __ldg(x + cc);
+            const bool live = d0 + u < ndiags;
+            const int d = live ? d0 + u : ndiags - 1;
+            const int c = i + dia_off<GLOBAL_OFF>(soff, offsets, d);
+            ok[u] = live && unsigned(c) < unsigned(ncols);
+            v[u] = ld_stream(vp + size_t(d) * size_t(nrows));
+            xv[u] = __ldg(x + (ok[u] ? c : 0));
         }
         // x + (-0.0) == x exactly for every x (round-to-nearest), so skipped
         // diagonals add -0.0: an unconditional chain keeps the loads hoisted
 #pragma unroll
         for (int u = 0; u < U; ++u) acc = fadd(acc, ok[u] ? fmul(v[u], xv[u]) : -0.0);
     }
-    for (; d0 < ndiags; ++d0) {
-        const int64_t c = i + off[d0];
-        if (c >= 0 && c < ncols) acc = fadd(acc, fmul(ld_stream(vals + int64_t(d0) * nrows + i), __ldg(x + c)));
-    }
     return acc;
 }
 
-__device__ __forceinline__ void stage_offsets(int64_t* soff, const int64_t* __restrict__ offsets, int ndiags) {
+__device__ __forceinline__ void stage_offsets(int* soff, const int64_t* __restrict__ offsets, int ndiags) {
     const int m = ndiags < kDiaSmem ? ndiags : kDiaSmem;
-    for (int d = threadIdx.x; d < m; d += blockDim.x) soff[d] = offsets[d];
+    for (int d = threadIdx.x; d < m; d += blockDim.x) soff[d] = int(offsets[d]);
     __syncthreads();
 }
 
 // ---------------------------------------------------------------- CSR -------
-// Streaming CSR ("CSR-stream"), persistent and software-pipelined.  Window w
-// owns rows [blk[w], blk[w+1]) whose entries [blk_k[w], blk_k[w+1]) (at most
-// 2*kWindow) are contiguous.  Phase 1 gathers x for the window's col/val
-// (already in registers) and stages the rounded products in shared memory;
-// then the col/val (and row_ptr) loads of the CTA's NEXT window are issued so
-// they are in flight while phase 2 gives each row to one thread that sums its
-// products in the reference order (bit-exact).  WITH_DIA fuses the HDC DIA
-// part in front of the CSR part (spmv.cpp:101-106).  Windows holding a single
-// row longer than 2*kWindow are skipped here: csr_long_pieces + csr_long_fixup
-// split them over many CTAs.
 // Warp-level CSR stream.  Group g = rows [grp[g], grp[g+1]) (<= 32 rows,
-// entries [grp_k[g], grp_k[g+1]) <= 32*IT) is owned by one warp: coalesced
-// col/val loads (IT per lane), x gather, rounded products into warp-private
-// shared memory, then lane i sums row grp[g]+i sequentially (reference order,
-// bit-exact).  The next group's loads are issued before the sums, so each
-// warp keeps 2*IT loads in flight with no CTA-wide barrier anywhere.
+// <= 32*IT entries starting at grp_k[g]; greedy partition, convert.cu
+// group_flags) is owned by one warp: coalesced col/val loads (IT per lane),
+// x gather, rounded products into warp-private shared memory, then lane i sums
+// row grp[g]+i sequentially -- the reference's order (spmv.cpp:32-43),
+// bit-exact.  The next group's col/val/row_ptr loads are issued before the
+// sums (register double buffer), so each warp keeps up to 2*IT loads in flight
+// with no CTA-wide barrier.  A group holding one row longer than 32*IT is
+// skipped here (csr_long_pieces + csr_long_fixup).  WITH_DIA fuses the HDC
+// DIA part in front of the CSR part (spmv.cpp:101-106).
 template <int IT, bool WITH_DIA>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
@@ -110,8 +105,9 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
                     int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                     const double* __restrict__ dvals) {
-    __shared__ double sp[8][32 * IT];
-    __shared__ int64_t soff[WITH_DIA ? kDiaSmem : 1];
+    constexpr int kCap = 32 * IT;
+    __shared__ double sp[8][kCap];
+    __shared__ int soff[WITH_DIA ? kDiaSmem : 1];
     if (WITH_DIA) stage_offsets(soff, offsets, ndiags);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double* prod = sp[wid];
@@ -119,66 +115,67 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     const int64_t stride = int64_t(gridDim.x) * 8;
     if (g >= ngrp) return;
     int r0 = grp[g], r1 = grp[g + 1];
-    int64_t k0 = grp_k[g], k1 = grp_k[g + 1];
+    int64_t k0 = grp_k[g];
+    // entry count, saturated at kCap + 1 (= long row, handled elsewhere)
+    int cnt = int(min(grp_k[g + 1] - k0, int64_t(kCap + 1)));
     int c[IT];
     double v[IT];
-    bool longrow = k1 - k0 > 32 * IT;
 #pragma unroll
     for (int u = 0; u < IT; ++u) {
-        const int64_t k = k0 + u * 32 + lane;
-        if (!longrow && k < k1) {
-            c[u] = ld_stream(col + k);
-            v[u] = ld_stream(val + k);
+        const int e = u * 32 + lane;
+        if (e < cnt && cnt <= kCap) {
+            c[u] = ld_stream(col + k0 + e);
+            v[u] = ld_stream(val + k0 + e);
         }
     }
-    int64_t pa = 0, pe = 0;
+    int pa = 0, pe = 0;
     if (r0 + lane < r1) {
-        pa = rp[r0 + lane];
-        pe = rp[r0 + lane + 1];
+        pa = int(rp[r0 + lane] - k0);
+        pe = int(rp[r0 + lane + 1] - k0);
     }
     while (true) {
         const int64_t gn = g + stride;
-        int nr0 = 0, nr1 = 0;
-        int64_t nk0 = 0, nk1 = 0;
+        int nr0 = 0, nr1 = 0, ncnt = 0;
+        int64_t nk0 = 0;
         if (gn < ngrp) {
             nr0 = grp[gn];
             nr1 = grp[gn + 1];
             nk0 = grp_k[gn];
-            nk1 = grp_k[gn + 1];
+            ncnt = int(min(grp_k[gn + 1] - nk0, int64_t(kCap + 1)));
         }
+        const bool longrow = cnt > kCap;
         if (!longrow) {
 #pragma unroll
             for (int u = 0; u < IT; ++u) {
-                const int64_t k = k0 + u * 32 + lane;
-                if (k < k1) prod[u * 32 + lane] = fmul(v[u], __ldg(x + c[u]));
+                const int e = u * 32 + lane;
+                if (e < cnt) prod[e] = fmul(v[u], __ldg(x + c[u]));
             }
         }
         __syncwarp();
-        const bool nlong = nk1 - nk0 > 32 * IT;
-        int64_t npa = 0, npe = 0;
+        int npa = 0, npe = 0;
         if (gn < ngrp) {
 #pragma unroll
             for (int u = 0; u < IT; ++u) {
-                const int64_t k = nk0 + u * 32 + lane;
-                if (!nlong && k < nk1) {
-                    c[u] = ld_stream(col + k);
-                    v[u] = ld_stream(val + k);
+                const int e = u * 32 + lane;
+                if (e < ncnt && ncnt <= kCap) {
+                    c[u] = ld_stream(col + nk0 + e);
+                    v[u] = ld_stream(val + nk0 + e);
                 }
             }
             if (nr0 + lane < nr1) {
-                npa = rp[nr0 + lane];
-                npe = rp[nr0 + lane + 1];
+                npa = int(rp[nr0 + lane] - nk0);
+                npe = int(rp[nr0 + lane + 1] - nk0);
             }
         }
         if (!longrow && r0 + lane < r1) {
             const int r = r0 + lane;
-            double s = 0.0;
-            for (int64_t j = pa - k0; j < pe - k0; ++j) s = fadd(s, prod[j]);
+            double acc = 0.0;
+            for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
             if (WITH_DIA)
-                s = fadd(ndiags <= kDiaSmem ? dia_row<false>(r, nrows, ncols, ndiags, soff, offsets, dvals, x)
-                                            : dia_row<true>(r, nrows, ncols, ndiags, soff, offsets, dvals, x),
-                         s);
-            y[r] = s;
+                acc = fadd(ndiags <= kDiaSmem ? dia_row<false>(r, int(nrows), int(ncols), ndiags, soff, offsets, dvals, x)
+                                              : dia_row<true>(r, int(nrows), int(ncols), ndiags, soff, offsets, dvals, x),
+                           acc);
+            y[r] = acc;
         }
         __syncwarp();
         if (gn >= ngrp) break;
@@ -186,14 +183,13 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
         r0 = nr0;
         r1 = nr1;
         k0 = nk0;
-        k1 = nk1;
+        cnt = ncnt;
         pa = npa;
         pe = npe;
-        longrow = nlong;
     }
 }
 
-// Rows longer than 2*grp_window: piece p covers entries [pk[2p], pk[2p+1]) of row
+// Rows longer than grp_cap: piece p covers entries [pk[2p], pk[2p+1]) of row
 // prow[p] (<= kPiece entries, 8 independent loads per thread), reduced with a
 // fixed tree into part[p]; csr_long_fixup then adds the pieces of each row in
 // piece order (deterministic, within the 1e-12 contract).
@@ -231,7 +227,7 @@ __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, 
     double t = 0.0;
     for (int64_t p = lpiece[l]; p < lpiece[l + 1]; ++p) t = fadd(t, part[p]);
     const int r = lrow[l];
-    if (WITH_DIA) t = fadd(dia_row<true>(r, nrows, ncols, ndiags, nullptr, offsets, dvals, x), t);
+    if (WITH_DIA) t = fadd(dia_row<true>(r, int(nrows), int(ncols), ndiags, nullptr, offsets, dvals, x), t);
     y[r] = t;
 }
 
@@ -239,15 +235,15 @@ __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, 
 // One thread per row, diagonals ascending: consecutive threads read
 // consecutive cells of each diagonal (diagonal-major layout => coalesced).
 template <bool GLOBAL_OFF>
-__global__ void __launch_bounds__(256, 8)
+__global__ void __launch_bounds__(256, 6)
     dia_kernel(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                const double* __restrict__ vals, const double* __restrict__ x,
                double* __restrict__ y, int64_t row_lo, int64_t row_hi) {
-    __shared__ int64_t soff[GLOBAL_OFF ? 1 : kDiaSmem];
+    __shared__ int soff[GLOBAL_OFF ? 1 : kDiaSmem];
     if (!GLOBAL_OFF) stage_offsets(soff, offsets, ndiags);
     const int64_t i = row_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= row_hi) return;
-    y[i] = dia_row<GLOBAL_OFF>(i, nrows, ncols, ndiags, soff, offsets, vals, x);
+    y[i] = dia_row<GLOBAL_OFF>(int(i), int(nrows), int(ncols), ndiags, soff, offsets, vals, x);
 }
 
 // ---------------------------------------------------------------- ELL -------
@@ -288,175 +284,137 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- COO -------
-// Segmented reduction over the row-sorted canonical COO.  CTA c owns the
-// fixed chunk [c*kCooChunk, (c+1)*kCooChunk) (perfect load balance whatever
-// the row lengths).  Products are staged in shared memory; each thread walks
-// kCooItems consecutive entries sequentially (reference order inside a
-// thread), pieces of a row that span threads are joined by a block-wide
-// segmented scan, and rows that span chunks are finished by coo_fixup in
-// chunk order.  Every pass has a fixed order => deterministic.
-// ACCUM (HYB coo part): a row's sum starts from the ELL result already in y,
-// exactly as the reference's coo_kernel adds into y (spmv.cpp:95-100).
-constexpr int kCooBlock = 256;
+// Segmented reduction over the row-sorted canonical COO, one warp per fixed
+// chunk of kCooChunk entries (perfect balance whatever the row-length skew).
+// Lane l owns kCooItems CONSECUTIVE entries (256-bit streaming loads of row/
+// col/val: each warp instruction covers 1 KB contiguous, L1 left to x),
+// gathers x and forms the rounded products.  Pass 1 sums the lane's
+// last row piece; one warp-wide segmented scan keyed on that row joins pieces
+// across lanes (rows are sorted, so equal keys are contiguous); pass 2 walks
+// the lane's entries sequentially starting from the carry of earlier lanes,
+// so a row spanning at most two lanes is summed in the reference's order
+// (spmv.cpp:21-30).  Rows that start and end inside the chunk are written
+// directly; pieces of rows spanning chunks go to per-chunk records combined
+// by coo_fixup in chunk order.  Fixed partition and combine order =>
+// deterministic, within the 1e-12 contract.  Empty rows are zero-filled by
+// the lane holding the next row's first entry (y written exactly once).
+// ACCUM (HYB COO part, spmv.cpp:95-100): the row sum is added to the ELL
+// result already in y.
 constexpr int kCooItems = 8;
-constexpr int kCooChunk = kCooBlock * kCooItems;
+constexpr int kCooChunk = 32 * kCooItems;
 
 struct CooChunkRec {
-    double first_sum;  // in-chunk piece of a segment that began in an earlier chunk
-    double last_sum;   // in-chunk piece of the segment that continues past the chunk
+    double first_sum;  // in-chunk piece of a row that began in an earlier chunk
+    double last_sum;   // in-chunk piece of the row that continues past the chunk
     int32_t last_row;
     int32_t flags;
 };
 enum : int32_t { kFirstCont = 1, kLastOpen = 2, kSingle = 4 };
 
-struct SegPair {
-    bool f;
-    double v;
-};
-
-__device__ __forceinline__ SegPair seg_combine(SegPair a, SegPair b) {
-    // a precedes b
-    return SegPair{a.f || b.f, b.f ? b.v : fadd(a.v, b.v)};
-}
-
-// Exclusive segmented scan over the CTA's threads (identity: {false, 0}).
-__device__ SegPair block_excl_seg_scan(SegPair in, SegPair* wsc) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    SegPair inc = in;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        SegPair up{bool(__shfl_up_sync(0xffffffffu, int(inc.f), o)),
-                   __shfl_up_sync(0xffffffffu, inc.v, o)};
-        if (lane >= o) inc = seg_combine(up, inc);
-    }
-    if (lane == 31) wsc[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        SegPair w = lane < kCooBlock / 32 ? wsc[lane] : SegPair{false, 0.0};
-        SegPair wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            SegPair up{bool(__shfl_up_sync(0xffffffffu, int(wi.f), o)),
-                       __shfl_up_sync(0xffffffffu, wi.v, o)};
-            if (lane >= o) wi = seg_combine(up, wi);
-        }
-        // exclusive per warp
-        SegPair ex{bool(__shfl_up_sync(0xffffffffu, int(wi.f), 1)), __shfl_up_sync(0xffffffffu, wi.v, 1)};
-        if (lane == 0) ex = SegPair{false, 0.0};
-        if (lane < kCooBlock / 32) wsc[lane] = ex;
-    }
-    __syncthreads();
-    SegPair wex = wsc[warp];
-    SegPair lex{bool(__shfl_up_sync(0xffffffffu, int(inc.f), 1)), __shfl_up_sync(0xffffffffu, inc.v, 1)};
-    SegPair res;
-    if (lane == 0)
-        res = wex;
-    else
-        res = seg_combine(wex, lex);
-    return res;
-}
-
-// shared-memory slot of chunk item e: one pad slot per kCooItems keeps the
-// per-thread sequential reads (items t*8 .. t*8+7) bank-conflict free
-__device__ __forceinline__ int coo_slot(int e) { return e + (e >> 3); }
-
 template <bool ACCUM>
-__global__ void __launch_bounds__(kCooBlock, 6)
-    coo_chunk_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row,
-                     const int32_t* __restrict__ col, const double* __restrict__ val,
-                     const double* __restrict__ x, double* __restrict__ y,
-                     CooChunkRec* __restrict__ rec) {
-    __shared__ double sp[kCooChunk + kCooChunk / kCooItems];
-    __shared__ int32_t sr[kCooChunk + kCooChunk / kCooItems];
-    __shared__ SegPair wsc[kCooBlock / 32 + 1];
-    const int64_t base = int64_t(blockIdx.x) * kCooChunk;
+__global__ void __launch_bounds__(256, 4)
+    coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                    CooChunkRec* __restrict__ rec) {
+    constexpr int IT = kCooItems;
+    constexpr int kNoRow = 0x7fffffff;
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t base = chunk * kCooChunk;
+    if (base >= z) return;
     const int cnt = int(z - base < kCooChunk ? z - base : int64_t(kCooChunk));
+    const int first = lane * IT;
+    const int64_t k = base + first;
+    const int nmine = cnt - first <= 0 ? 0 : (cnt - first >= IT ? IT : cnt - first);
+    int r[IT], c[IT];
+    double p[IT];
+    if (nmine == IT) {
+        ld_stream_v8(row + k, r);
+        ld_stream_v8(col + k, c);
+        ld_stream_v4(val + k, p);
+        ld_stream_v4(val + k + 4, p + 4);
+    } else {
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const bool ok = j < nmine;
+            r[j] = ok ? row[k + j] : kNoRow;
+            c[j] = ok ? col[k + j] : 0;
+            p[j] = ok ? val[k + j] : 0.0;
+        }
+    }
     const int prev_row = base > 0 ? row[base - 1] : -1;
     const int next_row = base + cnt < z ? row[base + cnt] : -1;
 #pragma unroll
-    for (int j = 0; j < kCooItems; ++j) {
-        const int e = j * kCooBlock + int(threadIdx.x);
-        if (e < cnt) {
-            const int64_t k = base + e;
-            sr[coo_slot(e)] = ld_stream(row + k);
-            sp[coo_slot(e)] = fmul(ld_stream(val + k), __ldg(x + ld_stream(col + k)));
-        }
-    }
-    __syncthreads();
+    for (int j = 0; j < IT; ++j) p[j] = j < nmine ? fmul(p[j], __ldg(x + c[j])) : 0.0;
 
-    // this thread's kCooItems consecutive entries, in registers
-    const int first = int(threadIdx.x) * kCooItems;
-    const int nmine = cnt - first < 0 ? 0 : (cnt - first > kCooItems ? kCooItems : cnt - first);
-    int rr[kCooItems];
-    double pp[kCooItems];
+    // pass 1: the lane's last row piece (kNoRow pieces of idle lanes never match)
+    int tr = kNoRow;
 #pragma unroll
-    for (int j = 0; j < kCooItems; ++j) {
-        rr[j] = j < nmine ? sr[coo_slot(first + j)] : -1;
-        pp[j] = j < nmine ? sp[coo_slot(first + j)] : 0.0;
-    }
-    const int r_before = nmine == 0 ? -1 : (first == 0 ? prev_row : sr[coo_slot(first - 1)]);
-    const int r_after = nmine == 0 ? -1 : (first + nmine < cnt ? sr[coo_slot(first + nmine)] : next_row);
-    const int chunk_first_row = sr[0];
-
-    // pass 1: this thread's tail piece (sum of its last segment)
-    SegPair mine{false, 0.0};
+    for (int j = 0; j < IT; ++j)
+        if (j < nmine) tr = r[j];
+    double tsum = 0.0;
 #pragma unroll
-    for (int j = 0; j < kCooItems; ++j) {
-        if (j < nmine) {
-            const bool head = rr[j] != (j == 0 ? r_before : rr[j - 1]);
-            if (head) {
-                mine.f = true;
-                mine.v = ACCUM ? y[rr[j]] : 0.0;
-            }
-            mine.v = fadd(mine.v, pp[j]);
-        }
+    for (int j = 0; j < IT; ++j)
+        if (j < nmine && r[j] == tr) tsum = fadd(tsum, p[j]);
+    // inclusive segmented scan over lanes keyed on the tail row: lanes between
+    // two equal keys hold nothing but that row (sorted), so the run is exact
+    double inc = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double up = __shfl_up_sync(kFull, inc, o);
+        const int ur = __shfl_up_sync(kFull, tr, o);
+        if (lane >= o && ur == tr) inc = fadd(up, inc);
     }
-    const SegPair carry = block_excl_seg_scan(mine, wsc);
+    const double prev_inc = __shfl_up_sync(kFull, inc, 1);
+    const int prev_tr = __shfl_up_sync(kFull, tr, 1);
+    const int nlane_r0 = __shfl_down_sync(kFull, r[0], 1);
+    const int first_row = __shfl_sync(kFull, r[0], 0);
+    const bool first_cont = first_row == prev_row;
     if (nmine == 0) return;
 
-    // pass 2: finish segments
-    const bool first_cont = chunk_first_row == prev_row;
-    const bool head0 = rr[0] != r_before;
-    bool orphan = !carry.f && !head0;  // piece of a segment begun before this chunk
-    double s = head0 ? (ACCUM ? y[rr[0]] : 0.0) : carry.v;
+    // pass 2: sequential walk from the carry of earlier lanes
+    int prv = lane == 0 ? prev_row : prev_tr;
+    double acc = (lane > 0 && prev_tr == r[0]) ? prev_inc : 0.0;
+    const bool chunk_end = first + nmine == cnt;
 #pragma unroll
-    for (int j = 0; j < kCooItems; ++j) {
+    for (int j = 0; j < IT; ++j) {
         if (j < nmine) {
-            const int prv = j == 0 ? r_before : rr[j - 1];
-            const bool head = rr[j] != prv;
-            if (j > 0 && head) {
-                s = ACCUM ? y[rr[j]] : 0.0;
-                orphan = false;
+            const int rw = r[j];
+            if (rw != prv) {
+                if (!ACCUM)  // rows strictly between consecutive entries are empty
+                    for (int q = prv + 1; q < rw; ++q) y[q] = 0.0;
+                if (j > 0) acc = 0.0;
             }
-            if (!ACCUM && head)  // rows strictly between consecutive entries are empty
-                for (int r = prv + 1; r < rr[j]; ++r) y[r] = 0.0;
-            s = fadd(s, pp[j]);
-            const int nxt = j + 1 < nmine ? rr[j + 1] : r_after;
-            const bool ends = nxt != rr[j];
-            const bool chunk_last = first + j == cnt - 1;
-            if (ends) {
+            acc = fadd(acc, p[j]);
+            const int nxt = j + 1 < nmine ? r[j + 1] : (chunk_end ? next_row : nlane_r0);
+            const bool orphan = first_cont && rw == first_row;  // began in an earlier chunk
+            if (rw != nxt) {
                 if (orphan)
-                    rec[blockIdx.x].first_sum = s;
+                    rec[chunk].first_sum = acc;
                 else
-                    y[rr[j]] = s;
-            } else if (chunk_last && orphan) {  // continues into the next chunk
-                rec[blockIdx.x].first_sum = s;
+                    y[rw] = ACCUM ? fadd(y[rw], acc) : acc;
             }
-            if (chunk_last) {
-                const bool open = !ends;
-                rec[blockIdx.x].flags = (first_cont ? kFirstCont : 0) | (open ? kLastOpen : 0) |
-                                        ((open && orphan) ? kSingle : 0);
-                rec[blockIdx.x].last_row = rr[j];
-                rec[blockIdx.x].last_sum = s;
+            if (chunk_end && j + 1 == nmine) {
+                const bool open = rw == nxt;
+                if (open) {
+                    rec[chunk].last_sum = acc;
+                    rec[chunk].last_row = rw;
+                    if (orphan) rec[chunk].first_sum = acc;
+                }
+                rec[chunk].flags = (first_cont ? kFirstCont : 0) | (open ? kLastOpen : 0) |
+                                   ((open && orphan) ? kSingle : 0);
                 if (!ACCUM && base + cnt == z)  // trailing empty rows
-                    for (int64_t r = int64_t(rr[j]) + 1; r < nrows; ++r) y[r] = 0.0;
+                    for (int64_t q = int64_t(rw) + 1; q < nrows; ++q) y[q] = 0.0;
             }
+            prv = rw;
         }
     }
 }
 
 // Rows spanning chunks: the chunk holding the row's first entry walks forward
 // in chunk order (deterministic) and writes the final value.
+template <bool ACCUM>
 __global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, double* __restrict__ y) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
@@ -467,17 +425,18 @@ __global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, 
         t = fadd(t, rec[j].first_sum);
         if (!(rec[j].flags & kSingle)) break;
     }
-    y[rec[c].last_row] = t;
+    const int32_t r = rec[c].last_row;
+    y[r] = ACCUM ? fadd(y[r], t) : t;
 }
 
 template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
     DBuf<CooChunkRec> rec(nchunks, s);
-    coo_chunk_kernel<ACCUM><<<unsigned(nchunks), kCooBlock, 0, s>>>(
+    coo_warp_kernel<ACCUM><<<unsigned(ceil_div(nchunks, 8)), 256, 0, s>>>(
         coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y, rec.get());
-    SOB_LAUNCH("coo_chunk_kernel");
-    coo_fixup<<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y);
+    SOB_LAUNCH("coo_warp_kernel");
+    coo_fixup<ACCUM><<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y);
     SOB_LAUNCH("coo_fixup");
 }
 
@@ -500,10 +459,10 @@ void launch_csr_warp(const so_matrix& m, bool with_dia, const double* x, double*
 void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     if (c.ngrp == 0) return;
-    if (c.grp_window == kGroupWindowShort)
-        launch_csr_warp<2 * kGroupWindowShort / 32>(m, with_dia, x, y, s);
+    if (c.grp_cap == 32 * kGroupItemsShort)
+        launch_csr_warp<kGroupItemsShort>(m, with_dia, x, y, s);
     else
-        launch_csr_warp<2 * kGroupWindowLong / 32>(m, with_dia, x, y, s);
+        launch_csr_warp<kGroupItemsLong>(m, with_dia, x, y, s);
     if (c.nlong > 0) {
         const int nd = with_dia ? int(m.dia.ndiags) : 0;
         DBuf<double> part(c.npieces, s);
@@ -545,7 +504,8 @@ void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s) 
 }  // namespace
 
 void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, cudaStream_t s) {
-    if (m.format != SO_DIA) fail(SO_INVALID_INPUT, "row-range SpMV is implemented for DIA matrices");
+    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0))
+        fail(SO_INVALID_INPUT, "row-range SpMV is implemented for DIA matrices (and HDC with an empty CSR part)");
     if (lo < 0 || hi > m.nrows || lo > hi) fail(SO_INVALID_INPUT, "row range outside the matrix");
     launch_dia(m, x, y, s, lo, hi);
 }

@@ -1,0 +1,725 @@
+// SpMV lab: standalone microbenchmark of kernel variants (not the product).
+// Measures each variant under three L2 policies between timed reps:
+//   none  - inputs larger than L2, no flush
+//   write - cudaMemset of a 512 MB buffer (leaves ~L2-sized dirty lines that
+//           are written back during the next kernel)
+//   read  - a kernel reading a 512 MB buffer (evicts without dirtying)
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -o /tmp/lab scripts/spmv_lab.cu
+#include <cuda_runtime.h>
+
+#include "sparseoracle_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); exit(1);} } while (0)
+
+__device__ __forceinline__ double lds(const double* p) {
+    double v; asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v;
+}
+__device__ __forceinline__ int lds(const int* p) {
+    int v; asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p)); return v;
+}
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+
+// ------------------------------------------------------------------ flush
+__global__ void read_flush(const double2* __restrict__ p, int64_t n, double* sink) {
+    double s = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        double2 v = __ldcs(p + i);
+        s += v.x + v.y;
+    }
+    if (s == 12345.678) *sink = s;
+}
+
+// ------------------------------------------------------------------ DIA (product copy)
+template <int U>
+__global__ void __launch_bounds__(256, 8) dia_cur(int64_t n, int nd, const int64_t* __restrict__ offsets,
+                                                  const double* __restrict__ vals, const double* __restrict__ x,
+                                                  double* __restrict__ y) {
+    __shared__ int64_t off[64];
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) off[d] = offsets[d];
+    __syncthreads();
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    int d0 = 0;
+    for (; d0 + U <= nd; d0 += U) {
+        double v[U], xv[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = i + off[d0 + u];
+            ok[u] = c >= 0 && c < n;
+            const int64_t cc = c < 0 ? 0 : (c >= n ? n - 1 : c);
+            v[u] = lds(vals + int64_t(d0 + u) * n + i);
+            xv[u] = __ldg(x + cc);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = xadd(acc, ok[u] ? xmul(v[u], xv[u]) : -0.0);
+    }
+    for (; d0 < nd; ++d0) {
+        const int64_t c = i + off[d0];
+        if (c >= 0 && c < n) acc = xadd(acc, xmul(lds(vals + int64_t(d0) * n + i), __ldg(x + c)));
+    }
+    y[i] = acc;
+}
+
+// DIA, int32 index math, diag base pointer advanced, all loads of a batch hoisted
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) dia_i32(int n, int nd, const int64_t* __restrict__ offsets,
+                                                     const double* __restrict__ vals, const double* __restrict__ x,
+                                                     double* __restrict__ y) {
+    __shared__ int off[64];
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) off[d] = int(offsets[d]);
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    const double* vp = vals + i;
+    int d0 = 0;
+    for (; d0 + U <= nd; d0 += U) {
+        double v[U], xv[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = i + off[d0 + u];
+            ok[u] = unsigned(c) < unsigned(n);
+            v[u] = lds(vp + size_t(d0 + u) * size_t(n));
+            xv[u] = __ldg(x + (ok[u] ? c : i));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = xadd(acc, ok[u] ? xmul(v[u], xv[u]) : -0.0);
+    }
+    for (; d0 < nd; ++d0) {
+        const int c = i + off[d0];
+        if (unsigned(c) < unsigned(n)) acc = xadd(acc, xmul(lds(vp + size_t(d0) * size_t(n)), __ldg(x + c)));
+    }
+    y[i] = acc;
+}
+
+// ------------------------------------------------------------------ ELL (product copy)
+__global__ void __launch_bounds__(256) ell_cur(int64_t nrows, int width, const int* __restrict__ col,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               double* __restrict__ y) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    constexpr int kU = 4;
+    double s = 0.0;
+    for (int k0 = 0; k0 < width; k0 += kU) {
+        int c[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) c[u] = (k0 + u < width) ? lds(col + int64_t(k0 + u) * nrows + i) : -1;
+        bool live[kU];
+        bool alive = true;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) { alive = alive && c[u] != -1; live[u] = alive; }
+        double p[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) p[u] = live[u] ? xmul(lds(val + int64_t(k0 + u) * nrows + i), __ldg(x + c[u])) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) if (live[u]) s = xadd(s, p[u]);
+        if (!alive) break;
+    }
+    y[i] = s;
+}
+
+// ------------------------------------------------------------------ CSR (product copy)
+template <int IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) csr_cur(const int* __restrict__ grp, const int64_t* __restrict__ grp_k,
+                                                     int64_t ngrp, const int64_t* __restrict__ rp,
+                                                     const int* __restrict__ col, const double* __restrict__ val,
+                                                     const double* __restrict__ x, double* __restrict__ y) {
+    __shared__ double sp[8][32 * IT];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* prod = sp[wid];
+    int64_t g = int64_t(blockIdx.x) * 8 + wid;
+    const int64_t stride = int64_t(gridDim.x) * 8;
+    if (g >= ngrp) return;
+    int r0 = grp[g], r1 = grp[g + 1];
+    int64_t k0 = grp_k[g], k1 = grp_k[g + 1];
+    int c[IT];
+    double v[IT];
+    bool longrow = k1 - k0 > 32 * IT;
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+        const int64_t k = k0 + u * 32 + lane;
+        if (!longrow && k < k1) { c[u] = lds(col + k); v[u] = lds(val + k); }
+    }
+    int64_t pa = 0, pe = 0;
+    if (r0 + lane < r1) { pa = rp[r0 + lane]; pe = rp[r0 + lane + 1]; }
+    while (true) {
+        const int64_t gn = g + stride;
+        int nr0 = 0, nr1 = 0;
+        int64_t nk0 = 0, nk1 = 0;
+        if (gn < ngrp) { nr0 = grp[gn]; nr1 = grp[gn + 1]; nk0 = grp_k[gn]; nk1 = grp_k[gn + 1]; }
+        if (!longrow) {
+#pragma unroll
+            for (int u = 0; u < IT; ++u) {
+                const int64_t k = k0 + u * 32 + lane;
+                if (k < k1) prod[u * 32 + lane] = xmul(v[u], __ldg(x + c[u]));
+            }
+        }
+        __syncwarp();
+        const bool nlong = nk1 - nk0 > 32 * IT;
+        int64_t npa = 0, npe = 0;
+        if (gn < ngrp) {
+#pragma unroll
+            for (int u = 0; u < IT; ++u) {
+                const int64_t k = nk0 + u * 32 + lane;
+                if (!nlong && k < nk1) { c[u] = lds(col + k); v[u] = lds(val + k); }
+            }
+            if (nr0 + lane < nr1) { npa = rp[nr0 + lane]; npe = rp[nr0 + lane + 1]; }
+        }
+        if (!longrow && r0 + lane < r1) {
+            double s = 0.0;
+            for (int64_t j = pa - k0; j < pe - k0; ++j) s = xadd(s, prod[j]);
+            y[r0 + lane] = s;
+        }
+        __syncwarp();
+        if (gn >= ngrp) break;
+        g = gn; r0 = nr0; r1 = nr1; k0 = nk0; k1 = nk1; pa = npa; pe = npe; longrow = nlong;
+    }
+}
+
+// CSR vector: V lanes per row, strided partial sums, xor-tree reduction (NOT the reference order)
+template <int V>
+__global__ void __launch_bounds__(256) csr_vec(int64_t n, const int64_t* __restrict__ rp, const int* __restrict__ col,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               double* __restrict__ y) {
+    const int sub = threadIdx.x & (V - 1);
+    const int64_t row = (int64_t(blockIdx.x) * 256 + threadIdx.x) / V;
+    double s = 0.0;
+    if (row < n) {
+        const int64_t a = rp[row], e = rp[row + 1];
+        int64_t k = a + sub;
+        for (; k + 3 * V < e; k += 4 * V) {
+            int c0 = lds(col + k), c1 = lds(col + k + V), c2 = lds(col + k + 2 * V), c3 = lds(col + k + 3 * V);
+            double v0 = lds(val + k), v1 = lds(val + k + V), v2 = lds(val + k + 2 * V), v3 = lds(val + k + 3 * V);
+            s = xadd(s, xmul(v0, __ldg(x + c0)));
+            s = xadd(s, xmul(v1, __ldg(x + c1)));
+            s = xadd(s, xmul(v2, __ldg(x + c2)));
+            s = xadd(s, xmul(v3, __ldg(x + c3)));
+        }
+        for (; k < e; k += V) s = xadd(s, xmul(lds(val + k), __ldg(x + lds(col + k))));
+    }
+#pragma unroll
+    for (int o = V / 2; o > 0; o >>= 1) s = xadd(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (row < n && sub == 0) y[row] = s;
+}
+
+// ------------------------------------------------------------------ CSR, TMA-staged warp groups (exact)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int MAXE>
+struct TmaStage {
+    double val[MAXE + 2];
+    int col[MAXE + 4];
+    int64_t rp[36];
+};
+
+template <int MAXE>
+__device__ __forceinline__ void tma_issue(TmaStage<MAXE>* st, uint64_t* bar, int r0, int r1, int64_t k0, int64_t k1,
+                                          const int64_t* rp, const int* col, const double* val) {
+    const int64_t va = k0 & ~int64_t(1), vb = (k1 + 1) & ~int64_t(1);
+    const int64_t ca = k0 & ~int64_t(3), cb = (k1 + 3) & ~int64_t(3);
+    const int ra = r0 & ~1, rb = (r1 + 2) & ~1;  // rp[r0..r1] inclusive
+    const uint32_t vbytes = uint32_t(vb - va) * 8, cbytes = uint32_t(cb - ca) * 4, rbytes = uint32_t(rb - ra) * 8;
+    mbar_expect(bar, vbytes + cbytes + rbytes);
+    if (vbytes) tma_1d(st->val, val + va, vbytes, bar);
+    if (cbytes) tma_1d(st->col, col + ca, cbytes, bar);
+    tma_1d(st->rp, rp + ra, rbytes, bar);
+}
+
+template <int MAXE, int S, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) csr_tma(const int* __restrict__ grp, const int64_t* __restrict__ grp_k,
+                                                      int64_t ngrp, const int64_t* __restrict__ rp,
+                                                      const int* __restrict__ col, const double* __restrict__ val,
+                                                      const double* __restrict__ x, double* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    TmaStage<MAXE>* stages = reinterpret_cast<TmaStage<MAXE>*>(smem) + wid * S;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(TmaStage<MAXE>) * S * WARPS) + wid * S;
+    const int64_t stride = int64_t(gridDim.x) * WARPS;
+    int64_t g = int64_t(blockIdx.x) * WARPS + wid;
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) {
+            const int64_t gg = g + s * stride;
+            if (gg < ngrp) tma_issue<MAXE>(&stages[s], &bars[s], grp[gg], grp[gg + 1], grp_k[gg], grp_k[gg + 1], rp, col, val);
+        }
+    }
+    uint32_t phase = 0;
+    int s = 0;
+    for (; g < ngrp; g += stride) {
+        const int r0 = grp[g], r1 = grp[g + 1];
+        const int64_t k0 = grp_k[g], k1 = grp_k[g + 1];
+        mbar_wait(&bars[s], phase);
+        TmaStage<MAXE>* st = &stages[s];
+        const int voff = int(k0 & 1), coff = int(k0 & 3);
+        const int cnt = int(k1 - k0);
+        for (int e = lane; e < cnt; e += 32) st->val[voff + e] = xmul(st->val[voff + e], __ldg(x + st->col[coff + e]));
+        __syncwarp();
+        if (r0 + lane < r1) {
+            const int ro = r0 & 1;
+            const int64_t pa = st->rp[ro + lane], pe = st->rp[ro + lane + 1];
+            const double* p = st->val + voff - k0;
+            double acc = 0.0;
+            for (int64_t j = pa; j < pe; ++j) acc = xadd(acc, p[j]);
+            y[r0 + lane] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t gg = g + S * stride;
+            if (gg < ngrp) {
+                fence_proxy_async();
+                tma_issue<MAXE>(st, &bars[s], grp[gg], grp[gg + 1], grp_k[gg], grp_k[gg + 1], rp, col, val);
+            }
+        }
+        if (++s == S) { s = 0; phase ^= 1; }
+    }
+}
+
+// ------------------------------------------------------------------ CSR, big groups (exact)
+// group = <= 32 rows, <= 32*IT entries (greedy); a row longer than 32*IT is a
+// group of its own flagged long (handled elsewhere, skipped here).
+// Register double buffer of the next group's col/val.
+template <int IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) csr_big(const int* __restrict__ grp, const int64_t* __restrict__ grp_k,
+                                                     int64_t ngrp, const int64_t* __restrict__ rp,
+                                                     const int* __restrict__ col, const double* __restrict__ val,
+                                                     const double* __restrict__ x, double* __restrict__ y) {
+    __shared__ double sp[8][32 * IT + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* prod = sp[wid];
+    int64_t g = int64_t(blockIdx.x) * 8 + wid;
+    const int64_t stride = int64_t(gridDim.x) * 8;
+    if (g >= ngrp) return;
+    int r0 = grp[g], r1 = grp[g + 1];
+    int64_t k0 = grp_k[g];
+    int cnt = int(min(grp_k[g + 1] - k0, int64_t(32 * IT + 1)));
+    int c[IT];
+    double v[IT];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+        const int e = u * 32 + lane;
+        if (e < cnt && cnt <= 32 * IT) { c[u] = lds(col + k0 + e); v[u] = lds(val + k0 + e); }
+    }
+    int pa = 0, pe = 0;
+    if (r0 + lane < r1) { pa = int(rp[r0 + lane] - k0); pe = int(rp[r0 + lane + 1] - k0); }
+    while (true) {
+        const int64_t gn = g + stride;
+        int nr0 = 0, nr1 = 0, ncnt = 0;
+        int64_t nk0 = 0;
+        if (gn < ngrp) { nr0 = grp[gn]; nr1 = grp[gn + 1]; nk0 = grp_k[gn]; ncnt = int(min(grp_k[gn + 1] - nk0, int64_t(32 * IT + 1))); }
+        const bool longrow = cnt > 32 * IT;
+        if (!longrow) {
+#pragma unroll
+            for (int u = 0; u < IT; ++u) {
+                const int e = u * 32 + lane;
+                if (e < cnt) prod[e] = xmul(v[u], __ldg(x + c[u]));
+            }
+        }
+        __syncwarp();
+        int npa = 0, npe = 0;
+        if (gn < ngrp) {
+#pragma unroll
+            for (int u = 0; u < IT; ++u) {
+                const int e = u * 32 + lane;
+                if (e < ncnt && ncnt <= 32 * IT) { c[u] = lds(col + nk0 + e); v[u] = lds(val + nk0 + e); }
+            }
+            if (nr0 + lane < nr1) { npa = int(rp[nr0 + lane] - nk0); npe = int(rp[nr0 + lane + 1] - nk0); }
+        }
+        if (!longrow && r0 + lane < r1) {
+            double s = 0.0;
+            for (int j = pa; j < pe; ++j) s = xadd(s, prod[j]);
+            y[r0 + lane] = s;
+        }
+        __syncwarp();
+        if (gn >= ngrp) break;
+        g = gn; r0 = nr0; r1 = nr1; k0 = nk0; cnt = ncnt; pa = npa; pe = npe;
+    }
+}
+
+// cp.async (LDGSTS) staged big groups: S smem stages per warp, no registers
+// held for in-flight data.
+__device__ __forceinline__ void cpa4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int E>
+struct LgsStage {
+    double val[E];
+    int64_t rp[33];
+    int col[E];
+};
+
+template <int IT>
+__device__ __forceinline__ void lgs_issue(LgsStage<32 * IT>* st, int lane, int r0, int r1, int64_t k0, int64_t k1,
+                                          const int64_t* rp, const int* col, const double* val) {
+    const int cnt = int(k1 - k0);
+    if (cnt <= 32 * IT) {
+        for (int e = lane; e < cnt; e += 32) { cpa4(&st->col[e], col + k0 + e); cpa8(&st->val[e], val + k0 + e); }
+    }
+    if (r0 + lane <= r1) cpa8(&st->rp[lane], rp + r0 + lane);
+    if (lane == 0 && r1 - r0 == 32) cpa8(&st->rp[32], rp + r1);
+}
+
+template <int IT, int S, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) csr_lgs(const int* __restrict__ grp, const int64_t* __restrict__ grp_k,
+                                                            int64_t ngrp, const int64_t* __restrict__ rp,
+                                                            const int* __restrict__ col, const double* __restrict__ val,
+                                                            const double* __restrict__ x, double* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    LgsStage<32 * IT>* st = reinterpret_cast<LgsStage<32 * IT>*>(smem) + wid * S;
+    const int64_t stride = int64_t(gridDim.x) * WARPS;
+    int64_t g = int64_t(blockIdx.x) * WARPS + wid;
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+        const int64_t gg = g + s * stride;
+        if (gg < ngrp) lgs_issue<IT>(&st[s], lane, grp[gg], grp[gg + 1], grp_k[gg], grp_k[gg + 1], rp, col, val);
+        cpa_commit();
+    }
+    int s = 0;
+    for (; g < ngrp; g += stride) {
+        {   // issue group g + (S-1)*stride into stage (s + S - 1) % S
+            const int64_t gg = g + (S - 1) * stride;
+            int sn = s + S - 1; if (sn >= S) sn -= S;
+            if (gg < ngrp) lgs_issue<IT>(&st[sn], lane, grp[gg], grp[gg + 1], grp_k[gg], grp_k[gg + 1], rp, col, val);
+            cpa_commit();
+        }
+        cpa_wait<S - 1>();
+        __syncwarp();
+        const int r0 = grp[g], r1 = grp[g + 1];
+        const int64_t k0 = grp_k[g];
+        const int cnt = int(grp_k[g + 1] - k0);
+        LgsStage<32 * IT>* t = &st[s];
+        if (cnt <= 32 * IT) {
+#pragma unroll 4
+            for (int e = lane; e < cnt; e += 32) t->val[e] = xmul(t->val[e], __ldg(x + t->col[e]));
+            __syncwarp();
+            if (r0 + lane < r1) {
+                const int pa = int(t->rp[lane] - k0), pe = int(t->rp[lane + 1] - k0);
+                double acc = 0.0;
+                for (int j = pa; j < pe; ++j) acc = xadd(acc, t->val[j]);
+                y[r0 + lane] = acc;
+            }
+        }
+        __syncwarp();
+        if (++s == S) s = 0;
+    }
+    cpa_wait<0>();
+}
+
+void groups_big(const struct Csr& m, int cap, std::vector<int>& gr, std::vector<int64_t>& gk);
+
+// ------------------------------------------------------------------ matrices
+struct Csr { int64_t n; std::vector<int64_t> rp; std::vector<int> col; std::vector<double> val; };
+
+Csr banded(int64_t n, int h) {
+    Csr m; m.n = n; m.rp.resize(n + 1); m.rp[0] = 0;
+    m.col.reserve(n * (2 * h + 1)); m.val.reserve(n * (2 * h + 1));
+    for (int64_t i = 0; i < n; ++i) {
+        for (int o = -h; o <= h; ++o) { int64_t j = i + o; if (j >= 0 && j < n) { m.col.push_back(int(j)); m.val.push_back(1.0 + ((i * 7 + j) % 13) / 8.0); } }
+        m.rp[i + 1] = int64_t(m.col.size());
+    }
+    return m;
+}
+Csr lap(int g) {
+    Csr m; m.n = int64_t(g) * g; m.rp.resize(m.n + 1); m.rp[0] = 0;
+    for (int64_t i = 0; i < m.n; ++i) {
+        int64_t x = i % g;
+        int64_t cs[5] = {i - g, i - 1, i, i + 1, i + g};
+        bool ok[5] = {i >= g, x > 0, true, x < g - 1, i < m.n - g};
+        for (int t = 0; t < 5; ++t) if (ok[t]) { m.col.push_back(int(cs[t])); m.val.push_back(t == 2 ? 4.0 : -1.0 - (i % 5) / 8.0); }
+        m.rp[i + 1] = int64_t(m.col.size());
+    }
+    return m;
+}
+// R-MAT scale s, 16*2^s draws, (0.57,0.19,0.19,0.05), duplicates merged
+Csr rmat(int scale, int deg, uint64_t seed) {
+    const int64_t n = int64_t(1) << scale, draws = n * deg;
+    std::mt19937_64 rng(seed);
+    std::vector<uint64_t> keys(draws);
+    for (int64_t e = 0; e < draws; ++e) {
+        uint64_t r = 0, c = 0;
+        for (int l = 0; l < scale; ++l) {
+            double p = (rng() >> 11) * (1.0 / 9007199254740992.0);
+            int q = p < 0.57 ? 0 : p < 0.76 ? 1 : p < 0.95 ? 2 : 3;
+            r = 2 * r + (q >> 1); c = 2 * c + (q & 1);
+        }
+        keys[e] = (r << 32) | c;
+    }
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    Csr m; m.n = n; m.rp.assign(n + 1, 0);
+    m.col.resize(keys.size()); m.val.resize(keys.size());
+    for (size_t k = 0; k < keys.size(); ++k) {
+        m.rp[(keys[k] >> 32) + 1]++;
+        m.col[k] = int(keys[k] & 0xffffffffu);
+        m.val[k] = 1.0 + double(k % 8) / 8.0;
+    }
+    for (int64_t i = 0; i < n; ++i) m.rp[i + 1] += m.rp[i];
+    return m;
+}
+
+void groups(const Csr& m, int W, std::vector<int>& gr, std::vector<int64_t>& gk) {
+    gr.clear(); gk.clear();
+    for (int64_t i = 0; i < m.n; ++i) {
+        int64_t len = m.rp[i + 1] - m.rp[i];
+        bool start = gr.empty() || (i - gr.back()) >= 32 || len > W ||
+                     (i > 0 && ((m.rp[i] / W) != (m.rp[i - 1] / W) || (m.rp[i] - m.rp[i - 1]) > W));
+        if (start) { gr.push_back(int(i)); gk.push_back(m.rp[i]); }
+    }
+    gr.push_back(int(m.n)); gk.push_back(m.rp[m.n]);
+}
+
+void groups_big(const Csr& m, int cap, std::vector<int>& gr, std::vector<int64_t>& gk) {
+    gr.clear(); gk.clear();
+    int64_t i = 0;
+    while (i < m.n) {
+        gr.push_back(int(i)); gk.push_back(m.rp[i]);
+        if (m.rp[i + 1] - m.rp[i] > cap) { ++i; continue; }
+        int64_t j = i + 1;
+        while (j < m.n && j - i < 32 && m.rp[j + 1] - m.rp[i] <= cap) ++j;
+        i = j;
+    }
+    gr.push_back(int(m.n)); gk.push_back(m.rp[m.n]);
+}
+
+// ------------------------------------------------------------------ harness
+static double* g_flush;
+static const size_t kFlush = size_t(512) << 20;
+static double* g_sink;
+
+void do_flush(int mode, int r) {
+    if (mode == 1) CK(cudaMemsetAsync(g_flush, r & 0xff, kFlush));
+    if (mode == 2) read_flush<<<148 * 8, 256>>>(reinterpret_cast<const double2*>(g_flush), int64_t(kFlush / 16), g_sink);
+}
+
+float timeit(const std::function<void()>& f, int mode, int reps = 20) {
+    if (const char* e = getenv("LAB_REPS")) reps = atoi(e);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float tot = 0;
+    for (int r = 0; r < reps + 3; ++r) {
+        do_flush(mode, r);
+        cudaEventRecord(e0); f(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (r >= 3) tot += ms;
+    }
+    CK(cudaGetLastError());
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return tot / reps;
+}
+
+const char* kMode[3] = {"none", "write", "read"};
+double PEAK = 6539.5;
+
+void report(const char* name, double bytes, const std::function<void()>& f, const std::function<std::string()>& check) {
+    printf("  %-28s", name);
+    for (int mode : {2, 0, 1}) {
+        float ms = timeit(f, mode);
+        printf("  %s %7.1fus %5.0fGB/s %.3f", kMode[mode], ms * 1e3, bytes / (ms * 1e-3) / 1e9, bytes / (ms * 1e-3) / 1e9 / PEAK);
+    }
+    printf("  %s\n", check().c_str());
+    fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+    const char* which = argc > 1 ? argv[1] : "band,lap,rmat";
+    if (const char* p = getenv("LAB_PEAK")) PEAK = atof(p);
+    int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaMalloc(&g_flush, kFlush)); CK(cudaMalloc(&g_sink, 8));
+    CK(cudaMemset(g_flush, 0, kFlush));
+    struct Case { const char* name; Csr m; };
+    std::vector<Case> cases;
+    if (strstr(which, "band")) cases.push_back({"banded 4M x27", banded(4000000, 13)});
+    if (strstr(which, "lap")) cases.push_back({"laplacian 1000^2", lap(1000)});
+    if (strstr(which, "rmat")) cases.push_back({"rmat 2^22 d16", rmat(22, 16, 42)});
+    for (auto& cs : cases) {
+        Csr& m = cs.m;
+        const int64_t n = m.n, z = m.rp[n];
+        std::vector<double> hx(n);
+        for (int64_t i = 0; i < n; ++i) hx[i] = 0.25 + (i % 97) / 128.0;
+        std::vector<double> yr(n);
+        for (int64_t i = 0; i < n; ++i) { double s = 0; for (int64_t k = m.rp[i]; k < m.rp[i + 1]; ++k) s += m.val[k] * hx[m.col[k]]; yr[i] = s; }
+        int64_t maxlen = 0;
+        for (int64_t i = 0; i < n; ++i) maxlen = std::max(maxlen, m.rp[i + 1] - m.rp[i]);
+        int64_t *drp; int* dcol; double *dval, *dx, *dy;
+        CK(cudaMalloc(&drp, (n + 4) * 8)); CK(cudaMalloc(&dcol, (z + 8) * 4)); CK(cudaMalloc(&dval, (z + 4) * 8));
+        CK(cudaMalloc(&dx, n * 8)); CK(cudaMalloc(&dy, n * 8));
+        CK(cudaMemcpy(drp, m.rp.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dcol, m.col.data(), z * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dval, m.val.data(), z * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dx, hx.data(), n * 8, cudaMemcpyHostToDevice));
+        std::vector<double> yy(n);
+        auto check = [&](bool exact, int64_t skip_longer) {
+            return [&, exact, skip_longer]() {
+                CK(cudaMemcpy(yy.data(), dy, n * 8, cudaMemcpyDeviceToHost));
+                int64_t bad = 0; double worst = 0;
+                for (int64_t i = 0; i < n; ++i) {
+                    if (m.rp[i + 1] - m.rp[i] > skip_longer) continue;
+                    double e = std::fabs(yy[i] - yr[i]) / std::max(1.0, std::fabs(yr[i]));
+                    worst = std::max(worst, e);
+                    bad += exact ? (yy[i] != yr[i]) : (e > 1e-12);
+                }
+                char b[96]; snprintf(b, 96, "%s bad=%lld worst=%.1e", exact ? "exact" : "tol", (long long)bad, worst);
+                return std::string(b);
+            };
+        };
+        printf("%s: n=%lld z=%lld maxlen=%lld\n", cs.name, (long long)n, (long long)z, (long long)maxlen);
+        const double csr_bytes = z * 12.0 + (n + 1) * 8.0 + 16.0 * n;
+        // --- CSR
+        const bool only_prod = getenv("LAB_ONLY_PROD") != nullptr;
+        if (!only_prod) {
+            std::vector<int> gr; std::vector<int64_t> gk; groups(m, 256, gr, gk);
+            const int64_t ng = int64_t(gr.size()) - 1;
+            int* dgr; int64_t* dgk;
+            CK(cudaMalloc(&dgr, gr.size() * 4)); CK(cudaMalloc(&dgk, gk.size() * 8));
+            CK(cudaMemcpy(dgr, gr.data(), gr.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dgk, gk.data(), gk.size() * 8, cudaMemcpyHostToDevice));
+            report("csr_cur IT16 B3 W256", csr_bytes, [&] { csr_cur<16, 3><<<sms * 3, 256>>>(dgr, dgk, ng, drp, dcol, dval, dx, dy); }, check(true, 512));
+            cudaFree(dgr); cudaFree(dgk);
+        }
+        auto big = [&](int IT, auto kern, int minb, const char* tag) {
+            std::vector<int> gr; std::vector<int64_t> gk; groups_big(m, 32 * IT, gr, gk);
+            const int64_t ng = int64_t(gr.size()) - 1;
+            int* dgr; int64_t* dgk;
+            CK(cudaMalloc(&dgr, gr.size() * 4)); CK(cudaMalloc(&dgk, gk.size() * 8));
+            CK(cudaMemcpy(dgr, gr.data(), gr.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dgk, gk.data(), gk.size() * 8, cudaMemcpyHostToDevice));
+            char nm[64]; snprintf(nm, 64, "csr_big IT%d B%d %s ng=%lld", IT, minb, tag, (long long)ng);
+            report(nm, csr_bytes, [&] { kern<<<sms * minb, 256>>>(dgr, dgk, ng, drp, dcol, dval, dx, dy); }, check(true, 32 * IT));
+            cudaFree(dgr); cudaFree(dgk);
+        };
+        if (!only_prod) {
+        big(8, csr_big<8, 4>, 4, "");
+        big(8, csr_big<8, 5>, 5, "");
+        big(12, csr_big<12, 3>, 3, "");
+        big(16, csr_big<16, 3>, 3, "");
+        big(20, csr_big<20, 2>, 2, "");
+        auto lgs = [&](int IT, int S, auto kern, const char* tag) {
+            std::vector<int> gr; std::vector<int64_t> gk; groups_big(m, 32 * IT, gr, gk);
+            const int64_t ng = int64_t(gr.size()) - 1;
+            int* dgr; int64_t* dgk;
+            CK(cudaMalloc(&dgr, gr.size() * 4)); CK(cudaMalloc(&dgk, gk.size() * 8));
+            CK(cudaMemcpy(dgr, gr.data(), gr.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dgk, gk.data(), gk.size() * 8, cudaMemcpyHostToDevice));
+            const size_t st = (size_t(32 * IT) * 12 + 33 * 8 + 15) / 16 * 16;
+            const size_t sm = st * S * 4;
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            int per = std::min(16, int(228000 / (sm + 1024)));
+            char nm[64]; snprintf(nm, 64, "csr_lgs IT%d S%d w4 x%d %s", IT, S, per, tag);
+            report(nm, csr_bytes, [&] { kern<<<sms * per, 128, sm>>>(dgr, dgk, ng, drp, dcol, dval, dx, dy); }, check(true, 32 * IT));
+            cudaFree(dgr); cudaFree(dgk);
+        };
+        lgs(8, 3, csr_lgs<8, 3, 4, 1>, "");
+        lgs(8, 4, csr_lgs<8, 4, 4, 1>, "");
+        lgs(16, 2, csr_lgs<16, 2, 4, 1>, "");
+        lgs(16, 3, csr_lgs<16, 3, 4, 1>, "");
+        lgs(32, 2, csr_lgs<32, 2, 4, 1>, "");
+        }
+        // --- the product library on the same matrix (all formats it can build)
+        {
+            so_matrix* pc = nullptr;
+            if (so_matrix_import_csr_device(n, n, z, drp, dcol, dval, &pc) != SO_OK) { printf("import: %s\n", so_last_error()); }
+            cudaStream_t ps = (cudaStream_t)so_default_stream();
+            const char* fn[6] = {"COO", "CSR", "DIA", "ELL", "HYB", "HDC"};
+            for (int f = 0; f < 6 && pc; ++f) {
+                so_matrix* pm = nullptr;
+                if (so_convert(pc, f, nullptr, &pm) != SO_OK) { printf("  prod %s: %s\n", fn[f], so_last_error()); continue; }
+                const double pb = double(so_spmv_bytes(pm));
+                char nm[64]; snprintf(nm, 64, "prod %s", fn[f]);
+                report(nm, pb, [&] {
+                    cudaEvent_t a; cudaEventCreate(&a); cudaEventRecord(a, 0); cudaStreamWaitEvent(ps, a, 0);
+                    so_spmv_device(pm, dx, dy, ps);
+                    cudaEvent_t b; cudaEventCreate(&b); cudaEventRecord(b, ps); cudaStreamWaitEvent(0, b, 0);
+                    cudaEventDestroy(a); cudaEventDestroy(b);
+                }, [&] { cudaStreamSynchronize(ps); return check(f == 1 || f == 5, 512)(); });
+                so_matrix_free(pm);
+            }
+            if (pc) so_matrix_free(pc);
+        }
+        if (!only_prod) {
+        report("csr_vec V4", csr_bytes, [&] { csr_vec<4><<<unsigned((n * 4 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
+        report("csr_vec V8", csr_bytes, [&] { csr_vec<8><<<unsigned((n * 8 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
+        report("csr_vec V16", csr_bytes, [&] { csr_vec<16><<<unsigned((n * 16 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
+        }
+        // --- DIA / ELL for the banded case
+        if (!only_prod && maxlen <= 27 && std::string(cs.name).find("banded") != std::string::npos) {
+            const int h = 13, nd = 2 * h + 1;
+            std::vector<int64_t> off(nd);
+            for (int d = 0; d < nd; ++d) off[d] = d - h;
+            std::vector<double> dv(size_t(nd) * n, 0.0);
+            std::vector<int> ec(size_t(nd) * n, -1);
+            std::vector<double> ev(size_t(nd) * n, 0.0);
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t k = m.rp[i]; k < m.rp[i + 1]; ++k) {
+                    const int d = int(m.col[k] - i + h);
+                    dv[size_t(d) * n + i] = m.val[k];
+                    const int slot = int(k - m.rp[i]);
+                    ec[size_t(slot) * n + i] = m.col[k];
+                    ev[size_t(slot) * n + i] = m.val[k];
+                }
+            int64_t* doff; double* ddv; int* dec; double* dev;
+            CK(cudaMalloc(&doff, nd * 8)); CK(cudaMalloc(&ddv, dv.size() * 8));
+            CK(cudaMemcpy(doff, off.data(), nd * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ddv, dv.data(), dv.size() * 8, cudaMemcpyHostToDevice));
+            double dia_bytes = 0;
+            for (int d = 0; d < nd; ++d) dia_bytes += 8.0 * double(std::min<int64_t>(n, n - off[d]) - std::max<int64_t>(0, -off[d]));
+            dia_bytes += 8.0 * nd + 16.0 * n;
+            const unsigned gb = unsigned((n + 255) / 256);
+            report("dia_cur U8", dia_bytes, [&] { dia_cur<8><<<gb, 256>>>(n, nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
+            report("dia_i32 U8 B8", dia_bytes, [&] { dia_i32<8, 8><<<gb, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
+            report("dia_i32 U9 B6", dia_bytes, [&] { dia_i32<9, 6><<<gb, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
+            report("dia_i32 U14 B4", dia_bytes, [&] { dia_i32<14, 4><<<gb, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
+            cudaFree(ddv);
+            CK(cudaMalloc(&dec, ec.size() * 4)); CK(cudaMalloc(&dev, ev.size() * 8));
+            CK(cudaMemcpy(dec, ec.data(), ec.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dev, ev.data(), ev.size() * 8, cudaMemcpyHostToDevice));
+            int64_t short_rows = 0;
+            for (int64_t i = 0; i < n; ++i) short_rows += (m.rp[i + 1] - m.rp[i]) < nd;
+            const double ell_bytes = 12.0 * z + 4.0 * short_rows + 16.0 * n;
+            report("ell_cur", ell_bytes, [&] { ell_cur<<<gb, 256>>>(n, nd, dec, dev, dx, dy); }, check(true, 1 << 30));
+            cudaFree(dec); cudaFree(dev); cudaFree(doff);
+        }
+        cudaFree(drp); cudaFree(dcol); cudaFree(dval); cudaFree(dx); cudaFree(dy);
+    }
+    return 0;
+}

@@ -344,7 +344,8 @@ def _structured(so, O, csr, ratio=0.2, formats=range(6)):
         m = d.convert(f)
         cmp_host(m.download(), want, f"fmt {f}")
         y, y_ref = m.spmv(x), O.oc_spmv(want, x)
-        if f in EXACT_FORMATS and np.diff(csr.row_ptr).max(initial=0) <= 2048:
+        # CSR rows up to the warp-group cap (>= 256 entries) keep the reference order
+        if f in EXACT_FORMATS and np.diff(csr.row_ptr).max(initial=0) <= 256:
             assert np.array_equal(y, y_ref), f
         else:
             assert max_rel(y, y_ref) <= SPMV_TOL, f
@@ -386,6 +387,29 @@ def test_hdc_with_long_rows(so, O):
         m = d.from_coo(f)
         cmp_host(m.download(), want, f"fmt {f}")
         assert max_rel(m.spmv(x), O.oc_spmv(want, x)) <= SPMV_TOL, f
+
+
+def test_pipelined_host_spmv_pinned(so, O):
+    """spmv(m, x) with pinned host buffers on a DIA-window matrix runs the
+    row-chunk pipeline (x windows up / chunks / y chunks down on two copy
+    streams): bit-identical to the oracle and to the one-shot path."""
+    import torch
+    from paper_2303_05098_b200 import synth
+
+    csr = synth.banded(700_000, 13, seed=2)
+    coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
+    d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+    xt = torch.empty(csr.ncols, dtype=torch.float64).pin_memory()
+    yt = torch.empty(csr.nrows, dtype=torch.float64).pin_memory()
+    xn, yn = xt.numpy(), yt.numpy()
+    xn[:] = np.random.default_rng(11).uniform(-1, 1, csr.ncols)
+    for f in (so.DIA, so.HDC):
+        m = d.convert(f)
+        want = O.oc_spmv(O.oc_convert(coo, f), xn)
+        yn[:] = np.nan
+        m.spmv_into(xn, yn)
+        assert np.array_equal(yn, want), f
+        assert np.array_equal(m.spmv(xn.copy()), want), f  # pageable -> one-shot path
 
 
 def test_stencil27_generator_and_row_slices(so, O):
