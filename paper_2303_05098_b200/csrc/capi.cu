@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <atomic>
 // extern "C" boundary (include/sparseoracle_b200.h): argument validation with
 // the reference's error types/messages, H2D/D2H staging between the
@@ -349,7 +350,11 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
     }
     Context& c = ctx(m.device);
     const int64_t n = m.nrows, nc = m.ncols;
-    const int64_t nchunks = std::min<int64_t>(16, ceil_div(n, kPipeRows));
+    static const int64_t max_chunks = [] {
+        const char* e = std::getenv("SOB_PIPE_CHUNKS");  // tuning knob (default 16)
+        return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(16);
+    }();
+    const int64_t nchunks = std::min<int64_t>(max_chunks, ceil_div(n, kPipeRows));
     const int64_t rows_per = ceil_div(n, nchunks);
     DBuf<double> dx(nc, s), dy(n, s);
     thread_local std::vector<cudaEvent_t> ev;

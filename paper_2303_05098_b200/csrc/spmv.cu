@@ -284,24 +284,28 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- COO -------
-// Segmented reduction over the row-sorted canonical COO, one warp per fixed
-// chunk of kCooChunk entries (perfect balance whatever the row-length skew).
-// Lane l owns kCooItems CONSECUTIVE entries (256-bit streaming loads of row/
-// col/val: each warp instruction covers 1 KB contiguous, L1 left to x),
-// gathers x and forms the rounded products.  Pass 1 sums the lane's
-// last row piece; one warp-wide segmented scan keyed on that row joins pieces
+// Segmented reduction over the row-sorted canonical COO.  The entries are cut
+// into fixed chunks of kCooChunk (perfect balance whatever the row-length
+// skew); a persistent warp walks chunks g, g + W, g + 2W, ... and issues the
+// NEXT chunk's loads before reducing the current one, so each warp keeps one
+// chunk of HBM reads in flight behind its x gathers and shuffles.
+// Lane l owns kCooItems CONSECUTIVE entries of a chunk (256-bit streaming
+// loads of row/col/val: a warp instruction covers 1 KB contiguous, L1 left to
+// x), gathers x and forms the rounded products.  Pass 1 sums the lane's last
+// row piece; one warp-wide segmented scan keyed on that row joins pieces
 // across lanes (rows are sorted, so equal keys are contiguous); pass 2 walks
-// the lane's entries sequentially starting from the carry of earlier lanes,
-// so a row spanning at most two lanes is summed in the reference's order
+// the lane's entries sequentially from the carry of earlier lanes, so a row
+// spanning at most two lanes is summed in the reference's order
 // (spmv.cpp:21-30).  Rows that start and end inside the chunk are written
 // directly; pieces of rows spanning chunks go to per-chunk records combined
 // by coo_fixup in chunk order.  Fixed partition and combine order =>
 // deterministic, within the 1e-12 contract.  Empty rows are zero-filled by
 // the lane holding the next row's first entry (y written exactly once).
 // ACCUM (HYB COO part, spmv.cpp:95-100): the row sum is added to the ELL
-// result already in y.
+// result already in y.  Variants measured in scripts/spmv_lab.cu.
 constexpr int kCooItems = 8;
 constexpr int kCooChunk = 32 * kCooItems;
+constexpr int kCooPerSm = 3;
 
 struct CooChunkRec {
     double first_sum;  // in-chunk piece of a row that began in an earlier chunk
@@ -310,44 +314,35 @@ struct CooChunkRec {
     int32_t flags;
 };
 enum : int32_t { kFirstCont = 1, kLastOpen = 2, kSingle = 4 };
+constexpr int kNoRow = 0x7fffffff;
 
-template <bool ACCUM>
-__global__ void __launch_bounds__(256, 4)
-    coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
-                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                    CooChunkRec* __restrict__ rec) {
-    constexpr int IT = kCooItems;
-    constexpr int kNoRow = 0x7fffffff;
-    constexpr unsigned kFull = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t base = chunk * kCooChunk;
-    if (base >= z) return;
-    const int cnt = int(z - base < kCooChunk ? z - base : int64_t(kCooChunk));
-    const int first = lane * IT;
-    const int64_t k = base + first;
-    const int nmine = cnt - first <= 0 ? 0 : (cnt - first >= IT ? IT : cnt - first);
-    int r[IT], c[IT];
-    double p[IT];
-    if (nmine == IT) {
+__device__ __forceinline__ void coo_load(const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                                         const double* __restrict__ val, int64_t k, int rem,
+                                         int (&r)[kCooItems], int (&c)[kCooItems], double (&v)[kCooItems]) {
+    if (rem >= kCooItems) {
         ld_stream_v8(row + k, r);
         ld_stream_v8(col + k, c);
-        ld_stream_v4(val + k, p);
-        ld_stream_v4(val + k + 4, p + 4);
+        ld_stream_v4(val + k, v);
+        ld_stream_v4(val + k + 4, v + 4);
     } else {
 #pragma unroll
-        for (int j = 0; j < IT; ++j) {
-            const bool ok = j < nmine;
+        for (int j = 0; j < kCooItems; ++j) {
+            const bool ok = j < rem;
             r[j] = ok ? row[k + j] : kNoRow;
             c[j] = ok ? col[k + j] : 0;
-            p[j] = ok ? val[k + j] : 0.0;
+            v[j] = ok ? val[k + j] : 0.0;
         }
     }
-    const int prev_row = base > 0 ? row[base - 1] : -1;
-    const int next_row = base + cnt < z ? row[base + cnt] : -1;
-#pragma unroll
-    for (int j = 0; j < IT; ++j) p[j] = j < nmine ? fmul(p[j], __ldg(x + c[j])) : 0.0;
+}
 
+template <bool ACCUM>
+__device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base, int cnt, int64_t z, int64_t nrows,
+                                           const int (&r)[kCooItems], const double (&p)[kCooItems], int prev_row,
+                                           int next_row, double* __restrict__ y, CooChunkRec* __restrict__ rec) {
+    constexpr int IT = kCooItems;
+    constexpr unsigned kFull = 0xffffffffu;
+    const int first = lane * IT;
+    const int nmine = cnt - first <= 0 ? 0 : (cnt - first >= IT ? IT : cnt - first);
     // pass 1: the lane's last row piece (kNoRow pieces of idle lanes never match)
     int tr = kNoRow;
 #pragma unroll
@@ -412,8 +407,46 @@ __global__ void __launch_bounds__(256, 4)
     }
 }
 
+template <bool ACCUM>
+__global__ void __launch_bounds__(256, kCooPerSm)
+    coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                    CooChunkRec* __restrict__ rec) {
+    constexpr int IT = kCooItems;
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = (z + kCooChunk - 1) / kCooChunk;
+    const int64_t stride = int64_t(gridDim.x) * (blockDim.x >> 5);
+    int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (chunk >= nchunks) return;
+    int r[IT], c[IT];
+    double v[IT];
+    coo_load(row, col, val, chunk * kCooChunk + lane * IT, int(min(z - chunk * kCooChunk, int64_t(kCooChunk))) - lane * IT,
+             r, c, v);
+    while (true) {
+        const int64_t base = chunk * kCooChunk;
+        const int cnt = int(min(z - base, int64_t(kCooChunk)));
+        double p[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? fmul(v[j], __ldg(x + c[j])) : 0.0;
+        const int prev_row = base > 0 ? row[base - 1] : -1;
+        const int next_row = base + cnt < z ? row[base + cnt] : -1;
+        int rc[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) rc[j] = r[j];
+        const int64_t nx = chunk + stride;
+        if (nx < nchunks)
+            coo_load(row, col, val, nx * kCooChunk + lane * IT, int(min(z - nx * kCooChunk, int64_t(kCooChunk))) - lane * IT,
+                     r, c, v);
+        coo_finish<ACCUM>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
+        if (nx >= nchunks) break;
+        chunk = nx;
+    }
+}
+
 // Rows spanning chunks: the chunk holding the row's first entry walks forward
-// in chunk order (deterministic) and writes the final value.
+// in chunk order (deterministic) and writes the final value; records are
+// fetched 8 at a time so a row spanning hundreds of chunks (R-MAT hubs) is
+// not one dependent load per chunk.
 template <bool ACCUM>
 __global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, double* __restrict__ y) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -421,9 +454,24 @@ __global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, 
     const int32_t f = rec[c].flags;
     if (!(f & kLastOpen) || (f & kSingle)) return;
     double t = rec[c].last_sum;
-    for (int64_t j = c + 1; j < nchunks; ++j) {
-        t = fadd(t, rec[j].first_sum);
-        if (!(rec[j].flags & kSingle)) break;
+    for (int64_t j0 = c + 1; j0 < nchunks; j0 += 8) {
+        double fs[8];
+        int32_t fl[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t j = j0 + u < nchunks ? j0 + u : nchunks - 1;
+            fs[u] = rec[j].first_sum;
+            fl[u] = rec[j].flags;
+        }
+        bool done = false;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (!done && j0 + u < nchunks) {
+                t = fadd(t, fs[u]);
+                if (!(fl[u] & kSingle)) done = true;
+            }
+        }
+        if (done) break;
     }
     const int32_t r = rec[c].last_row;
     y[r] = ACCUM ? fadd(y[r], t) : t;
@@ -433,8 +481,9 @@ template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
     DBuf<CooChunkRec> rec(nchunks, s);
-    coo_warp_kernel<ACCUM><<<unsigned(ceil_div(nchunks, 8)), 256, 0, s>>>(
-        coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y, rec.get());
+    const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * kCooPerSm));
+    coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
+                                                rec.get());
     SOB_LAUNCH("coo_warp_kernel");
     coo_fixup<ACCUM><<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y);
     SOB_LAUNCH("coo_fixup");

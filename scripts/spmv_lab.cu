@@ -449,6 +449,318 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) csr_lgs(const int* __restric
 
 void groups_big(const struct Csr& m, int cap, std::vector<int>& gr, std::vector<int64_t>& gk);
 
+// ------------------------------------------------------------------ COO variants
+struct CooRec { double first_sum, last_sum; int last_row, flags; };
+enum : int { kFC = 1, kLO = 2, kSG = 4 };
+__device__ __forceinline__ void ldv8(const int* p, int (&v)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "l"(p));
+}
+__device__ __forceinline__ void ldv4(const double* p, double* v) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+// blocked finish: lane owns entries [IT*lane, IT*lane+IT) of the chunk
+template <int IT>
+__device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base, int cnt, int64_t z, int64_t nrows,
+                                           const int (&r)[IT], const double (&p)[IT], int prev_row, int next_row,
+                                           double* __restrict__ y, CooRec* __restrict__ rec) {
+    constexpr int kNoRow = 0x7fffffff;
+    const int first = lane * IT;
+    const int nmine = cnt - first <= 0 ? 0 : (cnt - first >= IT ? IT : cnt - first);
+    int tr = kNoRow;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) if (j < nmine) tr = r[j];
+    double tsum = 0.0;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) if (j < nmine && r[j] == tr) tsum = xadd(tsum, p[j]);
+    double inc = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double up = __shfl_up_sync(~0u, inc, o);
+        const int ur = __shfl_up_sync(~0u, tr, o);
+        if (lane >= o && ur == tr) inc = xadd(up, inc);
+    }
+    const double prev_inc = __shfl_up_sync(~0u, inc, 1);
+    const int prev_tr = __shfl_up_sync(~0u, tr, 1);
+    const int nlane_r0 = __shfl_down_sync(~0u, r[0], 1);
+    const int first_row = __shfl_sync(~0u, r[0], 0);
+    const bool first_cont = first_row == prev_row;
+    if (nmine == 0) return;
+    int prv = lane == 0 ? prev_row : prev_tr;
+    double acc = (lane > 0 && prev_tr == r[0]) ? prev_inc : 0.0;
+    const bool chunk_end = first + nmine == cnt;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+        if (j < nmine) {
+            const int rw = r[j];
+            if (rw != prv) {
+                for (int q = prv + 1; q < rw; ++q) y[q] = 0.0;
+                if (j > 0) acc = 0.0;
+            }
+            acc = xadd(acc, p[j]);
+            const int nxt = j + 1 < nmine ? r[j + 1] : (chunk_end ? next_row : nlane_r0);
+            const bool orphan = first_cont && rw == first_row;
+            if (rw != nxt) {
+                if (orphan) rec[chunk].first_sum = acc; else y[rw] = acc;
+            }
+            if (chunk_end && j + 1 == nmine) {
+                const bool open = rw == nxt;
+                if (open) { rec[chunk].last_sum = acc; rec[chunk].last_row = rw; if (orphan) rec[chunk].first_sum = acc; }
+                rec[chunk].flags = (first_cont ? kFC : 0) | (open ? kLO : 0) | ((open && orphan) ? kSG : 0);
+                if (base + cnt == z) for (int64_t q = int64_t(rw) + 1; q < nrows; ++q) y[q] = 0.0;
+            }
+            prv = rw;
+        }
+    }
+}
+
+__global__ void coo_fix(int64_t nchunks, const CooRec* __restrict__ rec, double* __restrict__ y) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const int f = rec[c].flags;
+    if (!(f & kLO) || (f & kSG)) return;
+    double t = rec[c].last_sum;
+    for (int64_t j = c + 1; j < nchunks; ++j) { t = xadd(t, rec[j].first_sum); if (!(rec[j].flags & kSG)) break; }
+    y[rec[c].last_row] = t;
+}
+
+// walk prefetching 8 records at a time (same combine order)
+__global__ void coo_fix8(int64_t nchunks, const CooRec* __restrict__ rec, double* __restrict__ y) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const int f = rec[c].flags;
+    if (!(f & kLO) || (f & kSG)) return;
+    double t = rec[c].last_sum;
+    for (int64_t j0 = c + 1; j0 < nchunks; j0 += 8) {
+        double fs[8]; int fl[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { const int64_t j = j0 + u < nchunks ? j0 + u : nchunks - 1; fs[u] = rec[j].first_sum; fl[u] = rec[j].flags; }
+        bool done = false;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (!done && j0 + u < nchunks) { t = xadd(t, fs[u]); if (!(fl[u] & kSG)) done = true; }
+        }
+        if (done) break;
+    }
+    y[rec[c].last_row] = t;
+}
+
+template <int IT>
+__device__ __forceinline__ void ld_blk(const int* row, const int* col, const double* val, int64_t k, int rem,
+                                       int (&r)[IT], int (&c)[IT], double (&v)[IT]) {
+    if (rem >= IT) {
+        if constexpr (IT == 8) { ldv8(row + k, r); ldv8(col + k, c); ldv4(val + k, v); ldv4(val + k + 4, v + 4); }
+        else {
+#pragma unroll
+            for (int h = 0; h < IT / 4; ++h) {
+                int4 a = __ldg(reinterpret_cast<const int4*>(row + k) + h), b = __ldg(reinterpret_cast<const int4*>(col + k) + h);
+                r[4*h] = a.x; r[4*h+1] = a.y; r[4*h+2] = a.z; r[4*h+3] = a.w;
+                c[4*h] = b.x; c[4*h+1] = b.y; c[4*h+2] = b.z; c[4*h+3] = b.w;
+            }
+#pragma unroll
+            for (int h = 0; h < IT / 2; ++h) { double2 d = __ldg(reinterpret_cast<const double2*>(val + k) + h); v[2*h] = d.x; v[2*h+1] = d.y; }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < IT; ++j) { bool ok = j < rem; r[j] = ok ? row[k + j] : 0x7fffffff; c[j] = ok ? col[k + j] : 0; v[j] = ok ? val[k + j] : 0.0; }
+    }
+}
+
+// (a) blocked loads + blocked gathers, one chunk per warp
+template <int IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) coo_blk(int64_t z, int64_t nrows, const int* __restrict__ row,
+        const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
+        double* __restrict__ y, CooRec* __restrict__ rec) {
+    constexpr int CH = 32 * IT;
+    const int lane = threadIdx.x & 31;
+    const int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t base = chunk * CH;
+    if (base >= z) return;
+    const int cnt = int(min(z - base, int64_t(CH)));
+    int r[IT], c[IT]; double p[IT];
+    ld_blk<IT>(row, col, val, base + lane * IT, cnt - lane * IT, r, c, p);
+    const int prev_row = base > 0 ? row[base - 1] : -1;
+    const int next_row = base + cnt < z ? row[base + cnt] : -1;
+#pragma unroll
+    for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? xmul(p[j], __ldg(x + c[j])) : 0.0;
+    coo_finish<IT>(lane, chunk, base, cnt, z, nrows, r, p, prev_row, next_row, y, rec);
+}
+
+// (c) persistent, blocked, next chunk prefetched before the finish
+template <int IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) coo_pf(int64_t z, int64_t nrows, const int* __restrict__ row,
+        const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
+        double* __restrict__ y, CooRec* __restrict__ rec) {
+    constexpr int CH = 32 * IT;
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = (z + CH - 1) / CH;
+    const int64_t stride = int64_t(gridDim.x) * 8;
+    int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (chunk >= nchunks) return;
+    int r[IT], c[IT]; double v[IT];
+    ld_blk<IT>(row, col, val, chunk * CH + lane * IT, int(min(z - chunk * CH, int64_t(CH))) - lane * IT, r, c, v);
+    while (true) {
+        const int64_t base = chunk * CH;
+        const int cnt = int(min(z - base, int64_t(CH)));
+        double p[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? xmul(v[j], __ldg(x + c[j])) : 0.0;
+        const int prev_row = base > 0 ? row[base - 1] : -1;
+        const int next_row = base + cnt < z ? row[base + cnt] : -1;
+        int rc[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) rc[j] = r[j];
+        const int64_t nx = chunk + stride;
+        if (nx < nchunks) ld_blk<IT>(row, col, val, nx * CH + lane * IT, int(min(z - nx * CH, int64_t(CH))) - lane * IT, r, c, v);
+        coo_finish<IT>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
+        if (nx >= nchunks) break;
+        chunk = nx;
+    }
+}
+
+// (d) persistent warps over CONTIGUOUS chunk ranges: the open row of a chunk
+// is carried in registers into the warp's next chunk (no per-chunk records),
+// next chunk prefetched; one boundary record per warp, fixed up by the last
+// CTA to finish (ticket) -> a single launch.
+struct WarpRec { double first_sum, last_sum; int first_row, last_row, flags, pad; };
+enum : int { kWFirstCont = 1, kWSingle = 2, kWFirstEnded = 4 };
+
+template <int IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) coo_seq(int64_t z, int64_t nrows, const int* __restrict__ row,
+        const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
+        double* __restrict__ y, WarpRec* __restrict__ wrec, unsigned* __restrict__ ticket, int nw) {
+    constexpr int CH = 32 * IT;
+    constexpr int kNoRow = 0x7fffffff;
+    const int lane = threadIdx.x & 31;
+    const int w = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int64_t nchunks = (z + CH - 1) / CH;
+    if (w < nw) {
+        const int64_t c0 = nchunks * w / nw, c1 = nchunks * (w + 1) / nw;
+        int r[IT], c[IT]; double v[IT];
+        ld_blk<IT>(row, col, val, c0 * CH + lane * IT, int(min(z - c0 * CH, int64_t(CH))) - lane * IT, r, c, v);
+        const int range_prev = c0 > 0 ? row[c0 * CH - 1] : -1;
+        int carry_row = range_prev;     // row of the open segment (or the last row seen)
+        double carry = 0.0;
+        bool orphan_open = c0 > 0;       // carry row began in an earlier warp's range
+        int first_row_w = kNoRow;
+        bool first_ended = false;
+        double first_sum = 0.0;
+        for (int64_t ch = c0; ch < c1; ++ch) {
+            const int64_t base = ch * CH;
+            const int cnt = int(min(z - base, int64_t(CH)));
+            double p[IT];
+#pragma unroll
+            for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? xmul(v[j], __ldg(x + c[j])) : 0.0;
+            int rc[IT];
+#pragma unroll
+            for (int j = 0; j < IT; ++j) rc[j] = r[j];
+            if (ch + 1 < c1) ld_blk<IT>(row, col, val, (ch + 1) * CH + lane * IT, int(min(z - (ch + 1) * CH, int64_t(CH))) - lane * IT, r, c, v);
+            if (ch == c0) first_row_w = __shfl_sync(~0u, rc[0], 0);
+            // ---- finish chunk with incoming carry
+            const int first = lane * IT;
+            const int nmine = cnt - first <= 0 ? 0 : (cnt - first >= IT ? IT : cnt - first);
+            int tr = kNoRow;
+#pragma unroll
+            for (int j = 0; j < IT; ++j) if (j < nmine) tr = rc[j];
+            double tsum = (lane == 0 && rc[0] == carry_row && tr == carry_row) ? carry : 0.0;
+#pragma unroll
+            for (int j = 0; j < IT; ++j) if (j < nmine && rc[j] == tr) tsum = xadd(tsum, p[j]);
+            double inc = tsum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double up = __shfl_up_sync(~0u, inc, o);
+                const int ur = __shfl_up_sync(~0u, tr, o);
+                if (lane >= o && ur == tr) inc = xadd(up, inc);
+            }
+            const double prev_inc = __shfl_up_sync(~0u, inc, 1);
+            const int prev_tr = __shfl_up_sync(~0u, tr, 1);
+            const int nlane_r0 = __shfl_down_sync(~0u, rc[0], 1);
+            const int last_lane = (cnt - 1) / IT;
+            double acc = 0.0;
+            int prv = carry_row;
+            bool ended_orphan = false;
+            double ended_orphan_val = 0.0;
+            bool carry_ended = false;
+            if (nmine > 0) {
+                if (lane == 0) acc = rc[0] == carry_row ? carry : 0.0;
+                else { prv = prev_tr; acc = prev_tr == rc[0] ? prev_inc : 0.0; }
+                // the carried row ends right at the chunk start
+                if (lane == 0 && rc[0] != carry_row && carry_row >= 0) carry_ended = true;
+#pragma unroll
+                for (int j = 0; j < IT; ++j) {
+                    if (j < nmine) {
+                        const int rw = rc[j];
+                        if (rw != prv) {
+                            for (int q = prv + 1; q < rw; ++q) y[q] = 0.0;
+                            if (j > 0) acc = 0.0;
+                        }
+                        acc = xadd(acc, p[j]);
+                        const bool is_last = first + j == cnt - 1;
+                        const int nxt = j + 1 < nmine ? rc[j + 1] : nlane_r0;
+                        if (!is_last && rw != nxt) {
+                            if (orphan_open && rw == carry_row) { ended_orphan = true; ended_orphan_val = acc; }
+                            else y[rw] = acc;
+                        }
+                        prv = rw;
+                    }
+                }
+            }
+            // the carried row ended at the chunk boundary: lane 0 flushes it
+            if (carry_ended) {
+                if (orphan_open) { ended_orphan = true; ended_orphan_val = carry; }
+                else y[carry_row] = carry;
+            }
+            const unsigned eo = __ballot_sync(~0u, ended_orphan);
+            if (eo) {
+                const int src = __ffs(eo) - 1;
+                first_sum = __shfl_sync(~0u, ended_orphan_val, src);
+                first_ended = true;
+                orphan_open = false;
+            }
+            carry = __shfl_sync(~0u, acc, last_lane);
+            carry_row = __shfl_sync(~0u, rc[(cnt - 1) % IT < IT ? 0 : 0], 0);  // placeholder, fixed below
+            {
+                int lr = kNoRow;
+#pragma unroll
+                for (int j = 0; j < IT; ++j) if (first + j == cnt - 1) lr = rc[j];
+                carry_row = __shfl_sync(~0u, lr, last_lane);
+            }
+        }
+        if (lane == 0) {
+            WarpRec q;
+            q.first_row = first_row_w;
+            q.first_sum = first_ended ? first_sum : carry;
+            q.last_row = carry_row;
+            q.last_sum = carry;
+            q.flags = ((c0 > 0 && first_row_w == range_prev) ? kWFirstCont : 0) | (orphan_open ? kWSingle : 0) | (first_ended ? kWFirstEnded : 0);
+            wrec[w] = q;
+            if (c1 * CH >= z) for (int64_t qq = int64_t(carry_row) + 1; qq < nrows; ++qq) y[qq] = 0.0;
+        }
+    }
+    // ---- last CTA combines the boundary records (fixed order)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+        const WarpRec q = wrec[i];
+        if (q.flags & kWSingle) continue;  // a run's owner is an earlier warp
+        double t = q.last_sum;
+        for (int j = i + 1; j < nw; ++j) {
+            const WarpRec n2 = wrec[j];
+            if (!(n2.flags & kWFirstCont) || n2.first_row != q.last_row) break;
+            t = xadd(t, n2.first_sum);
+            if (!(n2.flags & kWSingle)) break;
+        }
+        y[q.last_row] = t;
+    }
+    if (threadIdx.x == 0) *ticket = 0;
+}
+
 // ------------------------------------------------------------------ matrices
 struct Csr { int64_t n; std::vector<int64_t> rp; std::vector<int> col; std::vector<double> val; };
 
@@ -680,6 +992,44 @@ int main(int argc, char** argv) {
         report("csr_vec V4", csr_bytes, [&] { csr_vec<4><<<unsigned((n * 4 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
         report("csr_vec V8", csr_bytes, [&] { csr_vec<8><<<unsigned((n * 8 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
         report("csr_vec V16", csr_bytes, [&] { csr_vec<16><<<unsigned((n * 16 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
+        }
+        // --- COO variants
+        if (getenv("LAB_COO")) {
+            std::vector<int> hr(z);
+            for (int64_t i = 0; i < n; ++i) for (int64_t kk = m.rp[i]; kk < m.rp[i + 1]; ++kk) hr[kk] = int(i);
+            int* drow; CK(cudaMalloc(&drow, (z + 64) * 4));
+            CK(cudaMemcpy(drow, hr.data(), z * 4, cudaMemcpyHostToDevice));
+            CooRec* drec; CK(cudaMalloc(&drec, ((z + 127) / 128) * sizeof(CooRec)));
+            const double coo_bytes = 16.0 * z + 16.0 * n;
+            auto go = [&](const char* name, int IT, auto kern, unsigned grid, bool fix8) {
+                const int64_t nch = (z + 32 * IT - 1) / (32 * IT);
+                report(name, coo_bytes, [&] {
+                    kern<<<grid, 256>>>(z, n, drow, dcol, dval, dx, dy, drec);
+                    if (fix8) coo_fix8<<<unsigned((nch + 255) / 256), 256>>>(nch, drec, dy);
+                    else coo_fix<<<unsigned((nch + 255) / 256), 256>>>(nch, drec, dy);
+                }, check(false, 1 << 30));
+            };
+            const unsigned g8 = unsigned(((z + 255) / 256 + 7) / 8), g4 = unsigned(((z + 127) / 128 + 7) / 8);
+            go("coo_blk8 B4 fix", 8, coo_blk<8, 4>, g8, false);
+            go("coo_blk8 B4 fix8", 8, coo_blk<8, 4>, g8, true);
+            go("coo_blk8 B5 fix8", 8, coo_blk<8, 5>, g8, true);
+            go("coo_blk8 B6 fix8", 8, coo_blk<8, 6>, g8, true);
+            go("coo_blk4 B8 fix8", 4, coo_blk<4, 8>, g4, true);
+            go("coo_pf8 B3 fix8", 8, coo_pf<8, 3>, sms * 3, true);
+            go("coo_pf4 B6 fix8", 4, coo_pf<4, 6>, sms * 6, true);
+            go("coo_pf4 B5 fix8", 4, coo_pf<4, 5>, sms * 5, true);
+            {
+                WarpRec* dw; unsigned* dt;
+                CK(cudaMalloc(&dw, sizeof(WarpRec) * 148 * 8 * 8)); CK(cudaMalloc(&dt, 4)); CK(cudaMemset(dt, 0, 4));
+                for (int per : {3, 4}) {
+                    const int nw = int(std::min<int64_t>(int64_t(sms) * per * 8, (z + 255) / 256));
+                    char nm[64]; snprintf(nm, 64, "coo_seq8 x%d", per);
+                    auto kern = per == 3 ? coo_seq<8, 3> : coo_seq<8, 4>;
+                    report(nm, coo_bytes, [&] { kern<<<unsigned((nw + 7) / 8), 256>>>(z, n, drow, dcol, dval, dx, dy, dw, dt, nw); }, check(false, 1 << 30));
+                }
+                cudaFree(dw); cudaFree(dt);
+            }
+            cudaFree(drow); cudaFree(drec);
         }
         // --- DIA / ELL for the banded case
         if (!only_prod && maxlen <= 27 && std::string(cs.name).find("banded") != std::string::npos) {
