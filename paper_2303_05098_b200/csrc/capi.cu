@@ -860,9 +860,16 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             np->ws.reset(new FeatWorkspace(*m, s));
             SOB_CUDA(cudaStreamSynchronize(s));
             cudaGraph_t g = nullptr;
+            // one graph: features, predict + feasibility, with event-record
+            // nodes around each so T_FE / T_PRED are device intervals of the
+            // graph itself (no host submission gap inside them)
             SOB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
+                SOB_CUDA(cudaEventRecordWithFlags(np->e0, s, cudaEventRecordExternal));
                 enqueue_features(*m, ratio, np->st, s, np->ws.get());
+                SOB_CUDA(cudaEventRecordWithFlags(np->e1, s, cudaEventRecordExternal));
+                enqueue_tune_predict(*f, np->st, cfg, m->format, np->out, s);
+                SOB_CUDA(cudaEventRecordWithFlags(np->e2, s, cudaEventRecordExternal));
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
                 if (g) cudaGraphDestroy(g);
@@ -874,12 +881,7 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             plan = np.get();
             m->tune_plan = std::move(np);
         }
-        // events bracket the graph (T_FE) and the predict kernel (T_PRED)
-        SOB_CUDA(cudaEventRecord(plan->e0, s));
         SOB_CUDA(cudaGraphLaunch(plan->exec, s));
-        SOB_CUDA(cudaEventRecord(plan->e1, s));
-        enqueue_tune_predict(*f, plan->st, cfg, m->format, plan->out, s);
-        SOB_CUDA(cudaEventRecord(plan->e2, s));
         so_tune_outcome h;
         SOB_CUDA(cudaMemcpyAsync(&h, plan->out, sizeof(h), cudaMemcpyDeviceToHost, s));
         SOB_CUDA(cudaStreamSynchronize(s));

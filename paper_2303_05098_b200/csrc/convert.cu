@@ -153,7 +153,7 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
 // entries; a row longer than cap stands alone (and is split into pieces).
 // One thread walks kGroupChunk rows (chunk starts are forced group starts,
 // so the partition is deterministic and parallel) and flags group starts.
-constexpr int kGroupChunk = 512;
+constexpr int kGroupChunk = 128;
 __global__ void group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t cap, int32_t* __restrict__ flag) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t lo = c * kGroupChunk;

@@ -326,21 +326,6 @@ __device__ __forceinline__ Mono shfl_mono_up(const Mono& m, int o) {
     return Mono{__shfl_up_sync(0xffffffffu, m.a0, o), __shfl_up_sync(0xffffffffu, m.a1, o),
                 __shfl_up_sync(0xffffffffu, m.p, o)};
 }
-// ordered warp reduction: lane 0 ends with M_0 . M_1 . ... . M_31
-__device__ __forceinline__ Mono warp_reduce_mono(Mono m, bool& ok) {
-    const unsigned lane = threadIdx.x & 31u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const Mono other = shfl_mono_down(m, o);
-        const bool ook = __shfl_down_sync(0xffffffffu, ok, o);
-        if ((lane & (2 * o - 1)) == 0) {
-            m = mono_cat(m, other);
-            ok = ok && ook;
-        }
-    }
-    return m;
-}
-
 // ordered inclusive scan across the warp
 __device__ __forceinline__ Mono warp_scan_mono(Mono m, bool& ok) {
     const unsigned lane = threadIdx.x & 31u;
@@ -411,13 +396,11 @@ __device__ __forceinline__ MonoRec ident_rec() { return MonoRec{0, 0, 2, 0, kMon
 // share one binade.  spread_walk descends to the sub-chunk records of a
 // chunk it cannot take whole, so the exact row-by-row path only ever runs
 // over the one sub-chunk where the running sum changes binade.
-__global__ void __launch_bounds__(kB)
-    spread_mono(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, const FeatState* __restrict__ st,
-                const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec,
-                MonoRec* __restrict__ fine) {
-    const int64_t c = blockIdx.x;
+__device__ __forceinline__ void mono_chunk(int64_t c, const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk,
+                                           double avg, double csum_c, double P_c, MonoRec* __restrict__ rec,
+                                           MonoRec* __restrict__ fine) {
     const int t = threadIdx.x, lane = t & 31;
-    if (csum[c] == 0.0) {  // every t == 0: identity at any binade
+    if (csum_c == 0.0) {  // every t == 0: identity at any binade
         if (t < kSubs) fine[c * kSubs + t] = ident_rec();
         if (t == 0) rec[c] = ident_rec();
         return;
@@ -425,7 +408,6 @@ __global__ void __launch_bounds__(kB)
     __shared__ double sub_sum[kSubs];
     __shared__ double psub[kSubs + 1];
     __shared__ MonoRec fr[kSubs];
-    const double avg = double(st->visits) / double(nrows);
     const int rpt = int(chunk / kB);  // rows per thread; 8 threads per sub-chunk
     const int64_t base = c * chunk + int64_t(t) * rpt;
     double ps = 0.0;  // approximate (order is irrelevant for the guess)
@@ -443,8 +425,8 @@ __global__ void __launch_bounds__(kB)
             const double w = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += w;
         }
-        psub[lane] = P[c] + (inc - v);
-        if (lane == 31) psub[kSubs] = P[c] + inc;
+        psub[lane] = P_c + (inc - v);
+        if (lane == 31) psub[kSubs] = P_c + inc;
     }
     __syncthreads();
     const int sj = t >> 3;
@@ -491,6 +473,16 @@ __global__ void __launch_bounds__(kB)
         }
         rec[c] = cok ? MonoRec{acc.a0, acc.a1, acc.p, ce, kMonoSafe, 0} : MonoRec{0, 0, 2, 0, 0, 0};
     }
+    __syncthreads();  // fr / sub_sum are reused by the next call
+}
+
+__global__ void __launch_bounds__(kB)
+    spread_mono(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, const FeatState* __restrict__ st,
+                const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec,
+                MonoRec* __restrict__ fine) {
+    const int64_t c = blockIdx.x;
+    const double avg = double(st->visits) / double(nrows);
+    mono_chunk(c, rc, nrows, chunk, avg, csum[c], P[c], rec, fine);
 }
 
 // Exact sequential semantics over rows [lo, hi), warp-cooperative (all 32
@@ -503,12 +495,25 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
 // Plain sequential IEEE additions, 32 rows per step: every lane holds one
 // t_i and all lanes run the same shuffle-fed chain (so S stays warp-uniform).
 __device__ double seq_rows(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
+    // lanes compute 32 terms into shared memory; lane 0 runs the dependent
+    // add chain from there (loads issue ahead of the adds), then broadcasts
+    __shared__ double tbuf[32];
     const unsigned lane = threadIdx.x & 31u;
     for (int64_t b = lo; b < hi; b += 32) {
         const int64_t i = b + lane;
-        const double t = i < hi ? sq_dev(rc[i], avg) : 0.0;
+        tbuf[lane] = i < hi ? sq_dev(rc[i], avg) : 0.0;
+        __syncwarp();
         const int cnt = int(hi - b < 32 ? hi - b : 32);
-        for (int j = 0; j < cnt; ++j) S = __dadd_rn(S, __shfl_sync(0xffffffffu, t, j));
+        if (lane == 0) {
+            double t[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) t[j] = tbuf[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < cnt) S = __dadd_rn(S, t[j]);
+        }
+        S = __shfl_sync(0xffffffffu, S, 0);
+        __syncwarp();
     }
     return S;
 }
@@ -658,10 +663,10 @@ __device__ double walk_records(double S, const MonoRec* __restrict__ rec, int64_
 // a chunk it cannot take whole and to the exact row-by-row path only for the
 // sub-chunk where S changes binade; then finalizes the FeatureVector
 // (features.cpp:121-152).
-__global__ void __launch_bounds__(32)
-    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
-                const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
-    const unsigned lane = threadIdx.x;
+__device__ __forceinline__ void walk_and_finalize(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols,
+                                                  int64_t nch, int64_t chunk, const MonoRec* __restrict__ rec,
+                                                  const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
+    const unsigned lane = threadIdx.x & 31u;
     const double avg = double(st->visits) / double(nrows);
     const int64_t sub = chunk / kSubs;
     const double S = walk_records(0.0, rec, nch, [&](double S, int64_t c) {
@@ -691,6 +696,12 @@ __global__ void __launch_bounds__(32)
         f.ndiags = int64_t(st->nd);
         f.ntrue_diags = int64_t(st->ntd);
     }
+}
+
+__global__ void __launch_bounds__(32)
+    spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
+                const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
+    walk_and_finalize(rc, nrows, ncols, nch, chunk, rec, fine, st);
 }
 
 __global__ void feat_init(FeatState* st) {

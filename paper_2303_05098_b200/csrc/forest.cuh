@@ -16,8 +16,18 @@ struct alignas(16) PackedNode {
     int32_t pad[2];
 };
 
+// Blocked layout for single-row (latency-bound) prediction: every tree is cut
+// into depth-5 subtrees, each stored BFS-ordered in one 32-slot block (31
+// nodes + pad) whose 32 records one warp fetches with a single coalesced 1 KB
+// load; a child id (global slot = block*32 + local) inside the same block is
+// followed through warp shuffles, so a depth-16 walk costs ~4 dependent loads
+// instead of 16.
+constexpr int kTreeBlock = 32;
+
 struct ForestDev {
     DBuf<PackedNode> nodes;
+    DBuf<PackedNode> bnodes;  // blocked layout (kTreeBlock slots per block)
+    DBuf<int32_t> broot;      // root slot of each tree in bnodes
     int kind = 1;  // 0 tree, 1 forest
     int n_trees = 0;
     int64_t n_nodes = 0;

@@ -20,9 +20,13 @@ struct ForestView {
     int kind, n_trees;
     const PackedNode* nodes;
     const int64_t* root;
+    const PackedNode* bnodes;
+    const int32_t* broot;
 };
 
-ForestView view(const so_forest& f) { return ForestView{f.f.kind, f.f.n_trees, f.f.nodes.get(), f.f.root.get()}; }
+ForestView view(const so_forest& f) {
+    return ForestView{f.f.kind, f.f.n_trees, f.f.nodes.get(), f.f.root.get(), f.f.bnodes.get(), f.f.broot.get()};
+}
 
 // features_to_row (features.cpp:155-166)
 __device__ __forceinline__ void to_row(const so_feature_vector& f, double* row) {
@@ -72,6 +76,76 @@ __global__ void __launch_bounds__(kPB) predict_rows_kernel(ForestView f, const d
     }
 }
 
+// Warp-cooperative walk over the blocked layout (forest.cuh).  Lane j holds
+// slot j of the current block and evaluates that node's own comparison
+// (x[feature] <= threshold, model.cpp:206-209), so following the path through
+// the block costs one shuffle per level; a leaf is encoded as -1 - class.
+// Two trees are walked together so their block fetches overlap.
+__device__ __forceinline__ int node_step(const PackedNode& nd, const double* row) {
+    if (nd.feature == -1) return -1 - nd.cls;
+    return row[nd.feature] <= nd.threshold ? nd.left : nd.right;
+}
+
+__device__ __forceinline__ void walk_warp2(const ForestView& f, int t0, int t1, const double* row, int& c0, int& c1) {
+    const unsigned lane = threadIdx.x & 31u;
+    int cur[2] = {f.broot[t0], t1 >= 0 ? f.broot[t1] : -1};
+    int res[2] = {-1, t1 >= 0 ? -1 : 0};
+    bool live[2] = {true, t1 >= 0};
+    while (live[0] || live[1]) {
+        int go[2] = {0, 0};
+        int blk[2] = {0, 0};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (live[k]) {
+                blk[k] = cur[k] / kTreeBlock;
+                const PackedNode nd = f.bnodes[int64_t(blk[k]) * kTreeBlock + lane];
+                go[k] = node_step(nd, row);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (!live[k]) continue;
+            while (true) {
+                const int nxt = __shfl_sync(0xffffffffu, go[k], cur[k] - blk[k] * kTreeBlock);
+                if (nxt < 0) {
+                    res[k] = -1 - nxt;
+                    live[k] = false;
+                    break;
+                }
+                cur[k] = nxt;
+                if (nxt / kTreeBlock != blk[k]) break;
+            }
+        }
+    }
+    c0 = res[0];
+    c1 = res[1];
+}
+
+// One CTA of kTB threads for one feature row: a warp per pair of trees over
+// the blocked layout, votes in shared memory, argmax with strict '>' so ties
+// go to the lowest FormatId (model.cpp:215-228).
+constexpr int kTB = 1024;
+__device__ int predict_block_warps(const ForestView& f, const double* row, int trees) {
+    __shared__ int votes[8];
+    if (threadIdx.x < 8) votes[threadIdx.x] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int t = 2 * warp; t < trees; t += 2 * nwarps) {
+        int c0, c1;
+        walk_warp2(f, t, t + 1 < trees ? t + 1 : -1, row, c0, c1);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&votes[c0], 1);
+            if (t + 1 < trees) atomicAdd(&votes[c1], 1);
+        }
+    }
+    __syncthreads();
+    int best = 0;
+    for (int c = 1; c < 6; ++c)
+        if (votes[c] > votes[best]) best = c;
+    __syncthreads();
+    return best;
+}
+
 struct CapCfg {
     int64_t kh_override;
     double max_padding_factor;
@@ -109,13 +183,13 @@ __device__ bool d_feasible(int target, const so_feature_vector& f, const CapCfg&
     return false;
 }
 
-__global__ void __launch_bounds__(kPB) tune_predict_kernel(ForestView f, const FeatState* __restrict__ st, CapCfg cfg,
+__global__ void __launch_bounds__(kTB) tune_predict_kernel(ForestView f, const FeatState* __restrict__ st, CapCfg cfg,
                                                            int active, so_tune_outcome* __restrict__ out) {
     __shared__ double row[10];
     if (threadIdx.x == 0) to_row(st->out, row);
     __syncthreads();
     // kind tree evaluates trees.front() only (tuners.cpp:103-105)
-    int chosen = predict_block(f, row, f.kind == 0 ? 1 : f.n_trees);
+    int chosen = predict_block_warps(f, row, f.kind == 0 ? 1 : f.n_trees);
     if (threadIdx.x == 0) {
         // the model saw row_to_features(features_to_row(f)); feasibility uses
         // the integer fields, identical for counts < 2^53
@@ -204,6 +278,52 @@ so_forest* forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off,
     for (int64_t i = 0; i < nn; ++i)
         packed[size_t(i)] = PackedNode{threshold[i], fe[size_t(i)], gl[size_t(i)], gr[size_t(i)], cl[size_t(i)], {0, 0}};
     up(d.nodes, packed.data(), nn);
+    // blocked layout: depth-5 subtrees, BFS inside each 32-slot block
+    std::vector<PackedNode> blk;
+    std::vector<int32_t> broot(size_t(n_trees), 0);
+    struct Pending {
+        int64_t node;  // flat (global) node id
+        int64_t parent_slot;
+        bool left;
+    };
+    for (int t = 0; t < n_trees; ++t) {
+        std::vector<Pending> q{{root[size_t(t)], -1, false}};
+        for (size_t qi = 0; qi < q.size(); ++qi) {
+            const Pending p = q[qi];
+            const int64_t B = int64_t(blk.size()) / kTreeBlock;
+            if (B * kTreeBlock + kTreeBlock > INT32_MAX) fail(SO_INVALID_INPUT, "forest too large");
+            blk.resize(blk.size() + kTreeBlock, PackedNode{0.0, -1, -1, -1, 0, {0, 0}});
+            const int32_t bslot = int32_t(B * kTreeBlock);
+            if (p.parent_slot < 0)
+                broot[size_t(t)] = bslot;
+            else if (p.left)
+                blk[size_t(p.parent_slot)].left = bslot;
+            else
+                blk[size_t(p.parent_slot)].right = bslot;
+            int64_t local[kTreeBlock - 1];
+            for (auto& v : local) v = -1;
+            local[0] = p.node;
+            for (int i = 0; i < kTreeBlock - 1; ++i) {
+                const int64_t nd = local[i];
+                if (nd < 0) continue;
+                const int64_t slot = B * kTreeBlock + i;
+                blk[size_t(slot)] = PackedNode{threshold[nd], fe[size_t(nd)], -1, -1, cl[size_t(nd)], {0, 0}};
+                if (fe[size_t(nd)] == -1) continue;
+                for (int side = 0; side < 2; ++side) {
+                    const int64_t child = side == 0 ? gl[size_t(nd)] : gr[size_t(nd)];
+                    const int ci = 2 * i + 1 + side;
+                    if (ci < kTreeBlock - 1) {
+                        local[ci] = child;
+                        (side == 0 ? blk[size_t(slot)].left : blk[size_t(slot)].right) = int32_t(B * kTreeBlock + ci);
+                    } else {
+                        q.push_back(Pending{child, slot, side == 0});
+                    }
+                }
+            }
+        }
+    }
+    up(d.bnodes, blk.data(), int64_t(blk.size()));
+    up(d.broot, broot.data(), n_trees);
     SOB_CUDA(cudaStreamSynchronize(s));  // host staging vectors go out of scope
     return f;
 }
@@ -217,7 +337,7 @@ void predict_rows(const so_forest& f, const double* rows_dev, int64_t n, int32_t
 void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,
                           so_tune_outcome* out_dev, cudaStream_t s) {
     CapCfg c{cfg.kh_override, cfg.max_padding_factor, cfg.max_padded_entries};
-    tune_predict_kernel<<<1, kPB, 0, s>>>(view(f), st, c, active, out_dev);
+    tune_predict_kernel<<<1, kTB, 0, s>>>(view(f), st, c, active, out_dev);
     SOB_LAUNCH("tune_predict_kernel");
 }
 

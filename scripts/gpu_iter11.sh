@@ -1,0 +1,6 @@
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/it_pytest.log
+timeout 600 python scripts/profile_features.py --ids 877 1843 555 165 706 1692 521 --reps 5 2>&1 | grep "^id"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/feat_small_launches.csv python scripts/profile_features.py --ids 165 1692 --reps 1 > /dev/null 2>&1; echo "ncu rc=$?"
+( time timeout 1500 python scripts/config4.py --count 2000 --reps 20 --out gpurun_out/c4_profile_2000.csv ) > gpurun_out/c4p.log 2>&1; echo "c4 rc=$?"
+tail -5 gpurun_out/c4p.log
