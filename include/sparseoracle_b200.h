@@ -196,6 +196,30 @@ so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev,
  * interior).  y_dev is indexed by matrix row.  Stream-ordered. */
 so_status so_spmv_device_rows(const so_matrix* m, const double* x_dev, double* y_dev,
                               int64_t row_lo, int64_t row_hi, void* stream);
+/* Row-partitioned iteration with the halo exchange fused into the multiply
+ * (config 5; no reference counterpart -- the reference is single-node CPU):
+ * rows [row_lo, row_hi) of y = A x are written to y_dev (indexed by matrix
+ * row) AND to remote_dev[i - row_lo], a neighbour's window mapped with
+ * so_ipc_open (NVLink peer memory).  When every CTA is done, the last one
+ * stores flag_value to *remote_flag (release, system scope).  ticket_dev: a
+ * zeroed device unsigned owned by this call site (left zeroed again).
+ * DIA / pure-DIA HDC only.  Stream-ordered. */
+so_status so_spmv_rows_push(const so_matrix* m, const double* x_dev, double* y_dev,
+                            int64_t row_lo, int64_t row_hi, double* remote_dev,
+                            unsigned* ticket_dev, unsigned long long* remote_flag,
+                            unsigned long long flag_value, void* stream);
+/* Stream-ordered wait until *flag_dev >= value (acquire, system scope);
+ * pairs with so_spmv_rows_push on the neighbour. */
+so_status so_wait_flag(const unsigned long long* flag_dev, unsigned long long value,
+                       void* stream);
+/* Peer-shareable device memory (cudaMalloc + CUDA IPC), zero-filled. */
+typedef struct so_ipc_handle {
+    unsigned char bytes[64];
+} so_ipc_handle;
+so_status so_ipc_alloc(int64_t bytes, void** dev_ptr, so_ipc_handle* handle);
+so_status so_ipc_open(const so_ipc_handle* handle, void** dev_ptr);
+so_status so_ipc_close(void* dev_ptr);
+so_status so_ipc_free(void* dev_ptr);
 /* spmv(m, x): host vectors, H2D x + kernel(s) + D2H y, synchronous. */
 so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y);
 /* time_spmv: x uploaded once, 1 untimed warm-up, then `reps` multiplies each

@@ -106,6 +106,12 @@ _SIGS = {
     "so_format_feasible": (i32, [i32, P(FeatureVector), P(ConversionConfig)]),
     "so_spmv_device": (C.c_int, [vp, vp, vp, vp]),
     "so_spmv_device_rows": (C.c_int, [vp, vp, vp, i64, i64, vp]),
+    "so_spmv_rows_push": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp, C.c_uint64, vp]),
+    "so_wait_flag": (C.c_int, [vp, C.c_uint64, vp]),
+    "so_ipc_alloc": (C.c_int, [i64, C.POINTER(vp), C.c_char_p]),
+    "so_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "so_ipc_close": (C.c_int, [vp]),
+    "so_ipc_free": (C.c_int, [vp]),
     "so_gen_stencil27_dia": (C.c_int, [i64, i64, i64, i64, i64, C.c_uint64, P(vp)]),
     "so_spmv": (C.c_int, [vp, vp, i64, vp]),
     "so_time_spmv": (C.c_int, [vp, vp, i64, i64, vp, P(f64)]),

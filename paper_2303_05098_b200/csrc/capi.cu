@@ -681,6 +681,61 @@ so_status so_spmv_device_rows(const so_matrix* m, const double* x_dev, double* y
     });
 }
 
+so_status so_spmv_rows_push(const so_matrix* m, const double* x_dev, double* y_dev, int64_t row_lo, int64_t row_hi,
+                            double* remote_dev, unsigned* ticket_dev, unsigned long long* remote_flag,
+                            unsigned long long flag_value, void* stream) {
+    return guard([&] {
+        on_device(m);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx(m->device).stream;
+        spmv_rows_push(*m, x_dev, y_dev, row_lo, row_hi, remote_dev, ticket_dev, remote_flag, flag_value, s);
+    });
+}
+
+so_status so_wait_flag(const unsigned long long* flag_dev, unsigned long long value, void* stream) {
+    return guard([&] {
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : current_ctx().stream;
+        wait_flag(flag_dev, value, s);
+    });
+}
+
+so_status so_ipc_alloc(int64_t bytes, void** dev_ptr, so_ipc_handle* handle) {
+    return guard([&] {
+        if (bytes <= 0 || !dev_ptr || !handle) fail(SO_INVALID_INPUT, "ipc_alloc: bad arguments");
+        current_ctx();
+        void* p = nullptr;
+        const cudaError_t e = cudaMalloc(&p, size_t(bytes));  // IPC needs a plain cudaMalloc allocation
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            fail(SO_OUT_OF_MEMORY, "ipc_alloc: out of device memory");
+        }
+        SOB_CUDA(e);
+        SOB_CUDA(cudaMemset(p, 0, size_t(bytes)));
+        cudaIpcMemHandle_t h;
+        SOB_CUDA(cudaIpcGetMemHandle(&h, p));
+        static_assert(sizeof(h) <= sizeof(handle->bytes), "IPC handle size");
+        std::memcpy(handle->bytes, &h, sizeof(h));
+        *dev_ptr = p;
+    });
+}
+
+so_status so_ipc_open(const so_ipc_handle* handle, void** dev_ptr) {
+    return guard([&] {
+        if (!handle || !dev_ptr) fail(SO_INVALID_INPUT, "ipc_open: bad arguments");
+        current_ctx();
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle->bytes, sizeof(h));
+        SOB_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+so_status so_ipc_close(void* dev_ptr) {
+    return guard([&] { SOB_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
+}
+
+so_status so_ipc_free(void* dev_ptr) {
+    return guard([&] { SOB_CUDA(cudaFree(dev_ptr)); });
+}
+
 so_status so_gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_t col_lo, int64_t col_hi,
                                uint64_t seed, so_matrix** out) {
     return make(out, [&] {

@@ -117,6 +117,10 @@ bool csr_rows_canonical(const so_matrix& csr, cudaStream_t s);
 // --- spmv (spmv.cu) ---
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s);
 void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, cudaStream_t s);
+void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, double* remote,
+                    unsigned* ticket, unsigned long long* remote_flag, unsigned long long flag_value,
+                    cudaStream_t s);
+void wait_flag(const unsigned long long* flag, unsigned long long value, cudaStream_t s);
 so_matrix* gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_t col_lo, int64_t col_hi,
                              uint64_t seed, cudaStream_t s);
 int64_t spmv_bytes(const so_matrix& m);

@@ -246,6 +246,48 @@ __global__ void __launch_bounds__(256, 6)
     y[i] = dia_row<GLOBAL_OFF>(int(i), int(nrows), int(ncols), ndiags, soff, offsets, vals, x);
 }
 
+// Row-partitioned iteration, fused boundary exchange (config 5, dist.py):
+// the rows a neighbour needs are computed once and stored twice -- into the
+// local window and straight into the neighbour's window over NVLink peer
+// memory (remote[i - row_lo], an IPC-mapped pointer).  Every thread fences at
+// system scope after its stores; the last CTA to finish (ticket) resets the
+// ticket and publishes `flag_value` to the neighbour's flag with a
+// release.sys store, which so_wait_flag acquires on the other side.
+template <bool GLOBAL_OFF>
+__global__ void __launch_bounds__(256, 6)
+    dia_push_kernel(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
+                    const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y,
+                    int64_t row_lo, int64_t row_hi, double* remote, unsigned* ticket,
+                    unsigned long long* remote_flag, unsigned long long flag_value) {
+    __shared__ int soff[GLOBAL_OFF ? 1 : kDiaSmem];
+    __shared__ bool last;
+    if (!GLOBAL_OFF) stage_offsets(soff, offsets, ndiags);
+    const int64_t i = row_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < row_hi) {
+        const double v = dia_row<GLOBAL_OFF>(int(i), int(nrows), int(ncols), ndiags, soff, offsets, vals, x);
+        y[i] = v;
+        remote[i - row_lo] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        *ticket = 0;
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote_flag), "l"(flag_value) : "memory");
+    }
+}
+
+__global__ void wait_flag_kernel(const unsigned long long* flag, unsigned long long value) {
+    while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v >= value) break;
+        __nanosleep(256);
+    }
+}
+
 // ---------------------------------------------------------------- ELL -------
 // Column-major ELL, one thread per row; slots are consumed in order and the
 // row stops at the first sentinel (spmv.cpp:59-71).  Column indices for
@@ -557,6 +599,31 @@ void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo
         fail(SO_INVALID_INPUT, "row-range SpMV is implemented for DIA matrices (and HDC with an empty CSR part)");
     if (lo < 0 || hi > m.nrows || lo > hi) fail(SO_INVALID_INPUT, "row range outside the matrix");
     launch_dia(m, x, y, s, lo, hi);
+}
+
+void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, double* remote,
+                    unsigned* ticket, unsigned long long* remote_flag, unsigned long long flag_value,
+                    cudaStream_t s) {
+    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0))
+        fail(SO_INVALID_INPUT, "row-range SpMV is implemented for DIA matrices (and HDC with an empty CSR part)");
+    if (lo < 0 || hi > m.nrows || lo >= hi) fail(SO_INVALID_INPUT, "row range outside the matrix or empty");
+    if (!remote || !ticket || !remote_flag) fail(SO_INVALID_INPUT, "null peer pointer");
+    const unsigned grid = unsigned(ceil_div(hi - lo, 256));
+    if (m.dia.ndiags <= kDiaSmem)
+        dia_push_kernel<false><<<grid, 256, 0, s>>>(m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                                    m.dia.values.get(), x, y, lo, hi, remote, ticket, remote_flag,
+                                                    flag_value);
+    else
+        dia_push_kernel<true><<<grid, 256, 0, s>>>(m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
+                                                   m.dia.values.get(), x, y, lo, hi, remote, ticket, remote_flag,
+                                                   flag_value);
+    SOB_LAUNCH("dia_push_kernel");
+}
+
+void wait_flag(const unsigned long long* flag, unsigned long long value, cudaStream_t s) {
+    if (!flag) fail(SO_INVALID_INPUT, "null flag");
+    wait_flag_kernel<<<1, 1, 0, s>>>(flag, value);
+    SOB_LAUNCH("wait_flag_kernel");
 }
 
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s) {

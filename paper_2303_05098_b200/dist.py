@@ -100,3 +100,106 @@ def iterate(s: Slice, x_cur, x_next, iters, spmv_rows, exchange, copy=None):
             pending()
         x_cur, x_next = x_next, x_cur
     return x_cur
+
+
+# ------------------------------------------------------ fused peer-memory halo
+
+class PeerWindows:
+    """The two x windows and the two halo flags of this rank in peer-shareable
+    device memory (so_ipc_alloc), plus the neighbours' windows and flags
+    mapped into this process (so_ipc_open: NVLink peer memory on an 8xB200
+    node; plain device memory when ranks share one GPU).
+
+    flags[0] is written by the left neighbour (my left halo is complete for
+    iteration value-1), flags[1] by the right neighbour.  Handles travel once
+    through `all_gather_object` (any torch.distributed backend)."""
+
+    def __init__(self, s: Slice, all_gather_object):
+        import ctypes as C
+
+        from . import _capi as A
+        if s.world > 1 and s.nloc < 2 * s.h:
+            raise ValueError("fused halo exchange needs >= 2h owned rows per rank")
+        self.s = s
+        self._lib = A.lib()
+        self._own = []
+
+        def alloc(nbytes):
+            p, h = C.c_void_p(), C.create_string_buffer(64)
+            self._check(self._lib.so_ipc_alloc(nbytes, C.byref(p), h))
+            self._own.append(p.value)
+            return p.value, h.raw
+
+        self.buf, hb = zip(*[alloc(8 * s.nwin) for _ in range(2)])
+        self.flags, hf = alloc(16)
+        self.tickets, _ = alloc(16)
+        infos = [None] * s.world
+        all_gather_object(infos, (s.rank, s.w0, list(hb), hf))
+        self.peer = {}
+        self._opened = []
+        for nb in (s.rank - 1, s.rank + 1):
+            if 0 <= nb < s.world:
+                _, w0, bh, fh = infos[nb]
+                ptrs = []
+                for h in (*bh, fh):
+                    p = C.c_void_p()
+                    self._check(self._lib.so_ipc_open(h, C.byref(p)))
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+                self.peer[nb] = {"w0": w0, "buf": ptrs[:2], "flags": ptrs[2]}
+        self.it = 0  # iterations completed (flag values are monotone)
+
+    def _check(self, st):
+        if st != 0:
+            raise RuntimeError(self._lib.so_last_error().decode(errors="replace"))
+
+    def tensor(self, k):
+        """torch view (zero-copy, __cuda_array_interface__) of window k."""
+        import torch
+
+        class _View:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                                  "version": 3, "strides": None}
+        return torch.as_tensor(_View(self.buf[k], self.s.nwin), device="cuda")
+
+    def iterate(self, m, iters, stream):
+        """`iters` steps of x <- A x on the windows, halo rows pushed to the
+        neighbours by the multiply itself (so_spmv_rows_push), no collective.
+        Returns the index of the window holding the last iterate."""
+        import ctypes as C
+        s, lib = self.s, self._lib
+        lo, hi = s.interior()
+        sp = C.c_void_p(stream)
+        for _ in range(iters):
+            it = self.it
+            cur, nxt = self.buf[it % 2], self.buf[(it + 1) % 2]
+            y = nxt + 8 * s.own_lo
+            # my halo of `cur` was pushed by the neighbours during iteration it-1
+            if s.rank > 0:
+                self._check(lib.so_wait_flag(C.c_void_p(self.flags), it, sp))
+            if s.rank < s.world - 1:
+                self._check(lib.so_wait_flag(C.c_void_p(self.flags + 8), it, sp))
+            if s.rank > 0:  # first h rows -> left neighbour's right halo
+                p = self.peer[s.rank - 1]
+                remote = p["buf"][(it + 1) % 2] + 8 * (s.r0 - p["w0"])
+                self._check(lib.so_spmv_rows_push(m._h, C.c_void_p(cur), C.c_void_p(y), 0, lo,
+                                                  C.c_void_p(remote), C.c_void_p(self.tickets),
+                                                  C.c_void_p(p["flags"] + 8), it + 1, sp))
+            if s.rank < s.world - 1:  # last h rows -> right neighbour's left halo
+                p = self.peer[s.rank + 1]
+                remote = p["buf"][(it + 1) % 2] + 8 * (s.r0 + hi - p["w0"])
+                self._check(lib.so_spmv_rows_push(m._h, C.c_void_p(cur), C.c_void_p(y), hi, s.nloc,
+                                                  C.c_void_p(remote), C.c_void_p(self.tickets + 4),
+                                                  C.c_void_p(p["flags"]), it + 1, sp))
+            if hi > lo:
+                self._check(lib.so_spmv_device_rows(m._h, C.c_void_p(cur), C.c_void_p(y), lo, hi, sp))
+            self.it += 1
+        return self.it % 2
+
+    def close(self):
+        for p in self._opened:
+            self._lib.so_ipc_close(p)
+        for p in self._own:
+            self._lib.so_ipc_free(p)
+        self._opened, self._own = [], []

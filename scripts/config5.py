@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--g", type=int, default=512)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="p2p: boundary rows pushed into the neighbours' windows by the multiply "
+                         "(so_spmv_rows_push over CUDA IPC); nccl: isend/irecv after the multiply")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -66,14 +69,26 @@ def main():
                 r.wait()
         return wait
 
-    out = D.iterate(s, xa, xb, a.warmup, spmv_rows, exchange)
-    other = xb if out is xa else xa
+    pw = None
+    if world > 1 and a.exchange == "p2p":
+        pw = D.PeerWindows(s, torch.distributed.all_gather_object)
+        pw.tensor(0).copy_(xa)
+        del xa, xb
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        pw.iterate(m, a.warmup, stream.cuda_stream)
+    else:
+        out = D.iterate(s, xa, xb, a.warmup, spmv_rows, exchange)
+        other = xb if out is xa else xa
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    out = D.iterate(s, out, other, a.iters, spmv_rows, exchange)
+    if pw is not None:
+        out = pw.tensor(pw.iterate(m, a.iters, stream.cuda_stream))
+    else:
+        out = D.iterate(s, out, other, a.iters, spmv_rows, exchange)
     e1.record(stream)
     torch.cuda.synchronize()
     sec = e0.elapsed_time(e1) * 1e-3 / a.iters
@@ -96,8 +111,12 @@ def main():
                           "n_gpus": world, "nrows": n, "iters": a.iters, "ms_per_iter": round(sec * 1e3, 4),
                           "value": round(nbytes / sec / 1e9, 1), "unit": "GB/s",
                           "frac_per_gpu": round(nbytes / sec / 1e9 / world / peak, 4),
-                          "halo_rows_per_side": h, "checksum": float(csum.item())}), flush=True)
+                          "halo_rows_per_side": h, "exchange": a.exchange if world > 1 else "none",
+                          "checksum": float(csum.item())}), flush=True)
     if world > 1:
+        torch.distributed.barrier()
+        if pw is not None:
+            pw.close()
         torch.distributed.destroy_process_group()
 
 
