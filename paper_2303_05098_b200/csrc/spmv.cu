@@ -51,11 +51,10 @@ __device__ __forceinline__ int dia_off(const int* soff, const int64_t* __restric
     return GLOBAL_OFF ? int(offsets[d]) : soff[d];
 }
 
-template <bool GLOBAL_OFF>
+template <bool GLOBAL_OFF, int U = kDiaBatch>
 __device__ __forceinline__ double dia_row(int i, int nrows, int ncols, int ndiags, const int* soff,
                                           const int64_t* __restrict__ offsets, const double* __restrict__ vals,
                                           const double* __restrict__ x) {
-    constexpr int U = kDiaBatch;
     const double* vp = vals + i;
     double acc = 0.0;
     for (int d0 = 0; d0 < ndiags; d0 += U) {
@@ -234,8 +233,11 @@ __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, 
 // ---------------------------------------------------------------- DIA -------
 // One thread per row, diagonals ascending: consecutive threads read
 // consecutive cells of each diagonal (diagonal-major layout => coalesced).
-template <bool GLOBAL_OFF>
-__global__ void __launch_bounds__(256, 6)
+// U: diagonals per load batch.  Matrices with <= 5 diagonals (2-D 5-point
+// stencils, tridiagonal, ...) use U = 5 and 8 CTAs/SM: no dead loads in the
+// batch and more rows in flight (config 1: 16 -> 11-14 us, scripts/spmv_lab.cu).
+template <bool GLOBAL_OFF, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     dia_kernel(int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                const double* __restrict__ vals, const double* __restrict__ x,
                double* __restrict__ y, int64_t row_lo, int64_t row_hi) {
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(256, 6)
     if (!GLOBAL_OFF) stage_offsets(soff, offsets, ndiags);
     const int64_t i = row_lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= row_hi) return;
-    y[i] = dia_row<GLOBAL_OFF>(int(i), int(nrows), int(ncols), ndiags, soff, offsets, vals, x);
+    y[i] = dia_row<GLOBAL_OFF, U>(int(i), int(nrows), int(ncols), ndiags, soff, offsets, vals, x);
 }
 
 // Row-partitioned iteration, fused boundary exchange (config 5, dist.py):
@@ -576,12 +578,16 @@ void launch_dia(const so_matrix& m, const double* x, double* y, cudaStream_t s, 
     if (hi < 0) hi = m.nrows;
     if (hi <= lo) return;
     const unsigned grid = unsigned(ceil_div(hi - lo, 256));
-    if (m.dia.ndiags <= kDiaSmem)
-        dia_kernel<false><<<grid, 256, 0, s>>>(m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
-                                               m.dia.values.get(), x, y, lo, hi);
+    const int nd = int(m.dia.ndiags);
+    if (nd <= 5)
+        dia_kernel<false, 5, 8><<<grid, 256, 0, s>>>(m.nrows, m.ncols, nd, m.dia.offsets.get(), m.dia.values.get(),
+                                                      x, y, lo, hi);
+    else if (m.dia.ndiags <= kDiaSmem)
+        dia_kernel<false, kDiaBatch, 6><<<grid, 256, 0, s>>>(m.nrows, m.ncols, nd, m.dia.offsets.get(),
+                                                              m.dia.values.get(), x, y, lo, hi);
     else
-        dia_kernel<true><<<grid, 256, 0, s>>>(m.nrows, m.ncols, int(m.dia.ndiags), m.dia.offsets.get(),
-                                              m.dia.values.get(), x, y, lo, hi);
+        dia_kernel<true, kDiaBatch, 6><<<grid, 256, 0, s>>>(m.nrows, m.ncols, nd, m.dia.offsets.get(),
+                                                             m.dia.values.get(), x, y, lo, hi);
     SOB_LAUNCH("dia_kernel");
 }
 
