@@ -20,6 +20,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_LIB = os.path.join(HERE, "_build", "liboracle.so")
 REF_LIB = os.path.join(HERE, "_ref", "libsparseoracle_ref.so")
+# the reference's pipeline / trainer / CSV wire formats (optional, oracle/Makefile refpipe)
+REFPIPE_LIB = os.path.join(HERE, "_ref", "libsparseoracle_refpipe.so")
 
 COO, CSR, DIA, ELL, HYB, HDC = range(6)
 vp = C.c_void_p
@@ -82,6 +84,66 @@ def oc():
         L.oc_predict_forest.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp]
         L.oc_format_feasible.argtypes = [C.c_int, vp, i64, f64, i64]
     return _oc
+
+
+_refpipe = None
+
+
+def refpipe_available():
+    return os.path.exists(REFPIPE_LIB)
+
+
+def refpipe():
+    """ctypes view of oracle/ref_pipeline_capi.cpp (reference cmd_train,
+    read_profile_csv, build_training_csv)."""
+    global _refpipe
+    if _refpipe is None:
+        L = C.CDLL(REFPIPE_LIB)
+        L.refp_last_error.restype = C.c_char_p
+        L.refp_cmd_train.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint64, C.c_int,
+                                     C.POINTER(f64), C.POINTER(f64), C.POINTER(i64), C.POINTER(i64)]
+        L.refp_read_profile_csv.argtypes = [C.c_char_p, i64, C.POINTER(i64), C.POINTER(C.c_int32),
+                                            C.POINTER(i64), C.POINTER(f64), C.POINTER(C.c_int32)]
+        L.refp_build_training_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(i64), C.POINTER(i64)]
+        _refpipe = L
+    return _refpipe
+
+
+def _pchk(L, st):
+    if st != 0:
+        raise RuntimeError(L.refp_last_error().decode(errors="replace"))
+
+
+def ref_cmd_train(features_csv, profiles_csv, model_out, seed=0, folds=5):
+    """The reference's cmd_train (pipeline.cpp:190-252) on CSV files."""
+    L = refpipe()
+    acc, bacc, ntr, nte = f64(), f64(), i64(), i64()
+    _pchk(L, L.refp_cmd_train(str(features_csv).encode(), str(profiles_csv).encode(), str(model_out).encode(),
+                              seed, folds, C.byref(acc), C.byref(bacc), C.byref(ntr), C.byref(nte)))
+    return {"heldout_accuracy": acc.value, "heldout_balanced_accuracy": bacc.value,
+            "n_train": ntr.value, "n_test": nte.value}
+
+
+def ref_read_profile_csv(path):
+    """[(format, repetitions, total_seconds, feasible)] via the reference reader."""
+    L = refpipe()
+    cnt, fm, reps, tot, feas = i64(), C.c_int32(), i64(), f64(), C.c_int32()
+    _pchk(L, L.refp_read_profile_csv(str(path).encode(), -1, C.byref(cnt), C.byref(fm), C.byref(reps),
+                                     C.byref(tot), C.byref(feas)))
+    out = []
+    for i in range(cnt.value):
+        _pchk(L, L.refp_read_profile_csv(str(path).encode(), i, C.byref(cnt), C.byref(fm), C.byref(reps),
+                                         C.byref(tot), C.byref(feas)))
+        out.append((fm.value, reps.value, tot.value, bool(feas.value)))
+    return out
+
+
+def ref_build_training_csv(features_csv, profiles_csv, out_csv):
+    L = refpipe()
+    w, sk = i64(), i64()
+    _pchk(L, L.refp_build_training_csv(str(features_csv).encode(), str(profiles_csv).encode(),
+                                       str(out_csv).encode(), C.byref(w), C.byref(sk)))
+    return w.value, sk.value
 
 
 def ref_available():

@@ -63,6 +63,9 @@ def main():
     ap.add_argument("--model", default=None)
     ap.add_argument("--nmax", type=int, default=5_000_000)
     ap.add_argument("--only", default=None, help="JSON with test_ids: restrict to the held-out matrices")
+    ap.add_argument("--ref-csv", default=None,
+                    help="directory: also write profile.csv / features.csv in the reference's wire "
+                         "formats (ingest.cpp:419-470) for the reference trainer (cmd_train)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -104,6 +107,7 @@ def main():
             tot[f] = float(np.sum(time_format(m, x, y, a.reps, stream)))
             del m
         label = min(range(6), key=lambda f: (tot[f], f))
+        row_ref = (f"c4_{s['id']:04d}", [(f, a.reps, tot[f], tot[f] != float("inf")) for f in range(6)])
         row = {"id": s["id"], "family": s["family"], "n": fv.nrows, "nnz": fv.nnz}
         row.update({f"f{k}": v for k, v in enumerate(fv.to_row())})
         row.update({f"t_{FMT[f]}": tot[f] / a.reps for f in range(6)})
@@ -115,6 +119,7 @@ def main():
             row["chosen"] = int(o.chosen)
             row["t_fe"] = float(np.median([q.feature_time_seconds for q in outs]))
             row["t_pred"] = float(np.median([q.predict_time_seconds for q in outs]))
+        row["_ref"] = row_ref
         rows.append(row)
         del base
     elapsed = time.perf_counter() - t_start
@@ -126,6 +131,16 @@ def main():
         elapsed = max(g[1] for g in gathered)
     if rank == 0:
         rows.sort(key=lambda r: r["id"])
+        if a.ref_csv:
+            from paper_2303_05098_b200 import wire
+            os.makedirs(a.ref_csv, exist_ok=True)
+            wire.write_profile_csv(os.path.join(a.ref_csv, "profile.csv"),
+                                   [(mid, f, reps, t, ok) for r in rows for mid, recs in [r["_ref"]]
+                                    for f, reps, t, ok in recs])
+            wire.write_feature_csv(os.path.join(a.ref_csv, "features.csv"),
+                                   [(r["_ref"][0], [r[f"f{k}"] for k in range(10)]) for r in rows])
+        for r in rows:
+            r.pop("_ref", None)
         os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
         with open(a.out, "w", newline="") as f:
             w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
