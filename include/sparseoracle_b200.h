@@ -40,7 +40,9 @@ typedef enum so_status {
     SO_ALL_FORMATS_INFEASIBLE = 7, /* errors.hpp:69  AllFormatsInfeasible*/
     SO_CUDA_ERROR = 8,
     SO_OUT_OF_MEMORY = 9,
-    SO_ERROR = 10
+    SO_ERROR = 10,
+    SO_PARSE_ERROR = 11,           /* errors.hpp:49  ParseError          */
+    SO_UNSUPPORTED_FORMAT = 12     /* errors.hpp:44  UnsupportedFormat   */
 } so_status;
 
 /* formats.hpp:17-24 -- stable ids (model files, CSVs) */
@@ -157,6 +159,17 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags,
 so_status so_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n,
                                const int64_t* row, const int64_t* col,
                                const double* val, so_matrix** out);
+/* read_matrix_market (ingest.hpp:25, ingest.cpp:135-208): the reference's
+ * accepted subset (matrix coordinate {real, integer, pattern} x {general,
+ * symmetric}), 1-based -> 0-based, symmetric off-diagonals mirrored, pattern
+ * values 1.0; same error types (SO_PARSE_ERROR "path:line: ...",
+ * SO_UNSUPPORTED_FORMAT, SO_INDEX_OUT_OF_RANGE) and the same first error in
+ * file order.  Parsed by all host threads, canonicalized on the device as
+ * so_coo_from_triplets.  Result: canonical device COO. */
+so_status so_read_matrix_market(const char* path, so_matrix** out);
+/* write_matrix_market (ingest.hpp:29, ingest.cpp:210-224) of a canonical
+ * COO matrix: 'real general', 1-based, shortest round-trip decimals. */
+so_status so_write_matrix_market(const so_matrix* coo, const char* path);
 /* CSR already in device memory (e.g. produced by a device generator or another
  * library): row_ptr int64[n+1], col int32[nnz], val f64[nnz], all device
  * pointers on the current device, fully written before the call (the copy

@@ -105,6 +105,10 @@ def refpipe():
         L.refp_read_profile_csv.argtypes = [C.c_char_p, i64, C.POINTER(i64), C.POINTER(C.c_int32),
                                             C.POINTER(i64), C.POINTER(f64), C.POINTER(C.c_int32)]
         L.refp_build_training_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(i64), C.POINTER(i64)]
+        L.refp_read_mm.argtypes = [C.c_char_p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(C.c_int32)]
+        L.refp_mm_arrays.argtypes = [vp, vp, vp]
+        L.refp_mm_arrays.restype = None
+        L.refp_write_mm.argtypes = [C.c_char_p, i64, i64, i64, vp, vp, vp]
         _refpipe = L
     return _refpipe
 
@@ -144,6 +148,28 @@ def ref_build_training_csv(features_csv, profiles_csv, out_csv):
     _pchk(L, L.refp_build_training_csv(str(features_csv).encode(), str(profiles_csv).encode(),
                                        str(out_csv).encode(), C.byref(w), C.byref(sk)))
     return w.value, sk.value
+
+
+MM_ERRORS = {1: "ParseError", 2: "UnsupportedFormat", 3: "IndexOutOfRange", 4: "Error"}
+
+
+def ref_read_matrix_market(path):
+    """The reference's read_matrix_market: ('ok', coo dict) or (error type
+    name, message)."""
+    L = refpipe()
+    n, m, z, kind = i64(), i64(), i64(), C.c_int32()
+    if L.refp_read_mm(str(path).encode(), C.byref(n), C.byref(m), C.byref(z), C.byref(kind)) != 0:
+        return MM_ERRORS[kind.value], L.refp_last_error().decode(errors="replace")
+    row, col, val = np.zeros(z.value, np.int64), np.zeros(z.value, np.int64), np.zeros(z.value)
+    L.refp_mm_arrays(_p(row), _p(col), _p(val))
+    return "ok", {"format": COO, "nrows": n.value, "ncols": m.value, "row": row, "col": col, "val": val}
+
+
+def ref_write_matrix_market(path, coo):
+    L = refpipe()
+    row, col, val = (np.ascontiguousarray(coo["row"], np.int64), np.ascontiguousarray(coo["col"], np.int64),
+                     np.ascontiguousarray(coo["val"], np.float64))
+    _pchk(L, L.refp_write_mm(str(path).encode(), coo["nrows"], coo["ncols"], val.size, _p(row), _p(col), _p(val)))
 
 
 def ref_available():

@@ -77,4 +77,55 @@ int refp_build_training_csv(const char* features_csv, const char* profiles_csv, 
     });
 }
 
+// read_matrix_market through the reference (ingest.cpp:135-208).  kind: 0 ok,
+// 1 ParseError, 2 UnsupportedFormat, 3 IndexOutOfRange, 4 other (message in
+// refp_last_error); the matrix is kept for refp_mm_arrays.
+thread_local sparseoracle::CooMatrix g_mm;
+
+int refp_read_mm(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz, int32_t* kind) {
+    *kind = 0;
+    try {
+        g_mm = sparseoracle::read_matrix_market(path);
+        *nrows = g_mm.nrows;
+        *ncols = g_mm.ncols;
+        *nnz = g_mm.nnz();
+        return 0;
+    } catch (const sparseoracle::ParseError& e) {
+        *kind = 1;
+        g_err = e.what();
+    } catch (const sparseoracle::UnsupportedFormat& e) {
+        *kind = 2;
+        g_err = e.what();
+    } catch (const sparseoracle::IndexOutOfRange& e) {
+        *kind = 3;
+        g_err = e.what();
+    } catch (const std::exception& e) {
+        *kind = 4;
+        g_err = e.what();
+    }
+    return 1;
+}
+
+void refp_mm_arrays(int64_t* row, int64_t* col, double* val) {
+    for (size_t k = 0; k < g_mm.values.size(); ++k) {
+        row[k] = g_mm.row_idx[k];
+        col[k] = g_mm.col_idx[k];
+        val[k] = g_mm.values[k];
+    }
+}
+
+// write_matrix_market of a canonical COO given as arrays
+int refp_write_mm(const char* path, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row,
+                  const int64_t* col, const double* val) {
+    return guard([&] {
+        sparseoracle::CooMatrix m;
+        m.nrows = nrows;
+        m.ncols = ncols;
+        m.row_idx.assign(row, row + nnz);
+        m.col_idx.assign(col, col + nnz);
+        m.values.assign(val, val + nnz);
+        sparseoracle::write_matrix_market(m, path);
+    });
+}
+
 }  // extern "C"

@@ -9,11 +9,11 @@ the ctypes view of the same C-ABI used by the tests and bench.py.
 from .device import (COO, CSR, DIA, ELL, FORMAT_NAMES, HDC, HYB, AllFormatsInfeasible,
                      ConversionConfig, DeviceForest, DeviceMatrix, DimensionMismatch,
                      EmptyMatrix, Error, FeatureVector, FlatForest, IndexOutOfRange,
-                     InvalidInput, MalformedModel, PaddingOverflow, format_feasible,
-                     set_device, tune_ml)
+                     InvalidInput, MalformedModel, PaddingOverflow, ParseError,
+                     UnsupportedFormat, format_feasible, set_device, tune_ml)
 
 __all__ = ["COO", "CSR", "DIA", "ELL", "HYB", "HDC", "FORMAT_NAMES", "DeviceMatrix",
            "DeviceForest", "FlatForest", "ConversionConfig", "FeatureVector", "tune_ml",
            "format_feasible", "set_device", "Error", "InvalidInput", "PaddingOverflow",
            "DimensionMismatch", "EmptyMatrix", "MalformedModel", "IndexOutOfRange",
-           "AllFormatsInfeasible"]
+           "AllFormatsInfeasible", "ParseError", "UnsupportedFormat"]

@@ -96,6 +96,8 @@ _SIGS = {
     "so_matrix_upload_hyb": (C.c_int, [i64, i64, i64, vp, vp, i64, i64, vp, vp, vp, i64, P(vp)]),
     "so_matrix_upload_hdc": (C.c_int, [i64, i64, i64, vp, vp, i64, i64, vp, vp, vp, i64, P(vp)]),
     "so_coo_from_triplets": (C.c_int, [i64, i64, i64, vp, vp, vp, P(vp)]),
+    "so_read_matrix_market": (C.c_int, [C.c_char_p, P(vp)]),
+    "so_write_matrix_market": (C.c_int, [vp, C.c_char_p]),
     "so_matrix_import_csr_device": (C.c_int, [i64, i64, i64, vp, vp, vp, P(vp)]),
     "so_matrix_free": (None, [vp]),
     "so_matrix_info_get": (C.c_int, [vp, P(MatrixInfo)]),

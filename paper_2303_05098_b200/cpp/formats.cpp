@@ -26,6 +26,8 @@ void check(so_status st) {
         case SO_ALL_FORMATS_INFEASIBLE: throw AllFormatsInfeasible(msg);
         case SO_OUT_OF_MEMORY: throw DeviceOutOfMemory(msg);
         case SO_CUDA_ERROR: throw DeviceError(msg);
+        case SO_PARSE_ERROR: throw ParseError(msg);
+        case SO_UNSUPPORTED_FORMAT: throw UnsupportedFormat(msg);
         default: throw Error(msg);
     }
 }

@@ -497,6 +497,31 @@ so_status so_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n, const in
     });
 }
 
+so_status so_read_matrix_market(const char* path, so_matrix** out) {
+    return make(out, [&] {
+        if (!path) fail(SO_INVALID_INPUT, "null path");
+        return read_matrix_market(std::string(path), current_ctx().stream);
+    });
+}
+
+so_status so_write_matrix_market(const so_matrix* m, const char* path) {
+    return guard([&] {
+        if (!path) fail(SO_INVALID_INPUT, "null path");
+        cudaStream_t s = on_device(m);
+        if (m->format != SO_COO) fail(SO_INVALID_INPUT, "write_matrix_market: expects a COO matrix");
+        if (!coo_is_canonical(*m, s)) fail(SO_INVALID_INPUT, "write_matrix_market: matrix is not canonical");
+        const int64_t z = m->coo.nnz;
+        std::vector<int32_t> r32(static_cast<size_t>(z)), c32(static_cast<size_t>(z));
+        std::vector<double> v(static_cast<size_t>(z));
+        d2h(r32.data(), m->coo.row, z, s);
+        d2h(c32.data(), m->coo.col, z, s);
+        d2h(v.data(), m->coo.val, z, s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> r(r32.begin(), r32.end()), c(c32.begin(), c32.end());
+        write_matrix_market(m->nrows, m->ncols, z, r.data(), c.data(), v.data(), std::string(path));
+    });
+}
+
 so_status so_matrix_import_csr_device(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr_dev,
                                       const int32_t* col_dev, const double* val_dev, so_matrix** out) {
     return make(out, [&] {

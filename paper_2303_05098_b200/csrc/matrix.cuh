@@ -3,6 +3,7 @@
 #pragma once
 
 #include <memory>
+#include <string>
 
 #include "common.cuh"
 
@@ -113,6 +114,11 @@ bool coo_is_canonical(const so_matrix& coo, cudaStream_t s);
 so_matrix* coo_from_triplets_device(int64_t nrows, int64_t ncols, int64_t n, const int64_t* row_h,
                                     const int64_t* col_h, const double* val_h, cudaStream_t s);
 bool csr_rows_canonical(const so_matrix& csr, cudaStream_t s);
+
+// --- Matrix Market I/O (ingest.cu) ---
+so_matrix* read_matrix_market(const std::string& path, cudaStream_t s);
+void write_matrix_market(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row, const int64_t* col,
+                         const double* val, const std::string& path);
 
 // --- spmv (spmv.cu) ---
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s);

@@ -58,13 +58,21 @@ class CudaError(Error):
     pass
 
 
+class ParseError(Error):
+    pass
+
+
+class UnsupportedFormat(Error):
+    pass
+
+
 class OutOfMemory(Error):
     pass
 
 
 _STATUS = {1: InvalidInput, 2: PaddingOverflow, 3: DimensionMismatch, 4: EmptyMatrix,
            5: MalformedModel, 6: IndexOutOfRange, 7: AllFormatsInfeasible, 8: CudaError,
-           9: OutOfMemory, 10: Error}
+           9: OutOfMemory, 10: Error, 11: ParseError, 12: UnsupportedFormat}
 
 
 def _check(st):
@@ -122,6 +130,19 @@ class DeviceMatrix:
         _check(A.lib().so_coo_from_triplets(nrows, ncols, val.size, _ptr(row), _ptr(col), _ptr(val),
                                             C.byref(out)))
         return cls(out)
+
+    @classmethod
+    def read_matrix_market(cls, path):
+        """read_matrix_market (ingest.cpp:135-208): host-parallel parse, device
+        canonicalization -> canonical COO.  Raises ParseError /
+        UnsupportedFormat / IndexOutOfRange like the reference."""
+        out = C.c_void_p()
+        _check(A.lib().so_read_matrix_market(str(path).encode(), C.byref(out)))
+        return cls(out)
+
+    def write_matrix_market(self, path):
+        """write_matrix_market (ingest.cpp:210-224) of a canonical COO."""
+        _check(A.lib().so_write_matrix_market(self._h, str(path).encode()))
 
     @classmethod
     def csr(cls, nrows, ncols, row_ptr, col, val):

@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(REPO, "build", "reftests")
-SUITES = ["formats", "spmv", "features", "model", "tuners"]
+# + the Matrix Market cases of test_ingest.cpp restated in tests/support/cpp
+SUITES = ["formats", "spmv", "features", "model", "tuners", "matrix_market"]
 
 
 @pytest.mark.parametrize("suite", SUITES)
