@@ -153,7 +153,7 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
 // entries; a row longer than cap stands alone (and is split into pieces).
 // One thread walks kGroupChunk rows (chunk starts are forced group starts,
 // so the partition is deterministic and parallel) and flags group starts.
-constexpr int kGroupChunk = 128;
+constexpr int kGroupChunk = 1024;
 __global__ void group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t cap, int32_t* __restrict__ flag) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t lo = c * kGroupChunk;
@@ -346,31 +346,44 @@ struct DiagHist : OpBase {
     }
 };
 
-// Per-row count of entries that stay in the CSR part (diag count < thr).
-__global__ void hdc_rest_counts(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                const int32_t* __restrict__ bins, int64_t nrows, int64_t thr,
-                                int64_t* __restrict__ cnt) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= nrows) return;
-    int64_t c = 0;
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) c += bins[int64_t(col[k]) - i + nrows - 1] < thr;
-    cnt[i] = c;
+// HDC CSR part, entry-parallel (no per-row serial loop: an R-MAT hub row of
+// ~10^5 entries used to cost one thread milliseconds).  keep[k] = the entry's
+// diagonal count is below the threshold (formats.cpp:191); an exclusive scan
+// of keep gives every kept entry its slot, which is also the stable per-row
+// compaction because entries are in row order; row_ptr[i] = pos[rp[i]].
+struct KeepFlag : OpBase {
+    const int32_t* col;
+    const int32_t* bins;
+    int64_t nrows, thr;
+    int32_t* keep;
+    __device__ void operator()(int r, int64_t k, bool valid) const {
+        if (valid) keep[k] = bins[int64_t(col[k]) - r + nrows - 1] < thr ? 1 : 0;
+    }
+};
+
+// entries on diagonals below the threshold = the CSR part's size
+__global__ void hdc_rest_total(const int32_t* __restrict__ bins, int64_t nbins, int64_t thr,
+                               unsigned long long* __restrict__ total) {
+    unsigned long long t = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nbins; i += int64_t(gridDim.x) * blockDim.x)
+        if (bins[i] < thr) t += unsigned(bins[i]);
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(total, t);
 }
 
-// Stable per-row compaction of the CSR-part entries.
-__global__ void hdc_rest_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                              const double* __restrict__ val, const int32_t* __restrict__ bins,
-                              int64_t nrows, int64_t thr, const int64_t* __restrict__ orp,
-                              int32_t* __restrict__ ocol, double* __restrict__ oval) {
+__global__ void hdc_rest_rowptr(const int64_t* __restrict__ rp, const int64_t* __restrict__ pos, int64_t nrows,
+                                int64_t* __restrict__ orp) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= nrows) return;
-    int64_t p = orp[i];
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-        if (bins[int64_t(col[k]) - i + nrows - 1] < thr) {
-            ocol[p] = col[k];
-            oval[p] = val[k];
-            ++p;
-        }
+    if (i <= nrows) orp[i] = pos[rp[i]];
+}
+
+__global__ void hdc_rest_fill(const int32_t* __restrict__ keep, const int64_t* __restrict__ pos, int64_t z,
+                              const int32_t* __restrict__ col, const double* __restrict__ val,
+                              int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < z && keep[k]) {
+        ocol[pos[k]] = col[k];
+        oval[pos[k]] = val[k];
     }
 }
 
@@ -820,21 +833,45 @@ so_matrix* csr_to_format(const so_matrix& csr, int32_t target, const so_conversi
             // entries on diagonals with count >= thr go to the DIA part
             build_dia_part(csr, bins.get(), thr, m->dia, cap, s);
             CsrPart& c = m->csr;
-            DBuf<int64_t> cnt(n, s);
+            const int64_t z = csr.csr.nnz;
             c.row_ptr.alloc(n + 1, s);
-            if (n) {
-                hdc_rest_counts<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.csr.row_ptr.get(), csr.csr.col.get(),
-                                                                           bins.get(), n, thr, cnt.get());
-                SOB_LAUNCH("hdc_rest_counts");
+            // banded / stencil inputs: every entry is on a true diagonal -> empty CSR part
+            DBuf<unsigned long long> rest(1, s);
+            SOB_CUDA(cudaMemsetAsync(rest.get(), 0, sizeof(unsigned long long), s));
+            if (nbins) {
+                hdc_rest_total<<<grid_for(nbins, 256), 256, 0, s>>>(bins.get(), nbins, thr, rest.get());
+                SOB_LAUNCH("hdc_rest_total");
             }
-            exclusive_scan_i64(cnt.get(), c.row_ptr.get(), n, s);
-            c.nnz = d2h_scalar(c.row_ptr.get() + n, s);
+            if (d2h_scalar(rest.get(), s) == 0) {
+                SOB_CUDA(cudaMemsetAsync(c.row_ptr.get(), 0, c.row_ptr.bytes(), s));
+                c.nnz = 0;
+                c.col.alloc(0, s);
+                c.val.alloc(0, s);
+                build_row_blocks(c, n, s);
+                return m.release();
+            }
+            DBuf<int32_t> keep(z, s);
+            DBuf<int64_t> pos(z + 1, s);
+            if (z > 0) {
+                KeepFlag kf;
+                kf.col = csr.csr.col.get();
+                kf.bins = bins.get();
+                kf.nrows = n;
+                kf.thr = thr;
+                kf.keep = keep.get();
+                sweep(csr, kf, s);
+            }
+            exclusive_scan_i32_to_i64(keep.get(), pos.get(), z, s);
+            hdc_rest_rowptr<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(csr.csr.row_ptr.get(), pos.get(), n,
+                                                                          c.row_ptr.get());
+            SOB_LAUNCH("hdc_rest_rowptr");
+            c.nnz = d2h_scalar(pos.get() + z, s);
             c.col.alloc(c.nnz, s);
             c.val.alloc(c.nnz, s);
             if (c.nnz) {
-                hdc_rest_fill<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(
-                    csr.csr.row_ptr.get(), csr.csr.col.get(), csr.csr.val.get(), bins.get(), n, thr,
-                    c.row_ptr.get(), c.col.get(), c.val.get());
+                hdc_rest_fill<<<unsigned(ceil_div(z, 256)), 256, 0, s>>>(keep.get(), pos.get(), z,
+                                                                       csr.csr.col.get(), csr.csr.val.get(),
+                                                                       c.col.get(), c.val.get());
                 SOB_LAUNCH("hdc_rest_fill");
             }
             build_row_blocks(c, n, s);
