@@ -34,7 +34,7 @@ CONFIGS = {
 }
 FMT = ("COO", "CSR", "DIA", "ELL", "HYB", "HDC")
 # dominant kernel per format on the workload (HDC with an empty CSR part runs the DIA kernel)
-KERNEL_OF = {"COO": "coo_chunk_kernel", "CSR": "csr_warp_kernel", "DIA": "dia_kernel", "ELL": "ell_kernel",
+KERNEL_OF = {"COO": "coo_warp_kernel", "CSR": "csr_warp_kernel", "DIA": "dia_kernel", "ELL": "ell_kernel",
              "HYB": "ell_kernel", "HDC": "dia_kernel"}
 
 
@@ -61,14 +61,18 @@ def build_workload(name):
     raise ValueError(name)
 
 
-def committed_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    capture (profiles/traffic.json, written by scripts/ncu_summary.py)."""
+def committed_traffic(kernel, workload):
+    """DRAM bytes per launch of `kernel` on `workload` from the committed ncu
+    --set full capture (profiles/traffic.json, written by
+    scripts/ncu_summary.py; keys "kernel@workload" or "kernel" = banded)."""
     try:
         with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
     except Exception:
         return None
+    if f"{kernel}@{workload}" in t:
+        return t[f"{kernel}@{workload}"]
+    return t.get(kernel) if workload == "banded" else None
 
 
 def peaks():
@@ -351,7 +355,7 @@ def main():
                        "nrows": csr.nrows, "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": round(nbytes / sec / 1e9, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(nbytes / sec / 1e9 / peak, 4),
-                         "traffic": committed_traffic(KERNEL_OF[FMT[tuned]]), "algorithmic_bytes": nbytes,
+                         "traffic": committed_traffic(KERNEL_OF[FMT[tuned]], args.workload), "algorithmic_bytes": nbytes,
                          "kernel": KERNEL_OF[FMT[tuned]], "peak_kind": peak_kind},
             "e2e": {"value": round(world * nbytes / e2e_sec / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * csr.ncols, "d2h_bytes_per_step": 8 * csr.nrows},
