@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kB) csr_sweep(const int32_t* __restrict__ blk,
 }
 
 struct OpBase {
+    static constexpr bool kHasEntry = false;  // op.entry(r, col, valid): column-prefetching sweep
     __device__ void begin() {}
     __device__ void row(int, bool, int64_t) {}
     __device__ void end() {}
@@ -95,7 +96,7 @@ void sweep(const so_matrix& csr, Op op, cudaStream_t s, int per_sm = 4) {
 // Row-lockstep sweep of every entry; rows longer than grp_cap go
 // through the piece-parallel sweep (no single-warp tail on skewed rows).
 template <class Op>
-void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s) {
+void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s, bool prefetch_cols = false) {
     if (csr.nrows <= 0) return;
     const CsrPart& c = csr.csr;
     const int64_t skip = c.nlong > 0 ? int64_t(c.grp_cap) : INT64_MAX;
@@ -104,8 +105,16 @@ void row_sweep_launch(const so_matrix& csr, Op op, cudaStream_t s) {
         ticket.alloc(1, s);
         SOB_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
     }
-    row_sweep<Op><<<grid_for(ceil_div(csr.nrows, 32) * 256 / 8, 256, 8), 256, 0, s>>>(c.row_ptr.get(), csr.nrows,
-                                                                                        op, skip, ticket.get());
+    const int g = grid_for(ceil_div(csr.nrows, 32) * 256 / 8, 256, 8);
+    if constexpr (Op::kHasEntry) {
+        if (prefetch_cols) {
+            row_sweep_cols<Op><<<g, 256, 0, s>>>(c.row_ptr.get(), c.col.get(), csr.nrows, op, skip, ticket.get());
+        } else {
+            row_sweep<Op><<<g, 256, 0, s>>>(c.row_ptr.get(), csr.nrows, op, skip, ticket.get());
+        }
+    } else {
+        row_sweep<Op><<<g, 256, 0, s>>>(c.row_ptr.get(), csr.nrows, op, skip, ticket.get());
+    }
     SOB_LAUNCH("row_sweep");
     if (c.nlong > 0) {
         piece_sweep<Op><<<unsigned(c.npieces), 256, 0, s>>>(c.piece_k.get(), c.long_row.get(), c.long_piece.get(),
@@ -326,6 +335,7 @@ struct FillHybCoo : OpBase {
 // ------------------------------------------------------------------- HDC
 
 struct DiagHist : OpBase {
+    static constexpr bool kHasEntry = true;
     const int32_t* col;
     int64_t nrows;
     int32_t* bins;
@@ -339,6 +349,9 @@ struct DiagHist : OpBase {
     __device__ void operator()(int r, int64_t k, bool valid) {
         const int32_t key = valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1;
         hash_add(*h, bins, key);
+    }
+    __device__ void entry(int r, int32_t c, bool valid) {
+        hash_add(*h, bins, valid ? int32_t(int64_t(c) - r + nrows - 1) : -1);
     }
     __device__ void end() {
         __syncthreads();
@@ -565,7 +578,7 @@ void diag_histogram(const so_matrix& csr, int32_t* bins, cudaStream_t s) {
     dh.col = csr.csr.col.get();
     dh.nrows = csr.nrows;
     dh.bins = bins;
-    row_sweep_launch(csr, dh, s);
+    row_sweep_launch(csr, dh, s, /*prefetch_cols=*/true);
 }
 
 void build_dia_part(const so_matrix& csr, const int32_t* bins_in, int64_t thr, DiaPart& dia, int64_t cap,

@@ -69,6 +69,9 @@ struct FeatCsrOp {
     __device__ void operator()(int r, int64_t k, bool valid) {
         hash_add(*h, bins, valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1);
     }
+    __device__ void entry(int r, int32_t c, bool valid) {
+        hash_add(*h, bins, valid ? int32_t(int64_t(c) - r + nrows - 1) : -1);
+    }
     __device__ void end() {
         const unsigned long long v = warp_sum(visits);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&st->visits, v);
@@ -755,10 +758,10 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         unsigned* ticket = c.nlong > 0 ? &st->ticket : nullptr;  // skewed rows: dynamic groups
         if (accum) {
             FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep<FeatCsrOp<true>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip, ticket);
+            row_sweep_cols<FeatCsrOp<true>><<<g, 256, 0, s>>>(c.row_ptr.get(), c.col.get(), n, op, skip, ticket);
         } else {
             FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep<FeatCsrOp<false>><<<g, 256, 0, s>>>(c.row_ptr.get(), n, op, skip, ticket);
+            row_sweep_cols<FeatCsrOp<false>><<<g, 256, 0, s>>>(c.row_ptr.get(), c.col.get(), n, op, skip, ticket);
         }
         SOB_LAUNCH("feat_csr");
         if (c.nlong > 0) {

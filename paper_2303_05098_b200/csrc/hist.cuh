@@ -36,9 +36,20 @@ __device__ __forceinline__ void hash_init(SmemHash& h) {
 // warp must call this (warp-synchronous).
 __device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbins, int32_t key) {
     const unsigned lane = threadIdx.x & 31u;
-    // distinct dummy keys for idle lanes so they never merge with real ones
-    const int32_t k = key >= 0 ? key : -2 - int32_t(lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    // fast path: every valid lane holds the same key (banded rows swept in
+    // lockstep) -- a vote instead of __match_any_sync
+    const unsigned valid = __ballot_sync(0xffffffffu, key >= 0);
+    if (!valid) return;
+    const int first = __ffs(valid) - 1;
+    const int32_t k0 = __shfl_sync(0xffffffffu, key, first);
+    unsigned peers;
+    if (__all_sync(0xffffffffu, key < 0 || key == k0)) {
+        peers = valid;
+    } else {
+        // distinct dummy keys for idle lanes so they never merge with real ones
+        const int32_t k = key >= 0 ? key : -2 - int32_t(lane);
+        peers = __match_any_sync(0xffffffffu, k);
+    }
     if (key < 0) return;
     const int leader = __ffs(peers) - 1;
     if (int(lane) != leader) return;
@@ -141,6 +152,57 @@ __global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp,
             const int64_t ll = __shfl_sync(0xffffffffu, elen, src);
             const int lr = __shfl_sync(0xffffffffu, int(r), src);
             for (int64_t j0 = kLockstepMax; j0 < ll; j0 += 32) op(lr, la + j0 + lane, j0 + lane < ll);
+        }
+    }
+    op.end();
+}
+
+// row_sweep for ops that only need the column of an entry (op.entry(r, col,
+// valid)): the columns of 8 lockstep slots are loaded before any is handed
+// to the op, so each lane keeps 8 independent loads in flight instead of one
+// load per (synchronising) hash update.
+template <class Op>
+__global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                      int64_t nrows, Op op, int64_t skip_above = INT64_MAX,
+                                                      unsigned* ticket = nullptr) {
+    constexpr int U = 8;
+    op.begin();
+    const int lane = int(threadIdx.x & 31u);
+    const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / 32);
+    for (int64_t wb = ticket ? next_group(ticket) : (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32;
+         wb < nrows; wb = ticket ? next_group(ticket) : wb + nwarps * 32) {
+        const int64_t r = wb + lane;
+        const bool has = r < nrows;
+        const int64_t a = has ? rp[r] : 0;
+        const int64_t len = has ? rp[r + 1] - a : 0;
+        op.row(int(r), has, len);
+        const int64_t elen = len > skip_above ? 0 : len;
+        const int64_t maxlen = warp_max(elen < kLockstepMax ? elen : int64_t(kLockstepMax));
+        for (int64_t j0 = 0; j0 < maxlen; j0 += U) {
+            int32_t cv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) cv[u] = (has && j0 + u < elen) ? ld_stream(col + a + j0 + u) : 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (j0 + u < maxlen) op.entry(int(r), cv[u], has && j0 + u < elen);
+        }
+        unsigned longm = __ballot_sync(0xffffffffu, elen > kLockstepMax);
+        while (longm) {
+            const int src = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t la = __shfl_sync(0xffffffffu, a, src);
+            const int64_t ll = __shfl_sync(0xffffffffu, elen, src);
+            const int lr = __shfl_sync(0xffffffffu, int(r), src);
+            for (int64_t j0 = kLockstepMax; j0 < ll; j0 += 32 * U) {
+                int32_t cv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t j = j0 + u * 32 + lane;
+                    cv[u] = j < ll ? ld_stream(col + la + j) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) op.entry(lr, cv[u], j0 + u * 32 + lane < ll);
+            }
         }
     }
     op.end();

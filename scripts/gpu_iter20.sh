@@ -1,0 +1,5 @@
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/it_pytest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/it_pytest.log
+timeout 600 python scripts/profile_features.py --ids 877 1843 555 165 706 1692 521 --reps 5 2>&1 | grep "^id"
+timeout 900 python scripts/convert_bench.py 2>&1 | tail -3
+timeout 1500 python scripts/config4.py --count 2000 --reps 20 --only profiles/config4_split_r01b.json --model paper_2303_05098_b200/models/b200_forest.txt --out gpurun_out/c4_tuned.csv > gpurun_out/c4.log 2>&1; echo "c4 rc=$?"
