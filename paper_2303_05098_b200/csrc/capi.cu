@@ -367,6 +367,9 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
     SOB_CUDA(cudaEventRecord(ev[0], s));
     SOB_CUDA(cudaStreamWaitEvent(c.copy_in, ev[0], 0));
     SOB_CUDA(cudaStreamWaitEvent(c.copy_out, ev[0], 0));
+    // every x window goes up first (the copy engine never waits on the host
+    // enqueueing kernels and read-backs), then chunk k's rows run as soon as
+    // their window has landed and chunk k's y goes down behind them
     int64_t x_hi = 0;
     for (int64_t k = 0; k < nchunks; ++k) {
         const int64_t a = k * rows_per, b = std::min(n, a + rows_per);
@@ -379,6 +382,10 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
             x_hi = want;
         }
         SOB_CUDA(cudaEventRecord(ev[1 + 2 * k], c.copy_in));
+    }
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int64_t a = k * rows_per, b = std::min(n, a + rows_per);
+        if (a >= b) break;
         SOB_CUDA(cudaStreamWaitEvent(s, ev[1 + 2 * k], 0));
         spmv_device_rows(m, dx.get(), dy.get(), a, b, s);
         SOB_CUDA(cudaEventRecord(ev[2 + 2 * k], s));

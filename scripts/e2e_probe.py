@@ -24,3 +24,36 @@ if os.environ.get("COPY_PROBE"):
         for _ in range(20): f()
         torch.cuda.synchronize(); dt = (time.perf_counter() - t0) / 20
         print(name, "%.3f ms %.1f GB/s" % (dt * 1e3, 32e6 / dt / 1e9))
+
+if os.environ.get("DUPLEX_PROBE"):
+    # full-duplex check: 32 MB H2D and 32 MB D2H on two streams at once
+    xd = torch.empty(csr.ncols, dtype=torch.float64, device="cuda")
+    yd = torch.empty(csr.nrows, dtype=torch.float64, device="cuda")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        with torch.cuda.stream(sa):
+            xd.copy_(xh, non_blocking=True)
+        with torch.cuda.stream(sb):
+            yh.copy_(yd, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(20):
+        with torch.cuda.stream(sa):
+            xd.copy_(xh, non_blocking=True)
+        with torch.cuda.stream(sb):
+            yh.copy_(yd, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 20
+    print("duplex h2d+d2h 2x32MB: %.3f ms, %.1f GB/s aggregate" % (dt * 1e3, 64e6 / dt / 1e9))
+    # chunked ping-pong: 16 x 2 MB each way, alternating
+    t0 = time.perf_counter()
+    for _ in range(20):
+        for k in range(16):
+            lo, hi = k * csr.nrows // 16, (k + 1) * csr.nrows // 16
+            with torch.cuda.stream(sa):
+                xd[lo:hi].copy_(xh[lo:hi], non_blocking=True)
+            with torch.cuda.stream(sb):
+                yh[lo:hi].copy_(yd[lo:hi], non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 20
+    print("duplex chunked 16x(2+2)MB: %.3f ms, %.1f GB/s aggregate" % (dt * 1e3, 64e6 / dt / 1e9))
