@@ -102,6 +102,24 @@ def iterate(s: Slice, x_cur, x_next, iters, spmv_rows, exchange, copy=None):
     return x_cur
 
 
+# ------------------------------------------------ batches of independent matrices
+
+def lpt_shard(weights, world: int, rank: int):
+    """Greedy longest-processing-time assignment of independent items (config
+    4: matrices weighted by their nnz) to `world` ranks; returns this rank's
+    item indices in ascending order.  Deterministic (ties -> lowest index /
+    rank), so every rank computes the same partition without communication;
+    the largest load is at most 4/3 of optimal (Graham's bound)."""
+    loads = [0.0] * world
+    mine = []
+    for i in sorted(range(len(weights)), key=lambda i: (-weights[i], i)):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        loads[r] += weights[i]
+        if r == rank:
+            mine.append(i)
+    return sorted(mine)
+
+
 # ------------------------------------------------------ fused peer-memory halo
 
 class PeerWindows:

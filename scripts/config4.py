@@ -31,14 +31,9 @@ FMT = P.FORMAT_NAMES
 
 
 def lpt_shard(specs, world, rank):
-    loads = [0] * world
-    mine = []
-    for s in sorted(specs, key=lambda s: -synth_dev.nnz_estimate(s)):
-        r = int(np.argmin(loads))
-        loads[r] += synth_dev.nnz_estimate(s)
-        if r == rank:
-            mine.append(s)
-    return sorted(mine, key=lambda s: s["id"])
+    from paper_2303_05098_b200 import dist as D
+    idx = D.lpt_shard([synth_dev.nnz_estimate(s) for s in specs], world, rank)
+    return sorted((specs[i] for i in idx), key=lambda s: s["id"])
 
 
 def time_format(m, x, y, reps, stream):

@@ -124,3 +124,36 @@ def test_partition_geometry():
             assert sb - sa == min(h, s.nloc)
             assert s.own_lo <= sa and sb <= s.own_hi
             assert (ra, rb) in [(0, s.own_lo), (s.own_hi, s.nwin)]
+
+
+def _lpt_worker(rank, world, port, weights, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    mine = D.lpt_shard(weights, world, rank)
+    got = [None] * world
+    dist.all_gather_object(got, (rank, mine))
+    q.put(got)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_sharding_covers_every_matrix_once(world):
+    """Config 4 batch sharding: each rank derives its LPT shard locally; the
+    gathered shards partition the corpus and respect Graham's 4/3 bound."""
+    rng = np.random.default_rng(4)
+    weights = list(np.exp(rng.uniform(np.log(5e4), np.log(1.3e8), 200)))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_lpt_worker, args=(r, world, port, weights, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    views = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shards = dict(views[0])
+    assert all(dict(v) == shards for v in views)  # every rank saw the same partition
+    flat = sorted(i for r in range(world) for i in shards[r])
+    assert flat == list(range(len(weights)))
+    loads = [sum(weights[i] for i in shards[r]) for r in range(world)]
+    assert max(loads) <= 4 / 3 * max(sum(weights) / world, max(weights)) + 1e-6
