@@ -587,6 +587,46 @@ __global__ void __launch_bounds__(256, MINB) coo_blk(int64_t z, int64_t nrows, c
     coo_finish<IT>(lane, chunk, base, cnt, z, nrows, r, p, prev_row, next_row, y, rec);
 }
 
+// (e) coo_pf + hot-column cache: the K most frequent columns are re-encoded
+// as -(slot+1) in the column array and their x values are staged in shared
+// memory once per CTA; a gather of a hot column is a shared-memory load.
+template <int IT, int MINB, int K>
+__global__ void __launch_bounds__(256, MINB) coo_hot(int64_t z, int64_t nrows, const int* __restrict__ row,
+        const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
+        const int* __restrict__ hot, double* __restrict__ y, CooRec* __restrict__ rec) {
+    extern __shared__ double xs[];
+    for (int i = threadIdx.x; i < K; i += blockDim.x) xs[i] = __ldg(x + hot[i]);
+    __syncthreads();
+    constexpr int CH = 32 * IT;
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = (z + CH - 1) / CH;
+    const int64_t stride = int64_t(gridDim.x) * 8;
+    int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (chunk >= nchunks) return;
+    int r[IT], c[IT]; double v[IT];
+    ld_blk<IT>(row, col, val, chunk * CH + lane * IT, int(min(z - chunk * CH, int64_t(CH))) - lane * IT, r, c, v);
+    while (true) {
+        const int64_t base = chunk * CH;
+        const int cnt = int(min(z - base, int64_t(CH)));
+        double p[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const double xv = c[j] < 0 ? xs[-c[j] - 1] : __ldg(x + c[j]);
+            p[j] = lane * IT + j < cnt ? xmul(v[j], xv) : 0.0;
+        }
+        const int prev_row = base > 0 ? row[base - 1] : -1;
+        const int next_row = base + cnt < z ? row[base + cnt] : -1;
+        int rc[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) rc[j] = r[j];
+        const int64_t nx = chunk + stride;
+        if (nx < nchunks) ld_blk<IT>(row, col, val, nx * CH + lane * IT, int(min(z - nx * CH, int64_t(CH))) - lane * IT, r, c, v);
+        coo_finish<IT>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
+        if (nx >= nchunks) break;
+        chunk = nx;
+    }
+}
+
 // (c) persistent, blocked, next chunk prefetched before the finish
 template <int IT, int MINB>
 __global__ void __launch_bounds__(256, MINB) coo_pf(int64_t z, int64_t nrows, const int* __restrict__ row,
@@ -1061,6 +1101,38 @@ int main(int argc, char** argv) {
             go("coo_blk8 B6 fix8", 8, coo_blk<8, 6>, g8, true);
             go("coo_blk4 B8 fix8", 4, coo_blk<4, 8>, g4, true);
             go("coo_pf8 B3 fix8", 8, coo_pf<8, 3>, sms * 3, true);
+            if (getenv("LAB_HOT")) {
+                // column frequencies -> hot set -> encoded column array
+                std::vector<int64_t> freq(n, 0);
+                for (int64_t k = 0; k < z; ++k) freq[m.col[k]]++;
+                std::vector<int> order(n);
+                for (int64_t i = 0; i < n; ++i) order[i] = int(i);
+                std::sort(order.begin(), order.end(), [&](int a, int b) { return freq[a] > freq[b] || (freq[a] == freq[b] && a < b); });
+                auto trial = [&](int K, auto kern, int per) {
+                    std::vector<int> slot(n, -1);
+                    int64_t covered = 0;
+                    for (int i = 0; i < K; ++i) { slot[order[i]] = i; covered += freq[order[i]]; }
+                    std::vector<int> enc(z);
+                    for (int64_t k = 0; k < z; ++k) enc[k] = slot[m.col[k]] >= 0 ? -(slot[m.col[k]] + 1) : m.col[k];
+                    int *dcolh, *dhot;
+                    CK(cudaMalloc(&dcolh, (z + 64) * 4)); CK(cudaMalloc(&dhot, K * 4));
+                    CK(cudaMemcpy(dcolh, enc.data(), z * 4, cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(dhot, order.data(), K * 4, cudaMemcpyHostToDevice));
+                    const size_t sm = size_t(K) * 8;
+                    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                    const int64_t nch = (z + 255) / 256;
+                    char nm[64]; snprintf(nm, 64, "coo_hot K%d x%d cov%.2f", K, per, double(covered) / z);
+                    report(nm, coo_bytes, [&] {
+                        kern<<<sms * per, 256, sm>>>(z, n, drow, dcolh, dval, dx, dhot, dy, drec);
+                        coo_fix8<<<unsigned((nch + 255) / 256), 256>>>(nch, drec, dy);
+                    }, check(false, 1 << 30));
+                    cudaFree(dcolh); cudaFree(dhot);
+                };
+                trial(4096, coo_hot<8, 3, 4096>, 3);
+                trial(8192, coo_hot<8, 3, 8192>, 3);
+                trial(12288, coo_hot<8, 2, 12288>, 2);
+                trial(24576, coo_hot<8, 1, 24576>, 1);
+            }
             go("coo_pf4 B6 fix8", 4, coo_pf<4, 6>, sms * 6, true);
             go("coo_pf4 B5 fix8", 4, coo_pf<4, 5>, sms * 5, true);
             {
