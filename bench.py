@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--workload", default="banded", choices=sorted(CONFIGS))
     p.add_argument("--all-formats", action="store_true", default=True)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-other-configs", action="store_true",
+                   help="skip the per-format lines of configs 1 and 3 (diagnostic, not the headline)")
     return p.parse_args()
 
 
@@ -278,6 +280,54 @@ def main():
                               "gbs": round(nbytes / sec / 1e9, 1),
                               "frac": round(nbytes / sec / 1e9 / peak, 3), "bytes": nbytes}
 
+    # ---- configs 1 and 3, per format (diagnostic lines beside the headline) ---
+    other = {}
+    if not args.no_other_configs and rank == 0:
+        from paper_2303_05098_b200 import synth, synth_dev
+        lap = synth.laplacian_2d(1000, seed=1)
+        work = {"config1 laplacian 1000^2 (host generator, seed 1)":
+                P.DeviceMatrix.csr(lap.nrows, lap.ncols, lap.row_ptr, lap.col, lap.val),
+                "config3 rmat 2^22 d16 (device generator, seed 42)":
+                synth_dev.rmat(1 << 22, 16, 42).to_device_matrix()}
+        for wname, wbase in work.items():
+            xo = torch.ones(wbase.ncols, dtype=torch.float64, device="cuda")
+            yo = torch.empty(wbase.nrows, dtype=torch.float64, device="cuda")
+            row = {}
+            for f in range(6):
+                try:
+                    mo = wbase.convert(f)
+                except P.PaddingOverflow:
+                    row[FMT[f]] = "infeasible"
+                    continue
+                # small matrices: rotate over enough copies (matrix and x) that
+                # every step reads cold inputs -- "inputs larger than L2"
+                # without the dirty-line write-back a write flush leaves behind
+                ncopy = int(np.ceil(3 * l2 / max(mo.spmv_bytes, 1))) + 1 if needs_flush(mo) else 1
+                mats_o = [mo] + [mo.convert(f) for _ in range(ncopy - 1)]
+                xs_o = [xo] + [torch.ones_like(xo) for _ in range(ncopy - 1)]
+                # steps enqueued back to back (events on the launching stream,
+                # one sync at the end), as in time_format
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(23)]
+                torch.cuda.synchronize()
+                for r, (a_, b_) in enumerate(evs):
+                    k = r % ncopy
+                    a_.record(stream)
+                    mats_o[k].spmv_device(xs_o[k].data_ptr(), yo.data_ptr(), sptr)
+                    b_.record(stream)
+                torch.cuda.synchronize()
+                ts = [a_.elapsed_time(b_) * 1e-3 for a_, b_ in evs[3:]]
+                fl = ncopy > 1
+                del mats_o, xs_o
+                sec_o = float(np.mean(ts))
+                row[FMT[f]] = {"ms": round(sec_o * 1e3, 4), "gbs": round(mo.spmv_bytes / sec_o / 1e9, 1),
+                               "frac": round(mo.spmv_bytes / sec_o / 1e9 / peak, 3),
+                               "l2": f"rotating {ncopy} copies (cold inputs)" if fl else "larger than L2"}
+                del mo
+            other[wname] = row
+            del wbase, xo, yo
+        torch.cuda.empty_cache()
+
     # ---- tuner: on-device features + predict (measured-optimal label model) ---
     best = min((f for f in mats), key=lambda f: per_format[FMT[f]]["ms"])
     tuned = best
@@ -361,6 +411,7 @@ def main():
                     "h2d_bytes_per_step": 8 * csr.ncols, "d2h_bytes_per_step": 8 * csr.nrows},
             "gpu_launches": launches,
             "clocks": clk, "cpu_baseline": cpu, "formats": per_format, "tune": tune,
+            "other_configs": other,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
