@@ -350,10 +350,13 @@ struct DiagHist : OpBase {
         const int32_t key = valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1;
         hash_add(*h, bins, key);
     }
-    __device__ void entry(int r, int32_t c, bool valid) {
-        hash_add(*h, bins, valid ? int32_t(int64_t(c) - r + nrows - 1) : -1);
+    SlotCache cache;
+    __device__ void entry(int r, int32_t c, bool valid, int slot) {
+        const int32_t key = valid ? int32_t(int64_t(c) - r + nrows - 1) : -1;
+        if (!cache.add(*h, bins, key, slot)) hash_add(*h, bins, key);
     }
     __device__ void end() {
+        cache.flush(*h, bins);
         __syncthreads();
         hash_flush(*h, bins);
     }

@@ -69,12 +69,15 @@ struct FeatCsrOp {
     __device__ void operator()(int r, int64_t k, bool valid) {
         hash_add(*h, bins, valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1);
     }
-    __device__ void entry(int r, int32_t c, bool valid) {
-        hash_add(*h, bins, valid ? int32_t(int64_t(c) - r + nrows - 1) : -1);
+    SlotCache cache;
+    __device__ void entry(int r, int32_t c, bool valid, int slot) {
+        const int32_t key = valid ? int32_t(int64_t(c) - r + nrows - 1) : -1;
+        if (!cache.add(*h, bins, key, slot)) hash_add(*h, bins, key);
     }
     __device__ void end() {
         const unsigned long long v = warp_sum(visits);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&st->visits, v);
+        cache.flush(*h, bins);
         __syncthreads();
         hash_flush(*h, bins);
     }

@@ -32,28 +32,54 @@ __device__ __forceinline__ void hash_init(SmemHash& h) {
     if (threadIdx.x == 0) h.used = 0;
 }
 
-// key >= 0 valid; key < 0 means "no entry for this lane".  Every lane of the
-// warp must call this (warp-synchronous).
-__device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbins, int32_t key) {
-    const unsigned lane = threadIdx.x & 31u;
-    // fast path: every valid lane holds the same key (banded rows swept in
-    // lockstep) -- a vote instead of __match_any_sync
-    const unsigned valid = __ballot_sync(0xffffffffu, key >= 0);
-    if (!valid) return;
-    const int first = __ffs(valid) - 1;
-    const int32_t k0 = __shfl_sync(0xffffffffu, key, first);
-    unsigned peers;
-    if (__all_sync(0xffffffffu, key < 0 || key == k0)) {
-        peers = valid;
-    } else {
-        // distinct dummy keys for idle lanes so they never merge with real ones
-        const int32_t k = key >= 0 ? key : -2 - int32_t(lane);
-        peers = __match_any_sync(0xffffffffu, k);
+__device__ __forceinline__ void hash_insert_one(SmemHash& h, int32_t* __restrict__ gbins, int32_t key, int32_t add);
+
+// Per-warp cache of the key seen at each lockstep slot (banded rows present
+// the same key at slot j in every row: offset_j + n - 1).  Slot j lives in
+// lane j % 32, register j / 32.  A uniform step costs one vote and one
+// register add instead of a hash update; a slot whose key changes spills its
+// count to the hash.  Call flush() (every lane) before the hash is flushed.
+struct SlotCache {
+    int32_t key[2] = {-1, -1};
+    int32_t cnt[2] = {0, 0};
+    // all 32 lanes call; returns true when the step was absorbed
+    __device__ __forceinline__ bool add(SmemHash& h, int32_t* gbins, int32_t k, int slot) {
+        if (slot < 0) return false;
+        const unsigned valid = __ballot_sync(0xffffffffu, k >= 0);
+        if (!valid) return true;
+        const int32_t k0 = __shfl_sync(0xffffffffu, k, __ffs(valid) - 1);
+        if (!__all_sync(0xffffffffu, k < 0 || k == k0)) return false;
+        if (int(threadIdx.x & 31u) == (slot & 31)) {
+            const int w = slot >> 5;
+            const int32_t ck = w ? key[1] : key[0];
+            const int32_t cc = w ? cnt[1] : cnt[0];
+            int32_t nk = k0, nc = __popc(valid);
+            if (ck == k0) {
+                nc += cc;
+            } else if (ck >= 0) {
+                hash_insert_one(h, gbins, ck, cc);
+            }
+            if (w) {
+                key[1] = nk;
+                cnt[1] = nc;
+            } else {
+                key[0] = nk;
+                cnt[0] = nc;
+            }
+        }
+        return true;
     }
-    if (key < 0) return;
-    const int leader = __ffs(peers) - 1;
-    if (int(lane) != leader) return;
-    const int32_t add = __popc(peers);
+    __device__ __forceinline__ void flush(SmemHash& h, int32_t* gbins) {
+        for (int w = 0; w < 2; ++w)
+            if (key[w] >= 0 && cnt[w] > 0) hash_insert_one(h, gbins, key[w], cnt[w]);
+        key[0] = key[1] = -1;
+        cnt[0] = cnt[1] = 0;
+    }
+};
+
+// One lane adds `add` to `key`: shared-memory hash, or the global bins when
+// the key finds no slot.  Not warp-synchronous.
+__device__ __forceinline__ void hash_insert_one(SmemHash& h, int32_t* __restrict__ gbins, int32_t key, int32_t add) {
     unsigned slot = unsigned(key) & (kHashSlots - 1);
     // scattered keys (hash half full): only the home slot is checked, so keys
     // that were hot early still merge in shared memory and the rest go
@@ -83,6 +109,30 @@ __device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbin
         slot = (slot + 1) & (kHashSlots - 1);
     }
     atomicAdd(gbins + key, add);
+}
+
+// key >= 0 valid; key < 0 means "no entry for this lane".  Every lane of the
+// warp must call this (warp-synchronous).
+__device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbins, int32_t key) {
+    const unsigned lane = threadIdx.x & 31u;
+    // fast path: every valid lane holds the same key (banded rows swept in
+    // lockstep) -- a vote instead of __match_any_sync
+    const unsigned valid = __ballot_sync(0xffffffffu, key >= 0);
+    if (!valid) return;
+    const int first = __ffs(valid) - 1;
+    const int32_t k0 = __shfl_sync(0xffffffffu, key, first);
+    unsigned peers;
+    if (__all_sync(0xffffffffu, key < 0 || key == k0)) {
+        peers = valid;
+    } else {
+        // distinct dummy keys for idle lanes so they never merge with real ones
+        const int32_t k = key >= 0 ? key : -2 - int32_t(lane);
+        peers = __match_any_sync(0xffffffffu, k);
+    }
+    if (key < 0) return;
+    const int leader = __ffs(peers) - 1;
+    if (int(lane) != leader) return;
+    hash_insert_one(h, gbins, key, __popc(peers));
 }
 
 __device__ __forceinline__ void hash_flush(SmemHash& h, int32_t* __restrict__ gbins) {
@@ -158,9 +208,10 @@ __global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp,
 }
 
 // row_sweep for ops that only need the column of an entry (op.entry(r, col,
-// valid)): the columns of 8 lockstep slots are loaded before any is handed
-// to the op, so each lane keeps 8 independent loads in flight instead of one
-// load per (synchronising) hash update.
+// valid, slot)): the columns of 8 lockstep slots are loaded before any is
+// handed to the op, so each lane keeps 8 independent loads in flight instead
+// of one load per (synchronising) hash update.  slot = the lockstep slot j
+// (< kLockstepMax), or -1 in the cooperative tail of a long row.
 template <class Op>
 __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                       int64_t nrows, Op op, int64_t skip_above = INT64_MAX,
@@ -181,10 +232,11 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
         for (int64_t j0 = 0; j0 < maxlen; j0 += U) {
             int32_t cv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) cv[u] = (has && j0 + u < elen) ? ld_stream(col + a + j0 + u) : 0;
+            // L1-allocating: a lane's 8 consecutive columns share one or two sectors
+            for (int u = 0; u < U; ++u) cv[u] = (has && j0 + u < elen) ? __ldg(col + a + j0 + u) : 0;
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (j0 + u < maxlen) op.entry(int(r), cv[u], has && j0 + u < elen);
+                if (j0 + u < maxlen) op.entry(int(r), cv[u], has && j0 + u < elen, int(j0 + u));
         }
         unsigned longm = __ballot_sync(0xffffffffu, elen > kLockstepMax);
         while (longm) {
@@ -201,7 +253,7 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
                     cv[u] = j < ll ? ld_stream(col + la + j) : 0;
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) op.entry(lr, cv[u], j0 + u * 32 + lane < ll);
+                for (int u = 0; u < U; ++u) op.entry(lr, cv[u], j0 + u * 32 + lane < ll, -1);
             }
         }
     }
