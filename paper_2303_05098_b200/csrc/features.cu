@@ -70,9 +70,17 @@ struct FeatCsrOp {
         hash_add(*h, bins, valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1);
     }
     SlotCache cache;
+    static constexpr bool kHasEntry8 = true;
     __device__ void entry(int r, int32_t c, bool valid, int slot) {
         const int32_t key = valid ? int32_t(int64_t(c) - r + nrows - 1) : -1;
         if (!cache.add(*h, bins, key, slot)) hash_add(*h, bins, key);
+    }
+    // eight full lockstep slots of one warp (row_sweep_cols)
+    __device__ bool entry8(int r, const int32_t (&c)[8], int j0, bool all_valid) {
+        int32_t k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) k[u] = int32_t(int64_t(c[u]) - r + nrows - 1);
+        return cache.add8(*h, bins, k, j0, all_valid);
     }
     __device__ void end() {
         const unsigned long long v = warp_sum(visits);

@@ -69,6 +69,43 @@ struct SlotCache {
         }
         return true;
     }
+    // Eight consecutive slots j0..j0+7 at once, when every lane holds a valid
+    // entry in each and all lanes agree slot by slot (the interior of banded
+    // matrices): one vote for the batch, lane (j0+d)%32 absorbs slot j0+d.
+    // All 32 lanes call; returns false (nothing done) otherwise.
+    __device__ __forceinline__ bool add8(SmemHash& h, int32_t* gbins, const int32_t (&k)[8], int j0, bool all_valid) {
+        if (!__all_sync(0xffffffffu, all_valid)) return false;
+        int32_t k0[8];
+        bool same = true;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            k0[u] = __shfl_sync(0xffffffffu, k[u], 0);
+            same = same && k[u] == k0[u];
+        }
+        if (!__all_sync(0xffffffffu, same)) return false;
+        const int d = int(threadIdx.x & 31u) - (j0 & 31);
+        if (d >= 0 && d < 8) {
+            int32_t kk = k0[0];
+#pragma unroll
+            for (int u = 1; u < 8; ++u) kk = d == u ? k0[u] : kk;
+            const int w = (j0 + d) >> 5;
+            const int32_t ck = w ? key[1] : key[0];
+            const int32_t cc = w ? cnt[1] : cnt[0];
+            int32_t nc = 32;
+            if (ck == kk)
+                nc += cc;
+            else if (ck >= 0)
+                hash_insert_one(h, gbins, ck, cc);
+            if (w) {
+                key[1] = kk;
+                cnt[1] = nc;
+            } else {
+                key[0] = kk;
+                cnt[0] = nc;
+            }
+        }
+        return true;
+    }
     __device__ __forceinline__ void flush(SmemHash& h, int32_t* gbins) {
         for (int w = 0; w < 2; ++w)
             if (key[w] >= 0 && cnt[w] > 0) hash_insert_one(h, gbins, key[w], cnt[w]);
@@ -234,6 +271,9 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
 #pragma unroll
             // L1-allocating: a lane's 8 consecutive columns share one or two sectors
             for (int u = 0; u < U; ++u) cv[u] = (has && j0 + u < elen) ? __ldg(col + a + j0 + u) : 0;
+            if constexpr (Op::kHasEntry8) {
+                if (op.entry8(int(r), cv, int(j0), has && j0 + U <= elen)) continue;
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (j0 + u < maxlen) op.entry(int(r), cv[u], has && j0 + u < elen, int(j0 + u));
