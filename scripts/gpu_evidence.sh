@@ -10,6 +10,8 @@ timeout 900 python bench.py --steps 50 --warmup 5 > gpurun_out/ev_bench.log 2>&1
 timeout 900 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/ev_bench_ref.log 2>&1; echo "bench ref rc=$?"
 LAB_ONLY_PROD=1 LAB_PEAK=$(python -c "import json;print(json.load(open('MEASURED_PEAKS.json'))['hbm_gbs'])") timeout 600 ./build/lab band,lap,rmat > gpurun_out/ev_lab.log 2>&1; echo "lab rc=$?"
 timeout 900 python scripts/config5.py --g 512 --iters 20 > gpurun_out/ev_config5.log 2>&1; echo "c5 rc=$?"
+timeout 900 python scripts/convert_bench.py > gpurun_out/ev_convert.log 2>&1; echo "convert rc=$?"
+timeout 1500 python scripts/config4.py --count 2000 --reps 20 --only profiles/config4_split_r01b.json --model paper_2303_05098_b200/models/b200_forest.txt --out gpurun_out/ev_c4_tuned.csv > gpurun_out/ev_c4.log 2>&1; echo "c4 rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv --log-file gpurun_out/ev_launches_bench.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench_under_ncu.log 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:dia_kernel -s 2 -c 1 -o gpurun_out/ev_full_dia python scripts/profile_spmv.py --workload banded --reps 2 --formats 5 > /dev/null 2>&1; echo "ncu dia rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:csr_warp_kernel -s 1 -c 1 -o gpurun_out/ev_full_csr python scripts/profile_spmv.py --workload banded --reps 1 --formats 1 > /dev/null 2>&1; echo "ncu csr rc=$?"
