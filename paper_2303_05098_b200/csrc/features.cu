@@ -309,6 +309,22 @@ __device__ __forceinline__ Mono mono_cat(const Mono& m, const Mono& n) {  // m f
 
 constexpr double kTwo53 = 9007199254740992.0;
 
+// Exact power-of-two scaling and binade of a positive double without the
+// library ldexp/ilogb call sequences (the binade walk is a serial chain of
+// these); out-of-range cases fall back to the library.
+__device__ __forceinline__ double scale2(double x, int k) {  // x * 2^k, exact
+    if (k >= -1022 && k <= 1023) {
+        const double p = __longlong_as_double((long long)(k + 1023) << 52);
+        const double r = x * p;
+        if (r == 0.0 || fabs(r) >= 2.2250738585072014e-308) return r;  // normal result: exact
+    }
+    return ldexp(x, k);
+}
+__device__ __forceinline__ int binade(double x) {  // ilogb for x > 0
+    const int be = int((__double_as_longlong(x) >> 52) & 0x7ff);
+    return be ? be - 1023 : ilogb(x);
+}
+
 // Element t added at binade e (ulp 2^(e-52)).  Returns false when t alone
 // reaches the next binade (q >= 2^53).
 __device__ __forceinline__ bool mono_elem(double t, int e, Mono& out) {
@@ -316,7 +332,7 @@ __device__ __forceinline__ bool mono_elem(double t, int e, Mono& out) {
         out = mono_id();
         return true;
     }
-    const double q = ldexp(t, 52 - e);  // exact (power-of-two scaling)
+    const double q = scale2(t, 52 - e);  // exact (power-of-two scaling)
     if (!(q < kTwo53)) return false;
     const double fl = floor(q);
     const double fr = q - fl;  // exact
@@ -446,8 +462,8 @@ __device__ __forceinline__ void mono_chunk(int64_t c, const int32_t* __restrict_
     const int sj = t >> 3;
     const double lo = psub[sj], hi = psub[sj + 1];
     const bool zero = sub_sum[sj] == 0.0;  // sum of non-negative terms: all zero
-    const bool safe = !zero && lo > 0.0 && ilogb(lo) == ilogb(hi);
-    const int e = safe ? ilogb(lo) : 0;
+    const bool safe = !zero && lo > 0.0 && binade(lo) == binade(hi);
+    const int e = safe ? binade(lo) : 0;
     Mono m = mono_id();
     bool ok = safe;
     if (safe) {
@@ -580,8 +596,8 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
         }
         const int64_t len = cur_hi - lo;
         const int64_t piece = (len + 31) / 32;
-        const int e = ilogb(S);
-        const long long m = (long long)ldexp(S, 52 - e);
+        const int e = binade(S);
+        const long long m = (long long)scale2(S, 52 - e);
         const int64_t a = lo + int64_t(lane) * piece;
         const int64_t b = a + piece < cur_hi ? a + piece : cur_hi;
         Mono mm = mono_id();
@@ -606,7 +622,7 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
         const int j = bad ? __ffs(bad) - 1 : 32;
         if (j > 0) {
             const long long mj = __shfl_sync(0xffffffffu, mi, j - 1);
-            S = ldexp(double(mj), e - 52);
+            S = scale2(double(mj), e - 52);
         }
         if (j == 32) {
             lo = cur_hi;
@@ -641,7 +657,7 @@ __device__ double walk_records(double S, const MonoRec* __restrict__ rec, int64_
         // prefetch the most likely next group (all 32 consumed) while this one is applied
         pre_c = c + 32;
         nxt = pre_c + lane < nrec ? rec[pre_c + lane] : ident_rec();
-        const int eS = S > 0.0 ? ilogb(S) : INT32_MIN;
+        const int eS = S > 0.0 ? binade(S) : INT32_MIN;
         const bool usable = ci < nrec && ((r.flags & kMonoIdent) || ((r.flags & kMonoSafe) && r.e == eS));
         const unsigned badm = __ballot_sync(0xffffffffu, !usable);
         int j = badm ? __ffs(badm) - 1 : 32;
@@ -655,14 +671,14 @@ __device__ double walk_records(double S, const MonoRec* __restrict__ rec, int64_
                 c += j;
                 continue;
             }
-            const long long m = (long long)ldexp(S, 52 - eS);
+            const long long m = (long long)scale2(S, 52 - eS);
             const long long mi = m + ((m & 1) ? pre.a1 : pre.a0);
             const bool good = double(mi) < kTwo53 || int(lane) >= j;
             const unsigned bad = __ballot_sync(0xffffffffu, !good);
             const int f = bad ? __ffs(bad) - 1 : j;  // first record whose prefix leaves the binade
             if (f > 0) {
                 const long long mf = __shfl_sync(0xffffffffu, mi, f - 1);
-                S = ldexp(double(mf), eS - 52);
+                S = scale2(double(mf), eS - 52);
             }
             c += f;
             if (f == j) continue;
