@@ -627,6 +627,73 @@ __global__ void __launch_bounds__(256, MINB) coo_hot(int64_t z, int64_t nrows, c
     }
 }
 
+// (f) coo with the NEXT chunk staged by cp.async (16-byte LDGSTS, no
+// registers held for in-flight data) into a warp-private 4 KB buffer
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) coo_as(int64_t z, int64_t nrows, const int* __restrict__ row,
+        const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
+        double* __restrict__ y, CooRec* __restrict__ rec) {
+    constexpr int IT = 8, CH = 256;
+    __shared__ __align__(16) int srow[8][CH];
+    __shared__ __align__(16) int scol[8][CH];
+    __shared__ __align__(16) double sval[8][CH];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t nfull = z / CH;  // full chunks go through the async path
+    const int64_t nchunks = (z + CH - 1) / CH;
+    const int64_t stride = int64_t(gridDim.x) * 8;
+    int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    auto issue = [&](int64_t ch) {
+        if (ch < nfull) {
+            const int64_t b = ch * CH;
+            // 1 KB row + 1 KB col + 2 KB val = 256 x 16 B, 8 per lane
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                cpa16(&srow[w][(q * 32 + lane) * 4], row + b + (q * 32 + lane) * 4);
+                cpa16(&scol[w][(q * 32 + lane) * 4], col + b + (q * 32 + lane) * 4);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cpa16(&sval[w][(q * 32 + lane) * 2], val + b + (q * 32 + lane) * 2);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (chunk >= nchunks) return;
+    issue(chunk);
+    while (true) {
+        const int64_t base = chunk * CH;
+        const int cnt = int(min(z - base, int64_t(CH)));
+        int r[IT], c[IT]; double v[IT];
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        if (chunk < nfull) {
+            const int4 ra = *reinterpret_cast<const int4*>(&srow[w][lane * 8]), rb = *reinterpret_cast<const int4*>(&srow[w][lane * 8 + 4]);
+            const int4 ca = *reinterpret_cast<const int4*>(&scol[w][lane * 8]), cb = *reinterpret_cast<const int4*>(&scol[w][lane * 8 + 4]);
+            r[0] = ra.x; r[1] = ra.y; r[2] = ra.z; r[3] = ra.w; r[4] = rb.x; r[5] = rb.y; r[6] = rb.z; r[7] = rb.w;
+            c[0] = ca.x; c[1] = ca.y; c[2] = ca.z; c[3] = ca.w; c[4] = cb.x; c[5] = cb.y; c[6] = cb.z; c[7] = cb.w;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 d = *reinterpret_cast<const double2*>(&sval[w][lane * 8 + 2 * q]);
+                v[2 * q] = d.x; v[2 * q + 1] = d.y;
+            }
+        } else {
+            ld_blk<IT>(row, col, val, base + lane * IT, cnt - lane * IT, r, c, v);
+        }
+        __syncwarp();
+        const int64_t nx = chunk + stride;
+        if (nx < nchunks) issue(nx);
+        double p[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? xmul(v[j], __ldg(x + c[j])) : 0.0;
+        const int prev_row = base > 0 ? row[base - 1] : -1;
+        const int next_row = base + cnt < z ? row[base + cnt] : -1;
+        coo_finish<IT>(lane, chunk, base, cnt, z, nrows, r, p, prev_row, next_row, y, rec);
+        if (nx >= nchunks) break;
+        chunk = nx;
+    }
+}
+
 // (c) persistent, blocked, next chunk prefetched before the finish
 template <int IT, int MINB>
 __global__ void __launch_bounds__(256, MINB) coo_pf(int64_t z, int64_t nrows, const int* __restrict__ row,
@@ -847,6 +914,28 @@ __global__ void __launch_bounds__(256, MINB) dia_rows(int n, int nd, const int64
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) if (base + r * 256 < n) y[base + r * 256] = acc[r];
+}
+
+// ------------------------------------------------------------------ gather bound probe
+// The x gathers of an SpMV on this matrix and nothing else: stream the column
+// array (coalesced, 8 per lane in flight) and fetch x[col] through L1/L2.
+// Its time is a lower bound for any SpMV that gathers x this way.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) gather_probe(int64_t z, const int* __restrict__ col,
+                                                          const double* __restrict__ x, double* __restrict__ sink) {
+    double acc = 0.0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x * 8;
+    for (int64_t base = (int64_t(blockIdx.x) * blockDim.x) * 8 + threadIdx.x; base < z; base += stride) {
+        int c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t k = base + int64_t(u) * blockDim.x;
+            c[u] = k < z ? lds(col + k) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += c[u] >= 0 ? __ldg(x + c[u]) : 0.0;
+    }
+    if (acc == 1.2345e300) *sink = acc;
 }
 
 // ------------------------------------------------------------------ matrices
@@ -1078,6 +1167,16 @@ int main(int argc, char** argv) {
         report("csr_vec V8", csr_bytes, [&] { csr_vec<8><<<unsigned((n * 8 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
         report("csr_vec V16", csr_bytes, [&] { csr_vec<16><<<unsigned((n * 16 + 255) / 256), 256>>>(n, drp, dcol, dval, dx, dy); }, check(false, 1 << 30));
         }
+        if (getenv("LAB_GATHER")) {
+            double* sink; CK(cudaMalloc(&sink, 8));
+            const double gbytes = 4.0 * z;  // the column stream alone
+            for (int per : {4, 8}) {
+                char nm[64]; snprintf(nm, 64, "gather_probe x%d (%.0f Mgathers)", per, z / 1e6);
+                auto kern = per == 4 ? gather_probe<4> : gather_probe<8>;
+                report(nm, gbytes, [&] { kern<<<sms * per, 256>>>(z, dcol, dx, sink); }, [] { return std::string(""); });
+            }
+            cudaFree(sink);
+        }
         // --- COO variants
         if (getenv("LAB_COO")) {
             std::vector<int> hr(z);
@@ -1101,6 +1200,9 @@ int main(int argc, char** argv) {
             go("coo_blk8 B6 fix8", 8, coo_blk<8, 6>, g8, true);
             go("coo_blk4 B8 fix8", 4, coo_blk<4, 8>, g4, true);
             go("coo_pf8 B3 fix8", 8, coo_pf<8, 3>, sms * 3, true);
+            go("coo_as B4 fix8", 8, coo_as<4>, sms * 4, true);
+            go("coo_as B5 fix8", 8, coo_as<5>, sms * 5, true);
+            go("coo_as B6 fix8", 8, coo_as<6>, sms * 6, true);
             if (getenv("LAB_HOT")) {
                 // column frequencies -> hot set -> encoded column array
                 std::vector<int64_t> freq(n, 0);
