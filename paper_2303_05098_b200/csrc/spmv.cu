@@ -350,6 +350,8 @@ __global__ void __launch_bounds__(256)
 constexpr int kCooItems = 8;
 constexpr int kCooChunk = 32 * kCooItems;
 constexpr int kCooPerSm = 3;
+// the accumulate variant (HYB) also reads y: 2 CTAs/SM leave it unspilled
+constexpr int coo_per_sm(bool accum) { return accum ? 2 : kCooPerSm; }
 
 struct CooChunkRec {
     double first_sum;  // in-chunk piece of a row that began in an earlier chunk
@@ -452,7 +454,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
 }
 
 template <bool ACCUM>
-__global__ void __launch_bounds__(256, kCooPerSm)
+__global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
                     CooChunkRec* __restrict__ rec) {
@@ -525,7 +527,7 @@ template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
     DBuf<CooChunkRec> rec(nchunks, s);
-    const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * kCooPerSm));
+    const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
     coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
                                                 rec.get());
     SOB_LAUNCH("coo_warp_kernel");
