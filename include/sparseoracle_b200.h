@@ -225,6 +225,9 @@ so_status so_spmv_rows_push(const so_matrix* m, const double* x_dev, double* y_d
  * pairs with so_spmv_rows_push on the neighbour. */
 so_status so_wait_flag(const unsigned long long* flag_dev, unsigned long long value,
                        void* stream);
+/* Waits that gave up after 60 s (a neighbour that never published) on the
+ * current device since the library loaded; the iterate is then invalid. */
+int64_t so_wait_flag_timeouts(void);
 /* Peer-shareable device memory (cudaMalloc + CUDA IPC), zero-filled. */
 typedef struct so_ipc_handle {
     unsigned char bytes[64];

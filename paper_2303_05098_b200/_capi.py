@@ -110,6 +110,7 @@ _SIGS = {
     "so_spmv_device_rows": (C.c_int, [vp, vp, vp, i64, i64, vp]),
     "so_spmv_rows_push": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp, C.c_uint64, vp]),
     "so_wait_flag": (C.c_int, [vp, C.c_uint64, vp]),
+    "so_wait_flag_timeouts": (C.c_int64, []),
     "so_ipc_alloc": (C.c_int, [i64, C.POINTER(vp), C.c_char_p]),
     "so_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
     "so_ipc_close": (C.c_int, [vp]),

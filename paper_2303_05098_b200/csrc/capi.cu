@@ -730,6 +730,15 @@ so_status so_wait_flag(const unsigned long long* flag_dev, unsigned long long va
     });
 }
 
+int64_t so_wait_flag_timeouts(void) {
+    int64_t v = -1;
+    guard([&] {
+        current_ctx();
+        v = int64_t(wait_flag_timeouts());
+    });
+    return v;
+}
+
 so_status so_ipc_alloc(int64_t bytes, void** dev_ptr, so_ipc_handle* handle) {
     return guard([&] {
         if (bytes <= 0 || !dev_ptr || !handle) fail(SO_INVALID_INPUT, "ipc_alloc: bad arguments");

@@ -127,6 +127,7 @@ void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, 
                     unsigned* ticket, unsigned long long* remote_flag, unsigned long long flag_value,
                     cudaStream_t s);
 void wait_flag(const unsigned long long* flag, unsigned long long value, cudaStream_t s);
+unsigned long long wait_flag_timeouts();
 so_matrix* gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_t col_lo, int64_t col_hi,
                              uint64_t seed, cudaStream_t s);
 int64_t spmv_bytes(const so_matrix& m);

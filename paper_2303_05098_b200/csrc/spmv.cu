@@ -281,11 +281,26 @@ __global__ void __launch_bounds__(256, 6)
     }
 }
 
+// Spins (acquire, system scope) until the neighbour's release store lands.
+// A neighbour that never publishes (crashed rank) must not wedge this GPU:
+// after kWaitTimeoutNs the wait gives up and bumps *timeouts, which
+// so_wait_flag_timeouts() reports to the host.
+constexpr unsigned long long kWaitTimeoutNs = 60ull * 1000 * 1000 * 1000;
+__device__ unsigned long long g_wait_timeouts = 0;
+
 __global__ void wait_flag_kernel(const unsigned long long* flag, unsigned long long value) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
         unsigned long long v;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
         if (v >= value) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > kWaitTimeoutNs) {
+            atomicAdd(&g_wait_timeouts, 1ull);
+            break;
+        }
         __nanosleep(256);
     }
 }
@@ -626,6 +641,12 @@ void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, 
                                                    m.dia.values.get(), x, y, lo, hi, remote, ticket, remote_flag,
                                                    flag_value);
     SOB_LAUNCH("dia_push_kernel");
+}
+
+unsigned long long wait_flag_timeouts() {
+    unsigned long long v = 0;
+    SOB_CUDA(cudaMemcpyFromSymbol(&v, g_wait_timeouts, sizeof(v)));
+    return v;
 }
 
 void wait_flag(const unsigned long long* flag, unsigned long long value, cudaStream_t s) {

@@ -215,6 +215,11 @@ class PeerWindows:
             self.it += 1
         return self.it % 2
 
+    def timeouts(self):
+        """Halo waits that gave up (a neighbour never published): nonzero means
+        the iterate is invalid (so_wait_flag_timeouts)."""
+        return int(self._lib.so_wait_flag_timeouts())
+
     def close(self):
         for p in self._opened:
             self._lib.so_ipc_close(p)

@@ -49,6 +49,7 @@ def _rank_main(rank, world, port, out_dir):
     dist.barrier()
     k = pw.iterate(m, ITERS, stream.cuda_stream)
     stream.synchronize()
+    assert pw.timeouts() == 0
     own = pw.tensor(k)[s.own_lo:s.own_hi].cpu().numpy()
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), own)
     dist.barrier()  # peers keep their mappings until everyone is done
