@@ -61,3 +61,20 @@ reftests: $(LIBDIR)/libsparseoracle.so
 	else echo "reftests: $(REF_PROJ)/tests absent, keeping prebuilt binaries"; fi
 
 .PHONY: reftests
+
+# Diagnostic micro-benchmarks (not the product): scripts/spmv_lab.cu (kernel
+# variants + the product kernels side by side), scripts/pipe_probe.cu (host
+# transfer pipeline stages).  Both link the product library.
+TOOL_FLAGS := -O3 $(ARCH) -std=c++17 -lineinfo -Iinclude -L$(LIBDIR) -lsparseoracle_b200 \
+              -Xlinker -rpath,'$$ORIGIN/../$(LIBDIR)'
+tools: build/lab build/pipe_probe
+
+build/lab: scripts/spmv_lab.cu $(LIBDIR)/libsparseoracle_b200.so include/sparseoracle_b200.h
+	@mkdir -p build
+	$(NVCC) -o $@ $< $(TOOL_FLAGS)
+
+build/pipe_probe: scripts/pipe_probe.cu $(LIBDIR)/libsparseoracle_b200.so include/sparseoracle_b200.h
+	@mkdir -p build
+	$(NVCC) -o $@ $< $(TOOL_FLAGS)
+
+.PHONY: tools

@@ -3,6 +3,7 @@
 # Everything lands in gpurun_out/ev_*.
 set -x
 make -j8 >/dev/null 2>&1 || make -j8
+make tools >/dev/null 2>&1 || make tools
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/ev_gpu.txt
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/ev_pytest_gpu.log 2>&1; echo "pytest rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1; echo "smoke rc=$?"
