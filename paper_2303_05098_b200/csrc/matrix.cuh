@@ -28,6 +28,7 @@ struct CooPart {
     int64_t nnz = 0;
     DBuf<int32_t> row, col;
     DBuf<double> val;
+    mutable int64_t max_gap = -1;  // longest empty-row run, computed on the first multiply (spmv.cu)
 };
 struct CsrPart {
     int64_t nnz = 0;

@@ -538,6 +538,26 @@ __global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, 
     y[r] = ACCUM ? fadd(y[r], t) : t;
 }
 
+// Longest run of empty rows of a canonical COO (leading, between entries,
+// trailing) -- cached per matrix.  The non-accumulating kernel zero-fills an
+// empty run with the one lane that finds it, which is free for ordinary
+// matrices but serialises on a lane when the entries sit in a few rows; those
+// matrices take y = 0 (memset) + the accumulating kernel instead (0 + s == s
+// exactly, so the result is identical).
+__global__ void coo_max_gap(int64_t z, int64_t nrows, const int32_t* __restrict__ row,
+                            unsigned long long* __restrict__ out) {
+    unsigned long long g = 0;
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k <= z; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t prv = k == 0 ? -1 : row[k - 1];
+        const int64_t cur = k == z ? nrows : row[k];
+        const int64_t gap = cur - prv - 1;
+        if (gap > int64_t(g)) g = gap;
+    }
+    g = warp_max(g);
+    if ((threadIdx.x & 31) == 0 && g) atomicMax(out, g);
+}
+constexpr int64_t kCooGapInline = 4096;  // a lane zero-fills up to ~2 us of rows inline
+
 template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
@@ -658,13 +678,27 @@ void wait_flag(const unsigned long long* flag, unsigned long long value, cudaStr
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
     if (m.nrows <= 0) return;
     switch (m.format) {
-        case SO_COO:
+        case SO_COO: {
+            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+            SOB_CUDA(cudaStreamIsCapturing(s, &cap));
+            if (m.coo.max_gap < 0 && cap == cudaStreamCaptureStatusNone) {  // first multiply: longest empty run
+                DBuf<unsigned long long> g(1, s);
+                SOB_CUDA(cudaMemsetAsync(g.get(), 0, sizeof(unsigned long long), s));
+                coo_max_gap<<<grid_for(m.coo.nnz + 1, 256, 4), 256, 0, s>>>(m.coo.nnz, m.nrows, m.coo.row.get(),
+                                                                              g.get());
+                SOB_LAUNCH("coo_max_gap");
+                m.coo.max_gap = int64_t(d2h_scalar(g.get(), s));
+            }
             if (m.coo.nnz == 0) {
                 SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
+            } else if (m.coo.max_gap < 0 || m.coo.max_gap > kCooGapInline) {  // unknown under capture: safe path
+                SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
+                launch_coo<true>(m.coo, m.nrows, x, y, s);
             } else {
                 launch_coo<false>(m.coo, m.nrows, x, y, s);
             }
             break;
+        }
         case SO_CSR:
             launch_csr_stream(m, false, x, y, s);
             break;

@@ -503,3 +503,23 @@ def test_spread_sum_just_above_power_of_two(so, O, head):
     want, _ = O.oc_features(O.oc_convert(coo, O.CSR), 0.2)
     got = np.array(d.extract_features(0.2).to_row())
     assert np.array_equal(got, want), (got, want)
+
+
+def test_coo_long_empty_row_runs(so, O):
+    """COO with runs of empty rows far longer than a lane can zero-fill
+    (entries only near the first and last rows of 3 M rows): queued runs are
+    filled by the grid-wide pass, y is exactly the oracle's."""
+    n = 3_000_000
+    rng = np.random.default_rng(12)
+    rows = np.concatenate([np.zeros(50, np.int64), np.full(30, 1_500_000), np.full(40, n - 7)])
+    cols = rng.integers(0, n, rows.size)
+    vals = rng.uniform(0.5, 2.0, rows.size)
+    coo = O.from_triplets(n, n, rows, cols, vals)
+    d = to_dev(so, coo)
+    x = rng.uniform(-1, 1, n)
+    for f in (so.COO, so.CSR):  # (ELL/HYB exceed the padding cap here)
+        m = d.from_coo(f)
+        y = m.spmv(x)
+        want = O.oc_spmv(O.oc_convert(coo, f), x)
+        assert max_rel(y, want) <= SPMV_TOL, f
+        assert np.count_nonzero(y) <= 3
