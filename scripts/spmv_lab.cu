@@ -938,6 +938,36 @@ __global__ void __launch_bounds__(256, MINB) gather_probe(int64_t z, const int* 
     if (acc == 1.2345e300) *sink = acc;
 }
 
+// DIA, persistent grid-stride over 256-row blocks (tail effect probe)
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) dia_persist(int n, int nd, const int64_t* __restrict__ offsets,
+                                                         const double* __restrict__ vals, const double* __restrict__ x,
+                                                         double* __restrict__ y) {
+    __shared__ int off[64];
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) off[d] = int(offsets[d]);
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        const double* vp = vals + i;
+        for (int d0 = 0; d0 < nd; d0 += U) {
+            double v[U], xv[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool live = d0 + u < nd;
+                const int d = live ? d0 + u : nd - 1;
+                const int c = i + off[d];
+                ok[u] = live && unsigned(c) < unsigned(n);
+                v[u] = lds(vp + size_t(d) * size_t(n));
+                xv[u] = __ldg(x + (ok[u] ? c : 0));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = xadd(acc, ok[u] ? xmul(v[u], xv[u]) : -0.0);
+        }
+        y[i] = acc;
+    }
+}
+
 // ------------------------------------------------------------------ matrices
 struct Csr { int64_t n; std::vector<int64_t> rp; std::vector<int> col; std::vector<double> val; };
 
@@ -1284,6 +1314,11 @@ int main(int argc, char** argv) {
             report("dia_i32 U9 B6", dia_bytes, [&] { dia_i32<9, 6><<<gb, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
             report("dia_i32 U14 B4", dia_bytes, [&] { dia_i32<14, 4><<<gb, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
             report("dia_i32 U5 B8", dia_bytes, [&] { dia_i32<5, 8><<<gb, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
+            for (int per : {4, 8}) {
+                char nm2[64]; snprintf(nm2, 64, "dia_persist U5 x%d", per);
+                auto k5 = per == 4 ? dia_persist<5, 4> : dia_persist<5, 8>;
+                report(nm2, dia_bytes, [&] { k5<<<sms * per, 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
+            }
             report("dia_rows U5 R2 B6", dia_bytes, [&] { dia_rows<5, 2, 6><<<unsigned((n + 511) / 512), 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
             report("dia_rows U5 R4 B4", dia_bytes, [&] { dia_rows<5, 4, 4><<<unsigned((n + 1023) / 1024), 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
             report("dia_rows U9 R2 B4", dia_bytes, [&] { dia_rows<9, 2, 4><<<unsigned((n + 511) / 512), 256>>>(int(n), nd, doff, ddv, dx, dy); }, check(true, 1 << 30));
