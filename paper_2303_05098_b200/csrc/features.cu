@@ -602,16 +602,20 @@ __device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t*
         const int64_t b = a + piece < cur_hi ? a + piece : cur_hi;
         Mono mm = mono_id();
         bool ok = true;
-        for (int64_t i0 = a; i0 < b; i0 += 8) {
-            int32_t cv[8];
+        if (piece == 1) {  // one row per lane (the common case near a crossing): no batch
+            if (a < b) ok = mono_elem(sq_dev(rc[a], avg), e, mm);
+        } else {
+            for (int64_t i0 = a; i0 < b; i0 += 8) {
+                int32_t cv[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cv[u] = i0 + u < b ? rc[i0 + u] : 0;
+                for (int u = 0; u < 8; ++u) cv[u] = i0 + u < b ? rc[i0 + u] : 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (i0 + u < b && ok) {
-                    Mono el;
-                    ok = mono_elem(sq_dev(cv[u], avg), e, el);
-                    if (ok) mm = mono_cat(mm, el);
+                for (int u = 0; u < 8; ++u) {
+                    if (i0 + u < b && ok) {
+                        Mono el;
+                        ok = mono_elem(sq_dev(cv[u], avg), e, el);
+                        if (ok) mm = mono_cat(mm, el);
+                    }
                 }
             }
         }
