@@ -55,9 +55,11 @@ reftests: $(LIBDIR)/libsparseoracle.so
 	    $(REF_PROJ)/tests/test_$$t.cpp -o build/reftests/test_$$t \
 	    -L$(LIBDIR) -lsparseoracle -lsparseoracle_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' || exit 1; \
 	done; \
-	  $(CXX) -std=c++20 -O1 -Iinclude -Itests/support/doctest_shim -I$(REF_PROJ)/tests \
-	    tests/support/cpp/test_matrix_market.cpp -o build/reftests/test_matrix_market \
+	  for t in matrix_market concurrency; do \
+	  $(CXX) -std=c++20 -O1 -pthread -Iinclude -Itests/support/doctest_shim -I$(REF_PROJ)/tests \
+	    tests/support/cpp/test_$$t.cpp -o build/reftests/test_$$t \
 	    -L$(LIBDIR) -lsparseoracle -lsparseoracle_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' || exit 1; \
+	  done; \
 	else echo "reftests: $(REF_PROJ)/tests absent, keeping prebuilt binaries"; fi
 
 .PHONY: reftests

@@ -4,6 +4,7 @@
 #include <cctype>
 #include <cmath>
 #include <limits>
+#include <mutex>
 #include <string>
 
 #include "sparseoracle/device.hpp"
@@ -253,20 +254,34 @@ index_t ConversionConfig::true_diag_threshold(index_t nrows, index_t ncols) cons
 
 // ---------------------------------------------------------------- DynamicMatrix
 
-DynamicMatrix::DynamicMatrix(const DynamicMatrix& o)
-    : payload_(o.host_valid_ ? o.payload_ : Payload(CooMatrix{})),
-      fmt_(o.fmt_),
-      host_valid_(o.host_valid_),
-      dev_(o.dev_) {}
+namespace {
+std::mutex& lazy_mu() {  // serialises lazy host downloads / device uploads
+    static std::mutex mu;
+    return mu;
+}
+}  // namespace
+
+DynamicMatrix::DynamicMatrix(const DynamicMatrix& o) : fmt_(o.fmt_) {
+    std::lock_guard<std::mutex> lk(lazy_mu());
+    const bool hv = o.host_valid_.load(std::memory_order_acquire);
+    payload_ = hv ? o.payload_ : Payload(CooMatrix{});
+    host_valid_.store(hv, std::memory_order_release);
+    dev_ = o.dev_;
+}
 
 DynamicMatrix::DynamicMatrix(DynamicMatrix&& o) noexcept
-    : payload_(std::move(o.payload_)), fmt_(o.fmt_), host_valid_(o.host_valid_), dev_(std::move(o.dev_)) {}
+    : payload_(std::move(o.payload_)),
+      fmt_(o.fmt_),
+      host_valid_(o.host_valid_.load(std::memory_order_acquire)),
+      dev_(std::move(o.dev_)) {}
 
 DynamicMatrix& DynamicMatrix::operator=(const DynamicMatrix& o) {
     if (this != &o) {
-        payload_ = o.host_valid_ ? o.payload_ : Payload(CooMatrix{});
+        std::lock_guard<std::mutex> lk(lazy_mu());
+        const bool hv = o.host_valid_.load(std::memory_order_acquire);
+        payload_ = hv ? o.payload_ : Payload(CooMatrix{});
         fmt_ = o.fmt_;
-        host_valid_ = o.host_valid_;
+        host_valid_.store(hv, std::memory_order_release);
         dev_ = o.dev_;  // device copies are immutable once built: share
     }
     return *this;
@@ -275,7 +290,7 @@ DynamicMatrix& DynamicMatrix::operator=(const DynamicMatrix& o) {
 DynamicMatrix& DynamicMatrix::operator=(DynamicMatrix&& o) noexcept {
     payload_ = std::move(o.payload_);
     fmt_ = o.fmt_;
-    host_valid_ = o.host_valid_;
+    host_valid_.store(o.host_valid_.load(std::memory_order_acquire), std::memory_order_release);
     dev_ = std::move(o.dev_);
     return *this;
 }
@@ -291,14 +306,17 @@ DynamicMatrix DynamicMatrix::adopt(std::shared_ptr<detail::DeviceMirror> device)
 }
 
 void DynamicMatrix::materialize() const {
-    if (host_valid_) return;
+    if (host_valid_.load(std::memory_order_acquire)) return;
+    std::lock_guard<std::mutex> lk(lazy_mu());
+    if (host_valid_.load(std::memory_order_relaxed)) return;
     payload_ = dev_->download();
-    host_valid_ = true;
+    host_valid_.store(true, std::memory_order_release);
 }
 
 void DynamicMatrix::detach_device() { dev_.reset(); }
 
 const detail::DeviceMirror& DynamicMatrix::device() const {
+    std::lock_guard<std::mutex> lk(lazy_mu());
     if (!dev_) dev_ = detail::DeviceMirror::upload(payload_);
     return *dev_;
 }

@@ -942,6 +942,10 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
         check_ratio(*m, ratio);
         so_conversion_config cfg = cfg_or_default(cfgp);
         cfg.true_diag_ratio = ratio;  // TunerConfig::effective_conversion (tuners.hpp:21-25)
+        // the cached plan (graph, workspace, events) belongs to the matrix:
+        // concurrent tune_ml calls on one const matrix take turns
+        static std::mutex plan_mu;
+        std::lock_guard<std::mutex> plan_lock(plan_mu);
         TunePlan* plan = m->tune_plan.get();
         if (!plan || !plan->matches(f->uid, cfg)) {
             m->tune_plan.reset();

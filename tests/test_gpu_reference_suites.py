@@ -14,8 +14,9 @@ pytestmark = pytest.mark.gpu
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(REPO, "build", "reftests")
-# + the Matrix Market cases of test_ingest.cpp restated in tests/support/cpp
-SUITES = ["formats", "spmv", "features", "model", "tuners", "matrix_market"]
+# + the Matrix Market cases of test_ingest.cpp restated in tests/support/cpp,
+# and concurrent readers of one lazily materialised matrix
+SUITES = ["formats", "spmv", "features", "model", "tuners", "matrix_market", "concurrency"]
 
 
 @pytest.mark.parametrize("suite", SUITES)
