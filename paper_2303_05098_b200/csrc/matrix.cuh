@@ -29,6 +29,7 @@ struct CooPart {
     DBuf<int32_t> row, col;
     DBuf<double> val;
     mutable int64_t max_gap = -1;  // longest empty-row run, computed on the first multiply (spmv.cu)
+    mutable int8_t long_runs = -1;  // some row covers > kFixupInline chunks (-1 unknown), same pass
 };
 struct CsrPart {
     int64_t nnz = 0;

@@ -190,8 +190,10 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
 
 // Rows longer than grp_cap: piece p covers entries [pk[2p], pk[2p+1]) of row
 // prow[p] (<= kPiece entries, 8 independent loads per thread), reduced with a
-// fixed tree into part[p]; csr_long_fixup then adds the pieces of each row in
-// piece order (deterministic, within the 1e-12 contract).
+// fixed tree into part[p]; csr_long_fixup then combines the pieces of each
+// row -- one warp per long row, lane-strided partial sums joined by a fixed
+// butterfly, so a row of 10^8 entries (5*10^4 pieces) is not one thread's
+// serial chain (deterministic, within the 1e-12 contract).
 __global__ void __launch_bounds__(kStreamBlock)
     csr_long_pieces(const int64_t* __restrict__ pk, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ part) {
@@ -221,13 +223,17 @@ __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, 
                                const double* __restrict__ part, double* __restrict__ y, int64_t nrows, int64_t ncols,
                                int ndiags, const int64_t* __restrict__ offsets, const double* __restrict__ dvals,
                                const double* __restrict__ x) {
-    const int64_t l = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t l = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (l >= nlong) return;
     double t = 0.0;
-    for (int64_t p = lpiece[l]; p < lpiece[l + 1]; ++p) t = fadd(t, part[p]);
-    const int r = lrow[l];
-    if (WITH_DIA) t = fadd(dia_row<true>(r, int(nrows), int(ncols), ndiags, nullptr, offsets, dvals, x), t);
-    y[r] = t;
+    for (int64_t p = lpiece[l] + lane; p < lpiece[l + 1]; p += 32) t = fadd(t, part[p]);
+    t = warp_sum(t);  // fixed butterfly: deterministic
+    if (lane == 0) {
+        const int r = lrow[l];
+        if (WITH_DIA) t = fadd(dia_row<true>(r, int(nrows), int(ncols), ndiags, nullptr, offsets, dvals, x), t);
+        y[r] = t;
+    }
 }
 
 // ---------------------------------------------------------------- DIA -------
@@ -478,6 +484,11 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     const int64_t nchunks = (z + kCooChunk - 1) / kCooChunk;
     const int64_t stride = int64_t(gridDim.x) * (blockDim.x >> 5);
     int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // coo_fixup's control words (after the records)
+        unsigned long long* ctl = reinterpret_cast<unsigned long long*>(rec + nchunks);
+        ctl[0] = 0;
+        ctl[1] = 0;
+    }
     if (chunk >= nchunks) return;
     int r[IT], c[IT];
     double v[IT];
@@ -507,35 +518,99 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
 // Rows spanning chunks: the chunk holding the row's first entry walks forward
 // in chunk order (deterministic) and writes the final value; records are
 // fetched 8 at a time so a row spanning hundreds of chunks (R-MAT hubs) is
-// not one dependent load per chunk.
+// not one dependent load per chunk.  A walk still open after kFixupInline
+// records is queued for coo_fixup_long, where a CTA finishes it 256 records
+// per step (a row of 10^8 entries spans ~4*10^5 chunks).
+constexpr int kFixupInline = 64;
+struct LongRun {
+    int64_t owner;  // chunk holding the row's first piece
+    int64_t next;   // first record not yet added
+    double partial; // last_sum[owner] + first_sum[owner+1 .. next)
+};
+
+// A CTA finishes the queued long runs, 256 records per step: the run ends at
+// the first record that is not a whole-chunk continuation; per-thread
+// partials are joined by a fixed block tree (deterministic).
 template <bool ACCUM>
-__global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, double* __restrict__ y) {
-    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= nchunks) return;
-    const int32_t f = rec[c].flags;
-    if (!(f & kLastOpen) || (f & kSingle)) return;
-    double t = rec[c].last_sum;
-    for (int64_t j0 = c + 1; j0 < nchunks; j0 += 8) {
-        double fs[8];
-        int32_t fl[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int64_t j = j0 + u < nchunks ? j0 + u : nchunks - 1;
-            fs[u] = rec[j].first_sum;
-            fl[u] = rec[j].flags;
+__device__ void finish_long_runs(int64_t nchunks, const CooChunkRec* __restrict__ rec, double* __restrict__ y,
+                                 const LongRun* __restrict__ runs, unsigned long long n) {
+    __shared__ double scratch[8];
+    __shared__ unsigned long long stop;
+    for (unsigned long long q = 0; q < n; ++q) {
+        const LongRun run = runs[q];
+        double t = 0.0;
+        for (int64_t j0 = run.next;; j0 += 256) {
+            if (threadIdx.x == 0) stop = ~0ull;
+            __syncthreads();
+            const int64_t j = j0 + threadIdx.x;
+            const bool in = j < nchunks;
+            const int32_t fl = in ? rec[j].flags : 0;
+            if ((in && !(fl & kSingle)) || (!in && j == nchunks)) atomicMin(&stop, (unsigned long long)(in ? j : j - 1));
+            __syncthreads();
+            const unsigned long long end = stop;  // last record of the run (inclusive), if in this step
+            if (in && (unsigned long long)j <= end) t = fadd(t, rec[j].first_sum);
+            __syncthreads();
+            if (end != ~0ull) break;
         }
-        bool done = false;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (!done && j0 + u < nchunks) {
-                t = fadd(t, fs[u]);
-                if (!(fl[u] & kSingle)) done = true;
-            }
+        const double sum = block_sum_det<256>(t, scratch);
+        if (threadIdx.x == 0) {
+            const int32_t r = rec[run.owner].last_row;
+            const double v = fadd(run.partial, sum);
+            y[r] = ACCUM ? fadd(y[r], v) : v;
         }
-        if (done) break;
+        __syncthreads();
     }
-    const int32_t r = rec[c].last_row;
-    y[r] = ACCUM ? fadd(y[r], t) : t;
+}
+
+// ctl[0] = queued long runs (zeroed by coo_warp_kernel)
+template <bool ACCUM>
+__global__ void __launch_bounds__(256) coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec,
+                                                 double* __restrict__ y, LongRun* __restrict__ runs,
+                                                 unsigned long long* __restrict__ ctl) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int32_t f = c < nchunks ? rec[c].flags : 0;
+    if ((f & kLastOpen) && !(f & kSingle)) {
+        double t = rec[c].last_sum;
+        bool queued = false;
+        for (int64_t j0 = c + 1; j0 < nchunks; j0 += 8) {
+            if (j0 - c > kFixupInline) {  // long run: the last CTA finishes it
+                const unsigned long long q = atomicAdd(&ctl[0], 1ull);
+                runs[q] = LongRun{c, j0, t};
+                queued = true;
+                break;
+            }
+            double fs[8];
+            int32_t fl[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t j = j0 + u < nchunks ? j0 + u : nchunks - 1;
+                fs[u] = rec[j].first_sum;
+                fl[u] = rec[j].flags;
+            }
+            bool done = false;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (!done && j0 + u < nchunks) {
+                    t = fadd(t, fs[u]);
+                    if (!(fl[u] & kSingle)) done = true;
+                }
+            }
+            if (done) break;
+        }
+        if (!queued) {
+            const int32_t r = rec[c].last_row;
+            y[r] = ACCUM ? fadd(y[r], t) : t;
+        }
+    }
+}
+
+// The queued long runs, one CTA each (grid-stride over the queue).
+template <bool ACCUM>
+__global__ void __launch_bounds__(256) coo_fixup_long(int64_t nchunks, const CooChunkRec* __restrict__ rec,
+                                                      double* __restrict__ y, const LongRun* __restrict__ runs,
+                                                      const unsigned long long* __restrict__ ctl) {
+    const unsigned long long n = ctl[0];
+    for (unsigned long long q = blockIdx.x; q < n; q += gridDim.x) finish_long_runs<ACCUM>(nchunks, rec, y, runs + q, 1);
 }
 
 // Longest run of empty rows of a canonical COO (leading, between entries,
@@ -546,28 +621,42 @@ __global__ void coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec, 
 // exactly, so the result is identical).
 __global__ void coo_max_gap(int64_t z, int64_t nrows, const int32_t* __restrict__ row,
                             unsigned long long* __restrict__ out) {
+    // out[0] = longest empty-row run; out[1] |= 1 when some row fully covers
+    // kFixupInline + 1 consecutive chunks (only then can coo_fixup queue a long run)
+    constexpr int64_t kSpan = int64_t(kFixupInline) * kCooChunk - 1;
     unsigned long long g = 0;
+    bool lng = false;
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k <= z; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t prv = k == 0 ? -1 : row[k - 1];
         const int64_t cur = k == z ? nrows : row[k];
         const int64_t gap = cur - prv - 1;
         if (gap > int64_t(g)) g = gap;
+        if (k % kCooChunk == 0 && k + kSpan < z && row[k] == row[k + kSpan]) lng = true;
     }
     g = warp_max(g);
     if ((threadIdx.x & 31) == 0 && g) atomicMax(out, g);
+    if (__any_sync(0xffffffffu, lng) && (threadIdx.x & 31) == 0) out[1] = 1;
 }
 constexpr int64_t kCooGapInline = 4096;  // a lane zero-fills up to ~2 us of rows inline
 
 template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
-    DBuf<CooChunkRec> rec(nchunks, s);
+    // chunk records, then the fix-up's control word pair and long-run queue
+    static_assert(sizeof(LongRun) == sizeof(CooChunkRec) && sizeof(CooChunkRec) >= 16, "record layout");
+    DBuf<CooChunkRec> rec(2 * nchunks + 1, s);
     const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
     coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
                                                 rec.get());
     SOB_LAUNCH("coo_warp_kernel");
-    coo_fixup<ACCUM><<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y);
+    LongRun* runs = reinterpret_cast<LongRun*>(rec.get() + nchunks + 1);
+    unsigned long long* ctl = reinterpret_cast<unsigned long long*>(rec.get() + nchunks);
+    coo_fixup<ACCUM><<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y, runs, ctl);
     SOB_LAUNCH("coo_fixup");
+    if (coo.long_runs != 0) {  // unknown (-1) or present
+        coo_fixup_long<ACCUM><<<current_ctx().num_sms, 256, 0, s>>>(nchunks, rec.get(), y, runs, ctl);
+        SOB_LAUNCH("coo_fixup_long");
+    }
 }
 
 template <int IT>
@@ -599,7 +688,7 @@ void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, doubl
         csr_long_pieces<<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(), c.val.get(), x,
                                                                      part.get());
         SOB_LAUNCH("csr_long_pieces");
-        const unsigned g = unsigned(ceil_div(c.nlong, 128));
+        const unsigned g = unsigned(ceil_div(c.nlong * 32, 128));  // one warp per long row
         if (with_dia)
             csr_long_fixup<true><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y,
                                                   m.nrows, m.ncols, nd, m.dia.offsets.get(), m.dia.values.get(), x);
@@ -675,20 +764,29 @@ void wait_flag(const unsigned long long* flag, unsigned long long value, cudaStr
     SOB_LAUNCH("wait_flag_kernel");
 }
 
+// First multiply of a COO part (outside stream capture): the longest empty
+// run and whether any row is long enough to need coo_fixup_long; cached.
+static void coo_profile(const CooPart& coo, int64_t nrows, cudaStream_t s) {
+    if (coo.max_gap >= 0 || coo.nnz == 0) return;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    SOB_CUDA(cudaStreamIsCapturing(s, &cap));
+    if (cap != cudaStreamCaptureStatusNone) return;  // stays unknown: safe paths
+    DBuf<unsigned long long> g(2, s);
+    SOB_CUDA(cudaMemsetAsync(g.get(), 0, 2 * sizeof(unsigned long long), s));
+    coo_max_gap<<<grid_for(coo.nnz + 1, 256, 4), 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), g.get());
+    SOB_LAUNCH("coo_max_gap");
+    unsigned long long h[2];
+    SOB_CUDA(cudaMemcpyAsync(h, g.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    SOB_CUDA(cudaStreamSynchronize(s));
+    coo.long_runs = h[1] ? 1 : 0;
+    coo.max_gap = int64_t(h[0]);
+}
+
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
     if (m.nrows <= 0) return;
     switch (m.format) {
         case SO_COO: {
-            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-            SOB_CUDA(cudaStreamIsCapturing(s, &cap));
-            if (m.coo.max_gap < 0 && cap == cudaStreamCaptureStatusNone) {  // first multiply: longest empty run
-                DBuf<unsigned long long> g(1, s);
-                SOB_CUDA(cudaMemsetAsync(g.get(), 0, sizeof(unsigned long long), s));
-                coo_max_gap<<<grid_for(m.coo.nnz + 1, 256, 4), 256, 0, s>>>(m.coo.nnz, m.nrows, m.coo.row.get(),
-                                                                              g.get());
-                SOB_LAUNCH("coo_max_gap");
-                m.coo.max_gap = int64_t(d2h_scalar(g.get(), s));
-            }
+            coo_profile(m.coo, m.nrows, s);
             if (m.coo.nnz == 0) {
                 SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
             } else if (m.coo.max_gap < 0 || m.coo.max_gap > kCooGapInline) {  // unknown under capture: safe path
@@ -709,6 +807,7 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
             launch_ell<false>(m, x, y, s);
             break;
         case SO_HYB:
+            coo_profile(m.coo, m.nrows, s);
             launch_ell<false>(m, x, y, s);
             if (m.coo.nnz > 0) launch_coo<true>(m.coo, m.nrows, x, y, s);
             break;

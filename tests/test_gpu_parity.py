@@ -523,3 +523,50 @@ def test_coo_long_empty_row_runs(so, O):
         want = O.oc_spmv(O.oc_convert(coo, f), x)
         assert max_rel(y, want) <= SPMV_TOL, f
         assert np.count_nonzero(y) <= 3
+
+
+def test_coo_rows_spanning_many_chunks(so, O):
+    """Rows of 3*10^5 entries span ~1200 COO chunks: the fix-up hands such
+    runs to the CTA-wide pass; COO and HYB (accumulating COO part) match the
+    oracle within the reordered-sum tolerance."""
+    n = 400_000
+    rng = np.random.default_rng(21)
+    dense = [0, 5, 199_999, n - 1]
+    rows = [np.repeat(np.array(dense, np.int64), 300_000)]
+    cols = [np.concatenate([rng.choice(n, 300_000, replace=False) for _ in dense])]
+    sparse_r = rng.integers(0, n, 200_000)
+    rows.append(sparse_r)
+    cols.append(rng.integers(0, n, sparse_r.size))
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    coo = O.from_triplets(n, n, r, c, rng.uniform(0.5, 2.0, r.size))
+    d = to_dev(so, coo)
+    x = rng.uniform(-1, 1, n)
+    for f in (so.COO, so.HYB, so.CSR):
+        want_m = O.oc_convert(coo, f)
+        m = d.from_coo(f)
+        assert max_rel(m.spmv(x), O.oc_spmv(want_m, x)) <= SPMV_TOL, f
+
+
+@pytest.mark.parametrize("prefix", [0, 1, 255, 300])
+def test_coo_long_run_threshold(so, O, prefix):
+    """Row lengths around the fix-up's inline limit (64 whole chunks of 256
+    entries after the owner chunk), shifted against the chunk grid by a short
+    prefix row: the cached 'long runs present' flag must never drop a queued
+    run; first (profiling) and later multiplies agree."""
+    rng = np.random.default_rng(100 + prefix)
+    lens = [64 * 256 - 1, 64 * 256, 65 * 256 - 1, 65 * 256, 65 * 256 + 1, 66 * 256 + 100]
+    n = 200_000
+    rows = [np.zeros(prefix, np.int64)] if prefix else []
+    cols = [rng.choice(n, prefix, replace=False)] if prefix else []
+    for i, L in enumerate(lens):
+        rows.append(np.full(L, 10 + 1000 * i, np.int64))
+        cols.append(rng.choice(n, L, replace=False))
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    coo = O.from_triplets(n, n, r, c, rng.uniform(0.5, 2.0, r.size))
+    x = rng.uniform(-1, 1, n)
+    for f in (so.COO, so.HYB):
+        want = O.oc_spmv(O.oc_convert(coo, f), x)
+        m = to_dev(so, coo).from_coo(f)
+        y1, y2 = m.spmv(x), m.spmv(x)
+        assert max_rel(y1, want) <= SPMV_TOL, f
+        assert np.array_equal(y1, y2), f
