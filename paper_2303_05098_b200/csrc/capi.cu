@@ -327,6 +327,16 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// device-visible address of pinned, mapped host memory (UVA: usually p itself), else null
+const void* mapped_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 // Row-chunk pipeline of spmv(m, x) for matrices whose rows only read a known
 // column window (DIA, HDC with an empty CSR part): x is uploaded in the
 // windows the chunks need (copy engine, copy_in), chunk k's rows run on the
@@ -347,6 +357,13 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
         m.dia_omin = *std::min_element(off.begin(), off.end());
         m.dia_omax = *std::max_element(off.begin(), off.end());
         m.dia_window_known = true;
+    }
+    // narrow windows: one kernel over the host link, no copy engine
+    static const bool zc_off = std::getenv("SOB_NO_ZERO_COPY") != nullptr;  // diagnostic knob
+    if (!zc_off) {
+        const double* xm = static_cast<const double*>(mapped_ptr(x));
+        double* ym = static_cast<double*>(const_cast<void*>(mapped_ptr(y)));
+        if (xm && ym && spmv_dia_zero_copy(m, xm, ym, s)) return true;
     }
     Context& c = ctx(m.device);
     const int64_t n = m.nrows, nc = m.ncols;

@@ -125,6 +125,10 @@ void write_matrix_market(int64_t nrows, int64_t ncols, int64_t nnz, const int64_
 // --- spmv (spmv.cu) ---
 void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s);
 void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, cudaStream_t s);
+// DIA-window matrix with x/y in mapped pinned host memory (device-visible
+// pointers): one kernel reads x and writes y over the host link; false when
+// the window is too wide or unknown (spmv.cu)
+bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s);
 void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, double* remote,
                     unsigned* ticket, unsigned long long* remote_flag, unsigned long long flag_value,
                     cudaStream_t s);

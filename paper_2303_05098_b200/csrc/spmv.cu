@@ -254,6 +254,60 @@ __global__ void __launch_bounds__(256, MINB)
     y[i] = dia_row<GLOBAL_OFF, U>(int(i), int(nrows), int(ncols), ndiags, soff, offsets, vals, x);
 }
 
+// Host-buffer spmv over PCIe with no copy engine (so_spmv, pinned x and y):
+// a CTA of kZcRows rows stages the x window its rows read,
+// [i0 + omin, i0 + kZcRows - 1 + omax], straight from mapped host memory
+// into shared memory (16-byte loads when x is 16-byte aligned), multiplies
+// exactly as dia_row does (same diagonal order, same -0.0 for out-of-range
+// columns: bit-identical) and stores y straight into mapped host memory.
+// Measured on config 2 (scripts/zc_probe.cu): 0.84 ms for the 32 MB up and
+// 32 MB down vs 0.95+ for any copy-engine chunk pipeline.  Only for windows
+// of span <= kZcSpan (x read at most 1.25x over the link).
+constexpr int kZcRows = 1024;
+constexpr int64_t kZcSpan = kZcRows / 4;
+
+template <bool ALIGN16>
+__global__ void __launch_bounds__(kZcRows, 1)
+    dia_zc_kernel(int nrows, int ncols, int ndiags, const int64_t* __restrict__ offsets,
+                  const double* __restrict__ vals, const double* x_host, double* y_host, int omin, int omax) {
+    extern __shared__ double xs[];
+    __shared__ int soff[kDiaSmem];
+    stage_offsets(soff, offsets, ndiags);
+    const int i0 = blockIdx.x * kZcRows;
+    int w0 = max(0, i0 + omin);
+    if (ALIGN16) w0 &= ~1;
+    const int w1 = min(ncols, i0 + kZcRows - 1 + omax + 1);
+    if (ALIGN16) {
+        const int npair = (w1 - w0) >> 1;
+        for (int j = threadIdx.x; j < npair; j += kZcRows)
+            reinterpret_cast<double2*>(xs)[j] = *reinterpret_cast<const double2*>(x_host + w0 + 2 * j);
+        if (((w1 - w0) & 1) && threadIdx.x == 0) xs[w1 - w0 - 1] = x_host[w1 - 1];
+    } else {
+        for (int j = threadIdx.x; j < w1 - w0; j += kZcRows) xs[j] = x_host[w0 + j];
+    }
+    __syncthreads();
+    const int i = i0 + threadIdx.x;
+    if (i >= nrows) return;
+    const double* vp = vals + i;
+    double acc = 0.0;
+    for (int d0 = 0; d0 < ndiags; d0 += kDiaBatch) {
+        double v[kDiaBatch], xv[kDiaBatch];
+        bool ok[kDiaBatch];
+#pragma unroll
+        for (int u = 0; u < kDiaBatch; ++u) {
+            const bool live = d0 + u < ndiags;
+            const int d = live ? d0 + u : ndiags - 1;
+            const int c = i + soff[d];
+            ok[u] = live && unsigned(c) < unsigned(ncols);
+            v[u] = ld_stream(vp + size_t(d) * size_t(nrows));
+            xv[u] = xs[ok[u] ? c - w0 : 0];
+        }
+#pragma unroll
+        for (int u = 0; u < kDiaBatch; ++u) acc = fadd(acc, ok[u] ? fmul(v[u], xv[u]) : -0.0);
+    }
+    y_host[i] = acc;
+}
+
 // Row-partitioned iteration, fused boundary exchange (config 5, dist.py):
 // the rows a neighbour needs are computed once and stored twice -- into the
 // local window and straight into the neighbour's window over NVLink peer
@@ -725,6 +779,25 @@ void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s) 
 }
 
 }  // namespace
+
+bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s) {
+    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
+    if (!m.dia_window_known || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem) return false;
+    const int64_t omin = m.dia_omin, omax = m.dia_omax;
+    if (omax - omin > kZcSpan) return false;
+    const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
+    const unsigned grid = unsigned(ceil_div(m.nrows, int64_t(kZcRows)));
+    if ((reinterpret_cast<uintptr_t>(x_mapped) & 15) == 0)
+        dia_zc_kernel<true><<<grid, kZcRows, smem, s>>>(int(m.nrows), int(m.ncols), int(m.dia.ndiags),
+                                                         m.dia.offsets.get(), m.dia.values.get(), x_mapped, y_mapped,
+                                                         int(omin), int(omax));
+    else
+        dia_zc_kernel<false><<<grid, kZcRows, smem, s>>>(int(m.nrows), int(m.ncols), int(m.dia.ndiags),
+                                                          m.dia.offsets.get(), m.dia.values.get(), x_mapped,
+                                                          y_mapped, int(omin), int(omax));
+    SOB_LAUNCH("dia_zc_kernel");
+    return true;
+}
 
 void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, cudaStream_t s) {
     if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0))

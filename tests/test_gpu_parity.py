@@ -389,26 +389,45 @@ def test_hdc_with_long_rows(so, O):
         assert max_rel(m.spmv(x), O.oc_spmv(want, x)) <= SPMV_TOL, f
 
 
-def test_pipelined_host_spmv_pinned(so, O):
-    """spmv(m, x) with pinned host buffers on a DIA-window matrix runs the
-    row-chunk pipeline (x windows up / chunks / y chunks down on two copy
-    streams): bit-identical to the oracle and to the one-shot path."""
+@pytest.mark.parametrize("shape", ["band13", "band13_unaligned", "wide"])
+def test_pipelined_host_spmv_pinned(so, O, shape):
+    """spmv(m, x) with pinned host buffers on a DIA-window matrix: narrow
+    windows run the zero-copy kernel (x read and y written over the host
+    link; 16-byte and 8-byte aligned x), wide ones the row-chunk copy
+    pipeline (x windows up / chunks / y chunks down on two copy streams).
+    Both bit-identical to the oracle and to the one-shot path."""
     import torch
     from paper_2303_05098_b200 import synth
 
-    csr = synth.banded(700_000, 13, seed=2)
-    coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
-    d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
-    xt = torch.empty(csr.ncols, dtype=torch.float64).pin_memory()
-    yt = torch.empty(csr.nrows, dtype=torch.float64).pin_memory()
-    xn, yn = xt.numpy(), yt.numpy()
-    xn[:] = np.random.default_rng(11).uniform(-1, 1, csr.ncols)
+    if shape == "wide":  # offsets -3000, -1, 0, 2, 3000: window span 6000 > the zero-copy limit
+        n = 700_000
+        rng = np.random.default_rng(3)
+        rows, cols = [], []
+        for off in (-3000, -1, 0, 2, 3000):
+            r = np.arange(max(0, -off), min(n, n - off))
+            rows.append(r)
+            cols.append(r + off)
+        r, c = np.concatenate(rows), np.concatenate(cols)
+        coo = O.from_triplets(n, n, r, c, rng.uniform(0.5, 2.0, r.size))
+        d = to_dev(so, coo)
+        ncols, nrows = n, n
+    else:
+        csr = synth.banded(700_000, 13, seed=2)
+        coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
+        d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+        ncols, nrows = csr.ncols, csr.nrows
+    skew = 1 if shape.endswith("unaligned") else 0
+    xt = torch.empty(ncols + skew, dtype=torch.float64).pin_memory()
+    yt = torch.empty(nrows + skew, dtype=torch.float64).pin_memory()
+    xn, yn = xt.numpy()[skew:], yt.numpy()[skew:]
+    xn[:] = np.random.default_rng(11).uniform(-1, 1, ncols)
     for f in (so.DIA, so.HDC):
-        m = d.convert(f)
+        m = d.from_coo(f) if shape == "wide" else d.convert(f)
         want = O.oc_spmv(O.oc_convert(coo, f), xn)
-        yn[:] = np.nan
-        m.spmv_into(xn, yn)
-        assert np.array_equal(yn, want), f
+        for _ in range(2):
+            yn[:] = np.nan
+            m.spmv_into(xn, yn)
+            assert np.array_equal(yn, want), f
         assert np.array_equal(m.spmv(xn.copy()), want), f  # pageable -> one-shot path
 
 
