@@ -61,8 +61,34 @@ reftests: $(LIBDIR)/libsparseoracle.so
 	    -L$(LIBDIR) -lsparseoracle -lsparseoracle_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' || exit 1; \
 	  done; \
 	else echo "reftests: $(REF_PROJ)/tests absent, keeping prebuilt binaries"; fi
+	@if [ -d $(REF_PROJ)/tests ]; then $(MAKE) --no-print-directory refaccept; fi
 
-.PHONY: reftests
+# The reference's acceptance suite (proj/tests/acceptance.cpp, 10 criteria)
+# and its pipeline / trainer suites, compiled unmodified: the hot-path headers
+# resolve to include/sparseoracle (this repo, over the sm_100a library), the
+# layers above the path (pipeline.hpp, trainer.hpp, ingest.hpp) to the
+# reference's own, whose sources (src/pipeline.cpp, trainer.cpp, ingest.cpp)
+# are compiled in place with the httplib stub.  The reference's
+# read/write_matrix_market definitions are renamed away (-D) so every caller,
+# its pipeline included, reads Matrix Market through this repo's parser.
+REF_LAYER := build/refinc/sparseoracle
+REF_ACC_OBJS := build/refacc/pipeline.o build/refacc/trainer.o build/refacc/ingest.o
+refaccept: $(LIBDIR)/libsparseoracle.so
+	@mkdir -p $(REF_LAYER) build/refacc build/reftests
+	@for h in errors features formats model rng spmv tuners; do ln -sfn $(CURDIR)/include/sparseoracle/$$h.hpp $(REF_LAYER)/$$h.hpp; done
+	@for h in pipeline trainer ingest; do ln -sfn $(REF_PROJ)/include/sparseoracle/$$h.hpp $(REF_LAYER)/$$h.hpp; done
+	$(CXX) -std=c++20 -O2 -Ibuild/refinc -Ioracle/httplib_stub -c $(REF_PROJ)/src/pipeline.cpp -o build/refacc/pipeline.o
+	$(CXX) -std=c++20 -O2 -Ibuild/refinc -c $(REF_PROJ)/src/trainer.cpp -o build/refacc/trainer.o
+	$(CXX) -std=c++20 -O2 -Ibuild/refinc -Ioracle/httplib_stub -Dread_matrix_market=ref_read_matrix_market_unused \
+	    -Dwrite_matrix_market=ref_write_matrix_market_unused -c $(REF_PROJ)/src/ingest.cpp -o build/refacc/ingest.o
+	@for t in acceptance test_pipeline test_trainer test_ingest; do \
+	  $(CXX) -std=c++20 -O1 -pthread -Ibuild/refinc -Itests/support/doctest_shim -I$(REF_PROJ)/tests \
+	    $(REF_PROJ)/tests/$$t.cpp $(REF_ACC_OBJS) -o build/reftests/$$t \
+	    -L$(LIBDIR) -lsparseoracle -lsparseoracle_b200 -lssl -lcrypto -lz \
+	    -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' || exit 1; \
+	done
+
+.PHONY: reftests refaccept
 
 # Diagnostic micro-benchmarks (not the product): scripts/spmv_lab.cu (kernel
 # variants + the product kernels side by side), scripts/pipe_probe.cu (host

@@ -343,7 +343,10 @@ def main():
         t_csr = per_format["CSR"]["ms"] * 1e-3
         tune = {"chosen": FMT[tuned], "measured_optimal": FMT[best], "t_fe_ms": round(t_fe * 1e3, 4),
                 "t_pred_ms": round(t_pr * 1e3, 4),
-                "overhead_csr_spmv_equiv": round((t_fe + t_pr) / t_csr, 3)}
+                "overhead_csr_spmv_equiv": round((t_fe + t_pr) / t_csr, 3),
+                # pipeline.cpp:298-302: T_CSR / (T_FE + T_PRED + T_OPT), reps = 1000 multiplies
+                "speedup_vs_csr_reps1000": round(1000 * t_csr / (t_fe + t_pr + 1000 * per_format[FMT[tuned]]["ms"] * 1e-3),
+                                                 3)}
     except Exception as e:  # model not available yet
         tune = {"error": str(e)[:200], "chosen": FMT[tuned], "measured_optimal": FMT[best]}
     m = mats[tuned]
