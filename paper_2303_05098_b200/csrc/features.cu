@@ -356,9 +356,31 @@ __device__ __forceinline__ Mono shfl_mono_up(const Mono& m, int o) {
     return Mono{__shfl_up_sync(0xffffffffu, m.a0, o), __shfl_up_sync(0xffffffffu, m.a1, o),
                 __shfl_up_sync(0xffffffffu, m.p, o)};
 }
-// ordered inclusive scan across the warp
+// No tie anywhere: the summary is "add k ulps" (a0 == a1) and the out parity
+// is the in parity flipped by k's parity -- composition is integer addition.
+__device__ __forceinline__ bool mono_canonical(const Mono& m) {
+    return m.a0 == m.a1 && m.p == (int(m.a0 & 1) | (int((m.a0 + 1) & 1) << 1));
+}
+
+// ordered inclusive scan across the warp (ok: AND over lanes <= this one).
+// When every lane is canonical (no exact ties: the usual case) it is a
+// plain 64-bit add-scan, a tenth of the instructions of the general
+// composition -- the walk is one warp's dependent chain, so instruction
+// count is its time.
 __device__ __forceinline__ Mono warp_scan_mono(Mono m, bool& ok) {
     const unsigned lane = threadIdx.x & 31u;
+    if (__all_sync(0xffffffffu, mono_canonical(m))) {
+        long long a = m.a0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, a, o);
+            if (lane >= unsigned(o)) a += t;
+        }
+        const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+        const unsigned le = lane == 31u ? 0xffffffffu : ((2u << lane) - 1u);
+        ok = (bad & le) == 0u;
+        return Mono{a, a, int(a & 1) | (int((a + 1) & 1) << 1)};
+    }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const Mono up = shfl_mono_up(m, o);
@@ -548,7 +570,13 @@ __device__ double seq_rows(double S, int64_t lo, int64_t hi, const int32_t* __re
     return S;
 }
 
+// Ranges up to kSeqRows rows are cheaper as plain sequential additions (one
+// lane, ~8 cycles per add) than as binade-replay rounds (a 5-level warp scan
+// of 64-bit summaries, ~1800 cycles per round on the walk's single warp).
+constexpr int64_t kSeqRows = 512;
+
 __device__ double advance_exact(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
+    if (hi - lo <= kSeqRows) return seq_rows(S, lo, hi, rc, avg);
     if (S == 0.0) {
         // the head of the matrix: S doubles every few rows, so binade
         // changes are dense -- cheaper to add the first rows one by one
@@ -701,6 +729,15 @@ __device__ __forceinline__ void walk_and_finalize(const int32_t* __restrict__ rc
                                                   int64_t nch, int64_t chunk, const MonoRec* __restrict__ rec,
                                                   const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
     const unsigned lane = threadIdx.x & 31u;
+#ifdef SOB_SPREAD_DEBUG
+    unsigned long long dbg_t0;
+    {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        dbg_t0 = gt;
+    }
+    unsigned long long dbg_exact_ns = 0, dbg_exact_n = 0;
+#endif
     const double avg = double(st->visits) / double(nrows);
     const int64_t sub = chunk / kSubs;
     const double S = walk_records(0.0, rec, nch, [&](double S, int64_t c) {
@@ -708,13 +745,28 @@ __device__ __forceinline__ void walk_and_finalize(const int32_t* __restrict__ rc
         const int64_t nsub = ceil_div(((r0 + chunk < nrows) ? r0 + chunk : nrows) - r0, sub);
         return walk_records(S, fine + c * kSubs, nsub, [&](double S, int64_t j) {
 #ifdef SOB_SPREAD_DEBUG
-            if (lane == 0)
-                printf("spread exact chunk %lld sub %lld S=%.17g\n", (long long)c, (long long)j, S);
-#endif
+            unsigned long long g0, g1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+            const int64_t lo = r0 + j * sub;
+            const double S2 = advance_exact(S, lo, lo + sub < nrows ? lo + sub : nrows, rc, avg);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+            dbg_exact_ns += g1 - g0;
+            ++dbg_exact_n;
+            return S2;
+#else
             const int64_t lo = r0 + j * sub;
             return advance_exact(S, lo, lo + sub < nrows ? lo + sub : nrows, rc, avg);
+#endif
         });
     });
+#ifdef SOB_SPREAD_DEBUG
+    {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        if (lane == 0)
+            printf("spread walk total %llu ns, %llu exact fallbacks %llu ns\n", gt - dbg_t0, dbg_exact_n, dbg_exact_ns);
+    }
+#endif
     if (lane == 0) {
         st->S = S;
         so_feature_vector& f = st->out;
@@ -732,10 +784,39 @@ __device__ __forceinline__ void walk_and_finalize(const int32_t* __restrict__ rc
     }
 }
 
-__global__ void __launch_bounds__(32)
+// The walk is one warp and a chain of dependent loads (records, then rows of
+// the sub-chunks where S changes binade), ~5 L2 round trips per binade
+// change.  When the row counts and both record levels fit in shared memory
+// (matrices up to ~32K rows: the config-4 corpus starts at 10^4) the CTA
+// first stages them there and warp 0 walks the staged copy -- same
+// arithmetic, same order; larger matrices walk global memory.
+constexpr int kWalkThreads = 512;
+constexpr size_t kWalkSmem = 200 * 1024;
+
+inline size_t walk_smem_bytes(int64_t nrows, int64_t nch) {
+    return size_t(nch) * (kSubs + 1) * sizeof(MonoRec) + size_t(nrows) * sizeof(int32_t);
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kWalkThreads)
     spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
                 const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
-    walk_and_finalize(rc, nrows, ncols, nch, chunk, rec, fine, st);
+    if (STAGED) {
+        extern __shared__ __align__(16) unsigned char wsm[];
+        MonoRec* srec = reinterpret_cast<MonoRec*>(wsm);
+        MonoRec* sfine = srec + nch;
+        int32_t* src = reinterpret_cast<int32_t*>(sfine + nch * kSubs);
+        for (int64_t i = threadIdx.x; i < nch; i += kWalkThreads) srec[i] = rec[i];
+        for (int64_t i = threadIdx.x; i < nch * kSubs; i += kWalkThreads) sfine[i] = fine[i];
+        const int4* rc4 = reinterpret_cast<const int4*>(rc);
+        int4* src4 = reinterpret_cast<int4*>(src);
+        for (int64_t i = threadIdx.x; i < nrows / 4; i += kWalkThreads) src4[i] = rc4[i];
+        for (int64_t i = (nrows / 4) * 4 + threadIdx.x; i < nrows; i += kWalkThreads) src[i] = rc[i];
+        __syncthreads();
+        if (threadIdx.x < 32) walk_and_finalize(src, nrows, ncols, nch, chunk, srec, sfine, st);
+    } else {
+        if (threadIdx.x < 32) walk_and_finalize(rc, nrows, ncols, nch, chunk, rec, fine, st);
+    }
 }
 
 __global__ void feat_init(FeatState* st) {
@@ -865,7 +946,18 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     MonoRec* fine = rec + nch;
     spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get(), P.get(), rec, fine);
     SOB_LAUNCH("spread_mono");
-    spread_walk<<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+    const size_t wsm = walk_smem_bytes(n, nch);
+    if (wsm <= kWalkSmem) {
+        static const bool attr = [] {
+            SOB_CUDA(cudaFuncSetAttribute(spread_walk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kWalkSmem)));
+            return true;
+        }();
+        (void)attr;
+        spread_walk<true><<<1, kWalkThreads, wsm, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+    } else {
+        spread_walk<false><<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+    }
     SOB_LAUNCH("spread_walk");
 }
 
