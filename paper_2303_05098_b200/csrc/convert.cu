@@ -161,34 +161,33 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
 
 // SpMV warp groups, greedy: a group is <= 32 consecutive rows holding <= cap
 // entries; a row longer than cap stands alone (and is split into pieces).
-// One thread walks kGroupChunk rows (chunk starts are forced group starts,
-// so the partition is deterministic and parallel) and flags group starts.
+// One warp per kGroupChunk rows (chunk starts are forced group starts, so
+// the partition is deterministic and parallel) flags group starts: the
+// chunk's row_ptr is staged in shared memory (coalesced), then each group
+// costs one ballot -- the next start is the first row whose end passes
+// base + cap (or base row itself when it is longer than cap), at most 32
+// rows on.  (A thread walking its chunk row by row took ~150 us at any size.)
 constexpr int kGroupChunk = 1024;
-__global__ void group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t cap, int32_t* __restrict__ flag) {
-    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t lo = c * kGroupChunk;
+constexpr int kGroupWarps = 4;
+__global__ void __launch_bounds__(32 * kGroupWarps)
+    group_flags(const int64_t* __restrict__ rp, int64_t n, int64_t cap, int32_t* __restrict__ flag) {
+    __shared__ int64_t srp[kGroupWarps][kGroupChunk + 1];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t lo = (int64_t(blockIdx.x) * kGroupWarps + w) * kGroupChunk;
     if (lo >= n) return;
-    const int64_t hi = lo + kGroupChunk < n ? lo + kGroupChunk : n;
-    int64_t i = lo;
-    int64_t next_start = lo;
-    int64_t base = 0;
-    int64_t rpi = rp[lo];
-    for (; i < hi; ++i) {
-        const int64_t rpn = rp[i + 1];
-        if (i == next_start) {
-            flag[i] = 1;
-            base = rpi;
-            next_start = i + 32;
-            if (rpn - rpi > cap) next_start = i + 1;  // long row: alone
-        } else if (rpn - base > cap) {
-            flag[i] = 1;  // row does not fit: starts the next group
-            base = rpi;
-            next_start = i + 32;
-            if (rpn - rpi > cap) next_start = i + 1;
-        } else {
-            flag[i] = 0;
-        }
-        rpi = rpn;
+    const int len = int(lo + kGroupChunk < n ? kGroupChunk : n - lo);
+    int64_t* r = srp[w];
+    for (int j = lane; j <= len; j += 32) r[j] = rp[lo + j];
+    for (int j = lane; j < len; j += 32) flag[lo + j] = 0;
+    __syncwarp();
+    for (int g = 0; g < len;) {
+        if (lane == 0) flag[lo + g] = 1;
+        const int64_t base = r[g];
+        const int j = g + lane;
+        const bool over = j < len && r[j + 1] - base > cap;
+        const unsigned b = __ballot_sync(0xffffffffu, over);
+        const int step = b ? __ffs(b) - 1 : 32;
+        g += step ? step : 1;  // step 0: the base row alone exceeds cap
     }
 }
 
@@ -672,8 +671,8 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     // SpMV warp groups; entries per lane follow the mean row length
     const int64_t nnz_total = d2h_scalar(csr.row_ptr.get() + n, s);
     csr.grp_cap = 32 * ((nnz_total <= 8 * n) ? kGroupItemsShort : kGroupItemsLong);
-    group_flags<<<unsigned(ceil_div(ceil_div(n, kGroupChunk), 128)), 128, 0, s>>>(csr.row_ptr.get(), n, csr.grp_cap,
-                                                                                 flag.get());
+    group_flags<<<unsigned(ceil_div(ceil_div(n, kGroupChunk), kGroupWarps)), 32 * kGroupWarps, 0, s>>>(
+        csr.row_ptr.get(), n, csr.grp_cap, flag.get());
     SOB_LAUNCH("group_flags");
     exclusive_scan_i32_to_i64(flag.get(), pos.get(), n, s);
     csr.ngrp = d2h_scalar(pos.get() + n, s);
