@@ -350,13 +350,13 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
     const bool dia_only = m.format == SO_DIA || (m.format == SO_HDC && m.csr.nnz == 0);
     if (!dia_only || m.dia.ndiags == 0 || m.nrows < 2 * kPipeRows) return false;
     if (!is_pinned(x) || !is_pinned(y)) return false;
-    if (!m.dia_window_known) {
+    if (!m.dia_window_known.load(std::memory_order_acquire)) {
         std::vector<int64_t> off(size_t(m.dia.ndiags));
         d2h(off.data(), m.dia.offsets, m.dia.ndiags, s);
         SOB_CUDA(cudaStreamSynchronize(s));
-        m.dia_omin = *std::min_element(off.begin(), off.end());
-        m.dia_omax = *std::max_element(off.begin(), off.end());
-        m.dia_window_known = true;
+        m.dia_omin.store(*std::min_element(off.begin(), off.end()), std::memory_order_relaxed);
+        m.dia_omax.store(*std::max_element(off.begin(), off.end()), std::memory_order_relaxed);
+        m.dia_window_known.store(true, std::memory_order_release);
     }
     // narrow windows: one kernel over the host link, no copy engine
     static const bool zc_off = std::getenv("SOB_NO_ZERO_COPY") != nullptr;  // diagnostic knob

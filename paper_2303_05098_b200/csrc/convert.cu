@@ -350,6 +350,10 @@ struct DiagHist : OpBase {
         const int32_t key = valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1;
         hash_add(*h, bins, key);
     }
+    static constexpr bool kPieceDirect = true;  // piece_sweep (hist.cuh)
+    __device__ void piece(int r, int64_t k, bool valid) {
+        if (valid) atomicAdd(bins + (int64_t(col[k]) - r + nrows - 1), 1);
+    }
     SlotCache cache;
     static constexpr bool kHasEntry8 = true;
     __device__ void entry(int r, int32_t c, bool valid, int slot) {
@@ -768,7 +772,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.val, src.csr.val);
     cp(m->csr.blk, src.csr.blk);
     cp(m->csr.blk_k, src.csr.blk_k);
-    m->csr.canonical = src.csr.canonical;
+    m->csr.canonical.store(src.csr.canonical.load());
     m->csr.ngrp = src.csr.ngrp;
     m->csr.grp_cap = src.csr.grp_cap;
     cp(m->csr.grp, src.csr.grp);
@@ -866,11 +870,26 @@ so_matrix* csr_to_format(const so_matrix& csr, int32_t target, const so_conversi
                 hdc_rest_total<<<grid_for(nbins, 256), 256, 0, s>>>(bins.get(), nbins, thr, rest.get());
                 SOB_LAUNCH("hdc_rest_total");
             }
-            if (d2h_scalar(rest.get(), s) == 0) {
+            const int64_t rest_total = int64_t(d2h_scalar(rest.get(), s));
+            if (rest_total == 0) {
                 SOB_CUDA(cudaMemsetAsync(c.row_ptr.get(), 0, c.row_ptr.bytes(), s));
                 c.nnz = 0;
                 c.col.alloc(0, s);
                 c.val.alloc(0, s);
+                build_row_blocks(c, n, s);
+                return m.release();
+            }
+            // scattered inputs (R-MAT): no diagonal reaches the threshold, the
+            // CSR part is the whole input -- copy it, no keep flags / compaction
+            if (rest_total == z) {
+                SOB_CUDA(cudaMemcpyAsync(c.row_ptr.get(), csr.csr.row_ptr.get(), c.row_ptr.bytes(),
+                                         cudaMemcpyDeviceToDevice, s));
+                c.nnz = z;
+                c.col.alloc(z, s);
+                c.val.alloc(z, s);
+                SOB_CUDA(cudaMemcpyAsync(c.col.get(), csr.csr.col.get(), c.col.bytes(), cudaMemcpyDeviceToDevice, s));
+                SOB_CUDA(cudaMemcpyAsync(c.val.get(), csr.csr.val.get(), c.val.bytes(), cudaMemcpyDeviceToDevice, s));
+                c.canonical.store(csr.csr.canonical.load());
                 build_row_blocks(c, n, s);
                 return m.release();
             }

@@ -69,6 +69,10 @@ struct FeatCsrOp {
     __device__ void operator()(int r, int64_t k, bool valid) {
         hash_add(*h, bins, valid ? int32_t(int64_t(col[k]) - r + nrows - 1) : -1);
     }
+    static constexpr bool kPieceDirect = true;  // piece_sweep (hist.cuh)
+    __device__ void piece(int r, int64_t k, bool valid) {
+        if (valid) atomicAdd(bins + (int64_t(col[k]) - r + nrows - 1), 1);
+    }
     SlotCache cache;
     static constexpr bool kHasEntry8 = true;
     __device__ void entry(int r, int32_t c, bool valid, int slot) {

@@ -10,6 +10,8 @@
 // global bins, where they are spread over many addresses anyway.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sob {
@@ -161,6 +163,12 @@ __device__ __forceinline__ void hash_add(SmemHash& h, int32_t* __restrict__ gbin
     unsigned peers;
     if (__all_sync(0xffffffffu, key < 0 || key == k0)) {
         peers = valid;
+    } else if (__shfl_sync(0xffffffffu, h.used >= kHashSlots / 2, 0)) {
+        // scattered keys (the CTA's hash is already half full): warp
+        // merging rarely pays for its __match_any_sync -- each lane goes on
+        // alone (home-slot check, else a global atomic)
+        if (key >= 0) hash_insert_one(h, gbins, key, 1);
+        return;
     } else {
         // distinct dummy keys for idle lanes so they never merge with real ones
         const int32_t k = key >= 0 ? key : -2 - int32_t(lane);
@@ -300,6 +308,14 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
     op.end();
 }
 
+// Ops whose piece(r, k, valid) bypasses shared-memory merging: the entries
+// of one row have distinct columns, so their diagonal keys never repeat
+// inside a piece and a direct global atomic per entry is the whole job.
+template <class Op, class = void>
+struct piece_direct : std::false_type {};
+template <class Op>
+struct piece_direct<Op, std::void_t<decltype(Op::kPieceDirect)>> : std::bool_constant<Op::kPieceDirect> {};
+
 // One CTA per long-row piece (CsrPart::piece_k): coalesced entries of a
 // single row, so no row search.  Same op interface (row() is not called).
 template <class Op>
@@ -317,7 +333,12 @@ __global__ void __launch_bounds__(256) piece_sweep(const int64_t* __restrict__ p
             hi = mid;
     }
     const int r = lrow[lo];
-    for (int64_t b = k0; b < k1; b += blockDim.x) op(r, b + threadIdx.x, b + threadIdx.x < k1);
+    for (int64_t b = k0; b < k1; b += blockDim.x) {
+        if constexpr (piece_direct<Op>::value)
+            op.piece(r, b + threadIdx.x, b + threadIdx.x < k1);
+        else
+            op(r, b + threadIdx.x, b + threadIdx.x < k1);
+    }
     op.end();
 }
 

@@ -1,6 +1,7 @@
 // Device-resident sparse containers (the HBM layout of DESIGN.md §3) and the
 // internal entry points shared by the .cu translation units.
 #pragma once
+#include <atomic>
 
 #include <memory>
 #include <string>
@@ -28,8 +29,11 @@ struct CooPart {
     int64_t nnz = 0;
     DBuf<int32_t> row, col;
     DBuf<double> val;
-    mutable int64_t max_gap = -1;  // longest empty-row run, computed on the first multiply (spmv.cu)
-    mutable int8_t long_runs = -1;  // some row covers > kFixupInline chunks (-1 unknown), same pass
+    // Lazily profiled on the first multiply (spmv.cu coo_profile); atomics
+    // because concurrent readers of one const matrix may race to fill them
+    // (each value is meaningful on its own: -1 = unknown = the safe path).
+    mutable std::atomic<int64_t> max_gap{-1};  // longest empty-row run
+    mutable std::atomic<int> long_runs{-1};    // some row covers > kFixupInline chunks
 };
 struct CsrPart {
     int64_t nnz = 0;
@@ -39,7 +43,7 @@ struct CsrPart {
     DBuf<int32_t> blk;    // row-block partition, nblk+1 entries
     DBuf<int64_t> blk_k;  // first entry of each row block (= row_ptr[blk[b]])
     int64_t nblk = 0;
-    mutable int canonical = -1;  // rows strictly increasing: -1 unknown, 0 no, 1 yes
+    mutable std::atomic<int> canonical{-1};  // rows strictly increasing: -1 unknown, 0 no, 1 yes (cached)
     // SpMV warp-group partition
     int64_t ngrp = 0;
     int grp_cap = 32 * kGroupItemsLong;
@@ -86,8 +90,9 @@ struct so_matrix {
     int64_t kh = 0;
     int64_t threshold = 0;
     // cached min/max DIA offset (pipelined host spmv), filled on first use
-    mutable bool dia_window_known = false;
-    mutable int64_t dia_omin = 0, dia_omax = 0;
+    // (published with release on dia_window_known; concurrent fillers write the same values)
+    mutable std::atomic<bool> dia_window_known{false};
+    mutable std::atomic<int64_t> dia_omin{0}, dia_omax{0};
 
     int64_t nnz() const {
         switch (format) {

@@ -53,33 +53,59 @@ __global__ void __launch_bounds__(kScanBlock) tile_reduce(const TIn* __restrict_
 }
 
 // Single CTA: exclusive scan of the tile sums in place; writes the grand total
-// to *total_out.
-__global__ void __launch_bounds__(kScanBlock) scan_tile_sums(int64_t* __restrict__ sums, int64_t m,
-                                                              int64_t* __restrict__ total_out) {
-    __shared__ int64_t warp_tot[kScanBlock / 32 + 1];
-    int64_t carry = 0;
-    for (int64_t base = 0; base < m; base += kScanBlock) {
-        int64_t i = base + threadIdx.x;
-        int64_t v = i < m ? sums[i] : 0;
-        int64_t tot;
-        int64_t ex = block_exclusive_scan(v, warp_tot, tot);
-        if (i < m) sums[i] = carry + ex;
-        carry += tot;
+// to *total_out.  Each of the 1024 threads owns a contiguous run of sums
+// (one block scan in total, not one per 256 sums).
+constexpr int kSumsBlock = 1024;
+__device__ int64_t block_exclusive_scan_1024(int64_t v, int64_t* warp_tot, int64_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t inc = warp_inclusive_sum(v);
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int64_t w = warp_tot[lane];  // 32 warps
+        const int64_t wi = warp_inclusive_sum(w);
+        warp_tot[lane] = wi - w;
+        if (lane == 31) warp_tot[32] = wi;
     }
-    if (threadIdx.x == 0) *total_out = carry;
+    __syncthreads();
+    total = warp_tot[32];
+    return warp_tot[warp] + inc - v;
 }
+
+__global__ void __launch_bounds__(kSumsBlock) scan_tile_sums(int64_t* __restrict__ sums, int64_t m,
+                                                              int64_t* __restrict__ total_out) {
+    __shared__ int64_t warp_tot[33];
+    const int64_t per = (m + kSumsBlock - 1) / kSumsBlock;
+    const int64_t a = int64_t(threadIdx.x) * per, b = a + per < m ? a + per : m;
+    int64_t loc = 0;
+    for (int64_t i = a; i < b; ++i) loc += sums[i];
+    int64_t tot;
+    int64_t run = block_exclusive_scan_1024(loc, warp_tot, tot);
+    for (int64_t i = a; i < b; ++i) {
+        const int64_t v = sums[i];
+        sums[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) *total_out = tot;
+}
+
+// Tile staged through shared memory with one pad word per 16 (the blocked
+// per-thread pass reads 16 consecutive int64 per thread: unpadded, a
+// half-warp's 8-byte accesses all hit one bank pair).
+__device__ __forceinline__ int tile_pad(int e) { return e + (e >> 4); }
 
 template <typename TIn>
 __global__ void __launch_bounds__(kScanBlock) tile_scan(const TIn* __restrict__ in, int64_t n,
                                                          const int64_t* __restrict__ tile_off,
                                                          int64_t* __restrict__ out) {
-    __shared__ int64_t tile[kScanTile];
+    __shared__ int64_t tile[kScanTile + kScanTile / 16];
     __shared__ int64_t warp_tot[kScanBlock / 32 + 1];
     const int64_t base = int64_t(blockIdx.x) * kScanTile;
+#pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        int e = j * kScanBlock + threadIdx.x;
-        int64_t i = base + e;
-        tile[e] = i < n ? int64_t(in[i]) : 0;
+        const int e = j * kScanBlock + threadIdx.x;
+        const int64_t i = base + e;
+        tile[tile_pad(e)] = i < n ? int64_t(in[i]) : 0;
     }
     __syncthreads();
     int64_t local[kScanItems];
@@ -87,17 +113,18 @@ __global__ void __launch_bounds__(kScanBlock) tile_scan(const TIn* __restrict__ 
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         local[j] = s;
-        s += tile[threadIdx.x * kScanItems + j];
+        s += tile[tile_pad(threadIdx.x * kScanItems + j)];
     }
     int64_t tot;
-    int64_t ex = block_exclusive_scan(s, warp_tot, tot) + tile_off[blockIdx.x];
+    const int64_t ex = block_exclusive_scan(s, warp_tot, tot) + tile_off[blockIdx.x];
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) tile[threadIdx.x * kScanItems + j] = ex + local[j];
+    for (int j = 0; j < kScanItems; ++j) tile[tile_pad(threadIdx.x * kScanItems + j)] = ex + local[j];
     __syncthreads();
+#pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        int e = j * kScanBlock + threadIdx.x;
-        int64_t i = base + e;
-        if (i < n) out[i] = tile[e];
+        const int e = j * kScanBlock + threadIdx.x;
+        const int64_t i = base + e;
+        if (i < n) out[i] = tile[tile_pad(e)];
     }
 }
 
@@ -111,7 +138,7 @@ void exclusive_scan_impl(const TIn* in, int64_t* out, int64_t n, cudaStream_t s)
     DBuf<int64_t> sums(tiles, s);
     tile_reduce<TIn><<<unsigned(tiles), kScanBlock, 0, s>>>(in, n, sums.get());
     SOB_LAUNCH("tile_reduce");
-    scan_tile_sums<<<1, kScanBlock, 0, s>>>(sums.get(), tiles, out + n);
+    scan_tile_sums<<<1, kSumsBlock, 0, s>>>(sums.get(), tiles, out + n);
     SOB_LAUNCH("scan_tile_sums");
     tile_scan<TIn><<<unsigned(tiles), kScanBlock, 0, s>>>(in, n, sums.get(), out);
     SOB_LAUNCH("tile_scan");

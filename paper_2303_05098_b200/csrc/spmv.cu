@@ -782,7 +782,8 @@ void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s) 
 
 bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s) {
     if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
-    if (!m.dia_window_known || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem) return false;
+    if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
+        return false;
     const int64_t omin = m.dia_omin, omax = m.dia_omax;
     if (omax - omin > kZcSpan) return false;
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
