@@ -73,6 +73,10 @@ struct FeatCsrOp {
     __device__ void piece(int r, int64_t k, bool valid) {
         if (valid) atomicAdd(bins + (int64_t(col[k]) - r + nrows - 1), 1);
     }
+    __device__ bool scattered() const { return __shfl_sync(0xffffffffu, h->used >= kHashSlots / 2, 0); }
+    __device__ void direct(int r, int32_t c, bool valid) {
+        if (valid) hash_insert_one(*h, bins, int32_t(int64_t(c) - r + nrows - 1), 1);
+    }
     SlotCache cache;
     static constexpr bool kHasEntry8 = true;
     __device__ void entry(int r, int32_t c, bool valid, int slot) {

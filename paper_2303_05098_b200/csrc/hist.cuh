@@ -201,6 +201,16 @@ __device__ __forceinline__ int row_in_block(const int64_t* srp, int nr, int64_t 
     return lo;
 }
 
+// Histogram ops with a direct path (kPieceDirect): piece(r, k, valid) for
+// long-row pieces (the entries of one row have distinct columns, so their
+// diagonal keys never repeat inside a piece: a global atomic each), and
+// scattered() / direct(r, c, valid) for row sweeps once the CTA's hash is
+// half full.
+template <class Op, class = void>
+struct piece_direct : std::false_type {};
+template <class Op>
+struct piece_direct<Op, std::void_t<decltype(Op::kPieceDirect)>> : std::bool_constant<Op::kPieceDirect> {};
+
 // ------------------------------------------------------------ row sweep
 // Row-lockstep traversal of a CSR: lane = row, slot j in lockstep across the
 // warp, so banded / stencil rows present the SAME diagonal key in every lane
@@ -273,6 +283,21 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
         const int64_t len = has ? rp[r + 1] - a : 0;
         op.row(int(r), has, len);
         const int64_t elen = len > skip_above ? 0 : len;
+        if constexpr (piece_direct<Op>::value) {
+            // scattered keys (the CTA's hash is half full): no lockstep
+            // votes, every lane inserts its own entries (hash home slot,
+            // else a global atomic)
+            if (op.scattered()) {
+                for (int64_t j0 = 0; j0 < elen; j0 += U) {
+                    int32_t cv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) cv[u] = j0 + u < elen ? __ldg(col + a + j0 + u) : 0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) op.direct(int(r), cv[u], j0 + u < elen);
+                }
+                continue;
+            }
+        }
         const int64_t maxlen = warp_max(elen < kLockstepMax ? elen : int64_t(kLockstepMax));
         for (int64_t j0 = 0; j0 < maxlen; j0 += U) {
             int32_t cv[U];
@@ -307,14 +332,6 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
     }
     op.end();
 }
-
-// Ops whose piece(r, k, valid) bypasses shared-memory merging: the entries
-// of one row have distinct columns, so their diagonal keys never repeat
-// inside a piece and a direct global atomic per entry is the whole job.
-template <class Op, class = void>
-struct piece_direct : std::false_type {};
-template <class Op>
-struct piece_direct<Op, std::void_t<decltype(Op::kPieceDirect)>> : std::bool_constant<Op::kPieceDirect> {};
 
 // One CTA per long-row piece (CsrPart::piece_k): coalesced entries of a
 // single row, so no row search.  Same op interface (row() is not called).
