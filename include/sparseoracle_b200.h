@@ -201,7 +201,9 @@ int32_t so_format_feasible(int32_t target, const so_feature_vector* f,
                            const so_conversion_config* cfg);
 
 /* ---- SpMV  (spmv.hpp:20-32, spmv.cpp:191-246) ------------------------------ */
-/* Device pointers, stream-ordered, no sync.  x has ncols, y has nrows slots. */
+/* Device pointers, stream-ordered, no sync.  x has ncols, y has nrows slots;
+ * x and y must not overlap (the kernels read x while y is written; the
+ * reference API returns a fresh vector, so it never aliases). */
 so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev,
                          void* stream);
 /* Row range [row_lo, row_hi) of y = A x only (DIA; the row-partitioned
@@ -236,7 +238,10 @@ so_status so_ipc_alloc(int64_t bytes, void** dev_ptr, so_ipc_handle* handle);
 so_status so_ipc_open(const so_ipc_handle* handle, void** dev_ptr);
 so_status so_ipc_close(void* dev_ptr);
 so_status so_ipc_free(void* dev_ptr);
-/* spmv(m, x): host vectors, H2D x + kernel(s) + D2H y, synchronous. */
+/* spmv(m, x): host vectors, synchronous; y may alias x (y = A x of the
+ * original x).  Pinned x and y on a DIA-window matrix: one zero-copy kernel
+ * (narrow windows) or a chunked copy pipeline; otherwise H2D x, kernel(s),
+ * D2H y. */
 so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y);
 /* time_spmv: x uploaded once, 1 untimed warm-up, then `reps` multiplies each
  * timed with a cudaEvent pair on the launching stream.  total = sum. */

@@ -349,6 +349,10 @@ constexpr int64_t kPipeRows = 1 << 18;
 bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
     const bool dia_only = m.format == SO_DIA || (m.format == SO_HDC && m.csr.nnz == 0);
     if (!dia_only || m.dia.ndiags == 0 || m.nrows < 2 * kPipeRows) return false;
+    // y overlapping x (in-place calls through the C-ABI): x must be read in
+    // full before any y lands -- the one-shot path does exactly that
+    const auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+    if (xa < ya + sizeof(double) * size_t(m.nrows) && ya < xa + sizeof(double) * size_t(m.ncols)) return false;
     if (!is_pinned(x) || !is_pinned(y)) return false;
     if (!m.dia_window_known.load(std::memory_order_acquire)) {
         std::vector<int64_t> off(size_t(m.dia.ndiags));

@@ -589,3 +589,19 @@ def test_coo_long_run_threshold(so, O, prefix):
         y1, y2 = m.spmv(x), m.spmv(x)
         assert max_rel(y1, want) <= SPMV_TOL, f
         assert np.array_equal(y1, y2), f
+
+
+def test_host_spmv_in_place_pinned(so, O):
+    """so_spmv with y aliasing x (one pinned buffer, square DIA matrix):
+    the result is A*x of the ORIGINAL x, as with separate buffers."""
+    import torch
+    from paper_2303_05098_b200 import synth
+
+    csr = synth.banded(600_000, 3, seed=9)
+    coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
+    m = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val).convert(so.DIA)
+    buf = torch.empty(csr.ncols, dtype=torch.float64).pin_memory().numpy()
+    buf[:] = np.random.default_rng(4).uniform(-1, 1, csr.ncols)
+    want = O.oc_spmv(O.oc_convert(coo, so.DIA), buf.copy())
+    m.spmv_into(buf, buf)
+    assert np.array_equal(buf, want)
