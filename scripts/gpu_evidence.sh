@@ -19,6 +19,9 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:csr_
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:coo_warp_kernel -s 1 -c 1 -o gpurun_out/ev_full_coo_band python scripts/profile_spmv.py --workload banded --reps 1 --formats 0 > /dev/null 2>&1; echo "ncu coo band rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:coo_warp_kernel -s 1 -c 1 -o gpurun_out/ev_full_coo_rmat python scripts/profile_spmv.py --workload rmat --reps 1 --formats 0 > /dev/null 2>&1; echo "ncu coo rmat rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:ell_kernel -s 1 -c 1 -o gpurun_out/ev_full_ell python scripts/profile_spmv.py --workload banded --reps 1 --formats 3 > /dev/null 2>&1; echo "ncu ell rc=$?"
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_rmat_features_convert.csv python scripts/profile_rmat_path.py > /dev/null 2>&1; echo "ncu rmat path rc=$?"
+timeout 600 python scripts/e2e_probe.py > gpurun_out/ev_e2e.log 2>&1; SOB_NO_ZERO_COPY=1 timeout 600 python scripts/e2e_probe.py >> gpurun_out/ev_e2e.log 2>&1; echo "e2e rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:dia_zc_kernel -c 1 -o gpurun_out/ev_full_dia_zc python scripts/e2e_probe.py > /dev/null 2>&1; echo "ncu zc rc=$?"
 tail -1 gpurun_out/ev_bench.log
 tail -1 gpurun_out/ev_bench_ref.log
 tail -3 gpurun_out/ev_config5.log
