@@ -206,7 +206,15 @@ def cpu_baseline_sample(csr, fmt, budget_s=15.0):
     while time.perf_counter() - t0 < budget_s and reps < 20:
         m.spmv(x, ncpu)
         reps += 1
-    return (time.perf_counter() - t0) / reps, reps, ncpu
+    sec = (time.perf_counter() - t0) / reps
+    # beside it: one thread, and the reference feature scan
+    t1 = time.perf_counter()
+    m.spmv(x, 1)
+    sec1 = time.perf_counter() - t1
+    t2 = time.perf_counter()
+    m.extract_features(0.2)
+    fe = time.perf_counter() - t2
+    return sec, reps, ncpu, {"single_thread_s": sec1, "extract_features_s": fe}
 
 
 def main():
@@ -393,11 +401,13 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             try:
-                cs, reps, cores = cpu_baseline_sample(csr, tuned)
+                cs, reps, cores, extra = cpu_baseline_sample(csr, tuned)
                 cpu = {"value": round(nbytes / cs / 1e9, 3), "unit": "GB/s", "cores": cores,
                        "kind": "reference",
                        "sample": f"reference spmv_parallel({cores}) on the same {FMT[tuned]} matrix, "
-                                 f"{reps} reps"}
+                                 f"{reps} reps",
+                       "single_thread_value": round(nbytes / extra["single_thread_s"] / 1e9, 3),
+                       "extract_features_ms": round(extra["extract_features_s"] * 1e3, 2)}
             except Exception as e:
                 cpu = {"error": str(e)[:200]}
         line = {

@@ -19,6 +19,7 @@
 // is the reference's double, not an approximation of it.
 #include <cfloat>
 #include <memory>
+#include <mutex>
 
 #include "features.cuh"
 #include "hist.cuh"
@@ -806,6 +807,24 @@ inline size_t walk_smem_bytes(int64_t nrows, int64_t nch) {
 }
 
 template <bool STAGED>
+__global__ void spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch,
+                            int64_t chunk, const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine,
+                            FeatState* __restrict__ st);
+
+// The staged walk's dynamic shared memory limit, once per device (a function
+// attribute is per device; set outside stream capture).
+void ensure_walk_smem_attr() {
+    static std::mutex mu;
+    static uint64_t done = 0;
+    int dev = 0;
+    SOB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && (done >> dev) & 1) return;
+    SOB_CUDA(cudaFuncSetAttribute(spread_walk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWalkSmem)));
+    if (dev < 64) done |= uint64_t(1) << dev;
+}
+
+template <bool STAGED>
 __global__ void __launch_bounds__(kWalkThreads)
     spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
                 const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
@@ -841,6 +860,7 @@ __global__ void feat_init(FeatState* st) {
 }  // namespace
 
 FeatWorkspace::FeatWorkspace(const so_matrix& m, cudaStream_t s) {
+    ensure_walk_smem_attr();
     const int64_t n = m.nrows;
     const int64_t nch = ceil_div(n, spread_chunk(n));
     rc.alloc(n, s);
@@ -956,12 +976,7 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     SOB_LAUNCH("spread_mono");
     const size_t wsm = walk_smem_bytes(n, nch);
     if (wsm <= kWalkSmem) {
-        static const bool attr = [] {
-            SOB_CUDA(cudaFuncSetAttribute(spread_walk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(kWalkSmem)));
-            return true;
-        }();
-        (void)attr;
+        ensure_walk_smem_attr();  // normally done by the workspace, before any capture
         spread_walk<true><<<1, kWalkThreads, wsm, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
     } else {
         spread_walk<false><<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
