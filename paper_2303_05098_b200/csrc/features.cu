@@ -546,15 +546,10 @@ __global__ void __launch_bounds__(kB)
     mono_chunk(c, rc, nrows, chunk, avg, csum[c], P[c], rec, fine);
 }
 
-// Exact sequential semantics over rows [lo, hi), warp-cooperative (all 32
-// lanes call with the same arguments; returns the same S in every lane).
-__device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg);
 
-// Binade changes cluster where S is still small (the first rows of a chunk),
-// and every change costs one pass over the rest of the current range, so the
-// range is consumed in windows that start small and double after each pass.
-// Plain sequential IEEE additions, 32 rows per step: every lane holds one
-// t_i and all lanes run the same shuffle-fed chain (so S stays warp-uniform).
+// Plain sequential IEEE additions over rows [lo, hi), 32 rows per step: the
+// lanes compute the terms, one lane runs the dependent add chain, and S is
+// broadcast back (warp-uniform).
 __device__ double seq_rows(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
     // lanes compute 32 terms into shared memory; lane 0 runs the dependent
     // add chain from there (loads issue ahead of the adds), then broadcasts
@@ -579,107 +574,13 @@ __device__ double seq_rows(double S, int64_t lo, int64_t hi, const int32_t* __re
     return S;
 }
 
-// Ranges up to kSeqRows rows are cheaper as plain sequential additions (one
-// lane, ~8 cycles per add) than as binade-replay rounds (a 5-level warp scan
-// of 64-bit summaries, ~1800 cycles per round on the walk's single warp).
-constexpr int64_t kSeqRows = 512;
-
+// The exact path over one sub-chunk (<= kMaxSpreadChunk / kSubs = 256 rows):
+// plain sequential additions by one lane (~8 cycles each) -- cheaper than
+// binade-replay rounds over so few rows.  Warp-cooperative call (all 32
+// lanes, same arguments; the same S comes back in every lane).
+static_assert(kMaxSpreadChunk / kSubs <= 256, "sub-chunks stay short enough for the sequential path");
 __device__ double advance_exact(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
-    if (hi - lo <= kSeqRows) return seq_rows(S, lo, hi, rc, avg);
-    if (S == 0.0) {
-        // the head of the matrix: S doubles every few rows, so binade
-        // changes are dense -- cheaper to add the first rows one by one
-        const int64_t h = lo + 256 < hi ? lo + 256 : hi;
-        S = seq_rows(S, lo, h, rc, avg);
-        lo = h;
-    }
-    int64_t w = 256;
-    while (lo < hi) {
-        const int64_t whi = lo + w < hi ? lo + w : hi;
-        S = advance_range(S, lo, whi, rc, avg);
-        lo = whi;
-        w *= 2;
-    }
-    return S;
-}
-
-__device__ double advance_range(double S, int64_t lo, int64_t hi, const int32_t* __restrict__ rc, double avg) {
-    const unsigned lane = threadIdx.x & 31u;
-    int64_t stack[12];
-    int sp = 0;
-    int64_t cur_hi = hi;
-    while (true) {
-        if (lo >= cur_hi) {
-            if (sp == 0) break;
-            cur_hi = stack[--sp];
-            continue;
-        }
-        if (S == 0.0) {
-            // 0 + t == t exactly: jump to the first nonzero t
-            int64_t found = -1;
-            for (int64_t b = lo; b < cur_hi && found < 0; b += 32) {
-                const int64_t i = b + lane;
-                const bool nz = i < cur_hi && sq_dev(rc[i], avg) != 0.0;
-                const unsigned bal = __ballot_sync(0xffffffffu, nz);
-                if (bal) found = b + (__ffs(bal) - 1);
-            }
-            if (found < 0) {
-                lo = cur_hi;
-                continue;
-            }
-            S = sq_dev(rc[found], avg);
-            lo = found + 1;
-            continue;
-        }
-        const int64_t len = cur_hi - lo;
-        const int64_t piece = (len + 31) / 32;
-        const int e = binade(S);
-        const long long m = (long long)scale2(S, 52 - e);
-        const int64_t a = lo + int64_t(lane) * piece;
-        const int64_t b = a + piece < cur_hi ? a + piece : cur_hi;
-        Mono mm = mono_id();
-        bool ok = true;
-        if (piece == 1) {  // one row per lane (the common case near a crossing): no batch
-            if (a < b) ok = mono_elem(sq_dev(rc[a], avg), e, mm);
-        } else {
-            for (int64_t i0 = a; i0 < b; i0 += 8) {
-                int32_t cv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) cv[u] = i0 + u < b ? rc[i0 + u] : 0;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (i0 + u < b && ok) {
-                        Mono el;
-                        ok = mono_elem(sq_dev(cv[u], avg), e, el);
-                        if (ok) mm = mono_cat(mm, el);
-                    }
-                }
-            }
-        }
-        Mono pre = warp_scan_mono(mm, ok);
-        const long long mi = m + ((m & 1) ? pre.a1 : pre.a0);
-        const bool good = ok && double(mi) < kTwo53;
-        const unsigned bad = __ballot_sync(0xffffffffu, !good);
-        const int j = bad ? __ffs(bad) - 1 : 32;
-        if (j > 0) {
-            const long long mj = __shfl_sync(0xffffffffu, mi, j - 1);
-            S = scale2(double(mj), e - 52);
-        }
-        if (j == 32) {
-            lo = cur_hi;
-            continue;
-        }
-        lo = lo + int64_t(j) * piece;
-        if (piece == 1) {  // the single step that changes binade: plain IEEE add
-            S = __dadd_rn(S, sq_dev(rc[lo], avg));
-            lo += 1;
-            continue;
-        }
-        const int64_t piece_hi = lo + piece < cur_hi ? lo + piece : cur_hi;
-        stack[sp++] = cur_hi;
-        cur_hi = piece_hi;
-    }
-    return S;
+    return seq_rows(S, lo, hi, rc, avg);
 }
 
 // Apply records rec[0..nrec) in order to S, 32 at a time (one per lane):
