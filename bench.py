@@ -297,6 +297,13 @@ def main():
                 P.DeviceMatrix.csr(lap.nrows, lap.ncols, lap.row_ptr, lap.col, lap.val),
                 "config3 rmat 2^22 d16 (device generator, seed 42)":
                 synth_dev.rmat(1 << 22, 16, 42).to_device_matrix()}
+        # HYB's favourable shape: config 3 is gather-bound for
+        # every format, so HYB is also reported on rows that fill
+        # its ELL part with 1 % of rows overflowing into the COO part
+        hyb = synth.hyb_skewed(4_000_000, 16, 160, 100, seed=6)
+        work["hyb-favourable n=4M, 16-entry rows, every 100th row 160 (K_H=18, COO part 8 %; host generator, seed 6)"] = \
+            P.DeviceMatrix.csr(hyb.nrows, hyb.ncols, hyb.row_ptr, hyb.col, hyb.val)
+        del hyb, lap
         for wname, wbase in work.items():
             xo = torch.ones(wbase.ncols, dtype=torch.float64, device="cuda")
             yo = torch.empty(wbase.nrows, dtype=torch.float64, device="cuda")

@@ -167,6 +167,30 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
 // costs one ballot -- the next start is the first row whose end passes
 // base + cap (or base row itself when it is longer than cap), at most 32
 // rows on.  (A thread walking its chunk row by row took ~150 us at any size.)
+// Shared-memory layout of each warp group's products (csr_warp_kernel):
+// lane i walks prod[pa_i + j], so rows of one even length (16 entries: every
+// lane on one bank) serialise the walk.  The padded layout stores entry e at
+// e + e / 16; a group takes it when its row starts cover more of the 16
+// double-wide banks that way, flagged in bit kGrpPadBit of grp_k[g] (decided
+// once here, so the SpMV pays no vote).
+__global__ void group_pad_flags(const int32_t* __restrict__ grp, int64_t* __restrict__ grp_k, int64_t ngrp,
+                                const int64_t* __restrict__ rp, int cap, unsigned long long* npad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (g >= ngrp) return;
+    const int r0 = grp[g], r1 = grp[g + 1];
+    const int64_t k0 = grp_k[g];
+    if (grp_k[g + 1] - k0 > cap) return;  // a long row: pieces, no walk
+    const bool act = r0 + lane < r1;
+    const int pa = act ? int(rp[r0 + lane] - k0) : 0;
+    const unsigned o0 = __reduce_or_sync(~0u, act ? 1u << (pa & 15) : 0u);
+    const unsigned o1 = __reduce_or_sync(~0u, act ? 1u << ((pa + (pa >> 4)) & 15) : 0u);
+    if (lane == 0 && __popc(o1) > __popc(o0)) {
+        grp_k[g] = k0 | kGrpPad;
+        atomicAdd(npad, 1ull);
+    }
+}
+
 constexpr int kGroupChunk = 1024;
 constexpr int kGroupWarps = 4;
 __global__ void __launch_bounds__(32 * kGroupWarps)
@@ -689,6 +713,15 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     row_block_scatter<<<unsigned(ceil_div(n + 1, 256)), 256, 0, s>>>(flag.get(), pos.get(), csr.row_ptr.get(), n,
                                                                      csr.grp.get(), csr.grp_k.get());
     SOB_LAUNCH("row_block_scatter");
+    csr.npad = 0;
+    if (csr.ngrp > 0) {
+        DBuf<unsigned long long> npad(1, s);
+        SOB_CUDA(cudaMemsetAsync(npad.get(), 0, sizeof(unsigned long long), s));
+        group_pad_flags<<<unsigned(ceil_div(csr.ngrp * 32, 256)), 256, 0, s>>>(
+            csr.grp.get(), csr.grp_k.get(), csr.ngrp, csr.row_ptr.get(), csr.grp_cap, npad.get());
+        SOB_LAUNCH("group_pad_flags");
+        csr.npad = int64_t(d2h_scalar(npad.get(), s));
+    }
     // long rows -> kPiece-entry pieces (SpMV splits them over many CTAs)
     long_row_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, int64_t(csr.grp_cap),
                                                               flag.get());
@@ -781,6 +814,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     m->csr.grp_cap = src.csr.grp_cap;
     cp(m->csr.grp, src.csr.grp);
     cp(m->csr.grp_k, src.csr.grp_k);
+    m->csr.npad = src.csr.npad;
     m->csr.nlong = src.csr.nlong;
     m->csr.npieces = src.csr.npieces;
     cp(m->csr.long_row, src.csr.long_row);

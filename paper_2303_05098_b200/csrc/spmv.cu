@@ -97,7 +97,7 @@ __device__ __forceinline__ void stage_offsets(int* soff, const int64_t* __restri
 // with no CTA-wide barrier.  A group holding one row longer than 32*IT is
 // skipped here (csr_long_pieces + csr_long_fixup).  WITH_DIA fuses the HDC
 // DIA part in front of the CSR part (spmv.cpp:101-106).
-template <int IT, bool WITH_DIA>
+template <int IT, bool WITH_DIA, bool PAD>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                     int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
                     const double* __restrict__ dvals) {
     constexpr int kCap = 32 * IT;
-    __shared__ double sp[8][kCap];
+    __shared__ double sp[8][kCap + (PAD ? kCap / 16 : 0)];  // + the padded layout's slots
     __shared__ int soff[WITH_DIA ? kDiaSmem : 1];
     if (WITH_DIA) stage_offsets(soff, offsets, ndiags);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -115,8 +115,10 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     if (g >= ngrp) return;
     int r0 = grp[g], r1 = grp[g + 1];
     int64_t k0 = grp_k[g];
+    bool pad = PAD && (k0 & kGrpPad);  // product layout (convert.cu group_pad_flags)
+    k0 &= ~kGrpPad;
     // entry count, saturated at kCap + 1 (= long row, handled elsewhere)
-    int cnt = int(min(grp_k[g + 1] - k0, int64_t(kCap + 1)));
+    int cnt = int(min((grp_k[g + 1] & ~kGrpPad) - k0, int64_t(kCap + 1)));
     int c[IT];
     double v[IT];
 #pragma unroll
@@ -136,18 +138,21 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
         const int64_t gn = g + stride;
         int nr0 = 0, nr1 = 0, ncnt = 0;
         int64_t nk0 = 0;
+        bool npad = false;
         if (gn < ngrp) {
             nr0 = grp[gn];
             nr1 = grp[gn + 1];
             nk0 = grp_k[gn];
-            ncnt = int(min(grp_k[gn + 1] - nk0, int64_t(kCap + 1)));
+            npad = PAD && (nk0 & kGrpPad);
+            nk0 &= ~kGrpPad;
+            ncnt = int(min((grp_k[gn + 1] & ~kGrpPad) - nk0, int64_t(kCap + 1)));
         }
         const bool longrow = cnt > kCap;
         if (!longrow) {
 #pragma unroll
             for (int u = 0; u < IT; ++u) {
                 const int e = u * 32 + lane;
-                if (e < cnt) prod[e] = fmul(v[u], __ldg(x + c[u]));
+                if (e < cnt) prod[pad ? e + (e >> 4) : e] = fmul(v[u], __ldg(x + c[u]));
             }
         }
         __syncwarp();
@@ -169,7 +174,10 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
         if (!longrow && r0 + lane < r1) {
             const int r = r0 + lane;
             double acc = 0.0;
-            for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
+            if (pad)
+                for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j + (j >> 4)]);
+            else
+                for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
             if (WITH_DIA)
                 acc = fadd(ndiags <= kDiaSmem ? dia_row<false>(r, int(nrows), int(ncols), ndiags, soff, offsets, dvals, x)
                                               : dia_row<true>(r, int(nrows), int(ncols), ndiags, soff, offsets, dvals, x),
@@ -182,6 +190,7 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
         r0 = nr0;
         r1 = nr1;
         k0 = nk0;
+        pad = npad;
         cnt = ncnt;
         pa = npa;
         pe = npe;
@@ -713,29 +722,35 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
     }
 }
 
-template <int IT>
+template <int IT, bool PAD>
 void launch_csr_warp(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
     if (with_dia)
-        csr_warp_kernel<IT, true><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
-                                                       c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
-                                                       int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get());
+        csr_warp_kernel<IT, true, PAD><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
+                                                            c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
+                                                            int(m.dia.ndiags), m.dia.offsets.get(),
+                                                            m.dia.values.get());
     else
-        csr_warp_kernel<IT, false><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
-                                                        c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
-                                                        nullptr, nullptr);
+        csr_warp_kernel<IT, false, PAD><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
+                                                             c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
+                                                             nullptr, nullptr);
     SOB_LAUNCH("csr_warp_kernel");
 }
 
 void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     if (c.ngrp == 0) return;
+    // matrices where under 1/64 of the groups prefer the padded layout run the
+    // plain-layout kernel (it ignores the flags; layouts differ only in speed)
+    const bool pad = c.npad > 0 && c.npad * 64 >= c.ngrp;
     if (c.grp_cap == 32 * kGroupItemsShort)
-        launch_csr_warp<kGroupItemsShort>(m, with_dia, x, y, s);
+        pad ? launch_csr_warp<kGroupItemsShort, true>(m, with_dia, x, y, s)
+            : launch_csr_warp<kGroupItemsShort, false>(m, with_dia, x, y, s);
     else
-        launch_csr_warp<kGroupItemsLong>(m, with_dia, x, y, s);
+        pad ? launch_csr_warp<kGroupItemsLong, true>(m, with_dia, x, y, s)
+            : launch_csr_warp<kGroupItemsLong, false>(m, with_dia, x, y, s);
     if (c.nlong > 0) {
         const int nd = with_dia ? int(m.dia.ndiags) : 0;
         DBuf<double> part(c.npieces, s);

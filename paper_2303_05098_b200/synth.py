@@ -178,3 +178,23 @@ def uniform_random(n: int, degree: int, seed: int = 4) -> HostCSR:
     cols = rng.integers(0, n, e, dtype=np.int64)
     v = (1.0 + rng.integers(0, 8, e) / 8.0) * np.where(rng.integers(0, 2, e) == 1, -1.0, 1.0)
     return _dedup(n, rows, cols, v)
+
+
+def hyb_skewed(n: int, short: int = 16, long: int = 160, every: int = 100, seed: int = 6) -> HostCSR:
+    """HYB-favourable evidence matrix (SURVEY.md §8d "favourable matrix per
+    format"): every row holds `short` consecutive columns centred on the
+    diagonal, except every `every`-th row (rows i with i % every == every//2)
+    which holds `long`; windows are shifted inward at the edges so every row is
+    full.  With the reference's default K_H = ceil(z/n) (formats.cpp:357-361)
+    the short rows fill the ELL part and each long row overflows
+    long - K_H entries into the COO part (16/160/100: K_H = 18, COO part 8 %)."""
+    rng = np.random.default_rng(seed)
+    lens = np.full(n, short, dtype=np.int64)
+    lens[every // 2::every] = long
+    lens = np.minimum(lens, n)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
+    start = np.clip(np.arange(n, dtype=np.int64) - lens // 2, 0, n - lens)
+    col = start[rows] + (np.arange(rp[-1], dtype=np.int64) - rp[rows])
+    return HostCSR(n, n, rp, col, _values(rng, col.size))

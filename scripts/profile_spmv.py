@@ -26,7 +26,8 @@ def main():
     a = ap.parse_args()
     csr = {"banded": lambda: synth.banded(4_000_000, 13, seed=2),
            "laplacian": lambda: synth.laplacian_2d(1000, seed=1),
-           "rmat": lambda: synth.rmat(22, 16, seed=42)}[a.workload]()
+           "rmat": lambda: synth.rmat(22, 16, seed=42),
+           "hyb": lambda: synth.hyb_skewed(4_000_000, 16, 160, 100, seed=6)}[a.workload]()
     base = P.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
     x = np.ones(csr.ncols)
     for f in [int(v) for v in a.formats.split(",")]:

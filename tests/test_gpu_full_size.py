@@ -89,6 +89,20 @@ def test_config3_rmat_full_size(so, O):
     _full(so, O, synth.rmat(22, 16, seed=42), exact_formats=(2, 3))
 
 
+def test_hyb_favourable_full_size(so, O):
+    """The HYB evidence matrix bench.py reports beside config 3 (n = 4M,
+    16-entry rows, every 100th row 160 entries: K_H = 18, COO part 8 %):
+    arrays, features and SpMV of every format against the oracle."""
+    from paper_2303_05098_b200 import synth
+    csr = synth.hyb_skewed(4_000_000)
+    d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+    h = d.convert(4).download()
+    assert h["ell"]["col"].shape == (4_000_000 * 18,)
+    assert h["coo"]["val"].size == 40_000 * (160 - 18)
+    del d
+    _full(so, O, csr)
+
+
 def test_config5_stencil512_sampled_rows(so, O):
     import torch
 
@@ -101,6 +115,9 @@ def test_config5_stencil512_sampled_rows(so, O):
     xd = 1.0 + (idx % 7).to(torch.float64) / 8.0 - (idx % 3).to(torch.float64) / 16.0
     del idx
     yd = torch.empty(n, dtype=torch.float64, device="cuda")
+    # x is built on torch's stream; the library's (non-blocking) stream does
+    # not wait for it
+    torch.cuda.synchronize()
     full.spmv_device(xd.data_ptr(), yd.data_ptr())
     torch.cuda.synchronize()
     del full

@@ -66,6 +66,7 @@ def _one_rank_reference():
     m = P.DeviceMatrix.stencil27(G, seed=SEED)
     xa = torch.tensor(_x0(0, n), device="cuda")
     xb = torch.empty_like(xa)
+    torch.cuda.synchronize()  # the library's stream does not wait for torch's
     for _ in range(ITERS):
         m.spmv_device(xa.data_ptr(), xb.data_ptr())
         xa, xb = xb, xa

@@ -369,6 +369,17 @@ def test_rmat_skewed(so, O):
     _structured(so, O, synth.rmat(16, 16, seed=42))
 
 
+@pytest.mark.parametrize("short,long,every", [(16, 16, 100), (16, 160, 100), (2, 2, 1), (4, 64, 7),
+                                               (8, 8, 1), (32, 32, 1), (10, 100, 3)])
+def test_even_row_lengths_padded_layout(so, O, short, long, every):
+    """CSR warp groups whose rows share an even length take the padded
+    shared-memory layout (convert.cu group_pad_flags); the per-row order, and
+    so the bit-exact result, is the same in either layout.  Mixed cases cover
+    partitions where only some groups are padded."""
+    from paper_2303_05098_b200 import synth
+    _structured(so, O, synth.hyb_skewed(50_000, short, long, every, seed=11), formats=(1, 4, 5))
+
+
 def test_hdc_with_long_rows(so, O):
     """HDC with a populated DIA part AND CSR rows longer than 2*kWindow
     (exercises the split-row pieces + fused DIA fix-up)."""
