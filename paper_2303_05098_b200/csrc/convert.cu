@@ -173,6 +173,11 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
 // e + e / 16; a group takes it when its row starts cover more of the 16
 // double-wide banks that way, flagged in bit kGrpPadBit of grp_k[g] (decided
 // once here, so the SpMV pays no vote).
+// Two launches: count (SET = false), then -- only when at least 1/64 of the
+// groups prefer the padded layout, i.e. when the SpMV will run the padded
+// kernel -- flag (SET = true); otherwise grp_k stays plain and the
+// plain-layout kernel reads it unmasked.
+template <bool SET>
 __global__ void group_pad_flags(const int32_t* __restrict__ grp, int64_t* __restrict__ grp_k, int64_t ngrp,
                                 const int64_t* __restrict__ rp, int cap, unsigned long long* npad) {
     const int lane = threadIdx.x & 31;
@@ -186,8 +191,10 @@ __global__ void group_pad_flags(const int32_t* __restrict__ grp, int64_t* __rest
     const unsigned o0 = __reduce_or_sync(~0u, act ? 1u << (pa & 15) : 0u);
     const unsigned o1 = __reduce_or_sync(~0u, act ? 1u << ((pa + (pa >> 4)) & 15) : 0u);
     if (lane == 0 && __popc(o1) > __popc(o0)) {
-        grp_k[g] = k0 | kGrpPad;
-        atomicAdd(npad, 1ull);
+        if (SET)
+            grp_k[g] = k0 | kGrpPad;
+        else
+            atomicAdd(npad, 1ull);
     }
 }
 
@@ -715,12 +722,22 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     SOB_LAUNCH("row_block_scatter");
     csr.npad = 0;
     if (csr.ngrp > 0) {
-        DBuf<unsigned long long> npad(1, s);
-        SOB_CUDA(cudaMemsetAsync(npad.get(), 0, sizeof(unsigned long long), s));
-        group_pad_flags<<<unsigned(ceil_div(csr.ngrp * 32, 256)), 256, 0, s>>>(
-            csr.grp.get(), csr.grp_k.get(), csr.ngrp, csr.row_ptr.get(), csr.grp_cap, npad.get());
+        // the counter lives in the (free until long_row_flags) flag scratch:
+        // no allocation between the matrix arrays
+        unsigned long long* npad = reinterpret_cast<unsigned long long*>(pos.get());
+        SOB_CUDA(cudaMemsetAsync(npad, 0, sizeof(unsigned long long), s));
+        const unsigned g = unsigned(ceil_div(csr.ngrp * 32, 256));
+        group_pad_flags<false><<<g, 256, 0, s>>>(csr.grp.get(), csr.grp_k.get(), csr.ngrp, csr.row_ptr.get(),
+                                                 csr.grp_cap, npad);
         SOB_LAUNCH("group_pad_flags");
-        csr.npad = int64_t(d2h_scalar(npad.get(), s));
+        csr.npad = int64_t(d2h_scalar(npad, s));
+        if (csr.npad * kGrpPadShare >= csr.ngrp) {
+            group_pad_flags<true><<<g, 256, 0, s>>>(csr.grp.get(), csr.grp_k.get(), csr.ngrp, csr.row_ptr.get(),
+                                                    csr.grp_cap, npad);
+            SOB_LAUNCH("group_pad_flags");
+        } else {
+            csr.npad = 0;  // too few to pay for the padded kernel: plain layout everywhere
+        }
     }
     // long rows -> kPiece-entry pieces (SpMV splits them over many CTAs)
     long_row_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, int64_t(csr.grp_cap),

@@ -18,6 +18,7 @@ namespace sob {
 constexpr int kWindow = 1024;
 constexpr int kGrpPadBit = 62;
 constexpr int64_t kGrpPad = int64_t(1) << kGrpPadBit;
+constexpr int64_t kGrpPadShare = 64;  // padded kernel when >= 1/64 of the groups prefer it
 constexpr int kPiece = 2048;  // entries per CTA for rows longer than grp_cap
 // SpMV warp groups: <= 32 consecutive rows holding <= grp_cap = 32*items
 // entries (greedy); short-row matrices (mean <= 8) load 8 entries per lane,
@@ -51,7 +52,7 @@ struct CsrPart {
     int grp_cap = 32 * kGroupItemsLong;
     DBuf<int32_t> grp;     // [ngrp+1]
     DBuf<int64_t> grp_k;   // [ngrp+1]; bit kGrpPadBit of grp_k[g]: group g's padded product layout
-    int64_t npad = 0;      // groups flagged padded (0: the SpMV runs the plain-layout kernel)
+    int64_t npad = 0;      // groups flagged padded (0: no flags set, the SpMV runs the plain-layout kernel)
     // rows longer than grp_cap, split into kPiece-entry pieces for SpMV
     int64_t nlong = 0, npieces = 0;
     DBuf<int32_t> long_row;     // [nlong]

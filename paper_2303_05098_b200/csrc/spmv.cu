@@ -115,10 +115,11 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     if (g >= ngrp) return;
     int r0 = grp[g], r1 = grp[g + 1];
     int64_t k0 = grp_k[g];
-    bool pad = PAD && (k0 & kGrpPad);  // product layout (convert.cu group_pad_flags)
-    k0 &= ~kGrpPad;
+    // product layout flag (convert.cu group_pad_flags; set only when PAD)
+    bool pad = PAD && (k0 & kGrpPad);
+    if (PAD) k0 &= ~kGrpPad;
     // entry count, saturated at kCap + 1 (= long row, handled elsewhere)
-    int cnt = int(min((grp_k[g + 1] & ~kGrpPad) - k0, int64_t(kCap + 1)));
+    int cnt = int(min((PAD ? grp_k[g + 1] & ~kGrpPad : grp_k[g + 1]) - k0, int64_t(kCap + 1)));
     int c[IT];
     double v[IT];
 #pragma unroll
@@ -144,8 +145,8 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
             nr1 = grp[gn + 1];
             nk0 = grp_k[gn];
             npad = PAD && (nk0 & kGrpPad);
-            nk0 &= ~kGrpPad;
-            ncnt = int(min((grp_k[gn + 1] & ~kGrpPad) - nk0, int64_t(kCap + 1)));
+            if (PAD) nk0 &= ~kGrpPad;
+            ncnt = int(min((PAD ? grp_k[gn + 1] & ~kGrpPad : grp_k[gn + 1]) - nk0, int64_t(kCap + 1)));
         }
         const bool longrow = cnt > kCap;
         if (!longrow) {
@@ -742,9 +743,9 @@ void launch_csr_warp(const so_matrix& m, bool with_dia, const double* x, double*
 void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     if (c.ngrp == 0) return;
-    // matrices where under 1/64 of the groups prefer the padded layout run the
-    // plain-layout kernel (it ignores the flags; layouts differ only in speed)
-    const bool pad = c.npad > 0 && c.npad * 64 >= c.ngrp;
+    // flags are set (npad > 0) only when >= 1/64 of the groups prefer the
+    // padded layout (convert.cu); otherwise grp_k is plain
+    const bool pad = c.npad > 0;
     if (c.grp_cap == 32 * kGroupItemsShort)
         pad ? launch_csr_warp<kGroupItemsShort, true>(m, with_dia, x, y, s)
             : launch_csr_warp<kGroupItemsShort, false>(m, with_dia, x, y, s);
