@@ -95,19 +95,18 @@ __device__ __forceinline__ void stage_offsets(int* soff, const int64_t* __restri
 // bit-exact.  The next group's col/val/row_ptr loads are issued before the
 // sums (register double buffer), so each warp keeps up to 2*IT loads in flight
 // with no CTA-wide barrier.  A group holding one row longer than 32*IT is
-// skipped here (csr_long_pieces + csr_long_fixup).  WITH_DIA fuses the HDC
-// DIA part in front of the CSR part (spmv.cpp:101-106).
-template <int IT, bool WITH_DIA, bool PAD>
+// skipped here (csr_long_pieces + csr_long_fixup).  ACCUM (HDC with both
+// parts): y already holds the DIA part (dia_kernel ran first) and the row
+// sum is added to it -- spmv.cpp:101-106, DIA part first, then y[i] += CSR
+// row sum: the same roundings, bit-exact.
+template <int IT, bool ACCUM, bool PAD>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                    int64_t nrows, int64_t ncols, int ndiags, const int64_t* __restrict__ offsets,
-                    const double* __restrict__ dvals) {
+                    int64_t nrows) {
     constexpr int kCap = 32 * IT;
     __shared__ double sp[8][kCap + (PAD ? kCap / 16 : 0)];  // + the padded layout's slots
-    __shared__ int soff[WITH_DIA ? kDiaSmem : 1];
-    if (WITH_DIA) stage_offsets(soff, offsets, ndiags);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double* prod = sp[wid];
     int64_t g = int64_t(blockIdx.x) * 8 + wid;
@@ -179,10 +178,7 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                 for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j + (j >> 4)]);
             else
                 for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
-            if (WITH_DIA)
-                acc = fadd(ndiags <= kDiaSmem ? dia_row<false>(r, int(nrows), int(ncols), ndiags, soff, offsets, dvals, x)
-                                              : dia_row<true>(r, int(nrows), int(ncols), ndiags, soff, offsets, dvals, x),
-                           acc);
+            if (ACCUM) acc = fadd(y[r], acc);
             y[r] = acc;
         }
         __syncwarp();
@@ -228,11 +224,9 @@ __global__ void __launch_bounds__(kStreamBlock)
     if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
-template <bool WITH_DIA>
+template <bool ACCUM>
 __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, const int64_t* __restrict__ lpiece,
-                               const double* __restrict__ part, double* __restrict__ y, int64_t nrows, int64_t ncols,
-                               int ndiags, const int64_t* __restrict__ offsets, const double* __restrict__ dvals,
-                               const double* __restrict__ x) {
+                               const double* __restrict__ part, double* __restrict__ y) {
     const int lane = threadIdx.x & 31;
     const int64_t l = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (l >= nlong) return;
@@ -241,8 +235,7 @@ __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, 
     t = warp_sum(t);  // fixed butterfly: deterministic
     if (lane == 0) {
         const int r = lrow[l];
-        if (WITH_DIA) t = fadd(dia_row<true>(r, int(nrows), int(ncols), ndiags, nullptr, offsets, dvals, x), t);
-        y[r] = t;
+        y[r] = ACCUM ? fadd(y[r], t) : t;
     }
 }
 
@@ -724,47 +717,42 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
 }
 
 template <int IT, bool PAD>
-void launch_csr_warp(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
+void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
-    if (with_dia)
+    if (accum)
         csr_warp_kernel<IT, true, PAD><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
-                                                            c.col.get(), c.val.get(), x, y, m.nrows, m.ncols,
-                                                            int(m.dia.ndiags), m.dia.offsets.get(),
-                                                            m.dia.values.get());
+                                                            c.col.get(), c.val.get(), x, y, m.nrows);
     else
         csr_warp_kernel<IT, false, PAD><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
-                                                             c.col.get(), c.val.get(), x, y, m.nrows, m.ncols, 0,
-                                                             nullptr, nullptr);
+                                                             c.col.get(), c.val.get(), x, y, m.nrows);
     SOB_LAUNCH("csr_warp_kernel");
 }
 
-void launch_csr_stream(const so_matrix& m, bool with_dia, const double* x, double* y, cudaStream_t s) {
+// accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x
+void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     if (c.ngrp == 0) return;
     // flags are set (npad > 0) only when >= 1/64 of the groups prefer the
     // padded layout (convert.cu); otherwise grp_k is plain
     const bool pad = c.npad > 0;
     if (c.grp_cap == 32 * kGroupItemsShort)
-        pad ? launch_csr_warp<kGroupItemsShort, true>(m, with_dia, x, y, s)
-            : launch_csr_warp<kGroupItemsShort, false>(m, with_dia, x, y, s);
+        pad ? launch_csr_warp<kGroupItemsShort, true>(m, accum, x, y, s)
+            : launch_csr_warp<kGroupItemsShort, false>(m, accum, x, y, s);
     else
-        pad ? launch_csr_warp<kGroupItemsLong, true>(m, with_dia, x, y, s)
-            : launch_csr_warp<kGroupItemsLong, false>(m, with_dia, x, y, s);
+        pad ? launch_csr_warp<kGroupItemsLong, true>(m, accum, x, y, s)
+            : launch_csr_warp<kGroupItemsLong, false>(m, accum, x, y, s);
     if (c.nlong > 0) {
-        const int nd = with_dia ? int(m.dia.ndiags) : 0;
         DBuf<double> part(c.npieces, s);
         csr_long_pieces<<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(), c.val.get(), x,
                                                                      part.get());
         SOB_LAUNCH("csr_long_pieces");
         const unsigned g = unsigned(ceil_div(c.nlong * 32, 128));  // one warp per long row
-        if (with_dia)
-            csr_long_fixup<true><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y,
-                                                  m.nrows, m.ncols, nd, m.dia.offsets.get(), m.dia.values.get(), x);
+        if (accum)
+            csr_long_fixup<true><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y);
         else
-            csr_long_fixup<false><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y,
-                                                   m.nrows, m.ncols, 0, nullptr, nullptr, x);
+            csr_long_fixup<false><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y);
         SOB_LAUNCH("csr_long_fixup");
     }
 }
@@ -902,11 +890,18 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
             if (m.coo.nnz > 0) launch_coo<true>(m.coo, m.nrows, x, y, s);
             break;
         case SO_HDC:
-            // one kernel per non-empty part; both parts -> fused per-row kernel
-            if (m.csr.nnz == 0)
+            // one kernel per non-empty part; both parts: the DIA kernel, then
+            // the CSR part accumulating into y (spmv.cpp:101-106 order).  A
+            // fused per-row DIA+CSR kernel measured slower on every shape
+            // tried (0.34-0.74 vs 0.38-0.90 of peak)
+            if (m.csr.nnz == 0) {
                 launch_dia(m, x, y, s);
-            else
-                launch_csr_stream(m, m.dia.ndiags > 0, x, y, s);
+            } else if (m.dia.ndiags == 0) {
+                launch_csr_stream(m, false, x, y, s);
+            } else {
+                launch_dia(m, x, y, s);
+                launch_csr_stream(m, true, x, y, s);
+            }
             break;
         default:
             fail(SO_INVALID_INPUT, "unknown format");

@@ -1,4 +1,4 @@
-"""Diagnostic: CSR SpMV time on near-banded matrices with a fraction of long
+"""Diagnostic: SpMV time (CSR by default; formats and cases from argv) on near-banded matrices with a fraction of long
 rows (synth.hyb_skewed variants), to separate the cost of row-length skew
 from the cost of the stream itself.  Not a benchmark line."""
 import json
@@ -17,6 +17,8 @@ PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
 CASES = [(16, 16, 100), (16, 32, 100), (16, 64, 100), (16, 160, 100), (16, 384, 100),
          (16, 160, 1000), (16, 160, 20), (27, 27, 100)]
 fmts = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "1").split(",")]
+if len(sys.argv) > 2:  # e.g. "16:16:100,9:9:100" (short:long:every)
+    CASES = [tuple(int(t) for t in c.split(":")) for c in sys.argv[2].split(",")]
 for short, long, every in CASES:
     c = synth.hyb_skewed(4_000_000, short, long, every, seed=6)
     base = P.DeviceMatrix.csr(c.nrows, c.ncols, c.row_ptr, c.col, c.val)
