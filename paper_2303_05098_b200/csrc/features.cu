@@ -100,6 +100,36 @@ struct FeatCsrOp {
     }
 };
 
+// Entry-parallel CSR sweep for small matrices (fewer than 16 row-lockstep
+// warps per SM): the row blocks of the CSR partition (<= kRowsPerBlock rows,
+// ~2*kWindow entries) with their row_ptr staged in shared memory, 256
+// consecutive entries per step (one per thread), keys into the same shared
+// hash.  The row-lockstep sweep gives such a matrix one warp per 32 rows, each
+// a serial chain over its rows' entries (config-4 id 1762: 41 us for 359 K
+// entries); here every thread of every block has independent work.  Covers
+// long rows too (no piece sweep).
+template <bool ACCUM_RC>
+__global__ void __launch_bounds__(kB)
+    feat_csr_entries(const int32_t* __restrict__ blk, int64_t nblk, const int64_t* __restrict__ rp,
+                     FeatCsrOp<ACCUM_RC> op) {
+    __shared__ int64_t srp[kRowsPerBlock + 1];
+    op.begin();
+    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const int r0 = blk[b], nr = blk[b + 1] - r0;
+        __syncthreads();
+        for (int j = threadIdx.x; j <= nr; j += kB) srp[j] = rp[r0 + j];
+        __syncthreads();
+        for (int j = threadIdx.x; j < nr; j += kB) op.row(r0 + j, true, srp[j + 1] - srp[j]);
+        const int64_t k0 = srp[0], k1 = srp[nr];
+        for (int64_t base = k0; base < k1; base += kB) {
+            const int64_t k = base + threadIdx.x;
+            const bool valid = k < k1;
+            op(valid ? r0 + row_in_block(srp, nr, k) : -1, k, valid);
+        }
+    }
+    op.end();
+}
+
 __global__ void __launch_bounds__(kB)
     feat_coo(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
              int32_t* __restrict__ rc, int32_t* __restrict__ bins, FeatState* __restrict__ st) {
@@ -792,8 +822,26 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
 
     auto scan_csr = [&](bool accum) {
         if (n == 0) return;
-        const int g = grid_for(ceil_div(n, 32) * 256 / 8, 256, 8);
         const CsrPart& c = m.csr;
+        // entry-parallel for small matrices and for skewed ones up to 2M rows
+        // (rows longer than the SpMV group cap: power-law corpus matrices
+        // 126 -> 43 us, 302 -> 239 us); the row-lockstep sweep for the rest
+        // (banded/stencil keys repeat across rows and its slot cache wins;
+        // config 3's 4M-row R-MAT: 0.87 vs 0.93 ms entry-parallel)
+        const bool entry = ceil_div(n, 32) < int64_t(current_ctx().num_sms) * 16 || (c.nlong > 0 && n < (1 << 21));
+        if (entry && c.nblk > 0) {
+            const int gb = grid_for(c.nblk * kB, kB, 4);
+            if (accum) {
+                FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+                feat_csr_entries<true><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op);
+            } else {
+                FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+                feat_csr_entries<false><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op);
+            }
+            SOB_LAUNCH("feat_csr_entries");
+            return;
+        }
+        const int g = grid_for(ceil_div(n, 32) * 256 / 8, 256, 8);
         // long rows (SpMV pieces) are swept piece-parallel instead of by one warp
         const int64_t skip = c.nlong > 0 ? int64_t(c.grp_cap) : INT64_MAX;
         unsigned* ticket = c.nlong > 0 ? &st->ticket : nullptr;  // skewed rows: dynamic groups
