@@ -95,7 +95,13 @@ refaccept: $(LIBDIR)/libsparseoracle.so
 # transfer pipeline stages).  Both link the product library.
 TOOL_FLAGS := -O3 $(ARCH) -std=c++17 -lineinfo -Iinclude -L$(LIBDIR) -lsparseoracle_b200 \
               -Xlinker -rpath,'$$ORIGIN/../$(LIBDIR)'
-tools: build/lab build/pipe_probe
+tools: build/lab build/pipe_probe build/e2e_api
+
+# the drop-in C++ API end to end (bench.py's e2e_cpp_api): pageable vectors
+build/e2e_api: scripts/e2e_api.cpp $(LIBDIR)/libsparseoracle.so $(CPP_HDRS)
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Iinclude $< -o $@ -L$(LIBDIR) -lsparseoracle -lsparseoracle_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
 
 build/lab: scripts/spmv_lab.cu $(LIBDIR)/libsparseoracle_b200.so include/sparseoracle_b200.h
 	@mkdir -p build

@@ -121,6 +121,7 @@ const char* so_version(void);
 /* Number of kernels this library has launched in the process (monotone). */
 int64_t so_kernel_launches(void);
 so_status so_set_device(int device);          /* device for new objects */
+so_status so_get_device(int* device);         /* the calling thread's current device */
 so_status so_device_sync(void);
 /* Opaque cudaStream_t used by every host-facing call on the current device. */
 void* so_default_stream(void);
@@ -266,9 +267,16 @@ so_status so_forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_of
 void so_forest_free(so_forest* f);
 /* predict on a host feature vector (one device launch). */
 so_status so_predict(const so_forest* f, const so_feature_vector* x, int32_t* out);
-/* Batched predict: rows is [n][10] in features_to_row order. */
+/* Batched predict: rows is [n][10] in features_to_row order (throughput
+ * path: one thread per (row, tree) over the flat node layout). */
 so_status so_predict_rows(const so_forest* f, int64_t n, const double* rows,
                           int32_t* out);
+/* The same prediction through the single-row latency path of so_tune_ml
+ * (blocked layout, warp-cooperative walk, one CTA per row); a kind-0 (tree)
+ * model evaluates its first tree only (tuners.cpp:103-105).  so_predict
+ * uses it. */
+so_status so_predict_rows_latency(const so_forest* f, int64_t n, const double* rows,
+                                  int32_t* out);
 
 /* ---- tuner  (tuners.hpp:57-63, tuners.cpp:92-114) ------------------------- */
 /* tune_ml: features -> predict -> feasibility/CSR fallback fully on the device;

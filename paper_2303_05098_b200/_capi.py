@@ -86,6 +86,7 @@ _SIGS = {
     "so_last_error": (C.c_char_p, []),
     "so_version": (C.c_char_p, []),
     "so_kernel_launches": (C.c_int64, []),
+    "so_get_device": (C.c_int, [P(C.c_int)]),
     "so_set_device": (C.c_int, [C.c_int]),
     "so_device_sync": (C.c_int, []),
     "so_default_stream": (vp, []),
@@ -124,6 +125,7 @@ _SIGS = {
     "so_forest_free": (None, [vp]),
     "so_predict": (C.c_int, [vp, P(FeatureVector), P(i32)]),
     "so_predict_rows": (C.c_int, [vp, i64, vp, vp]),
+    "so_predict_rows_latency": (C.c_int, [vp, i64, vp, vp]),
     "so_tune_ml": (C.c_int, [vp, vp, f64, P(ConversionConfig), P(TuneOutcome)]),
 }
 

@@ -21,6 +21,7 @@ so_forest* forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_off,
                          const double* threshold, const int32_t* left, const int32_t* right, const int32_t* cls,
                          cudaStream_t s);
 void predict_rows(const so_forest& f, const double* rows_dev, int64_t n, int32_t* out_dev, cudaStream_t s);
+void predict_rows_blocked(const so_forest& f, const double* rows_dev, int64_t n, int32_t* out_dev, cudaStream_t s);
 void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,
                           so_tune_outcome* out_dev, cudaStream_t s);
 
@@ -30,6 +31,11 @@ struct TunePlan {
     FeatState* st = nullptr;
     so_tune_outcome* out = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    cudaEvent_t ready = nullptr;  // orders the replay after the caller's work on the context stream
+    // private stream the graph is captured and replayed on: a capture on the
+    // shared context stream would swallow other threads' work (and the
+    // replay would re-run it); nothing but this plan ever uses it
+    cudaStream_t ps = nullptr;
     cudaGraphExec_t exec = nullptr;
     std::unique_ptr<FeatWorkspace> ws;
     bool matches(uint64_t uid, const so_conversion_config& c) const {
@@ -46,7 +52,9 @@ void destroy_tune_plan(TunePlan* p) {
     if (p->e0) cudaEventDestroy(p->e0);
     if (p->e1) cudaEventDestroy(p->e1);
     if (p->e2) cudaEventDestroy(p->e2);
+    if (p->ready) cudaEventDestroy(p->ready);
     p->ws.reset();
+    if (p->ps) cudaStreamDestroy(p->ps);
     delete p;
 }
 
@@ -318,6 +326,25 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace sob {
 namespace {
 
+// events owned by a scope (or a thread): destroyed on every exit path
+struct EventSet {
+    std::vector<cudaEvent_t> ev;
+    unsigned flags;
+    EventSet(size_t n, unsigned f) : flags(f) { grow(n); }
+    void grow(size_t n) {
+        while (ev.size() < n) {
+            cudaEvent_t e;
+            SOB_CUDA(cudaEventCreateWithFlags(&e, flags));
+            ev.push_back(e);
+        }
+    }
+    ~EventSet() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+    EventSet(const EventSet&) = delete;
+    EventSet& operator=(const EventSet&) = delete;
+};
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -346,6 +373,20 @@ const void* mapped_ptr(const void* p) {
 // are identical to the one-shot path (same kernel per row).
 constexpr int64_t kPipeRows = 1 << 18;
 
+}  // namespace
+
+void ensure_dia_window(const so_matrix& m, cudaStream_t s) {
+    if (m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0) return;
+    std::vector<int64_t> off(size_t(m.dia.ndiags));
+    d2h(off.data(), m.dia.offsets, m.dia.ndiags, s);
+    SOB_CUDA(cudaStreamSynchronize(s));
+    m.dia_omin.store(*std::min_element(off.begin(), off.end()), std::memory_order_relaxed);
+    m.dia_omax.store(*std::max_element(off.begin(), off.end()), std::memory_order_relaxed);
+    m.dia_window_known.store(true, std::memory_order_release);
+}
+
+namespace {
+
 bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
     const bool dia_only = m.format == SO_DIA || (m.format == SO_HDC && m.csr.nnz == 0);
     if (!dia_only || m.dia.ndiags == 0 || m.nrows < 2 * kPipeRows) return false;
@@ -354,14 +395,7 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
     const auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
     if (xa < ya + sizeof(double) * size_t(m.nrows) && ya < xa + sizeof(double) * size_t(m.ncols)) return false;
     if (!is_pinned(x) || !is_pinned(y)) return false;
-    if (!m.dia_window_known.load(std::memory_order_acquire)) {
-        std::vector<int64_t> off(size_t(m.dia.ndiags));
-        d2h(off.data(), m.dia.offsets, m.dia.ndiags, s);
-        SOB_CUDA(cudaStreamSynchronize(s));
-        m.dia_omin.store(*std::min_element(off.begin(), off.end()), std::memory_order_relaxed);
-        m.dia_omax.store(*std::max_element(off.begin(), off.end()), std::memory_order_relaxed);
-        m.dia_window_known.store(true, std::memory_order_release);
-    }
+    ensure_dia_window(m, s);
     // narrow windows: one kernel over the host link, no copy engine
     static const bool zc_off = std::getenv("SOB_NO_ZERO_COPY") != nullptr;  // diagnostic knob
     if (!zc_off) {
@@ -378,12 +412,9 @@ bool spmv_pipelined(const so_matrix& m, const double* x, double* y, cudaStream_t
     const int64_t nchunks = std::min<int64_t>(max_chunks, ceil_div(n, kPipeRows));
     const int64_t rows_per = ceil_div(n, nchunks);
     DBuf<double> dx(nc, s), dy(n, s);
-    thread_local std::vector<cudaEvent_t> ev;
-    while (ev.size() < size_t(2 * nchunks + 1)) {
-        cudaEvent_t e;
-        SOB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        ev.push_back(e);
-    }
+    thread_local EventSet pool(0, cudaEventDisableTiming);
+    pool.grow(size_t(2 * nchunks + 1));
+    std::vector<cudaEvent_t>& ev = pool.ev;
     // buffers come from the compute stream's pool: the copy streams wait on it
     SOB_CUDA(cudaEventRecord(ev[0], s));
     SOB_CUDA(cudaStreamWaitEvent(c.copy_in, ev[0], 0));
@@ -437,6 +468,13 @@ so_status so_set_device(int device) {
         SOB_CUDA(cudaSetDevice(device));
         g_dev = device;
         ctx(device);
+    });
+}
+
+so_status so_get_device(int* device) {
+    return guard([&] {
+        if (!device) fail(SO_INVALID_INPUT, "null out pointer");
+        *device = current_ctx().device;
     });
 }
 
@@ -817,6 +855,9 @@ so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) 
             SOB_CUDA(cudaStreamSynchronize(s));
             return;
         }
+        // pageable buffers (the reference API's std::vector): staged through
+        // pinned memory by host threads, overlapped with the device work
+        if (m->nrows > 0 && spmv_pageable(*m, x, y, s)) return;
         DBuf<double> dx, dy(m->nrows, s);
         h2d(dx, x, xlen, s);
         spmv_device(*m, dx.get(), dy.get(), s);
@@ -834,8 +875,8 @@ so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen, int64_
         DBuf<double> dx, dy(m->nrows, s);
         h2d(dx, x, xlen, s);
         spmv_device(*m, dx.get(), dy.get(), s);  // warm-up, untimed (spmv.cpp:231)
-        std::vector<cudaEvent_t> ev(size_t(reps) + 1);
-        for (auto& e : ev) SOB_CUDA(cudaEventCreate(&e));
+        EventSet evs(size_t(reps) + 1, 0);
+        std::vector<cudaEvent_t>& ev = evs.ev;
         SOB_CUDA(cudaEventRecord(ev[0], s));
         for (int64_t r = 0; r < reps; ++r) {
             spmv_device(*m, dx.get(), dy.get(), s);
@@ -849,7 +890,6 @@ so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen, int64_
             per_rep[r] = double(ms) * 1e-3;
             sum += per_rep[r];
         }
-        for (auto& e : ev) cudaEventDestroy(e);
         *total = sum;
     });
 }
@@ -927,26 +967,48 @@ so_status so_forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_of
 
 void so_forest_free(so_forest* f) { delete f; }
 
-so_status so_predict_rows(const so_forest* f, int64_t n, const double* rows, int32_t* out) {
+namespace sob {
+namespace {
+so_status predict_host_rows(const so_forest* f, int64_t n, const double* rows, int32_t* out, bool blocked) {
     return guard([&] {
         if (!f) fail(SO_INVALID_INPUT, "null forest");
+        if (n < 0 || (n > 0 && (!rows || !out))) fail(SO_INVALID_INPUT, "bad rows");
         SOB_CUDA(cudaSetDevice(f->device));
+        g_dev = f->device;
         cudaStream_t s = ctx(f->device).stream;
         DBuf<double> dr;
         h2d(dr, rows, n * 10, s);
         DBuf<int32_t> dout(n, s);
-        predict_rows(*f, dr.get(), n, dout.get(), s);
+        if (blocked)
+            predict_rows_blocked(*f, dr.get(), n, dout.get(), s);
+        else
+            predict_rows(*f, dr.get(), n, dout.get(), s);
         d2h(out, dout, n, s);
         SOB_CUDA(cudaStreamSynchronize(s));
     });
 }
+}  // namespace
+}  // namespace sob
+
+so_status so_predict_rows(const so_forest* f, int64_t n, const double* rows, int32_t* out) {
+    return predict_host_rows(f, n, rows, out, false);
+}
+
+so_status so_predict_rows_latency(const so_forest* f, int64_t n, const double* rows, int32_t* out) {
+    return predict_host_rows(f, n, rows, out, true);
+}
 
 so_status so_predict(const so_forest* f, const so_feature_vector* x, int32_t* out) {
+    if (!x) {
+        set_error("null feature vector");
+        return SO_INVALID_INPUT;
+    }
     double row[10] = {double(x->nrows),          double(x->ncols),          double(x->nnz),
                       x->avg_nnz_per_row,        x->density,                double(x->max_nnz_per_row),
                       double(x->min_nnz_per_row), x->nnz_row_spread,        double(x->ndiags),
                       double(x->ntrue_diags)};
-    return so_predict_rows(f, 1, row, out);
+    // one row: the blocked warp walk of the fused tuner (latency path)
+    return so_predict_rows_latency(f, 1, row, out);
 }
 
 // tune_ml with the feature pipeline (about ten kernels + stream-ordered
@@ -963,49 +1025,56 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
         check_ratio(*m, ratio);
         so_conversion_config cfg = cfg_or_default(cfgp);
         cfg.true_diag_ratio = ratio;  // TunerConfig::effective_conversion (tuners.hpp:21-25)
-        // the cached plan (graph, workspace, events) belongs to the matrix:
-        // concurrent tune_ml calls on one const matrix take turns
-        static std::mutex plan_mu;
-        std::lock_guard<std::mutex> plan_lock(plan_mu);
+        // the cached plan (graph, workspace, events, stream) belongs to the
+        // matrix: concurrent tune_ml calls on one const matrix take turns,
+        // different matrices tune concurrently
+        std::lock_guard<std::mutex> plan_lock(m->tune_mu);
         TunePlan* plan = m->tune_plan.get();
         if (!plan || !plan->matches(f->uid, cfg)) {
             m->tune_plan.reset();
             std::unique_ptr<TunePlan, TunePlanDeleter> np(new TunePlan());
             np->forest_uid = f->uid;
             np->cfg = cfg;
+            SOB_CUDA(cudaStreamCreateWithFlags(&np->ps, cudaStreamNonBlocking));
             SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np->st), sizeof(FeatState), s));
             SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np->out), sizeof(so_tune_outcome), s));
             SOB_CUDA(cudaEventCreate(&np->e0));
             SOB_CUDA(cudaEventCreate(&np->e1));
             SOB_CUDA(cudaEventCreate(&np->e2));
+            SOB_CUDA(cudaEventCreateWithFlags(&np->ready, cudaEventDisableTiming));
             np->ws.reset(new FeatWorkspace(*m, s));
             SOB_CUDA(cudaStreamSynchronize(s));
+            cudaStream_t ps = np->ps;
             cudaGraph_t g = nullptr;
             // one graph: features, predict + feasibility, with event-record
             // nodes around each so T_FE / T_PRED are device intervals of the
             // graph itself (no host submission gap inside them)
-            SOB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            SOB_CUDA(cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal));
             try {
-                SOB_CUDA(cudaEventRecordWithFlags(np->e0, s, cudaEventRecordExternal));
-                enqueue_features(*m, ratio, np->st, s, np->ws.get());
-                SOB_CUDA(cudaEventRecordWithFlags(np->e1, s, cudaEventRecordExternal));
-                enqueue_tune_predict(*f, np->st, cfg, m->format, np->out, s);
-                SOB_CUDA(cudaEventRecordWithFlags(np->e2, s, cudaEventRecordExternal));
+                SOB_CUDA(cudaEventRecordWithFlags(np->e0, ps, cudaEventRecordExternal));
+                enqueue_features(*m, ratio, np->st, ps, np->ws.get());
+                SOB_CUDA(cudaEventRecordWithFlags(np->e1, ps, cudaEventRecordExternal));
+                enqueue_tune_predict(*f, np->st, cfg, m->format, np->out, ps);
+                SOB_CUDA(cudaEventRecordWithFlags(np->e2, ps, cudaEventRecordExternal));
             } catch (...) {
-                cudaStreamEndCapture(s, &g);
+                cudaStreamEndCapture(ps, &g);
                 if (g) cudaGraphDestroy(g);
                 throw;
             }
-            SOB_CUDA(cudaStreamEndCapture(s, &g));
+            SOB_CUDA(cudaStreamEndCapture(ps, &g));
             SOB_CUDA(cudaGraphInstantiate(&np->exec, g, 0));
             cudaGraphDestroy(g);
             plan = np.get();
             m->tune_plan = std::move(np);
         }
-        SOB_CUDA(cudaGraphLaunch(plan->exec, s));
+        // after everything the caller queued on the context stream (the
+        // matrix may still be in flight from a conversion)
+        SOB_CUDA(cudaEventRecord(plan->ready, s));
+        SOB_CUDA(cudaStreamWaitEvent(plan->ps, plan->ready, 0));
+        SOB_CUDA(cudaGraphLaunch(plan->exec, plan->ps));
         so_tune_outcome h;
-        SOB_CUDA(cudaMemcpyAsync(&h, plan->out, sizeof(h), cudaMemcpyDeviceToHost, s));
-        SOB_CUDA(cudaStreamSynchronize(s));
+        SOB_CUDA(cudaMemcpyAsync(&h, plan->out, sizeof(h), cudaMemcpyDeviceToHost, plan->ps));
+        SOB_CUDA(cudaStreamSynchronize(plan->ps));
         float fe = 0.f, pr = 0.f;
         SOB_CUDA(cudaEventElapsedTime(&fe, plan->e0, plan->e1));
         SOB_CUDA(cudaEventElapsedTime(&pr, plan->e1, plan->e2));

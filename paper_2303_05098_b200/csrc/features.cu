@@ -107,11 +107,14 @@ struct FeatCsrOp {
 // hash.  The row-lockstep sweep gives such a matrix one warp per 32 rows, each
 // a serial chain over its rows' entries (config-4 id 1762: 41 us for 359 K
 // entries); here every thread of every block has independent work.  Covers
-// long rows too (no piece sweep).
+// long rows too, except rows longer than big_row (a block holding one such row
+// would be one CTA's serial walk -- an arrow matrix's dense row is ~4K steps):
+// their entries are left to piece_sweep, ~2K entries per CTA.
+constexpr int64_t kBigRowPieces = 8;  // rows of more than 8 SpMV pieces (16 K entries)
 template <bool ACCUM_RC>
 __global__ void __launch_bounds__(kB)
     feat_csr_entries(const int32_t* __restrict__ blk, int64_t nblk, const int64_t* __restrict__ rp,
-                     FeatCsrOp<ACCUM_RC> op) {
+                     FeatCsrOp<ACCUM_RC> op, int64_t big_row) {
     __shared__ int64_t srp[kRowsPerBlock + 1];
     op.begin();
     for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
@@ -120,6 +123,8 @@ __global__ void __launch_bounds__(kB)
         for (int j = threadIdx.x; j <= nr; j += kB) srp[j] = rp[r0 + j];
         __syncthreads();
         for (int j = threadIdx.x; j < nr; j += kB) op.row(r0 + j, true, srp[j + 1] - srp[j]);
+        // a row longer than kWindow stands alone in its block
+        if (nr == 1 && srp[1] - srp[0] > big_row) continue;
         const int64_t k0 = srp[0], k1 = srp[nr];
         for (int64_t base = k0; base < k1; base += kB) {
             const int64_t k = base + threadIdx.x;
@@ -831,14 +836,24 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         const bool entry = ceil_div(n, 32) < int64_t(current_ctx().num_sms) * 16 || (c.nlong > 0 && n < (1 << 21));
         if (entry && c.nblk > 0) {
             const int gb = grid_for(c.nblk * kB, kB, 4);
+            // a row of more than kBigRowPieces pieces exists only if the pieces
+            // outnumber the long rows by at least that much
+            const bool big = c.nlong > 0 && c.npieces - c.nlong >= kBigRowPieces;
+            const int64_t big_row = big ? kBigRowPieces * kPiece : INT64_MAX;
             if (accum) {
                 FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-                feat_csr_entries<true><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op);
+                feat_csr_entries<true><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
             } else {
                 FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-                feat_csr_entries<false><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op);
+                feat_csr_entries<false><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
             }
             SOB_LAUNCH("feat_csr_entries");
+            if (big) {
+                FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+                piece_sweep<FeatCsrOp<false>><<<unsigned(c.npieces), 256, 0, s>>>(
+                    c.piece_k.get(), c.long_row.get(), c.long_piece.get(), c.nlong, op, kBigRowPieces);
+                SOB_LAUNCH("feat_csr_pieces");
+            }
             return;
         }
         const int g = grid_for(ceil_div(n, 32) * 256 / 8, 256, 8);

@@ -335,10 +335,11 @@ __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict_
 
 // One CTA per long-row piece (CsrPart::piece_k): coalesced entries of a
 // single row, so no row search.  Same op interface (row() is not called).
+// Pieces of rows with at most min_pieces pieces exit at once.
 template <class Op>
 __global__ void __launch_bounds__(256) piece_sweep(const int64_t* __restrict__ pk, const int32_t* __restrict__ lrow,
-                                                   const int64_t* __restrict__ lpiece, int64_t nlong, Op op) {
-    op.begin();
+                                                   const int64_t* __restrict__ lpiece, int64_t nlong, Op op,
+                                                   int64_t min_pieces = 0) {
     const int64_t k0 = pk[2 * blockIdx.x], k1 = pk[2 * blockIdx.x + 1];
     // row of this piece: the long row whose piece range holds blockIdx.x
     int64_t lo = 0, hi = nlong;
@@ -349,6 +350,9 @@ __global__ void __launch_bounds__(256) piece_sweep(const int64_t* __restrict__ p
         else
             hi = mid;
     }
+    // rows of at most min_pieces pieces were swept by the caller's other kernel
+    if (lpiece[lo + 1] - lpiece[lo] <= min_pieces) return;
+    op.begin();
     const int r = lrow[lo];
     for (int64_t b = k0; b < k1; b += blockDim.x) {
         if constexpr (piece_direct<Op>::value)

@@ -4,6 +4,7 @@
 #include <atomic>
 
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -84,6 +85,7 @@ struct TunePlanDeleter {
 
 struct so_matrix {
     mutable std::unique_ptr<sob::TunePlan, sob::TunePlanDeleter> tune_plan;
+    mutable std::mutex tune_mu;  // guards tune_plan (one tune_ml at a time per matrix)
     int device = 0;
     int32_t format = SO_COO;
     int64_t nrows = 0, ncols = 0;
@@ -137,7 +139,16 @@ void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo
 // DIA-window matrix with x/y in mapped pinned host memory (device-visible
 // pointers): one kernel reads x and writes y over the host link; false when
 // the window is too wide or unknown (spmv.cu)
-bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s);
+// (row blocks [blk_lo, blk_hi) of zero_copy_rows_per_block() rows; -1 = all)
+bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s,
+                        int64_t blk_lo = 0, int64_t blk_hi = -1);
+int64_t zero_copy_rows_per_block();
+// min/max DIA offset of a DIA-window matrix (read once, cached on the matrix)
+void ensure_dia_window(const so_matrix& m, cudaStream_t s);
+// spmv(m, x) with PAGEABLE host x/y (stage.cu): host threads copy through a
+// cached pinned staging ring while the device multiplies chunk by chunk;
+// false when the call is too small to gain (the caller's one-shot path)
+bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t s);
 void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, double* remote,
                     unsigned* ticket, unsigned long long* remote_flag, unsigned long long flag_value,
                     cudaStream_t s);

@@ -146,6 +146,21 @@ __device__ int predict_block_warps(const ForestView& f, const double* row, int t
     return best;
 }
 
+// The single-row latency path (tune_predict_kernel's blocked warp walk) over
+// n host-given rows, one CTA of kTB threads per row: so_predict and the
+// parity tests of the fused tuner's predict step run exactly this code.
+__global__ void __launch_bounds__(kTB) predict_rows_blocked_kernel(ForestView f, const double* __restrict__ rows,
+                                                                   int64_t n, int32_t* __restrict__ out) {
+    __shared__ double row[10];
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        if (threadIdx.x < 10) row[threadIdx.x] = rows[r * 10 + threadIdx.x];
+        __syncthreads();
+        const int best = predict_block_warps(f, row, f.kind == 0 ? 1 : f.n_trees);
+        if (threadIdx.x == 0) out[r] = best;
+        __syncthreads();
+    }
+}
+
 struct CapCfg {
     int64_t kh_override;
     double max_padding_factor;
@@ -332,6 +347,12 @@ void predict_rows(const so_forest& f, const double* rows_dev, int64_t n, int32_t
     if (n <= 0) return;
     predict_rows_kernel<<<grid_for(n * kPB, kPB, 8), kPB, 0, s>>>(view(f), rows_dev, n, out_dev);
     SOB_LAUNCH("predict_rows_kernel");
+}
+
+void predict_rows_blocked(const so_forest& f, const double* rows_dev, int64_t n, int32_t* out_dev, cudaStream_t s) {
+    if (n <= 0) return;
+    predict_rows_blocked_kernel<<<grid_for(n * kTB, kTB, 2), kTB, 0, s>>>(view(f), rows_dev, n, out_dev);
+    SOB_LAUNCH("predict_rows_blocked_kernel");
 }
 
 void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,

@@ -272,11 +272,12 @@ constexpr int64_t kZcSpan = kZcRows / 4;
 template <bool ALIGN16>
 __global__ void __launch_bounds__(kZcRows, 1)
     dia_zc_kernel(int nrows, int ncols, int ndiags, const int64_t* __restrict__ offsets,
-                  const double* __restrict__ vals, const double* x_host, double* y_host, int omin, int omax) {
+                  const double* __restrict__ vals, const double* x_host, double* y_host, int omin, int omax,
+                  int blk0) {
     extern __shared__ double xs[];
     __shared__ int soff[kDiaSmem];
     stage_offsets(soff, offsets, ndiags);
-    const int i0 = blockIdx.x * kZcRows;
+    const int i0 = (blk0 + int(blockIdx.x)) * kZcRows;
     int w0 = max(0, i0 + omin);
     if (ALIGN16) w0 &= ~1;
     const int w1 = min(ncols, i0 + kZcRows - 1 + omax + 1);
@@ -784,22 +785,28 @@ void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s) 
 
 }  // namespace
 
-bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s) {
+int64_t zero_copy_rows_per_block() { return kZcRows; }
+
+bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s,
+                        int64_t blk_lo, int64_t blk_hi) {
     if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
     if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
         return false;
     const int64_t omin = m.dia_omin, omax = m.dia_omax;
     if (omax - omin > kZcSpan) return false;
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
-    const unsigned grid = unsigned(ceil_div(m.nrows, int64_t(kZcRows)));
+    const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
+    if (blk_hi < 0 || blk_hi > nblk) blk_hi = nblk;
+    if (blk_lo >= blk_hi) return true;
+    const unsigned grid = unsigned(blk_hi - blk_lo);
     if ((reinterpret_cast<uintptr_t>(x_mapped) & 15) == 0)
         dia_zc_kernel<true><<<grid, kZcRows, smem, s>>>(int(m.nrows), int(m.ncols), int(m.dia.ndiags),
                                                          m.dia.offsets.get(), m.dia.values.get(), x_mapped, y_mapped,
-                                                         int(omin), int(omax));
+                                                         int(omin), int(omax), int(blk_lo));
     else
         dia_zc_kernel<false><<<grid, kZcRows, smem, s>>>(int(m.nrows), int(m.ncols), int(m.dia.ndiags),
                                                           m.dia.offsets.get(), m.dia.values.get(), x_mapped,
-                                                          y_mapped, int(omin), int(omax));
+                                                          y_mapped, int(omin), int(omax), int(blk_lo));
     SOB_LAUNCH("dia_zc_kernel");
     return true;
 }

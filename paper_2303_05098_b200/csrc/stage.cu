@@ -1,0 +1,285 @@
+// spmv(m, x) with pageable host buffers -- the reference API's own call
+// (spmv.hpp:20, spmv.cpp:203-219: x is a std::vector, y comes back as a fresh
+// std::vector).  The device cannot DMA pageable memory directly; the driver's
+// pageable copies bounce through a small internal buffer one piece at a time.
+// Here host threads copy x into a cached pinned (mapped) staging buffer in
+// chunks, and the device starts on each chunk as soon as it has landed:
+//
+//   * DIA-window matrices (DIA, HDC with an empty CSR part, diagonal window
+//     <= 256): the zero-copy kernel reads x straight from the staging buffer
+//     and writes y straight into the pinned y staging buffer, row blocks
+//     launched as soon as the x prefix their window needs is staged;
+//   * every other matrix: chunk k of x goes up on the copy engine as soon as
+//     it is staged, the kernel runs on the full x, y comes back in chunks.
+//
+// In both cases the same host threads copy y out of the staging buffer chunk
+// by chunk as the device finishes it (a CUDA event per chunk), so the host
+// copies of x and y overlap the link transfers and the kernel.  Results are
+// bit-identical to the one-shot path (same kernels).
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "matrix.cuh"
+
+namespace sob {
+
+namespace {
+
+// Persistent host copy pool: workers sleep on a condition variable between
+// calls and spin (briefly) during one.
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    int size() const { return int(th_.size()); }
+    // run fn(worker) on every worker and on the caller (worker id size());
+    // returns when all are done
+    void run(const std::function<void(int)>& fn, const std::function<void()>& caller) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            pending_ = int(th_.size());
+            ++gen_;
+        }
+        cv_.notify_all();
+        caller();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+  private:
+    CopyPool() {
+        int n = int(std::thread::hardware_concurrency());
+        if (const char* e = std::getenv("SOB_HOST_THREADS")) n = std::atoi(e);  // tuning knob
+        n = std::max(1, std::min(n > 2 ? n / 2 : n, 16));
+        for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    void loop(int id) {
+        uint64_t seen = 0;
+        while (true) {
+            const std::function<void(int)>* fn;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                fn = fn_;
+            }
+            if (fn) (*fn)(id);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* fn_ = nullptr;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+};
+
+// Pinned, mapped staging buffers per device (grow-only, one pageable call at
+// a time per device).
+struct Staging {
+    std::mutex mu;
+    double* x = nullptr;
+    double* y = nullptr;
+    size_t capx = 0, capy = 0;
+    std::vector<cudaEvent_t> ev;
+    void reserve(size_t nx, size_t ny) {
+        auto grow = [](double*& p, size_t& cap, size_t want) {
+            if (cap >= want) return;
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), want * sizeof(double),
+                                   cudaHostAllocMapped | cudaHostAllocPortable));
+            cap = want;
+        };
+        grow(x, capx, std::max<size_t>(nx, 1));
+        grow(y, capy, std::max<size_t>(ny, 1));
+    }
+    void events(size_t n) {
+        while (ev.size() < n) {
+            cudaEvent_t e;
+            SOB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev.push_back(e);
+        }
+    }
+};
+Staging g_stage[64];
+
+struct Task {
+    double* dst;
+    const double* src;
+    size_t n;
+    int chunk;  // x chunk (>= 0) or -(y chunk) - 1
+};
+
+constexpr int64_t kMinStaged = int64_t(1) << 18;  // elements of x + y below which the one-shot path wins
+constexpr int64_t kTaskElems = int64_t(1) << 16;  // 512 KB per host copy task
+
+}  // namespace
+
+bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
+    static const bool off = std::getenv("SOB_NO_PAGEABLE_STAGING") != nullptr;  // diagnostic knob
+    const int64_t n = m.nrows, nc = m.ncols;
+    if (off || n + nc < kMinStaged || !x || !y) return false;
+    // in-place calls: x must be read in full before any y lands (one-shot path)
+    const auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+    if (xa < ya + sizeof(double) * size_t(n) && ya < xa + sizeof(double) * size_t(nc)) return false;
+    const int dev = m.device;
+    Staging& st = g_stage[dev];
+    std::lock_guard<std::mutex> lk(st.mu);
+    st.reserve(size_t(nc), size_t(n));
+    double* X = st.x;
+    double* Y = st.y;
+    double *Xd = nullptr, *Yd = nullptr;
+    SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&Xd), X, 0));
+    SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&Yd), Y, 0));
+
+    const bool dia_only = (m.format == SO_DIA || (m.format == SO_HDC && m.csr.nnz == 0)) && m.dia.ndiags > 0;
+    if (dia_only) ensure_dia_window(m, s);
+    const int64_t zr = zero_copy_rows_per_block();
+    // x chunks of ~1/8 of x (>= 1 MB), y chunks aligned to zero-copy blocks
+    const int64_t cx = std::max<int64_t>(int64_t(1) << 17, ceil_div(nc, 8));
+    const int64_t nxc = ceil_div(nc, cx);
+    const int64_t cy = std::max<int64_t>(ceil_div(int64_t(1) << 17, zr), ceil_div(ceil_div(n, 8), zr)) * zr;
+    const int64_t nyc = ceil_div(n, cy);
+    st.events(size_t(nyc));
+
+    // the task list: every x chunk (in order), then every y chunk
+    std::vector<Task> tasks;
+    std::vector<int> per_x(size_t(nxc), 0), per_y(size_t(nyc), 0);
+    for (int64_t k = 0; k < nxc; ++k)
+        for (int64_t a = k * cx, e = std::min(nc, a + cx); a < e; a += kTaskElems, ++per_x[size_t(k)])
+            tasks.push_back(Task{X + a, x + a, size_t(std::min(e, a + kTaskElems) - a), int(k)});
+    for (int64_t j = 0; j < nyc; ++j)
+        for (int64_t a = j * cy, e = std::min(n, a + cy); a < e; a += kTaskElems, ++per_y[size_t(j)])
+            tasks.push_back(Task{y + a, Y + a, size_t(std::min(e, a + kTaskElems) - a), -int(j) - 1});
+    std::unique_ptr<std::atomic<int>[]> xdone(new std::atomic<int>[size_t(nxc)]);
+    std::unique_ptr<std::atomic<int>[]> ygate(new std::atomic<int>[size_t(nyc)]);  // y chunk's event recorded
+    for (int64_t k = 0; k < nxc; ++k) xdone[size_t(k)].store(0);
+    for (int64_t j = 0; j < nyc; ++j) ygate[size_t(j)].store(0);
+    std::atomic<size_t> next{0};
+    std::atomic<int> failed{0};
+
+    auto worker = [&](int) {
+        cudaSetDevice(dev);
+        while (true) {
+            const size_t t = next.fetch_add(1);
+            if (t >= tasks.size() || failed.load(std::memory_order_relaxed)) return;
+            const Task& k = tasks[t];
+            if (k.chunk < 0) {
+                const int j = -k.chunk - 1;
+                while (!ygate[size_t(j)].load(std::memory_order_acquire)) {
+                    if (failed.load(std::memory_order_relaxed)) return;
+                    std::this_thread::yield();
+                }
+                while (true) {
+                    const cudaError_t q = cudaEventQuery(st.ev[size_t(j)]);
+                    if (q == cudaSuccess) break;
+                    if (q != cudaErrorNotReady) {
+                        failed.store(1);
+                        return;
+                    }
+                    std::this_thread::yield();
+                }
+            }
+            std::memcpy(k.dst, k.src, k.n * sizeof(double));
+            if (k.chunk >= 0) xdone[size_t(k.chunk)].fetch_add(1, std::memory_order_release);
+        }
+    };
+
+    std::exception_ptr err;
+    auto orchestrate = [&]() {
+        try {
+            auto wait_x = [&](int64_t k) {
+                while (xdone[size_t(k)].load(std::memory_order_acquire) < per_x[size_t(k)]) std::this_thread::yield();
+            };
+            // an empty launch range probes eligibility (window <= 256, offsets fit)
+            const bool zc = dia_only && spmv_dia_zero_copy(m, Xd, Yd, s, 0, 0);
+            if (zc) {
+                // zero-copy row blocks as their x window is staged
+                const int64_t nblk = ceil_div(n, zr);
+                const int64_t omax = m.dia_omax;
+                int64_t blk_done = 0, yrec = 0;
+                for (int64_t k = 0; k < nxc; ++k) {
+                    wait_x(k);
+                    const int64_t P = std::min(nc, (k + 1) * cx);
+                    // block b reads x up to min(nc, (b+1)*zr + omax)
+                    int64_t hi = P >= nc ? nblk : std::max<int64_t>(0, (P - omax) / zr);
+                    hi = std::min(hi, nblk);
+                    if (hi > blk_done) {
+                        spmv_dia_zero_copy(m, Xd, Yd, s, blk_done, hi);
+                        blk_done = hi;
+                        // y chunks whose rows are all launched
+                        while (yrec < nyc && std::min(n, (yrec + 1) * cy) <= std::min(n, blk_done * zr)) {
+                            SOB_CUDA(cudaEventRecord(st.ev[size_t(yrec)], s));
+                            ygate[size_t(yrec)].store(1, std::memory_order_release);
+                            ++yrec;
+                        }
+                    }
+                }
+                while (yrec < nyc) {
+                    SOB_CUDA(cudaEventRecord(st.ev[size_t(yrec)], s));
+                    ygate[size_t(yrec)].store(1, std::memory_order_release);
+                    ++yrec;
+                }
+                return;
+            }
+            // generic: x chunks up on the copy engine as staged, kernel, y down in chunks
+            DBuf<double> dx(nc, s), dy(n, s);
+            for (int64_t k = 0; k < nxc; ++k) {
+                wait_x(k);
+                const int64_t a = k * cx, e = std::min(nc, a + cx);
+                SOB_CUDA(cudaMemcpyAsync(dx.get() + a, X + a, sizeof(double) * size_t(e - a), cudaMemcpyHostToDevice, s));
+            }
+            spmv_device(m, dx.get(), dy.get(), s);
+            for (int64_t j = 0; j < nyc; ++j) {
+                const int64_t a = j * cy, e = std::min(n, a + cy);
+                SOB_CUDA(cudaMemcpyAsync(Y + a, dy.get() + a, sizeof(double) * size_t(e - a), cudaMemcpyDeviceToHost, s));
+                SOB_CUDA(cudaEventRecord(st.ev[size_t(j)], s));
+                ygate[size_t(j)].store(1, std::memory_order_release);
+            }
+        } catch (...) {
+            err = std::current_exception();
+            failed.store(1);
+        }
+    };
+    CopyPool& pool = CopyPool::get();
+    pool.run(worker, [&] {
+        orchestrate();
+        worker(pool.size());  // then help with the y copies
+    });
+    if (err) std::rethrow_exception(err);
+    if (failed.load()) {
+        cudaStreamSynchronize(s);
+        fail(SO_CUDA_ERROR, "pageable spmv: staging copy failed");
+    }
+    SOB_CUDA(cudaStreamSynchronize(s));
+    return true;
+}
+
+}  // namespace sob

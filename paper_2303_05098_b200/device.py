@@ -398,6 +398,13 @@ class DeviceForest:
         _check(A.lib().so_predict_rows(self._h, rows.shape[0], _ptr(rows), _ptr(out)))
         return out
 
+    def predict_rows_latency(self, rows) -> np.ndarray:
+        """The fused tuner's single-row path (blocked warp walk), one CTA per row."""
+        rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 10)
+        out = np.empty(rows.shape[0], dtype=np.int32)
+        _check(A.lib().so_predict_rows_latency(self._h, rows.shape[0], _ptr(rows), _ptr(out)))
+        return out
+
 
 def tune_ml(m: DeviceMatrix, forest: DeviceForest, true_diag_ratio=0.2,
             config: ConversionConfig | None = None) -> A.TuneOutcome:

@@ -1,0 +1,66 @@
+// End-to-end spmv through the drop-in C++ API exactly as a reference user
+// calls it (spmv.hpp:20, spmv.cpp:203-219): pageable std::vector x in, a
+// fresh std::vector y out, every host<->device byte inside the timed call.
+// Workload: config 2 (banded n = 4,000,000, 27 diagonals), DIA.
+//
+//   build/e2e_api [steps] [warmup]   -> one JSON line
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "sparseoracle/device.hpp"
+#include "sparseoracle/formats.hpp"
+#include "sparseoracle/spmv.hpp"
+
+using namespace sparseoracle;
+
+int main(int argc, char** argv) {
+    const int steps = argc > 1 ? std::atoi(argv[1]) : 20;
+    const int warmup = argc > 2 ? std::atoi(argv[2]) : 3;
+    const index_t n = 4'000'000, half = 13;
+    CooMatrix coo;  // generated in (row, col) order: canonical
+    coo.nrows = coo.ncols = n;
+    std::vector<index_t>& r = coo.row_idx;
+    std::vector<index_t>& c = coo.col_idx;
+    std::vector<double>& v = coo.values;
+    r.reserve(size_t(n) * 27);
+    c.reserve(size_t(n) * 27);
+    v.reserve(size_t(n) * 27);
+    uint64_t h = 2;
+    for (index_t i = 0; i < n; ++i)
+        for (index_t j = std::max<index_t>(0, i - half); j <= std::min<index_t>(n - 1, i + half); ++j) {
+            h = h * 6364136223846793005ULL + 1442695040888963407ULL;
+            r.push_back(i);
+            c.push_back(j);
+            v.push_back(0.5 + double(h >> 11) * (1.5 / 9007199254740992.0));
+        }
+    const DynamicMatrix m = from_coo(coo, FormatId::dia);
+    coo = CooMatrix{};
+    const int64_t bytes = so_spmv_bytes(m.device().get());
+    DenseVector x(static_cast<size_t>(n));
+    for (index_t i = 0; i < n; ++i) x[size_t(i)] = 1.0 + double(i % 7) / 8.0;
+    double check = 0.0;
+    for (int w = 0; w < warmup; ++w) check += spmv(m, x)[size_t(n / 2)];
+    std::vector<double> t;
+    for (int k = 0; k < steps; ++k) {
+        const auto t0 = std::chrono::steady_clock::now();
+        DenseVector y = spmv(m, x);
+        const auto t1 = std::chrono::steady_clock::now();
+        t.push_back(std::chrono::duration<double>(t1 - t0).count());
+        check += y[size_t(k % n)];
+    }
+    double mean = 0.0;
+    for (double s : t) mean += s;
+    mean /= double(t.size());
+    std::sort(t.begin(), t.end());
+    std::printf(
+        "{\"api\": \"sparseoracle::spmv(m, x) -> fresh std::vector (pageable)\", \"format\": \"DIA\", "
+        "\"nrows\": %lld, \"steps\": %d, \"ms_mean\": %.4f, \"ms_median\": %.4f, \"gbs_mean\": %.2f, "
+        "\"algorithmic_bytes\": %lld, \"h2d_bytes_per_step\": %lld, \"d2h_bytes_per_step\": %lld, "
+        "\"checksum\": %.17g}\n",
+        (long long)n, steps, mean * 1e3, t[t.size() / 2] * 1e3, double(bytes) / mean / 1e9, (long long)bytes,
+        (long long)(8 * n), (long long)(8 * n), check);
+    return 0;
+}

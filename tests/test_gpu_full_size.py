@@ -127,3 +127,38 @@ def test_config5_stencil512_sampled_rows(so, O):
         sl = so.DeviceMatrix.stencil27(g, r0, r1, w0, w1, seed=5).download()
         want = O.oc_spmv(sl, xd[w0:w1].cpu().numpy())
         assert np.array_equal(yd[r0:r1].cpu().numpy(), want), r0
+
+
+def test_config5_stencil512_features_exact(so):
+    """Config 5 features at full size (27-point stencil 512^3: 134M rows,
+    z = 3.6e9 > 2^31, the int64 count paths) against the analytic row counts
+    and the reference's SEQUENTIAL spread sum (features.cpp:137-144) replayed
+    on the host in row order: every field exact, spread bit-for-bit."""
+    g = 512
+    n = g ** 3
+    full = so.DeviceMatrix.stencil27(g, seed=5)
+    fv = full.extract_features(0.2)
+    del full
+    a = np.full(g, 3, np.int64)
+    a[0] = a[-1] = 2  # neighbours along one axis
+    nnz = int(a.sum()) ** 3
+    avg = float(nnz) / float(n)
+    # sequential sum of (c_i - avg)^2 over rows in order, chunk by chunk:
+    # np.add.accumulate is a strict left-to-right running sum
+    S = 0.0
+    ax = a.astype(np.float64)
+    for z in range(g):
+        plane = (a[z] * np.outer(a, a)).reshape(-1).astype(np.float64) - avg
+        d = plane * plane
+        acc = np.add.accumulate(np.concatenate(([S], d)))
+        S = float(acc[-1])
+    del ax
+    spread = S / float(n)
+    thr = int(np.ceil(0.2 * float(n)))
+    diag_counts = [(g - abs(dz)) * (g - abs(dy)) * (g - abs(dx))
+                   for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+    want = [float(n), float(n), float(nnz), avg, float(nnz) / (float(n) * float(n)), 27.0, 8.0, spread,
+            27.0, float(sum(c >= thr for c in diag_counts))]
+    got = fv.to_row()
+    assert got == want, (got, want)
+    assert fv.nnz == nnz and fv.nnz > 2 ** 31

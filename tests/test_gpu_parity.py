@@ -616,3 +616,72 @@ def test_host_spmv_in_place_pinned(so, O):
     want = O.oc_spmv(O.oc_convert(coo, so.DIA), buf.copy())
     m.spmv_into(buf, buf)
     assert np.array_equal(buf, want)
+
+
+@pytest.mark.parametrize("n,dense_len", [(200_000, 200_000), (60_000, 40_000)])
+def test_arrow_matrix_features(so, O, n, dense_len):
+    """A dense row far past the long-row cap (arrow matrix): its entries are
+    swept piece-parallel even where the entry-parallel sweep runs (ADVICE r1,
+    features.cu); features bit-exact, SpMV within the bar."""
+    rng = np.random.default_rng(n)
+    diag = np.arange(n)
+    dense_cols = np.sort(rng.choice(n, dense_len, replace=False))
+    rows = np.concatenate([diag, np.full(dense_len, 7), dense_cols])
+    cols = np.concatenate([diag, dense_cols, np.full(dense_len, 3)])
+    coo = O.from_triplets(n, n, rows, cols, rng.uniform(0.5, 2.0, rows.size))
+    d = to_dev(so, coo)
+    want, _ = O.oc_features(O.oc_convert(coo, O.CSR), 0.2)
+    x = rng.uniform(-1, 1, n)
+    for f in (0, 1, 4, 5):
+        m = d.from_coo(f)
+        assert np.array_equal(np.array(m.extract_features(0.2).to_row()), want), f
+        ref = O.oc_convert(coo, f)
+        assert max_rel(m.spmv(x), O.oc_spmv(ref, x)) <= SPMV_TOL, f
+
+
+@pytest.mark.parametrize("shape", ["band13", "wide", "rmat"])
+def test_pageable_host_spmv_staging(so, O, shape):
+    """spmv(m, x) with PAGEABLE host buffers (the reference API's
+    std::vector): host threads stage x/y through pinned memory chunk by chunk
+    while the device multiplies (stage.cu) -- zero-copy row blocks for narrow
+    DIA windows, copy-engine chunks for every other format.  Bit-identical to
+    the device-resident multiply and within the bar of the oracle; 8-byte
+    (not 16-byte) aligned x, y inside a larger array, in-place fallback."""
+    import torch
+    from paper_2303_05098_b200 import synth
+
+    if shape == "band13":
+        csr = synth.banded(700_000, 13, seed=2)
+    elif shape == "wide":
+        csr = synth.laplacian_2d(800, seed=1)  # offsets +-800: window wider than the zero-copy limit
+    else:
+        csr = synth.rmat(18, 8, seed=9)
+    coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
+    d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+    rng = np.random.default_rng(12)
+    for f in range(6):
+        try:
+            m = d.convert(f)
+        except so.PaddingOverflow:
+            continue
+        big = rng.uniform(-1, 1, csr.ncols + 3)
+        x = big[1:1 + csr.ncols]  # 8-byte aligned only
+        yb = np.full(csr.nrows + 2, np.nan)
+        y = yb[1:1 + csr.nrows]
+        m.spmv_into(x, y)
+        xd = torch.tensor(x, device="cuda")
+        yd = torch.empty(csr.nrows, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        m.spmv_device(xd.data_ptr(), yd.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(y, yd.cpu().numpy()), f
+        assert np.isnan(yb[0]) and np.isnan(yb[-1]), f  # nothing written outside y
+        assert max_rel(y, O.oc_spmv(O.oc_convert(coo, f), x)) <= SPMV_TOL, f
+        for _ in range(2):  # repeated calls reuse the cached staging buffers
+            assert np.array_equal(m.spmv(x), y), f
+    if csr.nrows == csr.ncols:  # in place (y aliases x): the one-shot path
+        m = d.convert(so.CSR)
+        z = rng.uniform(-1, 1, csr.ncols)
+        want = m.spmv(z)
+        m.spmv_into(z, z)
+        assert np.array_equal(z, want)
