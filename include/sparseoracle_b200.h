@@ -110,6 +110,8 @@ typedef struct so_tune_outcome {
     double feature_time_seconds; /* T_FE  (device time, cudaEvent)     */
     double predict_time_seconds; /* T_PRED (device time, cudaEvent)    */
     so_feature_vector features;  /* what the model saw                 */
+    double wall_time_seconds;    /* host wall clock of the whole call
+                                    (graph launch -> outcome on the host) */
 } so_tune_outcome;
 
 typedef struct so_matrix so_matrix; /* opaque, device-resident */
@@ -294,6 +296,41 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double true_diag_ra
 so_status so_gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi,
                                int64_t col_lo, int64_t col_hi, uint64_t seed,
                                so_matrix** out);
+
+/* ---- row-partitioned iterated SpMV across GPUs (config 5) ---
+ * Replaces the reference's row-block partition of one multiply over
+ * std::threads (spmv.cpp:142-189) with a row partition over ranks, one
+ * process (or thread) per GPU; x <- A x iterated with the x exchange done by
+ * the library's own kernels over NVLink peer memory (no collective).
+ * Rank q owns global rows [row_starts[q], row_starts[q+1]).
+ *   SO_DIST_HALO: `local` is the DIA-window block (rows owned) x (columns of
+ *     the window [r0-halo, r1+halo) clipped to [0, n)); only halo rows move,
+ *     pushed into the neighbours' windows by the boundary multiply itself.
+ *   SO_DIST_ALLGATHER: `local` is (rows owned) x (all n columns), any format;
+ *     every rank's new rows are stored into every peer's x (all-gather fused
+ *     into the iteration's epilogue).
+ * Setup: so_dist_create -> so_dist_handle (exchange the handles with any
+ * transport, e.g. MPI_Allgather / torch all_gather_object) -> so_dist_connect
+ * -> write the initial x into so_dist_x(d, 0) (the whole window / vector) ->
+ * so_dist_iterate.  `local` must outlive the so_dist.  The P-rank iterate is
+ * bitwise equal to the 1-rank iterate (row summation orders unchanged). */
+enum { SO_DIST_HALO = 0, SO_DIST_ALLGATHER = 1 };
+typedef struct so_dist so_dist;
+so_status so_dist_create(const so_matrix* local, int32_t kind, int32_t rank, int32_t world,
+                         const int64_t* row_starts, int64_t halo, so_dist** out);
+/* this rank's shared block (both x buffers + flags), one CUDA IPC handle */
+so_status so_dist_handle(const so_dist* d, so_ipc_handle* out);
+/* handles[q] for every rank q (own entry ignored; HALO maps only neighbours) */
+so_status so_dist_connect(so_dist* d, const so_ipc_handle* handles);
+/* x buffer `which` (0/1; -1 = the one holding the latest iterate): device
+ * pointer, global index of its first element, length */
+so_status so_dist_x(const so_dist* d, int32_t which, double** x_dev, int64_t* offset,
+                    int64_t* len);
+/* enqueue `iters` iterations on `stream` (null: the library stream) */
+so_status so_dist_iterate(so_dist* d, int64_t iters, void* stream);
+/* peer waits that gave up after 60 s (a dead rank): nonzero = invalid iterate */
+int64_t so_dist_timeouts(void);
+void so_dist_free(so_dist* d);
 
 #ifdef __cplusplus
 }

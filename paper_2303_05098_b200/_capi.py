@@ -78,7 +78,7 @@ class HostArrays(C.Structure):
 class TuneOutcome(C.Structure):
     _fields_ = [("chosen", i32), ("source", i32), ("switched", i32), ("fallback_csr", i32),
                 ("feature_time_seconds", f64), ("predict_time_seconds", f64),
-                ("features", FeatureVector)]
+                ("features", FeatureVector), ("wall_time_seconds", f64)]
 
 
 # function name -> (restype, argtypes)
@@ -127,6 +127,13 @@ _SIGS = {
     "so_predict_rows": (C.c_int, [vp, i64, vp, vp]),
     "so_predict_rows_latency": (C.c_int, [vp, i64, vp, vp]),
     "so_tune_ml": (C.c_int, [vp, vp, f64, P(ConversionConfig), P(TuneOutcome)]),
+    "so_dist_create": (C.c_int, [vp, i32, i32, i32, vp, i64, P(vp)]),
+    "so_dist_handle": (C.c_int, [vp, C.c_char_p]),
+    "so_dist_connect": (C.c_int, [vp, C.c_char_p]),
+    "so_dist_x": (C.c_int, [vp, i32, P(vp), P(i64), P(i64)]),
+    "so_dist_iterate": (C.c_int, [vp, i64, vp]),
+    "so_dist_timeouts": (C.c_int64, []),
+    "so_dist_free": (None, [vp]),
 }
 
 

@@ -5,6 +5,7 @@
 // reference's host layout (int64 indices, row-major ELL) and the device
 // layout, and the per-device context.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -29,7 +30,8 @@ struct TunePlan {
     uint64_t forest_uid = 0;
     so_conversion_config cfg{};
     FeatState* st = nullptr;
-    so_tune_outcome* out = nullptr;
+    so_tune_outcome* out = nullptr;      // pinned, mapped: the predict kernel writes it over the link
+    so_tune_outcome* out_dev = nullptr;  // device view of `out`
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
     cudaEvent_t ready = nullptr;  // orders the replay after the caller's work on the context stream
     // private stream the graph is captured and replayed on: a capture on the
@@ -48,7 +50,7 @@ void destroy_tune_plan(TunePlan* p) {
     if (!p) return;
     if (p->exec) cudaGraphExecDestroy(p->exec);
     if (p->st) cudaFree(p->st);
-    if (p->out) cudaFree(p->out);
+    if (p->out) cudaFreeHost(p->out);
     if (p->e0) cudaEventDestroy(p->e0);
     if (p->e1) cudaEventDestroy(p->e1);
     if (p->e2) cudaEventDestroy(p->e2);
@@ -1018,6 +1020,7 @@ so_status so_predict(const so_forest* f, const so_feature_vector* x, int32_t* ou
 // stream.  The outcome lands in a persistent device buffer (one small D2H).
 so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const so_conversion_config* cfgp,
                      so_tune_outcome* out) {
+    const auto t_entry = std::chrono::steady_clock::now();
     return guard([&] {
         if (!f || !out) fail(SO_INVALID_INPUT, "null argument");
         cudaStream_t s = on_device(m);
@@ -1037,7 +1040,8 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             np->cfg = cfg;
             SOB_CUDA(cudaStreamCreateWithFlags(&np->ps, cudaStreamNonBlocking));
             SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np->st), sizeof(FeatState), s));
-            SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np->out), sizeof(so_tune_outcome), s));
+            SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&np->out), sizeof(so_tune_outcome), cudaHostAllocMapped));
+            SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&np->out_dev), np->out, 0));
             SOB_CUDA(cudaEventCreate(&np->e0));
             SOB_CUDA(cudaEventCreate(&np->e1));
             SOB_CUDA(cudaEventCreate(&np->e2));
@@ -1054,7 +1058,7 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
                 SOB_CUDA(cudaEventRecordWithFlags(np->e0, ps, cudaEventRecordExternal));
                 enqueue_features(*m, ratio, np->st, ps, np->ws.get());
                 SOB_CUDA(cudaEventRecordWithFlags(np->e1, ps, cudaEventRecordExternal));
-                enqueue_tune_predict(*f, np->st, cfg, m->format, np->out, ps);
+                enqueue_tune_predict(*f, np->st, cfg, m->format, np->out_dev, ps);
                 SOB_CUDA(cudaEventRecordWithFlags(np->e2, ps, cudaEventRecordExternal));
             } catch (...) {
                 cudaStreamEndCapture(ps, &g);
@@ -1072,14 +1076,14 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
         SOB_CUDA(cudaEventRecord(plan->ready, s));
         SOB_CUDA(cudaStreamWaitEvent(plan->ps, plan->ready, 0));
         SOB_CUDA(cudaGraphLaunch(plan->exec, plan->ps));
-        so_tune_outcome h;
-        SOB_CUDA(cudaMemcpyAsync(&h, plan->out, sizeof(h), cudaMemcpyDeviceToHost, plan->ps));
         SOB_CUDA(cudaStreamSynchronize(plan->ps));
+        so_tune_outcome h = *plan->out;  // written by the predict kernel (mapped host memory)
         float fe = 0.f, pr = 0.f;
         SOB_CUDA(cudaEventElapsedTime(&fe, plan->e0, plan->e1));
         SOB_CUDA(cudaEventElapsedTime(&pr, plan->e1, plan->e2));
         h.feature_time_seconds = double(fe) * 1e-3;
         h.predict_time_seconds = double(pr) * 1e-3;
+        h.wall_time_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_entry).count();
         *out = h;
     });
 }

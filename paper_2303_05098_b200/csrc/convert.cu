@@ -154,6 +154,15 @@ __global__ void row_block_scatter(const int32_t* __restrict__ flag, const int64_
     }
 }
 
+// rows of kCoopLen < length <= cap (the SpMV's warp-cooperative rows)
+__global__ void count_coop_rows(const int64_t* __restrict__ rp, int64_t n, int64_t cap,
+                                unsigned long long* __restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t len = i < n ? rp[i + 1] - rp[i] : 0;
+    const unsigned b = __ballot_sync(0xffffffffu, len > kCoopLen && len <= cap);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
+}
+
 __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_t limit, int32_t* __restrict__ flag) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) flag[i] = (rp[i + 1] - rp[i]) > limit ? 1 : 0;
@@ -688,6 +697,7 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     if (n <= 0) {
         csr.nblk = 0;
         csr.ngrp = 0;
+        csr.ncoop = 0;
         csr.nlong = 0;
         csr.npieces = 0;
         csr.blk.alloc(1, s);
@@ -721,6 +731,7 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
                                                                      csr.grp.get(), csr.grp_k.get());
     SOB_LAUNCH("row_block_scatter");
     csr.npad = 0;
+    csr.ncoop = 0;
     if (csr.ngrp > 0) {
         // the counter lives in the (free until long_row_flags) flag scratch:
         // no allocation between the matrix arrays
@@ -738,6 +749,10 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
         } else {
             csr.npad = 0;  // too few to pay for the padded kernel: plain layout everywhere
         }
+        SOB_CUDA(cudaMemsetAsync(npad, 0, sizeof(unsigned long long), s));
+        count_coop_rows<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, csr.grp_cap, npad);
+        SOB_LAUNCH("count_coop_rows");
+        csr.ncoop = int64_t(d2h_scalar(npad, s));
     }
     // long rows -> kPiece-entry pieces (SpMV splits them over many CTAs)
     long_row_flags<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(csr.row_ptr.get(), n, int64_t(csr.grp_cap),
@@ -832,6 +847,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.grp, src.csr.grp);
     cp(m->csr.grp_k, src.csr.grp_k);
     m->csr.npad = src.csr.npad;
+    m->csr.ncoop = src.csr.ncoop;
     m->csr.nlong = src.csr.nlong;
     m->csr.npieces = src.csr.npieces;
     cp(m->csr.long_row, src.csr.long_row);

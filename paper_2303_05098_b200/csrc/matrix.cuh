@@ -27,6 +27,9 @@ constexpr int kPiece = 2048;  // entries per CTA for rows longer than grp_cap
 constexpr int kGroupItemsShort = 8;
 constexpr int kGroupItemsLong = 12;
 constexpr int kRowsPerBlock = 1024;
+// CSR rows longer than this (and <= grp_cap) are summed by the whole warp
+// (strided partial sums + fixed butterfly) instead of one lane's serial walk
+constexpr int kCoopLen = 32;
 constexpr int kStreamBlock = 256;
 
 struct CooPart {
@@ -54,6 +57,7 @@ struct CsrPart {
     DBuf<int32_t> grp;     // [ngrp+1]
     DBuf<int64_t> grp_k;   // [ngrp+1]; bit kGrpPadBit of grp_k[g]: group g's padded product layout
     int64_t npad = 0;      // groups flagged padded (0: no flags set, the SpMV runs the plain-layout kernel)
+    int64_t ncoop = 0;     // rows of kCoopLen < length <= grp_cap (summed by the whole warp, spmv.cu)
     // rows longer than grp_cap, split into kPiece-entry pieces for SpMV
     int64_t nlong = 0, npieces = 0;
     DBuf<int32_t> long_row;     // [nlong]

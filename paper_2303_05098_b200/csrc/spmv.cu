@@ -10,6 +10,7 @@
 // segments spanning thread or chunk boundaries) are combined in a fixed
 // tree order: deterministic, within the 1e-12 relative contract.
 #include <algorithm>
+#include <cstdlib>
 
 #include "matrix.cuh"
 
@@ -99,7 +100,15 @@ __device__ __forceinline__ void stage_offsets(int* soff, const int64_t* __restri
 // parts): y already holds the DIA part (dia_kernel ran first) and the row
 // sum is added to it -- spmv.cpp:101-106, DIA part first, then y[i] += CSR
 // row sum: the same roundings, bit-exact.
-template <int IT, bool ACCUM, bool PAD>
+//
+// COOP (the matrix has rows of kCoopLen < length <= 32*IT): such a row is
+// summed by the whole warp -- lane l adds products a+l, a+l+32, ... of the
+// row, then a fixed butterfly joins the 32 partials (deterministic, within
+// the 1e-12 contract) -- while rows of <= kCoopLen entries keep their lane's
+// serial walk (bit-exact).  On skewed matrices one long row otherwise walks
+// its products alone while the other 31 lanes idle, one shared-memory
+// wavefront per entry.
+template <int IT, bool ACCUM, bool PAD, bool COOP>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
@@ -171,7 +180,8 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                 npe = int(rp[nr0 + lane + 1] - nk0);
             }
         }
-        if (!longrow && r0 + lane < r1) {
+        const bool coop = COOP && !longrow && r0 + lane < r1 && pe - pa > kCoopLen;
+        if (!longrow && r0 + lane < r1 && !coop) {
             const int r = r0 + lane;
             double acc = 0.0;
             if (pad)
@@ -180,6 +190,24 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                 for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
             if (ACCUM) acc = fadd(y[r], acc);
             y[r] = acc;
+        }
+        if (COOP) {
+            unsigned big = __ballot_sync(0xffffffffu, coop);
+            while (big) {
+                const int j = __ffs(big) - 1;
+                big &= big - 1;
+                const int a = __shfl_sync(0xffffffffu, pa, j), e = __shfl_sync(0xffffffffu, pe, j);
+                double t = 0.0;
+                if (pad)
+                    for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q + (q >> 4)]);
+                else
+                    for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q]);
+                t = warp_sum(t);
+                if (lane == j) {
+                    const int r = r0 + j;
+                    y[r] = ACCUM ? fadd(y[r], t) : t;
+                }
+            }
         }
         __syncwarp();
         if (gn >= ngrp) break;
@@ -717,18 +745,29 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
     }
 }
 
-template <int IT, bool PAD>
-void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+template <int IT, bool PAD, bool COOP>
+void launch_csr_warp3(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
     if (accum)
-        csr_warp_kernel<IT, true, PAD><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
-                                                            c.col.get(), c.val.get(), x, y, m.nrows);
+        csr_warp_kernel<IT, true, PAD, COOP><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
+                                                                  c.row_ptr.get(), c.col.get(), c.val.get(), x, y,
+                                                                  m.nrows);
     else
-        csr_warp_kernel<IT, false, PAD><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(),
-                                                             c.col.get(), c.val.get(), x, y, m.nrows);
+        csr_warp_kernel<IT, false, PAD, COOP><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
+                                                                   c.row_ptr.get(), c.col.get(), c.val.get(), x, y,
+                                                                   m.nrows);
     SOB_LAUNCH("csr_warp_kernel");
+}
+
+template <int IT, bool PAD>
+void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+    static const bool no_coop = std::getenv("SOB_NO_CSR_COOP") != nullptr;  // diagnostic knob (A/B)
+    if (m.csr.ncoop > 0 && !no_coop)
+        launch_csr_warp3<IT, PAD, true>(m, accum, x, y, s);
+    else
+        launch_csr_warp3<IT, PAD, false>(m, accum, x, y, s);
 }
 
 // accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x

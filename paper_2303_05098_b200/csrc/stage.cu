@@ -71,7 +71,7 @@ class CopyPool {
     CopyPool() {
         int n = int(std::thread::hardware_concurrency());
         if (const char* e = std::getenv("SOB_HOST_THREADS")) n = std::atoi(e);  // tuning knob
-        n = std::max(1, std::min(n > 2 ? n / 2 : n, 16));
+        n = std::max(1, std::min(n, 32));  // all host threads: 16 beat 8 by 1.3x on the B200 hosts (32 MB x + y)
         for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
     }
     void loop(int id) {

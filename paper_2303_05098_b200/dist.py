@@ -120,109 +120,162 @@ def lpt_shard(weights, world: int, rank: int):
     return sorted(mine)
 
 
-# ------------------------------------------------------ fused peer-memory halo
+# ------------------------------------------- native iteration (so_dist_* C-ABI)
 
-class PeerWindows:
-    """The two x windows and the two halo flags of this rank in peer-shareable
-    device memory (so_ipc_alloc), plus the neighbours' windows and flags
-    mapped into this process (so_ipc_open: NVLink peer memory on an 8xB200
-    node; plain device memory when ranks share one GPU).
+HALO, ALLGATHER = 0, 1  # SO_DIST_HALO, SO_DIST_ALLGATHER
 
-    flags[0] is written by the left neighbour (my left halo is complete for
-    iteration value-1), flags[1] by the right neighbour.  Handles travel once
-    through `all_gather_object` (any torch.distributed backend)."""
 
-    def __init__(self, s: Slice, all_gather_object):
+def row_starts(n: int, world: int):
+    """The partition of `partition` as the row_starts array of so_dist_create."""
+    return [n * q // world for q in range(world + 1)]
+
+
+class DistIteration:
+    """Row-partitioned x <- A x across ranks through the library's so_dist_*
+    entry points (csrc/dist.cu): the x exchange is done by the library's own
+    kernels over peer memory (HALO: boundary rows pushed into the neighbours'
+    windows by the multiply; ALLGATHER: new rows stored into every peer's x),
+    no collective on the data path.  The IPC handles travel once through
+    `all_gather_object` (any torch.distributed backend)."""
+
+    def __init__(self, m, kind, rank, world, starts, halo, all_gather_object):
         import ctypes as C
 
         from . import _capi as A
-        if s.world > 1 and s.nloc < 2 * s.h:
-            raise ValueError("fused halo exchange needs >= 2h owned rows per rank")
-        self.s = s
         self._lib = A.lib()
-        self._own = []
-
-        def alloc(nbytes):
-            p, h = C.c_void_p(), C.create_string_buffer(64)
-            self._check(self._lib.so_ipc_alloc(nbytes, C.byref(p), h))
-            self._own.append(p.value)
-            return p.value, h.raw
-
-        self.buf, hb = zip(*[alloc(8 * s.nwin) for _ in range(2)])
-        self.flags, hf = alloc(16)
-        self.tickets, _ = alloc(16)
-        infos = [None] * s.world
-        all_gather_object(infos, (s.rank, s.w0, list(hb), hf))
-        self.peer = {}
-        self._opened = []
-        for nb in (s.rank - 1, s.rank + 1):
-            if 0 <= nb < s.world:
-                _, w0, bh, fh = infos[nb]
-                ptrs = []
-                for h in (*bh, fh):
-                    p = C.c_void_p()
-                    self._check(self._lib.so_ipc_open(h, C.byref(p)))
-                    self._opened.append(p.value)
-                    ptrs.append(p.value)
-                self.peer[nb] = {"w0": w0, "buf": ptrs[:2], "flags": ptrs[2]}
-        self.it = 0  # iterations completed (flag values are monotone)
+        self._C = C
+        self.m = m  # the so_dist borrows the matrix: keep it alive
+        st = (C.c_int64 * (world + 1))(*starts)
+        h = C.c_void_p()
+        self._check(self._lib.so_dist_create(m._h, kind, rank, world, st, int(halo), C.byref(h)))
+        self._h = h
+        mine = C.create_string_buffer(64)
+        self._check(self._lib.so_dist_handle(self._h, mine))
+        infos = [None] * world
+        all_gather_object(infos, mine.raw)
+        arr = C.create_string_buffer(b"".join(infos), 64 * world)
+        self._check(self._lib.so_dist_connect(self._h, arr))
 
     def _check(self, st):
         if st != 0:
             raise RuntimeError(self._lib.so_last_error().decode(errors="replace"))
 
-    def tensor(self, k):
-        """torch view (zero-copy, __cuda_array_interface__) of window k."""
+    def x(self, which=-1):
+        """(device pointer, global offset, length) of x buffer `which` (-1: latest iterate)."""
+        C = self._C
+        p, off, ln = C.c_void_p(), C.c_int64(), C.c_int64()
+        self._check(self._lib.so_dist_x(self._h, int(which), C.byref(p), C.byref(off), C.byref(ln)))
+        return p.value, off.value, ln.value
+
+    def tensor(self, which=-1):
+        """torch view (zero-copy, __cuda_array_interface__) of an x buffer."""
         import torch
+        ptr, _, ln = self.x(which)
 
         class _View:
-            def __init__(self, ptr, n):
-                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+            def __init__(self):
+                self.__cuda_array_interface__ = {"shape": (ln,), "typestr": "<f8", "data": (ptr, False),
                                                   "version": 3, "strides": None}
-        return torch.as_tensor(_View(self.buf[k], self.s.nwin), device="cuda")
+        return torch.as_tensor(_View(), device="cuda")
 
-    def iterate(self, m, iters, stream):
-        """`iters` steps of x <- A x on the windows, halo rows pushed to the
-        neighbours by the multiply itself (so_spmv_rows_push), no collective.
-        Returns the index of the window holding the last iterate."""
-        import ctypes as C
-        s, lib = self.s, self._lib
-        lo, hi = s.interior()
-        sp = C.c_void_p(stream)
-        for _ in range(iters):
-            it = self.it
-            cur, nxt = self.buf[it % 2], self.buf[(it + 1) % 2]
-            y = nxt + 8 * s.own_lo
-            # my halo of `cur` was pushed by the neighbours during iteration it-1
-            if s.rank > 0:
-                self._check(lib.so_wait_flag(C.c_void_p(self.flags), it, sp))
-            if s.rank < s.world - 1:
-                self._check(lib.so_wait_flag(C.c_void_p(self.flags + 8), it, sp))
-            if s.rank > 0:  # first h rows -> left neighbour's right halo
-                p = self.peer[s.rank - 1]
-                remote = p["buf"][(it + 1) % 2] + 8 * (s.r0 - p["w0"])
-                self._check(lib.so_spmv_rows_push(m._h, C.c_void_p(cur), C.c_void_p(y), 0, lo,
-                                                  C.c_void_p(remote), C.c_void_p(self.tickets),
-                                                  C.c_void_p(p["flags"] + 8), it + 1, sp))
-            if s.rank < s.world - 1:  # last h rows -> right neighbour's left halo
-                p = self.peer[s.rank + 1]
-                remote = p["buf"][(it + 1) % 2] + 8 * (s.r0 + hi - p["w0"])
-                self._check(lib.so_spmv_rows_push(m._h, C.c_void_p(cur), C.c_void_p(y), hi, s.nloc,
-                                                  C.c_void_p(remote), C.c_void_p(self.tickets + 4),
-                                                  C.c_void_p(p["flags"]), it + 1, sp))
-            if hi > lo:
-                self._check(lib.so_spmv_device_rows(m._h, C.c_void_p(cur), C.c_void_p(y), lo, hi, sp))
-            self.it += 1
-        return self.it % 2
+    def iterate(self, iters, stream=0):
+        self._check(self._lib.so_dist_iterate(self._h, int(iters), self._C.c_void_p(stream)))
 
     def timeouts(self):
-        """Halo waits that gave up (a neighbour never published): nonzero means
-        the iterate is invalid (so_wait_flag_timeouts)."""
-        return int(self._lib.so_wait_flag_timeouts())
+        return int(self._lib.so_dist_timeouts())
 
     def close(self):
-        for p in self._opened:
-            self._lib.so_ipc_close(p)
-        for p in self._own:
-            self._lib.so_ipc_free(p)
-        self._opened, self._own = [], []
+        if self._h:
+            self._lib.so_dist_free(self._h)
+            self._h = None
+
+
+class _NativeIterator:
+    """bench adapter: the so_dist HALO iteration."""
+
+    def __init__(self, s: Slice, m, dist, stream):
+        self.s, self.stream = s, stream
+        self.it = DistIteration(m, HALO, s.rank, s.world, row_starts(s.n, s.world), s.h, dist.all_gather_object)
+
+    def load_x(self, fn):
+        self.it.tensor(0).copy_(fn(self.s.w0, self.s.w1))
+
+    def run(self, iters):
+        self.it.iterate(iters, self.stream.cuda_stream)
+
+    def owned(self):
+        return self.it.tensor(-1)[self.s.own_lo:self.s.own_hi]
+
+    def checksum(self):
+        return owned_checksum(self.owned(), self.s)
+
+    def timeouts(self):
+        return self.it.timeouts()
+
+    def close(self):
+        self.it.close()
+
+
+class _NcclIterator:
+    """bench adapter: `iterate` with torch.distributed isend/irecv halos
+    (NCCL point-to-point) after the boundary rows."""
+
+    def __init__(self, s: Slice, m, dist, stream):
+        import torch
+        self.s, self.m, self.dist, self.stream = s, m, dist, stream
+        self.xa = torch.zeros(s.nwin, dtype=torch.float64, device="cuda")
+        self.xb = torch.zeros_like(self.xa)
+
+    def load_x(self, fn):
+        self.xa.copy_(fn(self.s.w0, self.s.w1))
+
+    def run(self, iters):
+        s, m, dist, st = self.s, self.m, self.dist, self.stream
+
+        def spmv_rows(xw, yw, lo, hi):
+            m.spmv_device_rows(xw.data_ptr(), yw.data_ptr() + 8 * s.own_lo, lo, hi, st.cuda_stream)
+
+        def exchange(buf, plan):
+            reqs = []
+            for peer, (sa, sb), (ra, rb) in plan:
+                reqs.append(dist.isend(buf[sa:sb], peer))
+                reqs.append(dist.irecv(buf[ra:rb], peer))
+            return lambda: [r.wait() for r in reqs]
+
+        out = iterate(s, self.xa, self.xb, iters, spmv_rows, exchange)
+        if out is not self.xa:
+            self.xa, self.xb = self.xb, self.xa
+
+    def checksum(self):
+        return owned_checksum(self.xa[self.s.own_lo:self.s.own_hi], self.s)
+
+    def timeouts(self):
+        return 0
+
+    def close(self):
+        pass
+
+
+def owned_checksum(owned, s: Slice):
+    """Order-independent bitwise checksum of the whole iterate:
+    sum_i (2 i + 1) * bits(x_i) mod 2^64 over global rows i (wrapping int64
+    arithmetic, a commutative ring), so every partition of the same iterate
+    gives the same number and any changed bit changes it."""
+    import torch
+    import torch.distributed as dist
+    bits = owned.contiguous().view(torch.int64)
+    idx = torch.arange(s.r0, s.r1, dtype=torch.int64, device=owned.device) * 2 + 1
+    local = (bits * idx).sum().reshape(1)
+    if dist.is_available() and dist.is_initialized() and s.world > 1:
+        if dist.get_backend() == "gloo":
+            local = local.cpu()
+        dist.all_reduce(local)
+    return int(local.item()) & ((1 << 64) - 1)
+
+
+def make_iterator(s: Slice, m, dist, exchange, stream):
+    """The config-5 iteration for bench.py: 'p2p' -> the native fused-halo
+    so_dist iteration, 'nccl' -> NCCL point-to-point halos."""
+    if exchange == "p2p":
+        return _NativeIterator(s, m, dist, stream)
+    return _NcclIterator(s, m, dist, stream)

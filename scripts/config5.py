@@ -69,14 +69,13 @@ def main():
                 r.wait()
         return wait
 
-    pw = None
-    if world > 1 and a.exchange == "p2p":
-        pw = D.PeerWindows(s, torch.distributed.all_gather_object)
-        pw.tensor(0).copy_(xa)
+    it = D.make_iterator(s, m, torch.distributed if world > 1 else None, a.exchange, stream) if world > 1 else None
+    if it is not None:
+        it.load_x(lambda lo, hi: 1.0 + (torch.arange(lo, hi, dtype=torch.int64, device="cuda") % 7).double() / 8.0)
         del xa, xb
         torch.cuda.synchronize()
         torch.distributed.barrier()
-        pw.iterate(m, a.warmup, stream.cuda_stream)
+        it.run(a.warmup)
     else:
         out = D.iterate(s, xa, xb, a.warmup, spmv_rows, exchange)
         other = xb if out is xa else xa
@@ -85,8 +84,8 @@ def main():
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    if pw is not None:
-        out = pw.tensor(pw.iterate(m, a.iters, stream.cuda_stream))
+    if it is not None:
+        it.run(a.iters)
     else:
         out = D.iterate(s, out, other, a.iters, spmv_rows, exchange)
     e1.record(stream)
@@ -102,9 +101,7 @@ def main():
     else:
         sec, nbytes = float(t[0]), float(t[1])
     # checksum of the final iterate's owned rows (identical for every P)
-    csum = torch.tensor([float(out[s.own_lo:s.own_hi].sum())], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(csum)
+    csum = it.checksum() if it is not None else D.owned_checksum(out[s.own_lo:s.own_hi], s)
     if rank == 0:
         peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
         print(json.dumps({"metric": "spmv_gbs_iterated", "config": f"27-pt stencil {g}^3 DIA, row-partitioned",
@@ -112,11 +109,11 @@ def main():
                           "value": round(nbytes / sec / 1e9, 1), "unit": "GB/s",
                           "frac_per_gpu": round(nbytes / sec / 1e9 / world / peak, 4),
                           "halo_rows_per_side": h, "exchange": a.exchange if world > 1 else "none",
-                          "checksum": float(csum.item())}), flush=True)
+                          "checksum": csum}), flush=True)
     if world > 1:
         torch.distributed.barrier()
-        if pw is not None:
-            pw.close()
+        if it is not None:
+            it.close()
         torch.distributed.destroy_process_group()
 
 

@@ -66,10 +66,12 @@ def _full(so, O, csr, exact_formats=(1, 2, 3, 5)):
         _cmp_arrays(m.download(), want, f"fmt {f}")
         y = m.spmv(x)
         y_ref = O.oc_spmv(want, x)
+        assert max_rel(y, y_ref) <= SPMV_TOL, f
         if f in exact_formats:
-            assert np.array_equal(y, y_ref), f
-        else:
-            assert max_rel(y, y_ref) <= SPMV_TOL, f
+            # CSR / HDC's CSR part: rows of <= 32 entries keep the reference
+            # order; longer ones are summed by the whole warp (reordered)
+            short = slice(None) if f in (2, 3) else np.diff(csr.row_ptr) <= 32
+            assert np.array_equal(y[short], y_ref[short]), f
         if f == 1:
             y_csr = y_ref
         fv = m.extract_features(0.2)
@@ -85,8 +87,7 @@ def test_config2_banded_full_size(so, O):
 
 def test_config3_rmat_full_size(so, O):
     from paper_2303_05098_b200 import synth
-    # CSR is bit-exact only for rows up to the warp-group cap; R-MAT hubs are split
-    _full(so, O, synth.rmat(22, 16, seed=42), exact_formats=(2, 3))
+    _full(so, O, synth.rmat(22, 16, seed=42))
 
 
 def test_hyb_favourable_full_size(so, O):

@@ -15,6 +15,19 @@ pytestmark = pytest.mark.gpu
 
 SPMV_TOL = 1e-12  # test_spmv.cpp:59, north star
 EXACT_FORMATS = (1, 2, 3, 5)  # CSR, DIA, ELL, HDC
+COOP_LEN = 32  # matrix.cuh kCoopLen: longer CSR rows are summed by the whole warp (reordered, <= 1e-12)
+
+
+def check_spmv(y, y_ref, fmt, row_len):
+    """Bit-exact rows where the kernel keeps the reference's per-row order
+    (DIA, ELL: every row; CSR / HDC's CSR part: rows of <= COOP_LEN entries),
+    <= 1e-12 relative per row under max(1, |y|) everywhere (north star)."""
+    assert max_rel(y, y_ref) <= SPMV_TOL, fmt
+    if fmt in (2, 3):
+        assert np.array_equal(y, y_ref), fmt
+    elif fmt in (1, 5):
+        short = np.asarray(row_len) <= COOP_LEN
+        assert np.array_equal(y[short], y_ref[short]), fmt
 
 
 def to_dev(so, coo):
@@ -138,10 +151,7 @@ def test_random_conversions_spmv_features(so, O, seed, trials):
             assert m.nnz() == coo["val"].size
             y = m.spmv(x)
             y_ref = O.oc_spmv(want, x)
-            if f in EXACT_FORMATS:
-                assert np.array_equal(y, y_ref), (t, f)
-            else:
-                assert max_rel(y, y_ref) <= SPMV_TOL, (t, f)
+            check_spmv(y, y_ref, f, np.bincount(coo["row"], minlength=coo["nrows"]))
             fv, st = m.extract_features(ratio, with_stats=True)
             fo, so_ = O.oc_features(want, ratio)
             assert np.array_equal(np.array(fv.to_row()), fo), (t, f, fv.to_row(), fo)
@@ -344,11 +354,7 @@ def _structured(so, O, csr, ratio=0.2, formats=range(6)):
         m = d.convert(f)
         cmp_host(m.download(), want, f"fmt {f}")
         y, y_ref = m.spmv(x), O.oc_spmv(want, x)
-        # CSR rows up to the warp-group cap (>= 256 entries) keep the reference order
-        if f in EXACT_FORMATS and np.diff(csr.row_ptr).max(initial=0) <= 256:
-            assert np.array_equal(y, y_ref), f
-        else:
-            assert max_rel(y, y_ref) <= SPMV_TOL, f
+        check_spmv(y, y_ref, f, np.diff(csr.row_ptr))
         fv = m.extract_features(ratio)
         assert np.array_equal(np.array(fv.to_row()), want_feats), (f, fv.to_row(), want_feats)
 
