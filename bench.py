@@ -595,23 +595,6 @@ def held_out_ids(count):
     return ids[:count]
 
 
-def kernel_identical(mats):
-    """Formats whose multiply runs the very same kernel on the same arrays as
-    another: HDC with an empty CSR part and every diagonal kept is
-    the DIA kernel on the DIA arrays; HYB with an empty COO part and the same
-    width is the ELL kernel on the ELL arrays.  Returns {format: twin}."""
-    tw = {}
-    if 2 in mats and 5 in mats:
-        a, b = mats[2].info, mats[5].info
-        if b.csr_nnz == 0 and b.ndiags == a.ndiags:
-            tw[5], tw[2] = 2, 5
-    if 3 in mats and 4 in mats:
-        a, b = mats[3].info, mats[4].info
-        if b.coo_nnz == 0 and b.ell_width == a.ell_width:
-            tw[4], tw[3] = 3, 4
-    return tw
-
-
 def profile_one(P, spec, forest, stream, reps=10):
     """One corpus matrix: every feasible format timed (time_spmv semantics:
     reps back-to-back multiplies after a warm-up, total time; label = argmin,
@@ -631,7 +614,7 @@ def profile_one(P, spec, forest, stream, reps=10):
         except P.PaddingOverflow:
             continue
         tot[f] = float(np.sum(time_steps(mats[f], x, y, stream, reps, 1)))
-    tw = kernel_identical(mats)
+    tw = P.kernel_twins(mats)
     del mats
     P.tune_ml(base, forest)  # first call builds the tune graph
     outs = [P.tune_ml(base, forest) for _ in range(3)]
@@ -654,9 +637,9 @@ def summarise_config4(rows, elapsed, world):
     twall = np.array([r["t_wall"] for r in rows])
     # kernel-identical twins collapse into one class (the measured "optimum"
     # between two identical kernels is timing noise)
-    canon = lambda r, f: min(f, r["twins"].get(f, f))  # noqa: E731
-    lab_c = np.array([canon(r, r["label"]) for r in rows])
-    ch_c = np.array([canon(r, r["chosen"]) for r in rows])
+    from paper_2303_05098_b200 import collapse_label
+    lab_c = np.array([collapse_label(r["label"], r["twins"]) for r in rows])
+    ch_c = np.array([collapse_label(r["chosen"], r["twins"]) for r in rows])
     recalls = [float((ch_c[lab_c == c] == c).mean()) for c in range(6) if (lab_c == c).any()]
     cost = (tfe + tpr) / t_csr
     cost_w = twall / t_csr

@@ -1,7 +1,8 @@
 #pragma once
 // Exception taxonomy of the reference API (proj/include/sparseoracle/
 // errors.hpp:8-71).  Every C-ABI status maps to exactly one of these
-// (paper_2303_05098_b200/cpp/status.cpp), so callers catch the same types.
+// (detail::check in paper_2303_05098_b200/cpp/formats.cpp), so callers catch
+// the same types.
 
 #include <stdexcept>
 #include <string>

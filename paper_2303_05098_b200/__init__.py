@@ -10,10 +10,11 @@ from .device import (COO, CSR, DIA, ELL, FORMAT_NAMES, HDC, HYB, AllFormatsInfea
                      ConversionConfig, DeviceForest, DeviceMatrix, DimensionMismatch,
                      EmptyMatrix, Error, FeatureVector, FlatForest, IndexOutOfRange,
                      InvalidInput, MalformedModel, PaddingOverflow, ParseError,
-                     UnsupportedFormat, format_feasible, set_device, tune_ml)
+                     UnsupportedFormat, collapse_label, format_feasible, kernel_twins, set_device,
+                     tune_ml)
 
 __all__ = ["COO", "CSR", "DIA", "ELL", "HYB", "HDC", "FORMAT_NAMES", "DeviceMatrix",
            "DeviceForest", "FlatForest", "ConversionConfig", "FeatureVector", "tune_ml",
            "format_feasible", "set_device", "Error", "InvalidInput", "PaddingOverflow",
            "DimensionMismatch", "EmptyMatrix", "MalformedModel", "IndexOutOfRange",
-           "AllFormatsInfeasible", "ParseError", "UnsupportedFormat"]
+           "AllFormatsInfeasible", "ParseError", "UnsupportedFormat", "kernel_twins", "collapse_label"]

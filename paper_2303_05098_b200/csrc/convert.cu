@@ -186,6 +186,7 @@ __global__ void long_row_flags(const int64_t* __restrict__ rp, int64_t n, int64_
 // groups prefer the padded layout, i.e. when the SpMV will run the padded
 // kernel -- flag (SET = true); otherwise grp_k stays plain and the
 // plain-layout kernel reads it unmasked.
+// npad[1] (count pass) counts groups of more than 32 rows.
 template <bool SET>
 __global__ void group_pad_flags(const int32_t* __restrict__ grp, int64_t* __restrict__ grp_k, int64_t ngrp,
                                 const int64_t* __restrict__ rp, int cap, unsigned long long* npad) {
@@ -193,6 +194,7 @@ __global__ void group_pad_flags(const int32_t* __restrict__ grp, int64_t* __rest
     const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (g >= ngrp) return;
     const int r0 = grp[g], r1 = grp[g + 1];
+    if (!SET && lane == 0 && r1 - r0 > 32) atomicAdd(npad + 1, 1ull);
     const int64_t k0 = grp_k[g];
     if (grp_k[g + 1] - k0 > cap) return;  // a long row: pieces, no walk
     const bool act = r0 + lane < r1;
@@ -223,10 +225,19 @@ __global__ void __launch_bounds__(32 * kGroupWarps)
     for (int g = 0; g < len;) {
         if (lane == 0) flag[lo + g] = 1;
         const int64_t base = r[g];
-        const int j = g + lane;
-        const bool over = j < len && r[j + 1] - base > cap;
-        const unsigned b = __ballot_sync(0xffffffffu, over);
-        const int step = b ? __ffs(b) - 1 : 32;
+        // the next start: the first row whose end passes base + cap, at most
+        // kGroupRowsMax rows on (one ballot per 32 rows)
+        int step = kGroupRowsMax;
+        for (int w = 0; w < kGroupRowsMax; w += 32) {
+            const int j = g + w + lane;
+            const bool over = j < len && r[j + 1] - base > cap;
+            const unsigned b = __ballot_sync(0xffffffffu, over);
+            if (b) {
+                step = w + __ffs(b) - 1;
+                break;
+            }
+            if (g + w + 32 >= len) break;  // the chunk ends first
+        }
         g += step ? step : 1;  // step 0: the base row alone exceeds cap
     }
 }
@@ -732,16 +743,21 @@ void build_row_blocks(CsrPart& csr, int64_t n, cudaStream_t s) {
     SOB_LAUNCH("row_block_scatter");
     csr.npad = 0;
     csr.ncoop = 0;
+    csr.grp_rpl = 1;
     if (csr.ngrp > 0) {
         // the counter lives in the (free until long_row_flags) flag scratch:
         // no allocation between the matrix arrays
         unsigned long long* npad = reinterpret_cast<unsigned long long*>(pos.get());
-        SOB_CUDA(cudaMemsetAsync(npad, 0, sizeof(unsigned long long), s));
+        SOB_CUDA(cudaMemsetAsync(npad, 0, 2 * sizeof(unsigned long long), s));
         const unsigned g = unsigned(ceil_div(csr.ngrp * 32, 256));
         group_pad_flags<false><<<g, 256, 0, s>>>(csr.grp.get(), csr.grp_k.get(), csr.ngrp, csr.row_ptr.get(),
                                                  csr.grp_cap, npad);
         SOB_LAUNCH("group_pad_flags");
-        csr.npad = int64_t(d2h_scalar(npad, s));
+        unsigned long long cnt[2];
+        SOB_CUDA(cudaMemcpyAsync(cnt, npad, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+        SOB_CUDA(cudaStreamSynchronize(s));
+        csr.npad = int64_t(cnt[0]);
+        csr.grp_rpl = cnt[1] > 0 ? kGroupRowsMax / 32 : 1;
         if (csr.npad * kGrpPadShare >= csr.ngrp) {
             group_pad_flags<true><<<g, 256, 0, s>>>(csr.grp.get(), csr.grp_k.get(), csr.ngrp, csr.row_ptr.get(),
                                                     csr.grp_cap, npad);
@@ -848,6 +864,7 @@ so_matrix* clone_matrix(const so_matrix& src, cudaStream_t s) {
     cp(m->csr.grp_k, src.csr.grp_k);
     m->csr.npad = src.csr.npad;
     m->csr.ncoop = src.csr.ncoop;
+    m->csr.grp_rpl = src.csr.grp_rpl;
     m->csr.nlong = src.csr.nlong;
     m->csr.npieces = src.csr.npieces;
     cp(m->csr.long_row, src.csr.long_row);

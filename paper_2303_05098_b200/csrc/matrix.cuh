@@ -21,15 +21,19 @@ constexpr int kGrpPadBit = 62;
 constexpr int64_t kGrpPad = int64_t(1) << kGrpPadBit;
 constexpr int64_t kGrpPadShare = 64;  // padded kernel when >= 1/64 of the groups prefer it
 constexpr int kPiece = 2048;  // entries per CTA for rows longer than grp_cap
-// SpMV warp groups: <= 32 consecutive rows holding <= grp_cap = 32*items
+// SpMV warp groups: <= kGroupRowsMax consecutive rows holding <= grp_cap = 32*items
 // entries (greedy); short-row matrices (mean <= 8) load 8 entries per lane,
 // others 12 (scripts/spmv_lab.cu measurements).
 constexpr int kGroupItemsShort = 8;
 constexpr int kGroupItemsLong = 12;
 constexpr int kRowsPerBlock = 1024;
+// a warp group holds at most kGroupRowsMax rows (lane i walks rows i, i+32,
+// ...): tiny rows (R-MAT's tail, sparse corpus matrices) fill a group's
+// entries instead of leaving most of its 32*IT slots empty
+constexpr int kGroupRowsMax = 128;
 // CSR rows longer than this (and <= grp_cap) are summed by the whole warp
 // (strided partial sums + fixed butterfly) instead of one lane's serial walk
-constexpr int kCoopLen = 32;
+constexpr int kCoopLen = 64;
 constexpr int kStreamBlock = 256;
 
 struct CooPart {
@@ -58,6 +62,7 @@ struct CsrPart {
     DBuf<int64_t> grp_k;   // [ngrp+1]; bit kGrpPadBit of grp_k[g]: group g's padded product layout
     int64_t npad = 0;      // groups flagged padded (0: no flags set, the SpMV runs the plain-layout kernel)
     int64_t ncoop = 0;     // rows of kCoopLen < length <= grp_cap (summed by the whole warp, spmv.cu)
+    int grp_rpl = 1;       // rows per lane of the widest group (1: every group <= 32 rows; else kGroupRowsMax / 32)
     // rows longer than grp_cap, split into kPiece-entry pieces for SpMV
     int64_t nlong = 0, npieces = 0;
     DBuf<int32_t> long_row;     // [nlong]

@@ -108,7 +108,42 @@ __device__ __forceinline__ void stage_offsets(int* soff, const int64_t* __restri
 // serial walk (bit-exact).  On skewed matrices one long row otherwise walks
 // its products alone while the other 31 lanes idle, one shared-memory
 // wavefront per entry.
-template <int IT, bool ACCUM, bool PAD, bool COOP>
+// One row per lane: products [pa, pe) of the warp's product array, serial in
+// the reference's order (bit-exact), or -- COOP, rows of more than kCoopLen
+// entries -- summed by the whole warp (strided partials, fixed butterfly).
+template <bool ACCUM, bool COOP>
+__device__ __forceinline__ void csr_rows_sum(const double* prod, bool pad, int r, bool act, int pa, int pe,
+                                             double* __restrict__ y, int lane) {
+    const bool coop = COOP && act && pe - pa > kCoopLen;
+    if (act && !coop) {
+        double acc = 0.0;
+        if (pad)
+            for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j + (j >> 4)]);
+        else
+            for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
+        if (ACCUM) acc = fadd(y[r], acc);
+        y[r] = acc;
+    }
+    if (COOP) {
+        unsigned big = __ballot_sync(0xffffffffu, coop);
+        while (big) {
+            const int j = __ffs(big) - 1;
+            big &= big - 1;
+            const int a = __shfl_sync(0xffffffffu, pa, j), e = __shfl_sync(0xffffffffu, pe, j);
+            double t = 0.0;
+            if (pad)
+                for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q + (q >> 4)]);
+            else
+                for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q]);
+            t = warp_sum(t);
+            if (lane == j) y[r] = ACCUM ? fadd(y[r], t) : t;
+        }
+    }
+}
+
+// RPL: rows per lane of the widest group (1, or kGroupRowsMax / 32 when the
+// partition has groups of more than 32 tiny rows).
+template <int IT, bool ACCUM, bool PAD, bool COOP, int RPL>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
@@ -180,33 +215,18 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                 npe = int(rp[nr0 + lane + 1] - nk0);
             }
         }
-        const bool coop = COOP && !longrow && r0 + lane < r1 && pe - pa > kCoopLen;
-        if (!longrow && r0 + lane < r1 && !coop) {
-            const int r = r0 + lane;
-            double acc = 0.0;
-            if (pad)
-                for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j + (j >> 4)]);
-            else
-                for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
-            if (ACCUM) acc = fadd(y[r], acc);
-            y[r] = acc;
-        }
-        if (COOP) {
-            unsigned big = __ballot_sync(0xffffffffu, coop);
-            while (big) {
-                const int j = __ffs(big) - 1;
-                big &= big - 1;
-                const int a = __shfl_sync(0xffffffffu, pa, j), e = __shfl_sync(0xffffffffu, pe, j);
-                double t = 0.0;
-                if (pad)
-                    for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q + (q >> 4)]);
-                else
-                    for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q]);
-                t = warp_sum(t);
-                if (lane == j) {
-                    const int r = r0 + j;
-                    y[r] = ACCUM ? fadd(y[r], t) : t;
+        if (!longrow) {
+            csr_rows_sum<ACCUM, COOP>(prod, pad, r0 + lane, r0 + lane < r1, pa, pe, y, lane);
+            // groups of tiny rows: lane i also walks rows i+32, i+64, ...
+            for (int q = 1; q < RPL && r0 + 32 * q < r1; ++q) {
+                const int rr = r0 + 32 * q + lane;
+                const bool act = rr < r1;
+                int qa = 0, qe = 0;
+                if (act) {
+                    qa = int(rp[rr] - k0);
+                    qe = int(rp[rr + 1] - k0);
                 }
+                csr_rows_sum<ACCUM, COOP>(prod, pad, rr, act, qa, qe, y, lane);
             }
         }
         __syncwarp();
@@ -488,7 +508,7 @@ __device__ __forceinline__ void coo_load(const int32_t* __restrict__ row, const 
     }
 }
 
-template <bool ACCUM>
+template <bool ACCUM, bool FILL>
 __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base, int cnt, int64_t z, int64_t nrows,
                                            const int (&r)[kCooItems], const double (&p)[kCooItems], int prev_row,
                                            int next_row, double* __restrict__ y, CooChunkRec* __restrict__ rec) {
@@ -530,7 +550,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
         if (j < nmine) {
             const int rw = r[j];
             if (rw != prv) {
-                if (!ACCUM)  // rows strictly between consecutive entries are empty
+                if (FILL)  // rows strictly between consecutive entries are empty
                     for (int q = prv + 1; q < rw; ++q) y[q] = 0.0;
                 if (j > 0) acc = 0.0;
             }
@@ -552,7 +572,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
                 }
                 rec[chunk].flags = (first_cont ? kFirstCont : 0) | (open ? kLastOpen : 0) |
                                    ((open && orphan) ? kSingle : 0);
-                if (!ACCUM && base + cnt == z)  // trailing empty rows
+                if (FILL && base + cnt == z)  // trailing empty rows
                     for (int64_t q = int64_t(rw) + 1; q < nrows; ++q) y[q] = 0.0;
             }
             prv = rw;
@@ -560,7 +580,11 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
     }
 }
 
-template <bool ACCUM>
+// FILL: empty rows are zero-filled by the lane that finds them (y written
+// exactly once); without FILL, y was zeroed beforehand (a memset) and only
+// rows holding entries are stored -- matrices with long empty-row runs, and
+// HYB's COO part ahead of the ELL part.
+template <bool ACCUM, bool FILL>
 __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
@@ -595,7 +619,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
         if (nx < nchunks)
             coo_load(row, col, val, nx * kCooChunk + lane * IT, int(min(z - nx * kCooChunk, int64_t(kCooChunk))) - lane * IT,
                      r, c, v);
-        coo_finish<ACCUM>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
+        coo_finish<ACCUM, FILL>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
         if (nx >= nchunks) break;
         chunk = nx;
     }
@@ -725,14 +749,14 @@ __global__ void coo_max_gap(int64_t z, int64_t nrows, const int32_t* __restrict_
 }
 constexpr int64_t kCooGapInline = 4096;  // a lane zero-fills up to ~2 us of rows inline
 
-template <bool ACCUM>
+template <bool ACCUM, bool FILL = !ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
     // chunk records, then the fix-up's control word pair and long-run queue
     static_assert(sizeof(LongRun) == sizeof(CooChunkRec) && sizeof(CooChunkRec) >= 16, "record layout");
     DBuf<CooChunkRec> rec(2 * nchunks + 1, s);
     const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
-    coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
+    coo_warp_kernel<ACCUM, FILL><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
                                                 rec.get());
     SOB_LAUNCH("coo_warp_kernel");
     LongRun* runs = reinterpret_cast<LongRun*>(rec.get() + nchunks + 1);
@@ -745,20 +769,28 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
     }
 }
 
-template <int IT, bool PAD, bool COOP>
-void launch_csr_warp3(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+template <int IT, bool PAD, bool COOP, int RPL>
+void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
     const CsrPart& c = m.csr;
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
     if (accum)
-        csr_warp_kernel<IT, true, PAD, COOP><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
-                                                                  c.row_ptr.get(), c.col.get(), c.val.get(), x, y,
-                                                                  m.nrows);
+        csr_warp_kernel<IT, true, PAD, COOP, RPL><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
+                                                                       c.row_ptr.get(), c.col.get(), c.val.get(),
+                                                                       x, y, m.nrows);
     else
-        csr_warp_kernel<IT, false, PAD, COOP><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
-                                                                   c.row_ptr.get(), c.col.get(), c.val.get(), x, y,
-                                                                   m.nrows);
+        csr_warp_kernel<IT, false, PAD, COOP, RPL><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
+                                                                        c.row_ptr.get(), c.col.get(), c.val.get(),
+                                                                        x, y, m.nrows);
     SOB_LAUNCH("csr_warp_kernel");
+}
+
+template <int IT, bool PAD, bool COOP>
+void launch_csr_warp3(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+    if (m.csr.grp_rpl > 1)
+        launch_csr_warp4<IT, PAD, COOP, kGroupRowsMax / 32>(m, accum, x, y, s);
+    else
+        launch_csr_warp4<IT, PAD, COOP, 1>(m, accum, x, y, s);
 }
 
 template <int IT, bool PAD>
@@ -915,7 +947,7 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
                 SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
             } else if (m.coo.max_gap < 0 || m.coo.max_gap > kCooGapInline) {  // unknown under capture: safe path
                 SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
-                launch_coo<true>(m.coo, m.nrows, x, y, s);
+                launch_coo<false, false>(m.coo, m.nrows, x, y, s);
             } else {
                 launch_coo<false>(m.coo, m.nrows, x, y, s);
             }
@@ -931,9 +963,19 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
             launch_ell<false>(m, x, y, s);
             break;
         case SO_HYB:
-            coo_profile(m.coo, m.nrows, s);
-            launch_ell<false>(m, x, y, s);
-            if (m.coo.nnz > 0) launch_coo<true>(m.coo, m.nrows, x, y, s);
+            // y = ELL part + COO part (spmv.cpp:95-100).  The COO part runs
+            // first into a zeroed y (stores only, no read of y: the 3-CTA/SM
+            // kernel), then the ELL kernel adds its row sum: fadd is
+            // commutative, so y[i] = coo_i + ell_i is bit-identical to
+            // ell_i + coo_i, and rows without COO entries get 0 + ell_i = ell_i
+            if (m.coo.nnz > 0) {
+                coo_profile(m.coo, m.nrows, s);
+                SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
+                launch_coo<false, false>(m.coo, m.nrows, x, y, s);
+                launch_ell<true>(m, x, y, s);
+            } else {
+                launch_ell<false>(m, x, y, s);
+            }
             break;
         case SO_HDC:
             // one kernel per non-empty part; both parts: the DIA kernel, then

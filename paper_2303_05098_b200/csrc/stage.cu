@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <immintrin.h>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -130,6 +131,40 @@ struct Staging {
 };
 Staging g_stage[64];
 
+// Host copy with non-temporal (streaming) stores: the destination is not
+// read first (no read-for-ownership) and does not evict the source from the
+// caches -- x lands in pinned memory that only the device reads next, y in a
+// buffer the caller reads later.  AVX2 when the CPU has it, else memcpy.
+__attribute__((target("avx2"))) void copy_nt_avx2(double* dst, const double* src, size_t n) {
+    size_t i = 0;
+    while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31)) {
+        dst[i] = src[i];
+        ++i;
+    }
+    for (; i + 16 <= n; i += 16) {
+        const __m256d a = _mm256_loadu_pd(src + i), b = _mm256_loadu_pd(src + i + 4);
+        const __m256d c = _mm256_loadu_pd(src + i + 8), d = _mm256_loadu_pd(src + i + 12);
+        _mm256_stream_pd(dst + i, a);
+        _mm256_stream_pd(dst + i + 4, b);
+        _mm256_stream_pd(dst + i + 8, c);
+        _mm256_stream_pd(dst + i + 12, d);
+    }
+    for (; i < n; ++i) dst[i] = src[i];
+    _mm_sfence();
+}
+
+void copy_host(double* dst, const double* src, size_t n) {
+    static const bool nt = [] {
+        if (std::getenv("SOB_NO_NT_COPY")) return false;  // diagnostic knob
+        __builtin_cpu_init();
+        return bool(__builtin_cpu_supports("avx2"));
+    }();
+    if (nt)
+        copy_nt_avx2(dst, src, n);
+    else
+        std::memcpy(dst, src, n * sizeof(double));
+}
+
 struct Task {
     double* dst;
     const double* src;
@@ -207,7 +242,7 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                     std::this_thread::yield();
                 }
             }
-            std::memcpy(k.dst, k.src, k.n * sizeof(double));
+            copy_host(k.dst, k.src, k.n);
             if (k.chunk >= 0) xdone[size_t(k.chunk)].fetch_add(1, std::memory_order_release);
         }
     };

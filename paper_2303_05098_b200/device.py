@@ -406,6 +406,36 @@ class DeviceForest:
         return out
 
 
+def kernel_twins(mats: dict) -> dict:
+    """Formats whose multiply runs the very same kernel on the very same
+    arrays as another format of the same matrix ({format: twin}): HDC with
+    an empty CSR part and every diagonal kept is the DIA kernel on the DIA
+    arrays, HDC with no diagonal at all is the CSR kernel on the CSR arrays,
+    HYB with an empty COO part and the ELL width is the ELL kernel on the ELL
+    arrays (spmv.cu spmv_device).  `mats` maps format id -> DeviceMatrix of
+    one matrix (infeasible formats absent).  A measured "optimum" between
+    twins is timing noise, so labels and accuracy treat them as one class."""
+    tw = {}
+    if DIA in mats and HDC in mats:
+        a, b = mats[DIA].info, mats[HDC].info
+        if b.csr_nnz == 0 and b.ndiags == a.ndiags:
+            tw[HDC], tw[DIA] = DIA, HDC
+    if CSR in mats and HDC in mats and HDC not in tw:
+        if mats[HDC].info.ndiags == 0:
+            tw[HDC], tw[CSR] = CSR, HDC
+    if ELL in mats and HYB in mats:
+        a, b = mats[ELL].info, mats[HYB].info
+        if b.coo_nnz == 0 and b.ell_width == a.ell_width:
+            tw[HYB], tw[ELL] = ELL, HYB
+    return tw
+
+
+def collapse_label(label: int, twins: dict) -> int:
+    """The lowest id of a format's twin class (the reference's argmin breaks
+    exact ties toward the lowest FormatId, pipeline.cpp:95-104)."""
+    return min(label, twins.get(label, label))
+
+
 def tune_ml(m: DeviceMatrix, forest: DeviceForest, true_diag_ratio=0.2,
             config: ConversionConfig | None = None) -> A.TuneOutcome:
     """tune_ml (tuners.cpp:92-114) fully on the device."""

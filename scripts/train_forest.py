@@ -25,7 +25,8 @@ def load(path):
     with open(path) as f:
         rows = list(csv.DictReader(f))
     X = np.array([[float(r[f"f{k}"]) for k in range(10)] for r in rows])
-    y = np.array([int(r["label"]) for r in rows])
+    key = "label_collapsed" if rows and "label_collapsed" in rows[0] else "label"
+    y = np.array([int(r[key]) for r in rows])
     return rows, X, y
 
 

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 SPMV_TOL = 1e-12  # test_spmv.cpp:59, north star
 EXACT_FORMATS = (1, 2, 3, 5)  # CSR, DIA, ELL, HDC
-COOP_LEN = 32  # matrix.cuh kCoopLen: longer CSR rows are summed by the whole warp (reordered, <= 1e-12)
+COOP_LEN = 64  # matrix.cuh kCoopLen: longer CSR rows are summed by the whole warp (reordered, <= 1e-12)
 
 
 def check_spmv(y, y_ref, fmt, row_len):
