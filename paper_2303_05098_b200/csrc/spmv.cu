@@ -508,7 +508,7 @@ __device__ __forceinline__ void coo_load(const int32_t* __restrict__ row, const 
     }
 }
 
-template <bool ACCUM, bool FILL>
+template <bool ACCUM>
 __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base, int cnt, int64_t z, int64_t nrows,
                                            const int (&r)[kCooItems], const double (&p)[kCooItems], int prev_row,
                                            int next_row, double* __restrict__ y, CooChunkRec* __restrict__ rec) {
@@ -550,7 +550,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
         if (j < nmine) {
             const int rw = r[j];
             if (rw != prv) {
-                if (FILL)  // rows strictly between consecutive entries are empty
+                if (!ACCUM)  // rows strictly between consecutive entries are empty
                     for (int q = prv + 1; q < rw; ++q) y[q] = 0.0;
                 if (j > 0) acc = 0.0;
             }
@@ -572,7 +572,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
                 }
                 rec[chunk].flags = (first_cont ? kFirstCont : 0) | (open ? kLastOpen : 0) |
                                    ((open && orphan) ? kSingle : 0);
-                if (FILL && base + cnt == z)  // trailing empty rows
+                if (!ACCUM && base + cnt == z)  // trailing empty rows
                     for (int64_t q = int64_t(rw) + 1; q < nrows; ++q) y[q] = 0.0;
             }
             prv = rw;
@@ -580,11 +580,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
     }
 }
 
-// FILL: empty rows are zero-filled by the lane that finds them (y written
-// exactly once); without FILL, y was zeroed beforehand (a memset) and only
-// rows holding entries are stored -- matrices with long empty-row runs, and
-// HYB's COO part ahead of the ELL part.
-template <bool ACCUM, bool FILL>
+template <bool ACCUM>
 __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
@@ -619,7 +615,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
         if (nx < nchunks)
             coo_load(row, col, val, nx * kCooChunk + lane * IT, int(min(z - nx * kCooChunk, int64_t(kCooChunk))) - lane * IT,
                      r, c, v);
-        coo_finish<ACCUM, FILL>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
+        coo_finish<ACCUM>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
         if (nx >= nchunks) break;
         chunk = nx;
     }
@@ -749,14 +745,14 @@ __global__ void coo_max_gap(int64_t z, int64_t nrows, const int32_t* __restrict_
 }
 constexpr int64_t kCooGapInline = 4096;  // a lane zero-fills up to ~2 us of rows inline
 
-template <bool ACCUM, bool FILL = !ACCUM>
+template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
     // chunk records, then the fix-up's control word pair and long-run queue
     static_assert(sizeof(LongRun) == sizeof(CooChunkRec) && sizeof(CooChunkRec) >= 16, "record layout");
     DBuf<CooChunkRec> rec(2 * nchunks + 1, s);
     const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
-    coo_warp_kernel<ACCUM, FILL><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
+    coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
                                                 rec.get());
     SOB_LAUNCH("coo_warp_kernel");
     LongRun* runs = reinterpret_cast<LongRun*>(rec.get() + nchunks + 1);
@@ -947,7 +943,7 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
                 SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
             } else if (m.coo.max_gap < 0 || m.coo.max_gap > kCooGapInline) {  // unknown under capture: safe path
                 SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
-                launch_coo<false, false>(m.coo, m.nrows, x, y, s);
+                launch_coo<true>(m.coo, m.nrows, x, y, s);
             } else {
                 launch_coo<false>(m.coo, m.nrows, x, y, s);
             }
@@ -963,19 +959,9 @@ void spmv_device(const so_matrix& m, const double* x, double* y, cudaStream_t s)
             launch_ell<false>(m, x, y, s);
             break;
         case SO_HYB:
-            // y = ELL part + COO part (spmv.cpp:95-100).  The COO part runs
-            // first into a zeroed y (stores only, no read of y: the 3-CTA/SM
-            // kernel), then the ELL kernel adds its row sum: fadd is
-            // commutative, so y[i] = coo_i + ell_i is bit-identical to
-            // ell_i + coo_i, and rows without COO entries get 0 + ell_i = ell_i
-            if (m.coo.nnz > 0) {
-                coo_profile(m.coo, m.nrows, s);
-                SOB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m.nrows), s));
-                launch_coo<false, false>(m.coo, m.nrows, x, y, s);
-                launch_ell<true>(m, x, y, s);
-            } else {
-                launch_ell<false>(m, x, y, s);
-            }
+            coo_profile(m.coo, m.nrows, s);
+            launch_ell<false>(m, x, y, s);
+            if (m.coo.nnz > 0) launch_coo<true>(m.coo, m.nrows, x, y, s);
             break;
         case SO_HDC:
             // one kernel per non-empty part; both parts: the DIA kernel, then

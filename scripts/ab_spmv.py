@@ -7,7 +7,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("AB_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2303_05098_b200 as P  # noqa: E402
 from paper_2303_05098_b200 import synth  # noqa: E402
 

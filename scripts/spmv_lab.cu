@@ -938,6 +938,67 @@ __global__ void __launch_bounds__(256, MINB) gather_probe(int64_t z, const int* 
     if (acc == 1.2345e300) *sink = acc;
 }
 
+// Access-pattern probes (r02): exactly the memory traffic of the product COO
+// and CSR kernels -- the same streams with the same load widths, the same x
+// gathers -- and none of their reductions, at full occupancy.  Their time is
+// the practical floor ("gather-aware bound") for an SpMV that must move these
+// bytes and issue these gathers on this matrix.
+__device__ __forceinline__ void lds_v8(const int* p, int (&v)[8]) {
+    asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "l"(p));
+}
+__device__ __forceinline__ void lds_v4d(const double* p, double* v) {
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) coo_traffic_probe(int64_t z, const int* __restrict__ row,
+                                                               const int* __restrict__ col, const double* __restrict__ val,
+                                                               const double* __restrict__ x, double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nch = z / 256;  // full chunks only (the tail is < 256 entries)
+    double acc = 0.0;
+    int last = 0;
+    for (int64_t ch = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; ch < nch;
+         ch += int64_t(gridDim.x) * (blockDim.x >> 5)) {
+        const int64_t k = ch * 256 + lane * 8;
+        int r[8], c[8];
+        double v[8];
+        lds_v8(row + k, r);
+        lds_v8(col + k, c);
+        lds_v4d(val + k, v);
+        lds_v4d(val + k + 4, v + 4);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += v[j] * __ldg(x + c[j]);
+        last = r[7];
+    }
+    y[last] = acc;  // one store per lane keeps every load alive
+}
+template <int IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) csr_traffic_probe(int64_t z, int64_t n, const int64_t* __restrict__ rp,
+                                                               const int* __restrict__ col, const double* __restrict__ val,
+                                                               const double* __restrict__ x, double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ng = z / (32 * IT);
+    double acc = 0.0;
+    for (int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < ng;
+         g += int64_t(gridDim.x) * (blockDim.x >> 5)) {
+        const int64_t k = g * 32 * IT + lane;
+        int c[IT];
+        double v[IT];
+#pragma unroll
+        for (int u = 0; u < IT; ++u) {
+            c[u] = lds(col + k + 32 * u);
+            v[u] = lds(val + k + 32 * u);
+        }
+        // the row pointers of this group's rows (one 8-byte read per row)
+        const int64_t r = (g * n) / ng + lane;
+        if (r < n) acc += double(lds(reinterpret_cast<const double*>(rp) + r) != 0.0);
+#pragma unroll
+        for (int u = 0; u < IT; ++u) acc += v[u] * __ldg(x + c[u]);
+    }
+    y[(int64_t(blockIdx.x) * blockDim.x + threadIdx.x) % n] = acc;
+}
+
 // DIA, persistent grid-stride over 256-row blocks (tail effect probe)
 template <int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) dia_persist(int n, int nd, const int64_t* __restrict__ offsets,
@@ -1206,6 +1267,24 @@ int main(int argc, char** argv) {
                 report(nm, gbytes, [&] { kern<<<sms * per, 256>>>(z, dcol, dx, sink); }, [] { return std::string(""); });
             }
             cudaFree(sink);
+        }
+        if (getenv("LAB_TRAFFIC")) {  // access-pattern floors of the product COO / CSR kernels
+            std::vector<int> hr(z);
+            for (int64_t i = 0; i < n; ++i) for (int64_t kk = m.rp[i]; kk < m.rp[i + 1]; ++kk) hr[kk] = int(i);
+            int* drow; CK(cudaMalloc(&drow, (z + 64) * 4));
+            CK(cudaMemcpy(drow, hr.data(), z * 4, cudaMemcpyHostToDevice));
+            const double coo_bytes = 16.0 * z + 16.0 * n;
+            for (int mb : {3, 4, 6, 8}) {
+                char nm[80]; snprintf(nm, 80, "coo_traffic_probe B%d (COO bytes)", mb);
+                auto kern = mb == 3 ? coo_traffic_probe<3> : mb == 4 ? coo_traffic_probe<4> : mb == 6 ? coo_traffic_probe<6> : coo_traffic_probe<8>;
+                report(nm, coo_bytes, [&] { kern<<<sms * mb, 256>>>(z, drow, dcol, dval, dx, dy); }, [] { return std::string(""); });
+            }
+            for (int mb : {3, 4, 6}) {
+                char nm[80]; snprintf(nm, 80, "csr_traffic_probe IT12 B%d (CSR bytes)", mb);
+                auto kern = mb == 3 ? csr_traffic_probe<12, 3> : mb == 4 ? csr_traffic_probe<12, 4> : csr_traffic_probe<12, 6>;
+                report(nm, csr_bytes, [&] { kern<<<sms * mb, 256>>>(z, n, drp, dcol, dval, dx, dy); }, [] { return std::string(""); });
+            }
+            cudaFree(drow);
         }
         // --- COO variants
         if (getenv("LAB_COO")) {
