@@ -590,7 +590,7 @@ def other_configs(P, synth, stream, l2, peak):
 # ----------------------------------------------------------- config 4 slice
 
 def held_out_ids(count):
-    with open(os.path.join(REPO, "profiles", "config4_split_r01b.json")) as f:
+    with open(os.path.join(REPO, "profiles", "config4_split_r02.json")) as f:
         ids = json.load(f)["test_ids"]
     return ids[:count]
 
@@ -651,7 +651,7 @@ def summarise_config4(rows, elapsed, world):
     return {
         "matrices": len(rows), "families": {f: int(sum(r["family"] == f for r in rows))
                                             for f in ("stencil", "banded", "uniform", "powerlaw")},
-        "source": "held-out ids of profiles/config4_split_r01b.json (device generators, synth_dev.corpus_spec)",
+        "source": "held-out ids of profiles/config4_split_r02.json (device generators, synth_dev.corpus_spec)",
         "model": "paper_2303_05098_b200/models/b200_forest.txt",
         "accuracy": round(float((ch == lab).mean()), 4),
         "accuracy_twins_collapsed": round(float((ch_c == lab_c).mean()), 4),

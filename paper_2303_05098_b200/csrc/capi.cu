@@ -33,7 +33,6 @@ struct TunePlan {
     so_tune_outcome* out = nullptr;      // pinned, mapped: the predict kernel writes it over the link
     so_tune_outcome* out_dev = nullptr;  // device view of `out`
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
-    cudaEvent_t ready = nullptr;  // orders the replay after the caller's work on the context stream
     // private stream the graph is captured and replayed on: a capture on the
     // shared context stream would swallow other threads' work (and the
     // replay would re-run it); nothing but this plan ever uses it
@@ -54,7 +53,6 @@ void destroy_tune_plan(TunePlan* p) {
     if (p->e0) cudaEventDestroy(p->e0);
     if (p->e1) cudaEventDestroy(p->e1);
     if (p->e2) cudaEventDestroy(p->e2);
-    if (p->ready) cudaEventDestroy(p->ready);
     p->ws.reset();
     if (p->ps) cudaStreamDestroy(p->ps);
     delete p;
@@ -1045,7 +1043,6 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             SOB_CUDA(cudaEventCreate(&np->e0));
             SOB_CUDA(cudaEventCreate(&np->e1));
             SOB_CUDA(cudaEventCreate(&np->e2));
-            SOB_CUDA(cudaEventCreateWithFlags(&np->ready, cudaEventDisableTiming));
             np->ws.reset(new FeatWorkspace(*m, s));
             SOB_CUDA(cudaStreamSynchronize(s));
             cudaStream_t ps = np->ps;
@@ -1071,10 +1068,9 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             plan = np.get();
             m->tune_plan = std::move(np);
         }
-        // after everything the caller queued on the context stream (the
-        // matrix may still be in flight from a conversion)
-        SOB_CUDA(cudaEventRecord(plan->ready, s));
-        SOB_CUDA(cudaStreamWaitEvent(plan->ps, plan->ready, 0));
+        // every call that produces or changes a matrix synchronises before it
+        // returns (make(), conversions), so the matrix arrays are complete:
+        // the replay needs no ordering against the context stream
         SOB_CUDA(cudaGraphLaunch(plan->exec, plan->ps));
         SOB_CUDA(cudaStreamSynchronize(plan->ps));
         so_tune_outcome h = *plan->out;  // written by the predict kernel (mapped host memory)

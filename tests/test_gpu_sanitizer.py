@@ -1,0 +1,36 @@
+"""compute-sanitizer gate: the library's kernels under memcheck
+on small inputs (scripts/sanitize_driver.py --quick: every SpMV kernel, the
+conversions, features incl. both spread walks, predict, the tune graph, the
+halo push / flag wait and so_dist kernels), zero errors required.  The full
+driver under memcheck, racecheck and synccheck (and two-process so_dist under
+memcheck) is logged in profiles/r02_sanitizer_*.log."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    pytest.skip("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_kernels_clean_under_sanitizer(tool):
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "9"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    cmd += [sys.executable, os.path.join(REPO, "scripts", "sanitize_driver.py"), "--quick"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=REPO)
+    tail = (p.stdout + p.stderr)[-3000:]
+    assert p.returncode == 0, tail
+    assert "sanitize driver done" in p.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in p.stdout + p.stderr, tail
