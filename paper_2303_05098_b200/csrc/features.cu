@@ -17,6 +17,7 @@
 // warp walks the chunk summaries, verifying every binade assumption exactly
 // and recursing (32-way) into any chunk where S changes binade.  The result
 // is the reference's double, not an approximation of it.
+#include <cstdlib>
 #include <cfloat>
 #include <memory>
 #include <mutex>
@@ -838,7 +839,8 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
             const int gb = grid_for(c.nblk * kB, kB, 4);
             // a row of more than kBigRowPieces pieces exists only if the pieces
             // outnumber the long rows by at least that much
-            const bool big = c.nlong > 0 && c.npieces - c.nlong >= kBigRowPieces;
+            static const bool no_big = std::getenv("SOB_NO_BIGROW_PIECES") != nullptr;  // diagnostic knob (A/B)
+            const bool big = !no_big && c.nlong > 0 && c.npieces - c.nlong >= kBigRowPieces;
             const int64_t big_row = big ? kBigRowPieces * kPiece : INT64_MAX;
             if (accum) {
                 FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};

@@ -968,10 +968,12 @@ __global__ void __launch_bounds__(256, MINB) coo_traffic_probe(int64_t z, const 
         lds_v4d(val + k, v);
         lds_v4d(val + k + 4, v + 4);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc += v[j] * __ldg(x + c[j]);
-        last = r[7];
+        for (int j = 0; j < 8; ++j) {
+            acc += v[j] * __ldg(x + c[j]);
+            last ^= r[j];  // every row index is consumed
+        }
     }
-    y[last] = acc;  // one store per lane keeps every load alive
+    y[unsigned(last) % unsigned(z)] = acc;  // one store per lane keeps every load alive
 }
 template <int IT, int MINB>
 __global__ void __launch_bounds__(256, MINB) csr_traffic_probe(int64_t z, int64_t n, const int64_t* __restrict__ rp,
