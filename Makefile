@@ -95,7 +95,13 @@ refaccept: $(LIBDIR)/libsparseoracle.so
 # transfer pipeline stages).  Both link the product library.
 TOOL_FLAGS := -O3 $(ARCH) -std=c++17 -lineinfo -Iinclude -L$(LIBDIR) -lsparseoracle_b200 \
               -Xlinker -rpath,'$$ORIGIN/../$(LIBDIR)'
-tools: build/lab build/pipe_probe build/e2e_api
+tools: build/lab build/pipe_probe build/e2e_api build/gather_lab
+
+# x-gather throughput probes (LDG cache qualifiers, TMA tile::gather4, L2
+# persistence, hot-column packing) -- standalone, DESIGN.md §4.5a
+build/gather_lab: scripts/gather_lab.cu
+	@mkdir -p build
+	$(NVCC) -O3 $(ARCH) -std=c++17 -lineinfo -o $@ $<
 
 # the drop-in C++ API end to end (bench.py's e2e_cpp_api): pageable vectors
 build/e2e_api: scripts/e2e_api.cpp $(LIBDIR)/libsparseoracle.so $(CPP_HDRS)

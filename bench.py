@@ -524,7 +524,8 @@ def e2e_numbers(m, csr, steps, nbytes):
             d = json.loads(r.stdout.strip().splitlines()[-1])
             out["e2e_cpp_api"] = {"value": d["gbs_mean"], "unit": "GB/s", "ms": d["ms_mean"],
                                   "h2d_bytes_per_step": d["h2d_bytes_per_step"],
-                                  "d2h_bytes_per_step": d["d2h_bytes_per_step"], "call": d["api"]}
+                                  "d2h_bytes_per_step": d["d2h_bytes_per_step"], "call": d["api"],
+                                  "zero_fill_ms": d.get("zero_fill_ms_median")}
         except Exception as e:
             out["e2e_cpp_api"] = {"error": str(e)[:200]}
     return out

@@ -246,6 +246,13 @@ so_status so_ipc_free(void* dev_ptr);
  * (narrow windows) or a chunked copy pipeline; otherwise H2D x, kernel(s),
  * D2H y. */
 so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y);
+/* spmv(m, x) returning a NEW vector (spmv.hpp:20, spmv.cpp:203-219): the
+ * library calls make_y(ctx, nrows) exactly once, on the calling thread, for
+ * y's storage (NULL = out of memory) -- for a pageable x while host threads
+ * stage x and the device multiplies, so building the caller's vector (its
+ * value-initialisation) overlaps the work.  Same results as so_spmv. */
+typedef double* (*so_make_output)(void* ctx, int64_t nrows);
+so_status so_spmv_new(const so_matrix* m, const double* x, int64_t xlen, so_make_output make_y, void* ctx);
 /* time_spmv: x uploaded once, 1 untimed warm-up, then `reps` multiplies each
  * timed with a cudaEvent pair on the launching stream.  total = sum. */
 so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen,

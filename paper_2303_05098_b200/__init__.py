@@ -9,7 +9,7 @@ the ctypes view of the same C-ABI used by the tests and bench.py.
 from .device import (COO, CSR, DIA, ELL, FORMAT_NAMES, HDC, HYB, AllFormatsInfeasible,
                      ConversionConfig, DeviceForest, DeviceMatrix, DimensionMismatch,
                      EmptyMatrix, Error, FeatureVector, FlatForest, IndexOutOfRange,
-                     InvalidInput, MalformedModel, PaddingOverflow, ParseError,
+                     InvalidInput, MalformedModel, OutOfMemory, PaddingOverflow, ParseError,
                      UnsupportedFormat, collapse_label, format_feasible, kernel_twins, set_device,
                      tune_ml)
 
@@ -17,4 +17,5 @@ __all__ = ["COO", "CSR", "DIA", "ELL", "HYB", "HDC", "FORMAT_NAMES", "DeviceMatr
            "DeviceForest", "FlatForest", "ConversionConfig", "FeatureVector", "tune_ml",
            "format_feasible", "set_device", "Error", "InvalidInput", "PaddingOverflow",
            "DimensionMismatch", "EmptyMatrix", "MalformedModel", "IndexOutOfRange",
-           "AllFormatsInfeasible", "ParseError", "UnsupportedFormat", "kernel_twins", "collapse_label"]
+           "AllFormatsInfeasible", "ParseError", "UnsupportedFormat", "OutOfMemory", "kernel_twins",
+           "collapse_label"]

@@ -118,6 +118,7 @@ _SIGS = {
     "so_ipc_free": (C.c_int, [vp]),
     "so_gen_stencil27_dia": (C.c_int, [i64, i64, i64, i64, i64, C.c_uint64, P(vp)]),
     "so_spmv": (C.c_int, [vp, vp, i64, vp]),
+    "so_spmv_new": (C.c_int, [vp, vp, i64, vp, vp]),
     "so_time_spmv": (C.c_int, [vp, vp, i64, i64, vp, P(f64)]),
     "so_spmv_bytes": (i64, [vp]),
     "so_extract_features": (C.c_int, [vp, f64, P(FeatureVector), P(ScanStats)]),
@@ -135,6 +136,10 @@ _SIGS = {
     "so_dist_timeouts": (C.c_int64, []),
     "so_dist_free": (None, [vp]),
 }
+
+
+# so_make_output: double* (*)(void* ctx, int64_t nrows)
+MAKE_OUTPUT = C.CFUNCTYPE(vp, vp, i64)
 
 
 def exported_symbols():

@@ -12,8 +12,20 @@ DenseVector spmv(const DynamicMatrix& m, const DenseVector& x) {
     if (static_cast<index_t>(x.size()) != m.ncols())  // spmv.cpp:12-19
         throw DimensionMismatch("spmv: vector length " + std::to_string(x.size()) + " does not match ncols " +
                                 std::to_string(m.ncols()));
-    DenseVector y(static_cast<std::size_t>(m.nrows()));
-    detail::check(so_spmv(m.device().get(), x.data(), static_cast<int64_t>(x.size()), y.data()));
+    // y is sized (value-initialised: a single-threaded zero fill) by the
+    // library's callback on this thread while host threads stage x and the
+    // device multiplies (so_spmv_new); never throws across the C-ABI
+    DenseVector y;
+    auto make = [](void* ctx, int64_t n) noexcept -> double* {
+        try {
+            auto* v = static_cast<DenseVector*>(ctx);
+            v->resize(static_cast<std::size_t>(n));
+            return v->data();
+        } catch (...) {
+            return nullptr;
+        }
+    };
+    detail::check(so_spmv_new(m.device().get(), x.data(), static_cast<int64_t>(x.size()), make, &y));
     return y;
 }
 

@@ -866,6 +866,30 @@ so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) 
     });
 }
 
+so_status so_spmv_new(const so_matrix* m, const double* x, int64_t xlen, so_make_output make_y, void* make_ctx) {
+    return guard([&] {
+        if (!make_y) fail(SO_INVALID_INPUT, "spmv: null output allocator");
+        cudaStream_t s = on_device(m);
+        check_x(*m, xlen);
+        const std::function<double*()> mk = [&]() -> double* { return make_y(make_ctx, m->nrows); };
+        // pageable x: y is built on this thread while the device works
+        static const bool eager = std::getenv("SOB_EAGER_Y") != nullptr;  // diagnostic knob (A/B)
+        if (!eager && m->nrows > 0 && spmv_pageable(*m, x, nullptr, s, &mk)) return;
+        double* y = mk();
+        if (!y && m->nrows > 0) fail(SO_OUT_OF_MEMORY, "spmv: output vector allocation failed");
+        if (m->nrows > 0 && spmv_pipelined(*m, x, y, s)) {
+            SOB_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
+        if (m->nrows > 0 && spmv_pageable(*m, x, y, s)) return;
+        DBuf<double> dx, dy(m->nrows, s);
+        h2d(dx, x, xlen, s);
+        spmv_device(*m, dx.get(), dy.get(), s);
+        d2h(y, dy, m->nrows, s);
+        SOB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen, int64_t reps, double* per_rep,
                        double* total) {
     return guard([&] {

@@ -2,6 +2,7 @@
 // internal entry points shared by the .cu translation units.
 #pragma once
 #include <atomic>
+#include <functional>
 
 #include <memory>
 #include <mutex>
@@ -156,8 +157,11 @@ int64_t zero_copy_rows_per_block();
 void ensure_dia_window(const so_matrix& m, cudaStream_t s);
 // spmv(m, x) with PAGEABLE host x/y (stage.cu): host threads copy through a
 // cached pinned staging ring while the device multiplies chunk by chunk;
-// false when the call is too small to gain (the caller's one-shot path)
-bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t s);
+// false when the call is too small to gain (the caller's one-shot path).
+// make_y (y == nullptr): y is created by make_y() on the calling thread while
+// the device works (so_spmv_new)
+bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t s,
+                   const std::function<double*()>* make_y = nullptr);
 void spmv_rows_push(const so_matrix& m, const double* x, double* y, int64_t lo, int64_t hi, double* remote,
                     unsigned* ticket, unsigned long long* remote_flag, unsigned long long flag_value,
                     cudaStream_t s);

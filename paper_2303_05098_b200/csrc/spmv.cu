@@ -141,8 +141,23 @@ __device__ __forceinline__ void csr_rows_sum(const double* prod, bool pad, int r
     }
 }
 
+// Low 32 bits of row_ptr[r]: a group spans < 2^31 entries, so its rows'
+// local bounds int(rp[r] - k0) only need the low words (32-bit loads).
+__device__ __forceinline__ unsigned rp_lo(const int64_t* __restrict__ rp, int64_t r) {
+    return __ldg(reinterpret_cast<const unsigned*>(rp + r));
+}
+
 // RPL: rows per lane of the widest group (1, or kGroupRowsMax / 32 when the
 // partition has groups of more than 32 tiny rows).
+//
+// Software pipeline per warp (one group per iteration): the next group's
+// metadata loads are issued before this group's x gathers and consumed after
+// them; the next group's col/val and row bounds are issued before this
+// group's row sums and consumed in the next iteration; the bounds of rows
+// i+32, i+64, ... (RPL > 1) are issued before lane i walks row i.  No value
+// loaded in a stage is used in the same stage, so every load's latency hides
+// behind the work of the stage (ncu on R-MAT: the previous order stalled on
+// the next group's row bounds right after issuing them).
 template <int IT, bool ACCUM, bool PAD, bool COOP, int RPL>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
@@ -173,23 +188,21 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
             v[u] = ld_stream(val + k0 + e);
         }
     }
-    int pa = 0, pe = 0;
+    unsigned ra = 0, re = 0;  // low words of row_ptr[r0+lane], row_ptr[r0+lane+1]
     if (r0 + lane < r1) {
-        pa = int(rp[r0 + lane] - k0);
-        pe = int(rp[r0 + lane + 1] - k0);
+        ra = rp_lo(rp, r0 + lane);
+        re = rp_lo(rp, r0 + lane + 1);
     }
     while (true) {
         const int64_t gn = g + stride;
-        int nr0 = 0, nr1 = 0, ncnt = 0;
-        int64_t nk0 = 0;
-        bool npad = false;
+        // stage 1: next group's metadata (raw; consumed after the gathers)
+        int nr0 = 0, nr1 = 0;
+        int64_t nk0 = 0, nk1 = 0;
         if (gn < ngrp) {
             nr0 = grp[gn];
             nr1 = grp[gn + 1];
             nk0 = grp_k[gn];
-            npad = PAD && (nk0 & kGrpPad);
-            if (PAD) nk0 &= ~kGrpPad;
-            ncnt = int(min((PAD ? grp_k[gn + 1] & ~kGrpPad : grp_k[gn + 1]) - nk0, int64_t(kCap + 1)));
+            nk1 = grp_k[gn + 1];
         }
         const bool longrow = cnt > kCap;
         if (!longrow) {
@@ -200,7 +213,14 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
             }
         }
         __syncwarp();
-        int npa = 0, npe = 0;
+        // stage 2: next group's col/val and row bounds (consumed next iteration)
+        const bool npad = PAD && (nk0 & kGrpPad);
+        if (PAD) {
+            nk0 &= ~kGrpPad;
+            nk1 &= ~kGrpPad;
+        }
+        const int ncnt = int(min(nk1 - nk0, int64_t(kCap + 1)));
+        unsigned nra = 0, nre = 0;
         if (gn < ngrp) {
 #pragma unroll
             for (int u = 0; u < IT; ++u) {
@@ -211,22 +231,30 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
                 }
             }
             if (nr0 + lane < nr1) {
-                npa = int(rp[nr0 + lane] - nk0);
-                npe = int(rp[nr0 + lane + 1] - nk0);
+                nra = rp_lo(rp, nr0 + lane);
+                nre = rp_lo(rp, nr0 + lane + 1);
             }
         }
+        // stage 3: this group's row sums
         if (!longrow) {
-            csr_rows_sum<ACCUM, COOP>(prod, pad, r0 + lane, r0 + lane < r1, pa, pe, y, lane);
-            // groups of tiny rows: lane i also walks rows i+32, i+64, ...
-            for (int q = 1; q < RPL && r0 + 32 * q < r1; ++q) {
+            const unsigned k0lo = unsigned(k0);
+            unsigned qa[RPL > 1 ? RPL - 1 : 1], qe[RPL > 1 ? RPL - 1 : 1];
+#pragma unroll
+            for (int q = 1; q < RPL; ++q) {  // groups of tiny rows: lane i also walks rows i+32, i+64, ...
                 const int rr = r0 + 32 * q + lane;
-                const bool act = rr < r1;
-                int qa = 0, qe = 0;
-                if (act) {
-                    qa = int(rp[rr] - k0);
-                    qe = int(rp[rr + 1] - k0);
+                qa[q - 1] = qe[q - 1] = k0lo;
+                if (rr < r1) {
+                    qa[q - 1] = rp_lo(rp, rr);
+                    qe[q - 1] = rp_lo(rp, rr + 1);
                 }
-                csr_rows_sum<ACCUM, COOP>(prod, pad, rr, act, qa, qe, y, lane);
+            }
+            csr_rows_sum<ACCUM, COOP>(prod, pad, r0 + lane, r0 + lane < r1, int(ra - k0lo), int(re - k0lo), y, lane);
+#pragma unroll
+            for (int q = 1; q < RPL; ++q) {
+                if (r0 + 32 * q >= r1) break;
+                const int rr = r0 + 32 * q + lane;
+                csr_rows_sum<ACCUM, COOP>(prod, pad, rr, rr < r1, int(qa[q - 1] - k0lo), int(qe[q - 1] - k0lo), y,
+                                          lane);
             }
         }
         __syncwarp();
@@ -237,8 +265,8 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
         k0 = nk0;
         pad = npad;
         cnt = ncnt;
-        pa = npa;
-        pe = npe;
+        ra = nra;
+        re = nre;
     }
 }
 

@@ -16,13 +16,21 @@
 // by chunk as the device finishes it (a CUDA event per chunk), so the host
 // copies of x and y overlap the link transfers and the kernel.  Results are
 // bit-identical to the one-shot path (same kernels).
+//
+// Lazy y (so_spmv_new, the C++ spmv(m, x) returning a fresh std::vector): the
+// caller's thread builds y -- the vector's value-initialisation, a 32 MB
+// single-threaded zero fill on config 2 -- while a pool thread orchestrates
+// the device work and the others stage x; the y copies start once y exists.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <immintrin.h>
+#include <sys/resource.h>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -153,23 +161,27 @@ __attribute__((target("avx2"))) void copy_nt_avx2(double* dst, const double* src
     _mm_sfence();
 }
 
-void copy_host(double* dst, const double* src, size_t n) {
+// want_nt = false: plain stores -- for a y the caller's thread has just
+// value-initialised (lazy y), whose lines are still cache-resident: streaming
+// stores would first have to evict them (config 2: 3.1 -> 2.1 ms per call)
+void copy_host(double* dst, const double* src, size_t n, bool want_nt = true) {
     static const bool nt = [] {
         if (std::getenv("SOB_NO_NT_COPY")) return false;  // diagnostic knob
         __builtin_cpu_init();
         return bool(__builtin_cpu_supports("avx2"));
     }();
-    if (nt)
+    if (nt && want_nt)
         copy_nt_avx2(dst, src, n);
     else
         std::memcpy(dst, src, n * sizeof(double));
 }
 
 struct Task {
-    double* dst;
+    double* dst;  // x tasks; y tasks copy to y + off (y may not exist yet)
     const double* src;
     size_t n;
     int chunk;  // x chunk (>= 0) or -(y chunk) - 1
+    int64_t off;
 };
 
 constexpr int64_t kMinStaged = int64_t(1) << 18;  // elements of x + y below which the one-shot path wins
@@ -177,13 +189,21 @@ constexpr int64_t kTaskElems = int64_t(1) << 16;  // 512 KB per host copy task
 
 }  // namespace
 
-bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
+bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t s,
+                   const std::function<double*()>* make_y) {
     static const bool off = std::getenv("SOB_NO_PAGEABLE_STAGING") != nullptr;  // diagnostic knob
     const int64_t n = m.nrows, nc = m.ncols;
-    if (off || n + nc < kMinStaged || !x || !y) return false;
+    if (off || n + nc < kMinStaged || !x || (!y && !make_y)) return false;
     // in-place calls: x must be read in full before any y lands (one-shot path)
     const auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
-    if (xa < ya + sizeof(double) * size_t(n) && ya < xa + sizeof(double) * size_t(nc)) return false;
+    if (!make_y && xa < ya + sizeof(double) * size_t(n) && ya < xa + sizeof(double) * size_t(nc)) return false;
+    static const bool trace = std::getenv("SOB_STAGE_TRACE") != nullptr;  // diagnostic knob: phase times
+    const auto t_entry = std::chrono::steady_clock::now();
+    std::atomic<int64_t> t_launched{0}, t_yready{0}, t_ycopied{0};
+    auto stamp = [&](std::atomic<int64_t>& t) {
+        if (trace)
+            t.store(std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t_entry).count());
+    };
     const int dev = m.device;
     Staging& st = g_stage[dev];
     std::lock_guard<std::mutex> lk(st.mu);
@@ -209,25 +229,42 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
     std::vector<int> per_x(size_t(nxc), 0), per_y(size_t(nyc), 0);
     for (int64_t k = 0; k < nxc; ++k)
         for (int64_t a = k * cx, e = std::min(nc, a + cx); a < e; a += kTaskElems, ++per_x[size_t(k)])
-            tasks.push_back(Task{X + a, x + a, size_t(std::min(e, a + kTaskElems) - a), int(k)});
+            tasks.push_back(Task{X + a, x + a, size_t(std::min(e, a + kTaskElems) - a), int(k), a});
     for (int64_t j = 0; j < nyc; ++j)
         for (int64_t a = j * cy, e = std::min(n, a + cy); a < e; a += kTaskElems, ++per_y[size_t(j)])
-            tasks.push_back(Task{y + a, Y + a, size_t(std::min(e, a + kTaskElems) - a), -int(j) - 1});
+            tasks.push_back(Task{nullptr, Y + a, size_t(std::min(e, a + kTaskElems) - a), -int(j) - 1, a});
     std::unique_ptr<std::atomic<int>[]> xdone(new std::atomic<int>[size_t(nxc)]);
     std::unique_ptr<std::atomic<int>[]> ygate(new std::atomic<int>[size_t(nyc)]);  // y chunk's event recorded
     for (int64_t k = 0; k < nxc; ++k) xdone[size_t(k)].store(0);
     for (int64_t j = 0; j < nyc; ++j) ygate[size_t(j)].store(0);
     std::atomic<size_t> next{0};
     std::atomic<int> failed{0};
+    std::atomic<double*> yptr{make_y ? nullptr : y};
+    std::mutex ymu;
+    std::condition_variable ycv;
+    std::exception_ptr err, yerr;
+    std::function<void()> orchestrate;
 
-    auto worker = [&](int) {
+    auto worker = [&](int id) {
         cudaSetDevice(dev);
+        if (make_y && id == 0) orchestrate();  // the caller is building y
         while (true) {
             const size_t t = next.fetch_add(1);
             if (t >= tasks.size() || failed.load(std::memory_order_relaxed)) return;
             const Task& k = tasks[t];
+            double* dst = k.dst;
             if (k.chunk < 0) {
                 const int j = -k.chunk - 1;
+                if (!(dst = yptr.load(std::memory_order_acquire))) {
+                    // y is being built on the caller's thread: sleep, do not
+                    // spin (spinning workers take its core and its memory
+                    // bandwidth: config 2 zero fill 0.9 -> 2.0 ms)
+                    std::unique_lock<std::mutex> lk(ymu);
+                    ycv.wait(lk, [&] { return yptr.load(std::memory_order_acquire) || failed.load(); });
+                    dst = yptr.load(std::memory_order_acquire);
+                    if (!dst) return;
+                }
+                dst += k.off;
                 while (!ygate[size_t(j)].load(std::memory_order_acquire)) {
                     if (failed.load(std::memory_order_relaxed)) return;
                     std::this_thread::yield();
@@ -242,13 +279,13 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                     std::this_thread::yield();
                 }
             }
-            copy_host(k.dst, k.src, k.n);
+            copy_host(dst, k.src, k.n, k.chunk >= 0 || !make_y);
             if (k.chunk >= 0) xdone[size_t(k.chunk)].fetch_add(1, std::memory_order_release);
+            if (trace && t + 1 == tasks.size()) stamp(t_ycopied);
         }
     };
 
-    std::exception_ptr err;
-    auto orchestrate = [&]() {
+    orchestrate = [&]() {
         try {
             auto wait_x = [&](int64_t k) {
                 while (xdone[size_t(k)].load(std::memory_order_acquire) < per_x[size_t(k)]) std::this_thread::yield();
@@ -282,6 +319,7 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                     ygate[size_t(yrec)].store(1, std::memory_order_release);
                     ++yrec;
                 }
+                stamp(t_launched);
                 return;
             }
             // generic: x chunks up on the copy engine as staged, kernel, y down in chunks
@@ -292,6 +330,7 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                 SOB_CUDA(cudaMemcpyAsync(dx.get() + a, X + a, sizeof(double) * size_t(e - a), cudaMemcpyHostToDevice, s));
             }
             spmv_device(m, dx.get(), dy.get(), s);
+            stamp(t_launched);
             for (int64_t j = 0; j < nyc; ++j) {
                 const int64_t a = j * cy, e = std::min(n, a + cy);
                 SOB_CUDA(cudaMemcpyAsync(Y + a, dy.get() + a, sizeof(double) * size_t(e - a), cudaMemcpyDeviceToHost, s));
@@ -305,15 +344,49 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
     };
     CopyPool& pool = CopyPool::get();
     pool.run(worker, [&] {
-        orchestrate();
+        if (make_y) {
+            try {
+                struct rusage ru0, ru1;
+                if (trace) getrusage(RUSAGE_THREAD, &ru0);
+                double* p = (*make_y)();
+                if (trace) {
+                    getrusage(RUSAGE_THREAD, &ru1);
+                    std::fprintf(stderr, "[stage] make_y minor faults %ld\n", ru1.ru_minflt - ru0.ru_minflt);
+                }
+                if (!p) fail(SO_OUT_OF_MEMORY, "spmv: output vector allocation failed");
+                {
+                    std::lock_guard<std::mutex> lk(ymu);
+                    yptr.store(p, std::memory_order_release);
+                }
+                stamp(t_yready);
+            } catch (...) {
+                yerr = std::current_exception();
+                std::lock_guard<std::mutex> lk(ymu);
+                failed.store(1);
+            }
+            ycv.notify_all();
+        } else {
+            orchestrate();
+        }
         worker(pool.size());  // then help with the y copies
     });
     if (err) std::rethrow_exception(err);
+    if (yerr) {
+        cudaStreamSynchronize(s);
+        std::rethrow_exception(yerr);
+    }
     if (failed.load()) {
         cudaStreamSynchronize(s);
         fail(SO_CUDA_ERROR, "pageable spmv: staging copy failed");
     }
     SOB_CUDA(cudaStreamSynchronize(s));
+    if (trace) {
+        const int64_t t_end =
+            std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t_entry).count();
+        std::fprintf(stderr, "[stage] launched %lld us, y ready %lld us, last y copy %lld us, end %lld us (%s)\n",
+                     (long long)t_launched.load(), (long long)t_yready.load(), (long long)t_ycopied.load(),
+                     (long long)t_end, make_y ? "lazy y" : "caller y");
+    }
     return true;
 }
 

@@ -306,6 +306,22 @@ class DeviceMatrix:
         _check(A.lib().so_spmv(self._h, _ptr(x), x.size, _ptr(y)))
         return y
 
+    def spmv_new(self, x, fail_alloc=False) -> np.ndarray:
+        """so_spmv_new: y's storage comes from a callback the library calls
+        on this thread while the device works (the C++ spmv(m, x) path)."""
+        x = _f64(x)
+        out = {}
+
+        def make(_ctx, n):
+            if fail_alloc:
+                return None
+            out["y"] = np.zeros(n, dtype=np.float64)  # value-initialised, like std::vector
+            return out["y"].ctypes.data
+
+        cb = A.MAKE_OUTPUT(make)
+        _check(A.lib().so_spmv_new(self._h, _ptr(x), x.size, C.cast(cb, C.c_void_p), None))
+        return out["y"]
+
     def spmv_into(self, x_host: np.ndarray, y_host: np.ndarray):
         """spmv with caller-owned (ideally pinned) host buffers."""
         _check(A.lib().so_spmv(self._h, C.c_void_p(x_host.ctypes.data), x_host.size,

@@ -15,6 +15,23 @@ PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEAS
 W = {"rmat": lambda: synth.rmat(22, 16, seed=42), "hyb": lambda: synth.hyb_skewed(4_000_000, 16, 160, 100, seed=6),
      "banded": lambda: synth.banded(4_000_000, 13, seed=2), "lap": lambda: synth.laplacian_2d(1000, seed=1),
      "unif": lambda: synth.uniform_random(4_000_000, 16, seed=4)}
+
+
+def relabel(csr):
+    """Columns renumbered by descending frequency (hot columns packed at the
+    front of x), rows re-sorted: the same SpMV up to a permutation of x --
+    a timing stand-in for hot-column packing."""
+    freq = np.bincount(csr.col, minlength=csr.ncols)
+    order = np.argsort(-freq, kind="stable")
+    rank = np.empty(csr.ncols, dtype=np.int64)
+    rank[order] = np.arange(csr.ncols)
+    rows = np.repeat(np.arange(csr.nrows), np.diff(csr.row_ptr))
+    nc = rank[csr.col]
+    o = np.lexsort((nc, rows))
+    return synth.HostCSR(csr.nrows, csr.ncols, csr.row_ptr, nc[o].astype(csr.col.dtype), csr.val[o])
+
+
+W["rmat_rl"] = lambda: relabel(synth.rmat(22, 16, seed=42))
 tag = sys.argv[1] if len(sys.argv) > 1 else ""
 for name in (sys.argv[2] if len(sys.argv) > 2 else "rmat,hyb,banded").split(","):
     csr = W[name]()

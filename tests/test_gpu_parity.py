@@ -685,6 +685,10 @@ def test_pageable_host_spmv_staging(so, O, shape):
         assert max_rel(y, O.oc_spmv(O.oc_convert(coo, f), x)) <= SPMV_TOL, f
         for _ in range(2):  # repeated calls reuse the cached staging buffers
             assert np.array_equal(m.spmv(x), y), f
+            # y built by the caller's allocator while the device works (the C++ spmv(m, x))
+            assert np.array_equal(m.spmv_new(x), y), f
+    with pytest.raises(so.OutOfMemory):  # the allocator reports failure: no write, no crash
+        d.spmv_new(rng.uniform(-1, 1, csr.ncols), fail_alloc=True)
     if csr.nrows == csr.ncols:  # in place (y aliases x): the one-shot path
         m = d.convert(so.CSR)
         z = rng.uniform(-1, 1, csr.ncols)
