@@ -95,7 +95,12 @@ refaccept: $(LIBDIR)/libsparseoracle.so
 # transfer pipeline stages).  Both link the product library.
 TOOL_FLAGS := -O3 $(ARCH) -std=c++17 -lineinfo -Iinclude -L$(LIBDIR) -lsparseoracle_b200 \
               -Xlinker -rpath,'$$ORIGIN/../$(LIBDIR)'
-tools: build/lab build/pipe_probe build/e2e_api build/gather_lab
+tools: build/lab build/pipe_probe build/e2e_api build/gather_lab build/stream_lab
+
+# size-matched streaming floor (cold read of B bytes + write of W bytes)
+build/stream_lab: scripts/stream_lab.cu
+	@mkdir -p build
+	$(NVCC) -O3 $(ARCH) -std=c++17 -lineinfo -o $@ $<
 
 # x-gather throughput probes (LDG cache qualifiers, TMA tile::gather4, L2
 # persistence, hot-column packing) -- standalone, DESIGN.md §4.5a
