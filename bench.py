@@ -716,13 +716,33 @@ def config5_single(P, stream, peak, iters=10):
         torch.cuda.synchronize()
         sec = e0.elapsed_time(e1) * 1e-3 / iters
         nbytes = m.spmv_bytes
+        # the N>1 lines' checksum protocol: x0 reloaded, CHECK_ITERS multiplies
+        from paper_2303_05098_b200 import dist as D
+        xa.copy_(config5_x0(0, n))
+        for k in range(CHECK_ITERS):
+            src, dst = (xa, xb) if k % 2 == 0 else (xb, xa)
+            m.spmv_device(src.data_ptr(), dst.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        out = xa if CHECK_ITERS % 2 == 0 else xb
+        csum = D.owned_checksum(out, D.partition(n, g * g + g + 1, 0, 1))
         del m, xa, xb
         torch.cuda.empty_cache()
         return {"config": config5_config(1), "iters": iters, "ms_per_iter": round(sec * 1e3, 4),
                 "value": round(nbytes / sec / 1e9, 1), "unit": "GB/s", "frac": round(nbytes / sec / 1e9 / peak, 4),
-                "algorithmic_bytes": nbytes}
+                "algorithmic_bytes": nbytes, "checksum": csum,
+                "checksum_protocol": CHECKSUM_PROTOCOL}
     except Exception as e:
         return {"error": str(e)[:300]}
+
+
+CHECK_ITERS = 4
+CHECKSUM_PROTOCOL = (f"x0[i] = 1 + (i % 7) / 8, {CHECK_ITERS} iterations of x <- A x, "
+                     "sum_i (2i+1) * bits(x_i) mod 2^64 (dist.owned_checksum): identical at every N")
+
+
+def config5_x0(lo, hi):
+    import torch
+    return 1.0 + (torch.arange(lo, hi, dtype=torch.int64, device="cuda") % 7).double() / 8.0
 
 
 def run_partitioned(args, world, rank, dev):
@@ -743,7 +763,7 @@ def run_partitioned(args, world, rank, dev):
     m = P.DeviceMatrix.stencil27(g, s.r0, s.r1, s.w0, s.w1, seed=5)
     nbytes_local = m.spmv_bytes
     it = D.make_iterator(s, m, dist, args.exchange, stream)
-    it.load_x(lambda lo, hi: 1.0 + (torch.arange(lo, hi, dtype=torch.int64, device="cuda") % 7).double() / 8.0)
+    it.load_x(config5_x0)
     torch.cuda.synchronize()
     dist.barrier()
     it.run(max(args.warmup, 3))
@@ -767,6 +787,14 @@ def run_partitioned(args, world, rank, dev):
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
     sec, nbytes = float(tmax[0]), float(tsum[1])
+    # checksum protocol shared with config5_n1 (N = 1): x0 reloaded on every
+    # rank while all GPUs are idle, CHECK_ITERS iterations, then the checksum
+    dist.barrier()
+    it.load_x(config5_x0)
+    torch.cuda.synchronize()
+    dist.barrier()
+    it.run(CHECK_ITERS)
+    torch.cuda.synchronize()
     csum = it.checksum()
     dist.barrier()
     it.close()
@@ -783,8 +811,8 @@ def run_partitioned(args, world, rank, dev):
                              "frac": round(value / world / peak, 4), "traffic": None,
                              "algorithmic_bytes": nbytes, "kernel": "dia_kernel (+ dia_push_kernel halo rows)",
                              "peak_kind": peak_kind, "per": "GPU"},
-                "exchange": args.exchange, "halo_wait_timeouts": int(tsum[2]),
-                "checksum": csum, "gpu_launches": launches, "clocks": clk,
+                "exchange": it.exchange, "exchange_fallback": it.fallback, "halo_wait_timeouts": int(tsum[2]),
+                "checksum": csum, "checksum_protocol": CHECKSUM_PROTOCOL, "gpu_launches": launches, "clocks": clk,
                 "e2e": {"value": round(value, 2), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                         "note": "iterated: x stays in HBM between steps by construction"},
                 "config4_shard": cfg4}

@@ -125,6 +125,10 @@ def lpt_shard(weights, world: int, rank: int):
 HALO, ALLGATHER = 0, 1  # SO_DIST_HALO, SO_DIST_ALLGATHER
 
 
+class DistSetupError(RuntimeError):
+    """so_dist setup failed on at least one rank (raised on every rank)."""
+
+
 def row_starts(n: int, world: int):
     """The partition of `partition` as the row_starts array of so_dist_create."""
     return [n * q // world for q in range(world + 1)]
@@ -136,7 +140,13 @@ class DistIteration:
     kernels over peer memory (HALO: boundary rows pushed into the neighbours'
     windows by the multiply; ALLGATHER: new rows stored into every peer's x),
     no collective on the data path.  The IPC handles travel once through
-    `all_gather_object` (any torch.distributed backend)."""
+    `all_gather_object` (any torch.distributed backend).
+
+    Setup is collective-safe: every rank reaches both `all_gather_object`
+    calls whatever fails locally (create, handle export, peer mapping), and a
+    failure on ANY rank raises `DistSetupError` on EVERY rank (after freeing
+    what was built), so callers can fall back together instead of one rank
+    hanging in a collective the others never enter."""
 
     def __init__(self, m, kind, rank, world, starts, halo, all_gather_object):
         import ctypes as C
@@ -144,17 +154,35 @@ class DistIteration:
         from . import _capi as A
         self._lib = A.lib()
         self._C = C
+        self._h = None
         self.m = m  # the so_dist borrows the matrix: keep it alive
         st = (C.c_int64 * (world + 1))(*starts)
-        h = C.c_void_p()
-        self._check(self._lib.so_dist_create(m._h, kind, rank, world, st, int(halo), C.byref(h)))
-        self._h = h
+        err = None
         mine = C.create_string_buffer(64)
-        self._check(self._lib.so_dist_handle(self._h, mine))
+        try:
+            h = C.c_void_p()
+            self._check(self._lib.so_dist_create(m._h, kind, rank, world, st, int(halo), C.byref(h)))
+            self._h = h
+            self._check(self._lib.so_dist_handle(self._h, mine))
+        except RuntimeError as e:
+            err = f"rank {rank}: {e}"
         infos = [None] * world
-        all_gather_object(infos, mine.raw)
-        arr = C.create_string_buffer(b"".join(infos), 64 * world)
-        self._check(self._lib.so_dist_connect(self._h, arr))
+        all_gather_object(infos, None if err else mine.raw)
+        bad = [i for i, v in enumerate(infos) if v is None]
+        if not err and bad:
+            err = f"rank(s) {bad} could not export their x block"
+        if not err:
+            arr = C.create_string_buffer(b"".join(infos), 64 * world)
+            try:
+                self._check(self._lib.so_dist_connect(self._h, arr))
+            except RuntimeError as e:
+                err = f"rank {rank}: {e}"
+        errs = [None] * world
+        all_gather_object(errs, err)
+        errs = [e for e in errs if e]
+        if errs:
+            self.close()
+            raise DistSetupError("; ".join(errs))
 
     def _check(self, st):
         if st != 0:
@@ -198,7 +226,8 @@ class _NativeIterator:
         self.it = DistIteration(m, HALO, s.rank, s.world, row_starts(s.n, s.world), s.h, dist.all_gather_object)
 
     def load_x(self, fn):
-        self.it.tensor(0).copy_(fn(self.s.w0, self.s.w1))
+        # the buffer the next iteration reads (halo cells included)
+        self.it.tensor(-1).copy_(fn(self.s.w0, self.s.w1))
 
     def run(self, iters):
         self.it.iterate(iters, self.stream.cuda_stream)
@@ -275,7 +304,19 @@ def owned_checksum(owned, s: Slice):
 
 def make_iterator(s: Slice, m, dist, exchange, stream):
     """The config-5 iteration for bench.py: 'p2p' -> the native fused-halo
-    so_dist iteration, 'nccl' -> NCCL point-to-point halos."""
+    so_dist iteration, 'nccl' -> NCCL point-to-point halos.  If the peer
+    mapping cannot be set up on some rank (no peer access between the
+    devices, IPC refused), every rank falls back to NCCL together; the
+    returned iterator's `exchange` / `fallback` say what ran and why."""
     if exchange == "p2p":
-        return _NativeIterator(s, m, dist, stream)
-    return _NcclIterator(s, m, dist, stream)
+        try:
+            it = _NativeIterator(s, m, dist, stream)
+            it.exchange, it.fallback = "p2p", None
+            return it
+        except DistSetupError as e:
+            it = _NcclIterator(s, m, dist, stream)
+            it.exchange, it.fallback = "nccl", f"p2p setup failed: {e}"[:300]
+            return it
+    it = _NcclIterator(s, m, dist, stream)
+    it.exchange, it.fallback = "nccl", None
+    return it

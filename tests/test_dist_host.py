@@ -157,3 +157,79 @@ def test_batch_sharding_covers_every_matrix_once(world):
     assert flat == list(range(len(weights)))
     loads = [sum(weights[i] for i in shards[r]) for r in range(world)]
     assert max(loads) <= 4 / 3 * max(sum(weights) / world, max(weights)) + 1e-6
+
+
+class _StubDistLib:
+    """so_dist_* stand-in: create/handle succeed except on `fail_rank`, where
+    the step named by `fail_at` returns an error (as a rank whose GPU cannot
+    map its peers would)."""
+
+    def __init__(self, rank, fail_rank, fail_at):
+        self.rank, self.fail_rank, self.fail_at = rank, fail_rank, fail_at
+        self.freed = 0
+
+    def _st(self, step):
+        return 7 if (self.rank == self.fail_rank and step == self.fail_at) else 0
+
+    def so_dist_create(self, m, kind, rank, world, st, halo, out):
+        out._obj.value = 1234
+        return self._st("create")
+
+    def so_dist_handle(self, h, buf):
+        buf.raw = bytes([self.rank]) * 64
+        return self._st("handle")
+
+    def so_dist_connect(self, h, arr):
+        return self._st("connect")
+
+    def so_last_error(self):
+        return f"stub failure on rank {self.rank}".encode()
+
+    def so_dist_free(self, h):
+        self.freed += 1
+
+
+def _setup_fail_worker(rank, world, port, fail_rank, fail_at, q):
+    from unittest import mock
+
+    from paper_2303_05098_b200 import _capi
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    lib = _StubDistLib(rank, fail_rank, fail_at)
+
+    class _M:
+        _h = None
+    with mock.patch.object(_capi, "lib", lambda: lib):
+        try:
+            D.DistIteration(_M(), D.HALO, rank, world, D.row_starts(60, world), 2, dist.all_gather_object)
+            outcome = "ok"
+        except D.DistSetupError as e:
+            outcome = str(e)
+    dist.barrier()  # every rank got here: nobody is stuck in a collective
+    q.put((rank, outcome, lib.freed))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_at", ["create", "handle", "connect", None])
+def test_dist_setup_failure_is_seen_by_every_rank(fail_at):
+    """A so_dist setup failure on one rank raises DistSetupError on EVERY
+    rank (so bench.py falls back to NCCL on all of them together) instead of
+    leaving the healthy ranks blocked in all_gather_object."""
+    world, fail_rank = 3, 1
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_setup_fail_worker, args=(r, world, port, fail_rank, fail_at, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, outcome, freed in got:
+        if fail_at is None:
+            assert outcome == "ok" and freed == 0
+        else:
+            assert "stub failure on rank 1" in outcome or "could not export" in outcome, outcome
+            # whatever this rank created is freed again
+            assert freed == (0 if (rank == fail_rank and fail_at == "create") else 1)
