@@ -495,6 +495,7 @@ void* so_default_stream(void) {
 so_status so_matrix_upload_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row, const int64_t* col,
                                const double* val, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_matrix_upload_coo");
         std::unique_ptr<so_matrix> m(new_host_matrix(SO_COO, nrows, ncols));
         upload_coo_part(m->coo, nrows, ncols, nnz, row, col, val, ctx(m->device).stream);
         return m.release();
@@ -504,6 +505,7 @@ so_status so_matrix_upload_coo(int64_t nrows, int64_t ncols, int64_t nnz, const 
 so_status so_matrix_upload_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr, const int64_t* col,
                                const double* val, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_matrix_upload_csr");
         std::unique_ptr<so_matrix> m(new_host_matrix(SO_CSR, nrows, ncols));
         upload_csr_part(m->csr, nrows, ncols, nnz, row_ptr, col, val, ctx(m->device).stream);
         return m.release();
@@ -513,6 +515,7 @@ so_status so_matrix_upload_csr(int64_t nrows, int64_t ncols, int64_t nnz, const 
 so_status so_matrix_upload_dia(int64_t nrows, int64_t ncols, int64_t ndiags, const int64_t* offsets,
                                const double* values, int64_t stored_nnz, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_matrix_upload_dia");
         std::unique_ptr<so_matrix> m(new_host_matrix(SO_DIA, nrows, ncols));
         upload_dia_part(m->dia, nrows, ncols, ndiags, offsets, values, stored_nnz, ctx(m->device).stream);
         return m.release();
@@ -522,6 +525,7 @@ so_status so_matrix_upload_dia(int64_t nrows, int64_t ncols, int64_t ndiags, con
 so_status so_matrix_upload_ell(int64_t nrows, int64_t ncols, int64_t width, const int64_t* col, const double* val,
                                int64_t stored_nnz, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_matrix_upload_ell");
         std::unique_ptr<so_matrix> m(new_host_matrix(SO_ELL, nrows, ncols));
         upload_ell_part(m->ell, nrows, ncols, width, col, val, stored_nnz, ctx(m->device).stream);
         return m.release();
@@ -532,6 +536,7 @@ so_status so_matrix_upload_hyb(int64_t nrows, int64_t ncols, int64_t width, cons
                                const double* ell_val, int64_t ell_stored_nnz, int64_t coo_nnz, const int64_t* coo_row,
                                const int64_t* coo_col, const double* coo_val, int64_t kh, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_matrix_upload_hyb");
         std::unique_ptr<so_matrix> m(new_host_matrix(SO_HYB, nrows, ncols));
         cudaStream_t s = ctx(m->device).stream;
         upload_ell_part(m->ell, nrows, ncols, width, ell_col, ell_val, ell_stored_nnz, s);
@@ -545,6 +550,7 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags, con
                                const double* values, int64_t dia_stored_nnz, int64_t csr_nnz, const int64_t* row_ptr,
                                const int64_t* col, const double* val, int64_t threshold, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_matrix_upload_hdc");
         std::unique_ptr<so_matrix> m(new_host_matrix(SO_HDC, nrows, ncols));
         cudaStream_t s = ctx(m->device).stream;
         upload_dia_part(m->dia, nrows, ncols, ndiags, offsets, values, dia_stored_nnz, s);
@@ -557,6 +563,7 @@ so_status so_matrix_upload_hdc(int64_t nrows, int64_t ncols, int64_t ndiags, con
 so_status so_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n, const int64_t* row, const int64_t* col,
                                const double* val, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_coo_from_triplets");
         check_dims(nrows, ncols);
         if (n > 0 && (!row || !col || !val)) fail(SO_INVALID_INPUT, "null host array");
         return coo_from_triplets_device(nrows, ncols, n, row, col, val, current_ctx().stream);
@@ -565,6 +572,7 @@ so_status so_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n, const in
 
 so_status so_read_matrix_market(const char* path, so_matrix** out) {
     return make(out, [&] {
+        SOB_RANGE("so_read_matrix_market");
         if (!path) fail(SO_INVALID_INPUT, "null path");
         return read_matrix_market(std::string(path), current_ctx().stream);
     });
@@ -572,6 +580,7 @@ so_status so_read_matrix_market(const char* path, so_matrix** out) {
 
 so_status so_write_matrix_market(const so_matrix* m, const char* path) {
     return guard([&] {
+        SOB_RANGE("so_write_matrix_market");
         if (!path) fail(SO_INVALID_INPUT, "null path");
         cudaStream_t s = on_device(m);
         if (m->format != SO_COO) fail(SO_INVALID_INPUT, "write_matrix_market: expects a COO matrix");
@@ -646,6 +655,7 @@ so_status so_matrix_info_get(const so_matrix* m, so_matrix_info* out) {
 
 so_status so_matrix_download(const so_matrix* m, const so_host_arrays* a) {
     return guard([&] {
+        SOB_RANGE("so_matrix_download");
         if (!a) fail(SO_INVALID_INPUT, "null host arrays");
         cudaStream_t s = on_device(m);
         const int64_t n = m->nrows;
@@ -688,6 +698,7 @@ so_status so_matrix_download(const so_matrix* m, const so_host_arrays* a) {
 
 so_status so_from_coo(const so_matrix* coo, int32_t target, const so_conversion_config* cfg, so_matrix** out) {
     return make(out, [&]() -> so_matrix* {
+        SOB_RANGE("so_from_coo");
         cudaStream_t s = on_device(coo);
         if (coo->format != SO_COO) fail(SO_INVALID_INPUT, "from_coo: source is not a COO matrix");
         if (target < 0 || target > 5)
@@ -704,6 +715,7 @@ so_status so_from_coo(const so_matrix* coo, int32_t target, const so_conversion_
 
 so_status so_convert(const so_matrix* src, int32_t target, const so_conversion_config* cfg, so_matrix** out) {
     return make(out, [&]() -> so_matrix* {
+        SOB_RANGE("so_convert");
         cudaStream_t s = on_device(src);
         if (target < 0 || target > 5)
             fail(SO_INVALID_INPUT, "format id " + std::to_string(target) + " outside 0..5");
@@ -723,6 +735,7 @@ so_status so_convert(const so_matrix* src, int32_t target, const so_conversion_c
 
 so_status so_to_coo(const so_matrix* src, so_matrix** out) {
     return make(out, [&]() -> so_matrix* {
+        SOB_RANGE("so_to_coo");
         cudaStream_t s = on_device(src);
         if (src->format == SO_COO) return clone_matrix(*src, s);  // formats.cpp:436-437
         std::unique_ptr<so_matrix> csr(any_to_csr(*src, s));
@@ -757,6 +770,7 @@ int32_t so_format_feasible(int32_t target, const so_feature_vector* f, const so_
 
 so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev, void* stream) {
     return guard([&] {
+        SOB_RANGE("so_spmv_device");
         on_device(m);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx(m->device).stream;
         spmv_device(*m, x_dev, y_dev, s);
@@ -766,6 +780,7 @@ so_status so_spmv_device(const so_matrix* m, const double* x_dev, double* y_dev,
 so_status so_spmv_device_rows(const so_matrix* m, const double* x_dev, double* y_dev, int64_t row_lo,
                               int64_t row_hi, void* stream) {
     return guard([&] {
+        SOB_RANGE("so_spmv_device_rows");
         on_device(m);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx(m->device).stream;
         spmv_device_rows(*m, x_dev, y_dev, row_lo, row_hi, s);
@@ -776,6 +791,7 @@ so_status so_spmv_rows_push(const so_matrix* m, const double* x_dev, double* y_d
                             double* remote_dev, unsigned* ticket_dev, unsigned long long* remote_flag,
                             unsigned long long flag_value, void* stream) {
     return guard([&] {
+        SOB_RANGE("so_spmv_rows_push");
         on_device(m);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx(m->device).stream;
         spmv_rows_push(*m, x_dev, y_dev, row_lo, row_hi, remote_dev, ticket_dev, remote_flag, flag_value, s);
@@ -849,6 +865,7 @@ so_status so_gen_stencil27_dia(int64_t g, int64_t row_lo, int64_t row_hi, int64_
 
 so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) {
     return guard([&] {
+        SOB_RANGE("so_spmv");
         cudaStream_t s = on_device(m);
         check_x(*m, xlen);
         if (m->nrows > 0 && spmv_pipelined(*m, x, y, s)) {
@@ -868,6 +885,7 @@ so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) 
 
 so_status so_spmv_new(const so_matrix* m, const double* x, int64_t xlen, so_make_output make_y, void* make_ctx) {
     return guard([&] {
+        SOB_RANGE("so_spmv_new");
         if (!make_y) fail(SO_INVALID_INPUT, "spmv: null output allocator");
         cudaStream_t s = on_device(m);
         check_x(*m, xlen);
@@ -893,6 +911,7 @@ so_status so_spmv_new(const so_matrix* m, const double* x, int64_t xlen, so_make
 so_status so_time_spmv(const so_matrix* m, const double* x, int64_t xlen, int64_t reps, double* per_rep,
                        double* total) {
     return guard([&] {
+        SOB_RANGE("so_time_spmv");
         if (reps < 1) fail(SO_INVALID_INPUT, "time_spmv: repetitions must be >= 1");  // spmv.cpp:223-225
         cudaStream_t s = on_device(m);
         check_x(*m, xlen);
@@ -963,6 +982,7 @@ int64_t so_spmv_bytes(const so_matrix* m) {
 
 so_status so_extract_features(const so_matrix* m, double ratio, so_feature_vector* out, so_scan_stats* stats) {
     return guard([&] {
+        SOB_RANGE("so_extract_features");
         cudaStream_t s = on_device(m);
         check_ratio(*m, ratio);
         DBuf<FeatState> st(1, s);
@@ -984,6 +1004,7 @@ so_status so_forest_upload(int32_t kind, int32_t n_trees, const int64_t* node_of
                            const double* threshold, const int32_t* left, const int32_t* right, const int32_t* cls,
                            so_forest** out) {
     return guard([&] {
+        SOB_RANGE("so_forest_upload");
         *out = nullptr;
         *out = forest_upload(kind, n_trees, node_off, feature, threshold, left, right, cls, current_ctx().stream);
     });
@@ -995,6 +1016,7 @@ namespace sob {
 namespace {
 so_status predict_host_rows(const so_forest* f, int64_t n, const double* rows, int32_t* out, bool blocked) {
     return guard([&] {
+        SOB_RANGE("so_predict_rows");
         if (!f) fail(SO_INVALID_INPUT, "null forest");
         if (n < 0 || (n > 0 && (!rows || !out))) fail(SO_INVALID_INPUT, "bad rows");
         SOB_CUDA(cudaSetDevice(f->device));
@@ -1044,6 +1066,7 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
                      so_tune_outcome* out) {
     const auto t_entry = std::chrono::steady_clock::now();
     return guard([&] {
+        SOB_RANGE("so_tune_ml");
         if (!f || !out) fail(SO_INVALID_INPUT, "null argument");
         cudaStream_t s = on_device(m);
         if (f->device != m->device) fail(SO_INVALID_INPUT, "forest and matrix live on different devices");

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -36,6 +37,17 @@ void count_launch();
 #define SOB_LAUNCH(what) (::sob::count_launch(), ::sob::cuda_check(cudaGetLastError(), what))
 
 void set_error(const std::string& m);
+
+// NVTX range over a C-ABI call (convert / features / predict / tune / SpMV /
+// dist iterate), visible in nsys / ncu --nvtx timelines; header-only NVTX v3,
+// a no-op unless a tool is attached (SURVEY §5 tracing).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define SOB_RANGE(name) ::sob::NvtxRange sob_nvtx_range_(name)
 
 template <typename F>
 so_status guard(F&& f) {

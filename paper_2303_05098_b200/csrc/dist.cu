@@ -224,6 +224,7 @@ so_status so_dist_handle(const so_dist* d, so_ipc_handle* out) {
 
 so_status so_dist_connect(so_dist* d, const so_ipc_handle* handles) {
     return guard([&] {
+        SOB_RANGE("so_dist_connect");
         if (!d || (!handles && d->world > 1)) fail(SO_INVALID_INPUT, "dist_connect: null argument");
         if (d->connected) fail(SO_INVALID_INPUT, "dist_connect: already connected");
         SOB_CUDA(cudaSetDevice(d->device));
@@ -275,6 +276,7 @@ so_status so_dist_x(const so_dist* d, int32_t which, double** x_dev, int64_t* of
 
 so_status so_dist_iterate(so_dist* d, int64_t iters, void* stream) {
     return guard([&] {
+        SOB_RANGE("so_dist_iterate");
         if (!d) fail(SO_INVALID_INPUT, "dist_iterate: null argument");
         if (!d->connected && d->world > 1) fail(SO_INVALID_INPUT, "dist_iterate: not connected");
         if (iters < 0) fail(SO_INVALID_INPUT, "dist_iterate: negative iteration count");
