@@ -153,6 +153,12 @@ void spmv_device_rows(const so_matrix& m, const double* x, double* y, int64_t lo
 bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_mapped, cudaStream_t s,
                         int64_t blk_lo = 0, int64_t blk_hi = -1);
 int64_t zero_copy_rows_per_block();
+// pinned host x (copied up by ONE copy-engine H2D on `copy`) and mapped host
+// y on a narrow-window DIA matrix: a persistent kernel follows the copy front
+// (spmv.cu dia_follow_kernel); synchronous; false = not eligible (or the copy
+// never arrived: y must be recomputed)
+bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
+                     cudaStream_t copy);
 // min/max DIA offset of a DIA-window matrix (read once, cached on the matrix)
 void ensure_dia_window(const so_matrix& m, cudaStream_t s);
 // spmv(m, x) with PAGEABLE host x/y (stage.cu): host threads copy through a

@@ -11,6 +11,7 @@
 // tree order: deterministic, within the 1e-12 relative contract.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "matrix.cuh"
 
@@ -386,6 +387,93 @@ __global__ void __launch_bounds__(kZcRows, 1)
         for (int u = 0; u < kDiaBatch; ++u) acc = fadd(acc, ok[u] ? fmul(v[u], xv[u]) : -0.0);
     }
     y_host[i] = acc;
+}
+
+// Host-buffer DIA spmv that FOLLOWS one copy-engine upload of x (so_spmv
+// with pinned buffers, narrow window).  The device copy of x is pre-filled
+// with a NaN sentinel (both 32-bit halves kFollowSent); x goes up as ONE
+// H2D on the copy stream, followed by a 4-byte copy that sets `flag`.  A
+// persistent grid (one 1024-thread CTA per SM) walks the row blocks in
+// address order behind the copy front: a block's x window is read from
+// device memory (L1 bypassed) until no element still holds a sentinel half
+// -- or the flag says the copy is complete (an x element that happens to
+// equal the sentinel) -- then its rows are computed exactly as dia_zc_kernel
+// does (bit-identical) and y is stored straight into mapped host memory.
+// The copy engine reads x over the link at its full rate (~55 GB/s; SM loads
+// from host memory reach ~44) while the SMs write y the other way.
+// A copy that never arrives (a serialising tool) gives up after
+// kFollowTimeoutNs and reports it through `timed_out` (mapped host memory):
+// the caller then recomputes on another path.
+constexpr unsigned kFollowSent = 0x7FF5A5A5u;
+constexpr unsigned long long kFollowTimeoutNs = 2000ull * 1000 * 1000;
+
+__global__ void follow_fill(unsigned* __restrict__ p, int64_t n32, unsigned* __restrict__ flag) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n32; i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = kFollowSent;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 0;
+}
+
+__device__ __forceinline__ bool follow_ready(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    return unsigned(b) != kFollowSent && unsigned(b >> 32) != kFollowSent;
+}
+
+__global__ void __launch_bounds__(kZcRows, 1)
+    dia_follow_kernel(int nrows, int ncols, int ndiags, const int64_t* __restrict__ offsets,
+                      const double* __restrict__ vals, const double* dx, double* y_host, const unsigned* flag,
+                      int omin, int omax, unsigned* timed_out) {
+    extern __shared__ double xs[];
+    __shared__ int soff[kDiaSmem];
+    stage_offsets(soff, offsets, ndiags);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const int nblk = (nrows + kZcRows - 1) / kZcRows;
+    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int i0 = blk * kZcRows;
+        const int w0 = max(0, i0 + omin), w1 = min(ncols, i0 + kZcRows - 1 + omax + 1);
+        while (true) {
+            unsigned fl;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(fl) : "l"(flag) : "memory");
+            bool ok = true;
+            for (int j = threadIdx.x; j < w1 - w0; j += kZcRows) {
+                const double v = __ldcg(dx + w0 + j);
+                xs[j] = v;
+                ok = ok && (fl != 0 || follow_ready(v));
+            }
+            // one barrier publishes xs and agrees on readiness
+            if (!__syncthreads_or(!ok)) break;
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            // thread 0's clock decides for the whole CTA (uniform exit)
+            if (__syncthreads_or(threadIdx.x == 0 && t - t0 > kFollowTimeoutNs)) {
+                if (threadIdx.x == 0) atomicExch_system(timed_out, 1u);
+                return;
+            }
+            __nanosleep(500);
+        }
+        const int i = i0 + threadIdx.x;
+        if (i < nrows) {
+            const double* vp = vals + i;
+            double acc = 0.0;
+            for (int d0 = 0; d0 < ndiags; d0 += kDiaBatch) {
+                double v[kDiaBatch], xv[kDiaBatch];
+                bool ok[kDiaBatch];
+#pragma unroll
+                for (int u = 0; u < kDiaBatch; ++u) {
+                    const bool live = d0 + u < ndiags;
+                    const int d = live ? d0 + u : ndiags - 1;
+                    const int c = i + soff[d];
+                    ok[u] = live && unsigned(c) < unsigned(ncols);
+                    v[u] = ld_stream(vp + size_t(d) * size_t(nrows));
+                    xv[u] = xs[ok[u] ? c - w0 : 0];
+                }
+#pragma unroll
+                for (int u = 0; u < kDiaBatch; ++u) acc = fadd(acc, ok[u] ? fmul(v[u], xv[u]) : -0.0);
+            }
+            y_host[i] = acc;
+        }
+        __syncthreads();  // xs is reused by the next block
+    }
 }
 
 // Row-partitioned iteration, fused boundary exchange (config 5, dist.py):
@@ -903,6 +991,85 @@ bool spmv_dia_zero_copy(const so_matrix& m, const double* x_mapped, double* y_ma
                                                           m.dia.offsets.get(), m.dia.values.get(), x_mapped,
                                                           y_mapped, int(omin), int(omax), int(blk_lo));
     SOB_LAUNCH("dia_zc_kernel");
+    return true;
+}
+
+namespace {
+// Per-device state of the follow path: the sentinel-filled device copy of x
+// (grow-only), the copy-complete flag, the pinned word copied into it, the
+// mapped timeout word, and the event after which the copy may refill x.
+struct FollowStage {
+    std::mutex mu;
+    double* dx = nullptr;
+    int64_t cap = 0;
+    unsigned* flag = nullptr;
+    unsigned* one_host = nullptr;
+    unsigned* timed_out = nullptr;  // pinned + mapped
+    unsigned* timed_out_dev = nullptr;
+    cudaEvent_t refilled = nullptr, copied = nullptr;
+};
+FollowStage g_follow[64];
+}  // namespace
+
+bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
+                     cudaStream_t copy) {
+    static const bool off = std::getenv("SOB_NO_FOLLOW") != nullptr;  // diagnostic knob (A/B)
+    if (off) return false;
+    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
+    if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
+        return false;
+    const int64_t omin = m.dia_omin, omax = m.dia_omax;
+    if (omax - omin > kZcSpan) return false;
+    const int64_t nc = m.ncols;
+    FollowStage& f = g_follow[m.device];
+    std::lock_guard<std::mutex> lk(f.mu);
+    if (!f.flag) {
+        SOB_CUDA(cudaMalloc(reinterpret_cast<void**>(&f.flag), sizeof(unsigned)));
+        SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.one_host), sizeof(unsigned), cudaHostAllocPortable));
+        *f.one_host = 1;
+        SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.timed_out), sizeof(unsigned),
+                               cudaHostAllocMapped | cudaHostAllocPortable));
+        *f.timed_out = 0;
+        SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&f.timed_out_dev), f.timed_out, 0));
+        SOB_CUDA(cudaEventCreateWithFlags(&f.refilled, cudaEventDisableTiming));
+        SOB_CUDA(cudaEventCreateWithFlags(&f.copied, cudaEventDisableTiming));
+    }
+    const int grid_fill = current_ctx().num_sms * 4;
+    if (f.cap < nc) {
+        // the previous buffer may still be read by an earlier call's kernel: order its release on s
+        if (f.dx) SOB_CUDA(cudaFreeAsync(f.dx, s));
+        f.dx = nullptr;
+        f.cap = 0;
+        SOB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&f.dx), sizeof(double) * size_t(nc), s));
+        f.cap = nc;
+        follow_fill<<<grid_fill, 256, 0, s>>>(reinterpret_cast<unsigned*>(f.dx), 2 * f.cap, f.flag);
+        SOB_LAUNCH("follow_fill");
+        SOB_CUDA(cudaEventRecord(f.refilled, s));
+    }
+    // x up in one copy once the device copy holds sentinels again, then the flag
+    SOB_CUDA(cudaStreamWaitEvent(copy, f.refilled, 0));
+    SOB_CUDA(cudaMemcpyAsync(f.dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
+    SOB_CUDA(cudaMemcpyAsync(f.flag, f.one_host, sizeof(unsigned), cudaMemcpyHostToDevice, copy));
+    SOB_CUDA(cudaEventRecord(f.copied, copy));
+    const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
+    const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
+    const unsigned grid = unsigned(std::min<int64_t>(nblk, current_ctx().num_sms));
+    dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags), m.dia.offsets.get(),
+                                                  m.dia.values.get(), f.dx, y_mapped, f.flag, int(omin), int(omax),
+                                                  f.timed_out_dev);
+    SOB_LAUNCH("dia_follow_kernel");
+    // refill the sentinels for the next call once the copy has finished (x
+    // columns past the last row's window are not waited for by the kernel)
+    SOB_CUDA(cudaStreamWaitEvent(s, f.copied, 0));
+    follow_fill<<<grid_fill, 256, 0, s>>>(reinterpret_cast<unsigned*>(f.dx), 2 * nc, f.flag);
+    SOB_LAUNCH("follow_fill");
+    SOB_CUDA(cudaEventRecord(f.refilled, s));
+    SOB_CUDA(cudaStreamSynchronize(s));
+    if (*reinterpret_cast<volatile unsigned*>(f.timed_out)) {  // the copy never showed up: recompute elsewhere
+        *f.timed_out = 0;
+        SOB_CUDA(cudaStreamSynchronize(copy));
+        return false;
+    }
     return true;
 }
 

@@ -1,0 +1,185 @@
+// Diagnostic: host-buffer DIA spmv on config 2 (banded n = 4M, 27 diagonals)
+// with x brought up by ONE copy-engine H2D while a persistent kernel follows
+// the copy front (device x pre-filled with a NaN sentinel; a row block runs
+// once its x window holds no sentinel half-word, or once a flag copied
+// after x says the copy is complete) and stores y straight into mapped host
+// memory -- vs the product's so_spmv (zero-copy x and y over the SMs).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Iinclude -o build/cezc_probe scripts/cezc_probe.cu \
+//        -Lpaper_2303_05098_b200/lib -lsparseoracle_b200 -Xlinker -rpath,'$ORIGIN/../paper_2303_05098_b200/lib'
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "sparseoracle_b200.h"
+
+constexpr unsigned kSent = 0x7FF5A5A5u;  // both 32-bit halves of the sentinel (a NaN)
+
+__global__ void fill_sentinel(unsigned* p, size_t n32, unsigned* flag) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n32; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = kSent;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 0;
+}
+
+__device__ __forceinline__ bool ready(double v) {
+    const unsigned long long b = __double_as_longlong(v);
+    return unsigned(b) != kSent && unsigned(b >> 32) != kSent;
+}
+
+// persistent: CTA c walks row blocks c, c + G, ... (the copy front moves in
+// address order, so every CTA trails it)
+template <int kRows>
+__global__ void __launch_bounds__(kRows, 1)
+    follow_kernel(int n, int nd, const int* __restrict__ off, const double* __restrict__ vals, const double* dx,
+                  double* y_host, const volatile unsigned* flag, int omin, int omax, unsigned long long* spins,
+                  int sleep_ns, int probe_last) {
+    extern __shared__ double xs[];
+    __shared__ int soff[64];
+    if (threadIdx.x < nd) soff[threadIdx.x] = off[threadIdx.x];
+    const int nblk = (n + kRows - 1) / kRows;
+    unsigned long long my_spins = 0;
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const int i0 = b * kRows;
+        const int w0 = max(0, i0 + omin), w1 = min(n, i0 + kRows - 1 + omax + 1);
+        if (probe_last) {  // cheap wait on the window's last element (the copy front moves in address order)
+            if (threadIdx.x == 0)
+                while (*flag == 0 && !ready(__ldcg(dx + w1 - 1))) {
+                    ++my_spins;
+                    __nanosleep(sleep_ns);
+                }
+            __syncthreads();
+        }
+        while (true) {
+            unsigned fl;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(fl) : "l"(flag) : "memory");
+            const bool done = fl != 0;
+            bool ok = true;
+            for (int j = threadIdx.x; j < w1 - w0; j += kRows) {
+                const double v = __ldcg(dx + w0 + j);
+                xs[j] = v;
+                ok = ok && (done || ready(v));
+            }
+            // one barrier both publishes xs and agrees on readiness (a shared
+            // flag reset by thread 0 would race with slower readers)
+            if (!__syncthreads_or(!ok)) break;
+            ++my_spins;
+            __nanosleep(sleep_ns);
+        }
+        const int i = i0 + threadIdx.x;
+        if (i < n) {
+            double acc = 0.0;
+#pragma unroll 9
+            for (int d = 0; d < nd; ++d) {
+                const int c = i + soff[d];
+                const bool in = unsigned(c) < unsigned(n);
+                const double v = __ldcs(vals + size_t(d) * n + i);
+                acc = __dadd_rn(acc, in ? __dmul_rn(v, xs[in ? c - w0 : 0]) : -0.0);
+            }
+            y_host[i] = acc;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && my_spins) atomicAdd(spins, my_spins);
+}
+
+int main(int argc, char** argv) {
+    const int64_t n = 4000000, h = 13, nd = 2 * h + 1;
+    const int reps = argc > 1 ? atoi(argv[1]) : 20;
+    std::vector<int64_t> off(nd);
+    std::vector<int> offi(nd);
+    for (int d = 0; d < nd; ++d) off[d] = offi[d] = d - h;
+    std::vector<double> vals(size_t(nd) * n);
+    for (int d = 0; d < nd; ++d)
+        for (int64_t i = 0; i < n; ++i) vals[size_t(d) * n + i] = 0.5 + double((i * 31 + d * 7) % 97) / 64.0;
+    so_matrix* m = nullptr;
+    if (so_matrix_upload_dia(n, n, nd, off.data(), vals.data(), nd * n, &m) != SO_OK) {
+        printf("upload: %s\n", so_last_error());
+        return 1;
+    }
+    double *x, *y, *y2, *dx, *dvals, *ymap;
+    int* doff;
+    unsigned *flag, *hone, *dspins;
+    cudaHostAlloc(&x, n * 8, cudaHostAllocMapped);
+    cudaHostAlloc(&y, n * 8, cudaHostAllocMapped);
+    cudaHostAlloc(&y2, n * 8, cudaHostAllocMapped);
+    cudaHostAlloc(&hone, 4, 0);
+    *hone = 1;
+    cudaHostGetDevicePointer((void**)&ymap, y, 0);
+    cudaMalloc(&dx, n * 8);
+    cudaMalloc(&dvals, size_t(nd) * n * 8);
+    cudaMalloc(&doff, nd * 4);
+    cudaMalloc(&flag, 4);
+    cudaMalloc(&dspins, 8);
+    cudaMemset(dspins, 0, 8);
+    cudaMemcpy(dvals, vals.data(), size_t(nd) * n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(doff, offi.data(), nd * 4, cudaMemcpyHostToDevice);
+    for (int64_t i = 0; i < n; ++i) x[i] = 1.0 + double(i % 7) / 8.0;
+    cudaStream_t s, ci;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ci, cudaStreamNonBlocking);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, fillev, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventCreateWithFlags(&fillev, cudaEventDisableTiming);
+
+    // product path first (reference numbers, and y2 for the bit check)
+    for (int w = 0; w < 3; ++w) so_spmv(m, x, n, y2);
+    std::vector<double> tp;
+    for (int r = 0; r < reps; ++r) {
+        auto t0 = std::chrono::steady_clock::now();
+        so_spmv(m, x, n, y2);
+        tp.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    std::sort(tp.begin(), tp.end());
+    printf("product so_spmv (pinned, zero-copy x+y): median %.3f ms, min %.3f ms\n", tp[tp.size() / 2], tp[0]);
+
+    auto run = [&](auto kern, int rows, int grid, int sleep_ns, int probe_last) {
+        const size_t smem = sizeof(double) * (rows + 2 * h + 2);
+        std::vector<double> tw, te;
+        for (int r = 0; r < reps + 3; ++r) {
+            fill_sentinel<<<4 * nsm, 256, 0, s>>>(reinterpret_cast<unsigned*>(dx), size_t(n) * 2, flag);
+            cudaStreamSynchronize(s);
+            auto t0 = std::chrono::steady_clock::now();
+            cudaEventRecord(a, s);
+            cudaStreamWaitEvent(ci, a, 0);
+            cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, ci);
+            cudaMemcpyAsync(flag, hone, 4, cudaMemcpyHostToDevice, ci);
+            kern<<<grid, rows, smem, s>>>(int(n), int(nd), doff, dvals, dx, ymap, flag, -int(h), int(h),
+                                          reinterpret_cast<unsigned long long*>(dspins), sleep_ns, probe_last);
+            cudaEventRecord(b, s);
+            cudaStreamSynchronize(s);
+            cudaStreamSynchronize(ci);
+            const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            float ev;
+            cudaEventElapsedTime(&ev, a, b);
+            if (r >= 3) {
+                tw.push_back(wall);
+                te.push_back(ev);
+            }
+        }
+        std::sort(tw.begin(), tw.end());
+        std::sort(te.begin(), te.end());
+        unsigned long long sp = 0;
+        cudaMemcpy(&sp, dspins, 8, cudaMemcpyDeviceToHost);
+        cudaMemset(dspins, 0, 8);
+        const bool same = std::memcmp(y, y2, n * 8) == 0;
+        printf("rows %4d grid %3d sleep %4d last %d: wall median %.3f ms (min %.3f), events %.3f ms; spins %llu; %s\n",
+               rows, grid, sleep_ns, probe_last, tw[tw.size() / 2], tw[0], te[te.size() / 2], sp,
+               same ? "bit-identical" : "DIFFERS");
+    };
+    for (int sl : {200, 500, 2000})
+        for (int pl : {0, 1}) run(follow_kernel<1024>, 1024, nsm, sl, pl);
+    for (int pl : {0, 1}) {
+        run(follow_kernel<512>, 512, nsm, 500, pl);
+        run(follow_kernel<512>, 512, 2 * nsm, 500, pl);
+        run(follow_kernel<256>, 256, 4 * nsm, 500, pl);
+        run(follow_kernel<1024>, 1024, nsm / 2, 500, pl);
+    }
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

@@ -11,7 +11,8 @@ Covers: uploads / downloads, every conversion pair, the six SpMV kernels
 (CSR warp groups plain / padded / cooperative, long-row pieces + fix-up, COO
 chunk fix-up incl. queued long runs and the empty-row-gap path, DIA with <= 5
 and > 5 diagonals, ELL, HYB, HDC both parts), the pageable staging path
-(zero-copy DIA row blocks and the copy-engine path), features on every format
+(zero-copy DIA row blocks and the copy-engine path), pinned host buffers (the
+follow-the-copy DIA kernel), features on every format
 (both spread-walk variants, entry and lockstep sweeps, big-row pieces),
 predict (flat and blocked), the tune graph, device from_triplets, Matrix
 Market I/O, the halo push / flag wait kernels and so_dist (1 rank; 2 ranks in
@@ -29,6 +30,27 @@ import paper_2303_05098_b200 as P  # noqa: E402
 from paper_2303_05098_b200 import _capi as A  # noqa: E402
 from paper_2303_05098_b200 import dist as D  # noqa: E402
 from paper_2303_05098_b200 import synth  # noqa: E402
+
+
+_pinned_keep = []
+
+
+def pinned(n):
+    """n doubles of pinned, mapped host memory (cudaHostAlloc through the
+    CUDA runtime's shared library; no torch), or None when unavailable."""
+    for name in ("libcudart.so", "/usr/local/cuda/lib64/libcudart.so", "libcudart.so.12"):
+        try:
+            rt = C.CDLL(name)
+            break
+        except OSError:
+            rt = None
+    if rt is None:
+        return None
+    p = C.c_void_p()
+    if rt.cudaHostAlloc(C.byref(p), C.c_size_t(8 * n), C.c_uint(2)) != 0:  # cudaHostAllocMapped
+        return None
+    _pinned_keep.append((rt, p))
+    return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n,))
 
 
 def csr_from(n, m, rows, cols, rng):
@@ -181,6 +203,17 @@ def main():
     xb = rng.uniform(-1, 1, big.ncols)
     for f in (P.DIA, P.CSR, P.COO):
         bm.convert(f).spmv(xb)
+    # pinned host buffers: the follow-the-copy kernel (and, with
+    # SOB_NO_FOLLOW=1, the zero-copy kernel) on a narrow DIA window
+    # (>= 2^19 rows: smaller calls take the one-shot path)
+    band = synth.banded(600_000, 4, seed=9)
+    dm = P.DeviceMatrix.csr(band.nrows, band.ncols, band.row_ptr, band.col, band.val).convert(P.DIA)
+    hx, hy = pinned(band.ncols), pinned(band.nrows)
+    if hx is not None and hy is not None:
+        hx[:] = rng.uniform(-1, 1, band.ncols)
+        for _ in range(2):
+            dm.spmv_into(hx, hy)
+            assert np.array_equal(hy, dm.spmv(np.array(hx))), "pinned spmv differs from the one-shot path"
     # large enough for the global-memory spread walk and the lockstep sweep
     big2 = synth.uniform_random(60_000, 5, seed=8)
     P.DeviceMatrix.csr(big2.nrows, big2.ncols, big2.row_ptr, big2.col, big2.val).extract_features(0.2)

@@ -448,6 +448,46 @@ def test_pipelined_host_spmv_pinned(so, O, shape):
         assert np.array_equal(m.spmv(xn.copy()), want), f  # pageable -> one-shot path
 
 
+def test_follow_copy_path_edge_cases(so, O):
+    """Pinned spmv(m, x) on a narrow DIA window runs dia_follow_kernel behind
+    ONE copy-engine upload of x (spmv.cu): the device copy of x holds a NaN
+    sentinel until the copy lands.  Cases: x elements whose bits ARE the
+    sentinel (the kernel must finish on the copy-complete flag), x with one
+    sentinel half-word, a matrix with more columns than its rows' window
+    reaches (the kernel ends before the copy; the sentinel refill must wait
+    for it), and consecutive calls with different x (no stale x from the
+    previous call).  Every result bit-identical to the oracle."""
+    import torch
+
+    sent = np.array([0x7FF5A5A57FF5A5A5], dtype=np.uint64).view(np.float64)[0]
+    half = np.array([0x7FF5A5A53FF00000], dtype=np.uint64).view(np.float64)[0]  # high half only
+    rng = np.random.default_rng(21)
+    for nrows, ncols in ((600_000, 600_000), (600_000, 1_500_000)):
+        rows, cols = [], []
+        for off in (-7, -1, 0, 3, 9):
+            r = np.arange(max(0, -off), min(nrows, ncols - off))
+            rows.append(r)
+            cols.append(r + off)
+        r, c = np.concatenate(rows), np.concatenate(cols)
+        coo = O.from_triplets(nrows, ncols, r, c, rng.uniform(0.5, 2.0, r.size))
+        d = to_dev(so, coo)
+        xt = torch.empty(ncols, dtype=torch.float64).pin_memory()
+        yt = torch.empty(nrows, dtype=torch.float64).pin_memory()
+        xn, yn = xt.numpy(), yt.numpy()
+        m = d.from_coo(so.DIA)
+        want_m = O.oc_convert(coo, so.DIA)
+        for trial in range(4):
+            xn[:] = rng.uniform(-1, 1, ncols)
+            if trial == 1:
+                xn[::997] = sent  # a NaN with the sentinel's bits: NaN rows in y, on the flag path
+            if trial == 2:
+                xn[5::1013] = half
+            want = O.oc_spmv(want_m, xn)
+            yn[:] = 0.0
+            m.spmv_into(xn, yn)
+            assert np.array_equal(yn, want, equal_nan=True), (nrows, ncols, trial)
+
+
 def test_stencil27_generator_and_row_slices(so, O):
     """Device 27-pt stencil (config 5 shape): the full DIA matrix matches the
     oracle's SpMV bit-for-bit, and 3 row slices with x windows (the
