@@ -88,6 +88,20 @@ __device__ __forceinline__ void stage_offsets(int* soff, const int64_t* __restri
     __syncthreads();
 }
 
+// Accumulating kernels (HYB's COO part after its ELL part, HDC's CSR part
+// after its DIA part) add each row's sum to y exactly once (rows split over
+// chunks or pieces are combined first), so y[r] + s can be a fire-and-forget
+// reduction (RED.ADD.F64.RN: the same single rounding as fadd(y[r], s),
+// bit-identical) -- no load of y whose latency and register the kernel would
+// carry (HYB on R-MAT 372 -> 344 us, profiles/r02h_ab_red.txt).
+template <bool ACCUM>
+__device__ __forceinline__ void y_store(double* p, double s) {
+    if (ACCUM)
+        atomicAdd(p, s);
+    else
+        *p = s;
+}
+
 // ---------------------------------------------------------------- CSR -------
 // Warp-level CSR stream.  Group g = rows [grp[g], grp[g+1]) (<= 32 rows,
 // <= 32*IT entries starting at grp_k[g]; greedy partition, convert.cu
@@ -122,8 +136,7 @@ __device__ __forceinline__ void csr_rows_sum(const double* prod, bool pad, int r
             for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j + (j >> 4)]);
         else
             for (int j = pa; j < pe; ++j) acc = fadd(acc, prod[j]);
-        if (ACCUM) acc = fadd(y[r], acc);
-        y[r] = acc;
+        y_store<ACCUM>(y + r, acc);
     }
     if (COOP) {
         unsigned big = __ballot_sync(0xffffffffu, coop);
@@ -137,7 +150,7 @@ __device__ __forceinline__ void csr_rows_sum(const double* prod, bool pad, int r
             else
                 for (int q = a + lane; q < e; q += 32) t = fadd(t, prod[q]);
             t = warp_sum(t);
-            if (lane == j) y[r] = ACCUM ? fadd(y[r], t) : t;
+            if (lane == j) y_store<ACCUM>(y + r, t);
         }
     }
 }
@@ -677,7 +690,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
                 if (orphan)
                     rec[chunk].first_sum = acc;
                 else
-                    y[rw] = ACCUM ? fadd(y[rw], acc) : acc;
+                    y_store<ACCUM>(y + rw, acc);
             }
             if (chunk_end && j + 1 == nmine) {
                 const bool open = rw == nxt;
