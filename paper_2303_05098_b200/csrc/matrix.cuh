@@ -159,6 +159,22 @@ int64_t zero_copy_rows_per_block();
 // never arrived: y must be recomputed)
 bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
                      cudaStream_t copy);
+// The same, in two halves (pageable staging, stage.cu): follow_launch locks
+// the device's follow stage, launches the kernel -- one launch per y chunk of
+// rows_per_chunk rows (a multiple of zero_copy_rows_per_block(); 0 = one
+// launch), calling after_chunk(j) after launch j (e.g. to record an event) --
+// then calls upload(dx) to enqueue the caller's H2D copies of x into dx on
+// `copy`, then the copy-complete flag and the sentinel refill.  After s is
+// synchronised, follow_finish unlocks and returns false when the copy never
+// arrived (y invalid).
+struct FollowToken {
+    std::unique_lock<std::mutex> lk;
+    unsigned* timed_out = nullptr;
+};
+bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
+                   const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
+                   FollowToken& tok);
+bool follow_finish(FollowToken& tok);
 // min/max DIA offset of a DIA-window matrix (read once, cached on the matrix)
 void ensure_dia_window(const so_matrix& m, cudaStream_t s);
 // spmv(m, x) with PAGEABLE host x/y (stage.cu): host threads copy through a

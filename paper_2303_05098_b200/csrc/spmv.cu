@@ -11,6 +11,7 @@
 // tree order: deterministic, within the 1e-12 relative contract.
 #include <algorithm>
 #include <cstdlib>
+#include <functional>
 #include <mutex>
 
 #include "matrix.cuh"
@@ -415,10 +416,13 @@ __global__ void __launch_bounds__(kZcRows, 1)
 // The copy engine reads x over the link at its full rate (~55 GB/s; SM loads
 // from host memory reach ~44) while the SMs write y the other way.
 // A copy that never arrives (a serialising tool) gives up after
-// kFollowTimeoutNs and reports it through `timed_out` (mapped host memory):
-// the caller then recomputes on another path.
+// `timeout_ns` and reports it through `timed_out` (mapped host memory): the
+// caller then recomputes on another path.  A launch covers row blocks
+// [blk_lo, blk_hi): the pageable staging launches one kernel per y chunk so
+// that an event after each tells host threads the chunk has landed (per-block
+// completion flags need a system fence per block: 0.70 -> 1.17 ms on config
+// 2; system-scope atomics 4.4 ms, scripts/cezc_probe.cu).
 constexpr unsigned kFollowSent = 0x7FF5A5A5u;
-constexpr unsigned long long kFollowTimeoutNs = 2000ull * 1000 * 1000;
 
 __global__ void follow_fill(unsigned* __restrict__ p, int64_t n32, unsigned* __restrict__ flag) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n32; i += int64_t(gridDim.x) * blockDim.x)
@@ -434,14 +438,14 @@ __device__ __forceinline__ bool follow_ready(double v) {
 __global__ void __launch_bounds__(kZcRows, 1)
     dia_follow_kernel(int nrows, int ncols, int ndiags, const int64_t* __restrict__ offsets,
                       const double* __restrict__ vals, const double* dx, double* y_host, const unsigned* flag,
-                      int omin, int omax, unsigned* timed_out) {
+                      int omin, int omax, unsigned* timed_out, unsigned long long timeout_ns, int blk_lo,
+                      int blk_hi) {
     extern __shared__ double xs[];
     __shared__ int soff[kDiaSmem];
     stage_offsets(soff, offsets, ndiags);
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    const int nblk = (nrows + kZcRows - 1) / kZcRows;
-    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    for (int blk = blk_lo + int(blockIdx.x); blk < blk_hi; blk += gridDim.x) {
         const int i0 = blk * kZcRows;
         const int w0 = max(0, i0 + omin), w1 = min(ncols, i0 + kZcRows - 1 + omax + 1);
         while (true) {
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(kZcRows, 1)
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             // thread 0's clock decides for the whole CTA (uniform exit)
-            if (__syncthreads_or(threadIdx.x == 0 && t - t0 > kFollowTimeoutNs)) {
+            if (__syncthreads_or(threadIdx.x == 0 && t - t0 > timeout_ns)) {
                 if (threadIdx.x == 0) atomicExch_system(timed_out, 1u);
                 return;
             }
@@ -1024,8 +1028,9 @@ struct FollowStage {
 FollowStage g_follow[64];
 }  // namespace
 
-bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
-                     cudaStream_t copy) {
+bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
+                   const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
+                   FollowToken& tok) {
     static const bool off = std::getenv("SOB_NO_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     if (off) return false;
     if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
@@ -1033,9 +1038,10 @@ bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped,
         return false;
     const int64_t omin = m.dia_omin, omax = m.dia_omax;
     if (omax - omin > kZcSpan) return false;
+    if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
     const int64_t nc = m.ncols;
     FollowStage& f = g_follow[m.device];
-    std::lock_guard<std::mutex> lk(f.mu);
+    tok.lk = std::unique_lock<std::mutex>(f.mu);
     if (!f.flag) {
         SOB_CUDA(cudaMalloc(reinterpret_cast<void**>(&f.flag), sizeof(unsigned)));
         SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.one_host), sizeof(unsigned), cudaHostAllocPortable));
@@ -1047,6 +1053,7 @@ bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped,
         SOB_CUDA(cudaEventCreateWithFlags(&f.refilled, cudaEventDisableTiming));
         SOB_CUDA(cudaEventCreateWithFlags(&f.copied, cudaEventDisableTiming));
     }
+    tok.timed_out = f.timed_out;
     const int grid_fill = current_ctx().num_sms * 4;
     if (f.cap < nc) {
         // the previous buffer may still be read by an earlier call's kernel: order its release on s
@@ -1059,27 +1066,55 @@ bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped,
         SOB_LAUNCH("follow_fill");
         SOB_CUDA(cudaEventRecord(f.refilled, s));
     }
-    // x up in one copy once the device copy holds sentinels again, then the flag
+    // uploads may start once the device copy holds sentinels again
     SOB_CUDA(cudaStreamWaitEvent(copy, f.refilled, 0));
-    SOB_CUDA(cudaMemcpyAsync(f.dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
-    SOB_CUDA(cudaMemcpyAsync(f.flag, f.one_host, sizeof(unsigned), cudaMemcpyHostToDevice, copy));
-    SOB_CUDA(cudaEventRecord(f.copied, copy));
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
     const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
-    const unsigned grid = unsigned(std::min<int64_t>(nblk, current_ctx().num_sms));
-    dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags), m.dia.offsets.get(),
-                                                  m.dia.values.get(), f.dx, y_mapped, f.flag, int(omin), int(omax),
-                                                  f.timed_out_dev);
-    SOB_LAUNCH("dia_follow_kernel");
+    const int64_t per = rows_per_chunk > 0 ? rows_per_chunk / kZcRows : nblk;  // blocks per launch
+    // 2 s plus 1 ns per byte of x (a slowly staged pageable x still arrives)
+    const unsigned long long timeout = 2000ull * 1000 * 1000 + 8ull * uint64_t(nc);
+    for (int64_t b0 = 0, j = 0; b0 < nblk; b0 += per, ++j) {
+        const int64_t b1 = std::min(nblk, b0 + per);
+        const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));
+        dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags),
+                                                      m.dia.offsets.get(), m.dia.values.get(), f.dx, y_mapped, f.flag,
+                                                      int(omin), int(omax), f.timed_out_dev, timeout, int(b0),
+                                                      int(b1));
+        SOB_LAUNCH("dia_follow_kernel");
+        if (after_chunk) (*after_chunk)(j);
+    }
+    upload(f.dx);  // the caller's H2D copies of x into f.dx on `copy`
+    SOB_CUDA(cudaMemcpyAsync(f.flag, f.one_host, sizeof(unsigned), cudaMemcpyHostToDevice, copy));
+    SOB_CUDA(cudaEventRecord(f.copied, copy));
     // refill the sentinels for the next call once the copy has finished (x
     // columns past the last row's window are not waited for by the kernel)
     SOB_CUDA(cudaStreamWaitEvent(s, f.copied, 0));
     follow_fill<<<grid_fill, 256, 0, s>>>(reinterpret_cast<unsigned*>(f.dx), 2 * nc, f.flag);
     SOB_LAUNCH("follow_fill");
     SOB_CUDA(cudaEventRecord(f.refilled, s));
+    return true;
+}
+
+bool follow_finish(FollowToken& tok) {
+    bool ok = true;
+    if (tok.timed_out && *reinterpret_cast<volatile unsigned*>(tok.timed_out)) {
+        *tok.timed_out = 0;
+        ok = false;
+    }
+    if (tok.lk.owns_lock()) tok.lk.unlock();
+    return ok;
+}
+
+bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
+                     cudaStream_t copy) {
+    FollowToken tok;
+    const int64_t nc = m.ncols;
+    const bool launched = follow_launch(m, y_mapped, s, copy, 0, nullptr, [&](double* dx) {
+        SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
+    }, tok);
+    if (!launched) return false;
     SOB_CUDA(cudaStreamSynchronize(s));
-    if (*reinterpret_cast<volatile unsigned*>(f.timed_out)) {  // the copy never showed up: recompute elsewhere
-        *f.timed_out = 0;
+    if (!follow_finish(tok)) {  // the copy never showed up: recompute elsewhere
         SOB_CUDA(cudaStreamSynchronize(copy));
         return false;
     }

@@ -223,6 +223,8 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
     const int64_t cy = std::max<int64_t>(ceil_div(int64_t(1) << 17, zr), ceil_div(ceil_div(n, 8), zr)) * zr;
     const int64_t nyc = ceil_div(n, cy);
     st.events(size_t(nyc));
+    std::atomic<bool> follow{false};  // narrow DIA windows: the follow-the-copy kernel (one launch per y chunk)
+    FollowToken ftok;
 
     // the task list: every x chunk (in order), then every y chunk
     std::vector<Task> tasks;
@@ -290,6 +292,30 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
             auto wait_x = [&](int64_t k) {
                 while (xdone[size_t(k)].load(std::memory_order_acquire) < per_x[size_t(k)]) std::this_thread::yield();
             };
+            // narrow DIA windows: each staged x chunk goes up on the copy
+            // engine while a kernel per y chunk follows the copy front
+            // (spmv.cu dia_follow_kernel); an event after each launch gates
+            // that chunk's copy-out
+            if (dia_only && cy % zr == 0) {
+                cudaStream_t copy = ctx(dev).copy_in;
+                const std::function<void(int64_t)> after = [&](int64_t j) {
+                    SOB_CUDA(cudaEventRecord(st.ev[size_t(j)], s));
+                    ygate[size_t(j)].store(1, std::memory_order_release);
+                };
+                const bool launched = follow_launch(m, Yd, s, copy, cy, &after, [&](double* dx) {
+                    for (int64_t k = 0; k < nxc; ++k) {
+                        wait_x(k);
+                        const int64_t a = k * cx, e = std::min(nc, a + cx);
+                        SOB_CUDA(cudaMemcpyAsync(dx + a, X + a, sizeof(double) * size_t(e - a), cudaMemcpyHostToDevice,
+                                                 copy));
+                    }
+                }, ftok);
+                if (launched) {
+                    follow.store(true, std::memory_order_release);
+                    stamp(t_launched);
+                    return;
+                }
+            }
             // an empty launch range probes eligibility (window <= 256, offsets fit)
             const bool zc = dia_only && spmv_dia_zero_copy(m, Xd, Yd, s, 0, 0);
             if (zc) {
@@ -374,6 +400,22 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
     if (yerr) {
         cudaStreamSynchronize(s);
         std::rethrow_exception(yerr);
+    }
+    if (follow.load()) {
+        SOB_CUDA(cudaStreamSynchronize(s));
+        if (!follow_finish(ftok)) {
+            // the copy never reached the kernel (a serialising tool): y is
+            // recomputed on the one-shot path into whatever y exists now
+            double* yy = yptr.load();
+            if (!yy) fail(SO_CUDA_ERROR, "pageable spmv: follow kernel timed out before y existed");
+            SOB_CUDA(cudaStreamSynchronize(ctx(dev).copy_in));
+            DBuf<double> dx(nc, s), dy(n, s);
+            SOB_CUDA(cudaMemcpyAsync(dx.get(), x, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, s));
+            spmv_device(m, dx.get(), dy.get(), s);
+            SOB_CUDA(cudaMemcpyAsync(yy, dy.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, s));
+            SOB_CUDA(cudaStreamSynchronize(s));
+            return true;
+        }
     }
     if (failed.load()) {
         cudaStreamSynchronize(s);

@@ -35,7 +35,7 @@ template <int kRows>
 __global__ void __launch_bounds__(kRows, 1)
     follow_kernel(int n, int nd, const int* __restrict__ off, const double* __restrict__ vals, const double* dx,
                   double* y_host, const volatile unsigned* flag, int omin, int omax, unsigned long long* spins,
-                  int sleep_ns, int probe_last) {
+                  int sleep_ns, int probe_last, int sig, unsigned* sigmem) {
     extern __shared__ double xs[];
     __shared__ int soff[64];
     if (threadIdx.x < nd) soff[threadIdx.x] = off[threadIdx.x];
@@ -80,7 +80,12 @@ __global__ void __launch_bounds__(kRows, 1)
             }
             y_host[i] = acc;
         }
+        if (sig == 1 || sig == 2) __threadfence_system();
         __syncthreads();
+        if (threadIdx.x == 0) {
+            if (sig == 1) atomicAdd_system(sigmem + b / 488, 1u);
+            if (sig == 2 || sig == 3) *(volatile unsigned*)(sigmem + b) = 1u;
+        }
     }
     if (threadIdx.x == 0 && my_spins) atomicAdd(spins, my_spins);
 }
@@ -138,6 +143,11 @@ int main(int argc, char** argv) {
     std::sort(tp.begin(), tp.end());
     printf("product so_spmv (pinned, zero-copy x+y): median %.3f ms, min %.3f ms\n", tp[tp.size() / 2], tp[0]);
 
+    unsigned* sigmem = nullptr;
+    cudaHostAlloc(&sigmem, 8192 * 4, cudaHostAllocMapped);
+    unsigned* sigdev = nullptr;
+    cudaHostGetDevicePointer((void**)&sigdev, sigmem, 0);
+    int sig = 0;
     auto run = [&](auto kern, int rows, int grid, int sleep_ns, int probe_last) {
         const size_t smem = sizeof(double) * (rows + 2 * h + 2);
         std::vector<double> tw, te;
@@ -150,7 +160,8 @@ int main(int argc, char** argv) {
             cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, ci);
             cudaMemcpyAsync(flag, hone, 4, cudaMemcpyHostToDevice, ci);
             kern<<<grid, rows, smem, s>>>(int(n), int(nd), doff, dvals, dx, ymap, flag, -int(h), int(h),
-                                          reinterpret_cast<unsigned long long*>(dspins), sleep_ns, probe_last);
+                                          reinterpret_cast<unsigned long long*>(dspins), sleep_ns, probe_last, sig,
+                                          sigdev);
             cudaEventRecord(b, s);
             cudaStreamSynchronize(s);
             cudaStreamSynchronize(ci);
@@ -168,18 +179,11 @@ int main(int argc, char** argv) {
         cudaMemcpy(&sp, dspins, 8, cudaMemcpyDeviceToHost);
         cudaMemset(dspins, 0, 8);
         const bool same = std::memcmp(y, y2, n * 8) == 0;
-        printf("rows %4d grid %3d sleep %4d last %d: wall median %.3f ms (min %.3f), events %.3f ms; spins %llu; %s\n",
-               rows, grid, sleep_ns, probe_last, tw[tw.size() / 2], tw[0], te[te.size() / 2], sp,
+        printf("sig %d rows %4d grid %3d sleep %4d last %d: wall median %.3f ms (min %.3f), events %.3f ms; spins %llu; %s\n",
+               sig, rows, grid, sleep_ns, probe_last, tw[tw.size() / 2], tw[0], te[te.size() / 2], sp,
                same ? "bit-identical" : "DIFFERS");
     };
-    for (int sl : {200, 500, 2000})
-        for (int pl : {0, 1}) run(follow_kernel<1024>, 1024, nsm, sl, pl);
-    for (int pl : {0, 1}) {
-        run(follow_kernel<512>, 512, nsm, 500, pl);
-        run(follow_kernel<512>, 512, 2 * nsm, 500, pl);
-        run(follow_kernel<256>, 256, 4 * nsm, 500, pl);
-        run(follow_kernel<1024>, 1024, nsm / 2, 500, pl);
-    }
+    for (sig = 0; sig < 4; ++sig) run(follow_kernel<1024>, 1024, nsm, 500, 0);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
