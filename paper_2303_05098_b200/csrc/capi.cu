@@ -1094,8 +1094,29 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             SOB_CUDA(cudaEventCreate(&np->e1));
             SOB_CUDA(cudaEventCreate(&np->e2));
             np->ws.reset(new FeatWorkspace(*m, s));
+            np->ws->enable_fork();  // the graph gets the bins branch beside the spread chain
             SOB_CUDA(cudaStreamSynchronize(s));
             cudaStream_t ps = np->ps;
+            // which CSR sweep suits this matrix depends on how its diagonal
+            // keys repeat (banded/stencil rows: the lockstep sweep's slot
+            // cache; scattered keys: the entry-parallel sweep, e.g. a 172K-row
+            // uniform matrix 88 -> 80 us): time both once, keep the faster
+            if ((m->format == SO_CSR || m->format == SO_HDC) && m->csr.nblk > 0 && m->nrows > 0 &&
+                !std::getenv("SOB_FEAT_ENTRY")) {
+                float best[2] = {1e30f, 1e30f};
+                for (int rep = 0; rep < 2; ++rep)
+                    for (int mode = 0; mode < 2; ++mode) {
+                        np->ws->sweep = mode;
+                        SOB_CUDA(cudaEventRecord(np->e0, ps));
+                        enqueue_features(*m, ratio, np->st, ps, np->ws.get());
+                        SOB_CUDA(cudaEventRecord(np->e1, ps));
+                        SOB_CUDA(cudaEventSynchronize(np->e1));
+                        float ms = 0.f;
+                        SOB_CUDA(cudaEventElapsedTime(&ms, np->e0, np->e1));
+                        best[mode] = std::min(best[mode], ms);
+                    }
+                np->ws->sweep = best[1] < best[0] ? 1 : 0;
+            }
             cudaGraph_t g = nullptr;
             // one graph: features, predict + feasibility, with event-record
             // nodes around each so T_FE / T_PRED are device intervals of the

@@ -742,8 +742,9 @@ constexpr size_t kWalkSmem = 200 * 1024;
 inline size_t walk_smem_bytes(int64_t nrows, int64_t nch) {
     return size_t(nch) * (kSubs + 1) * sizeof(MonoRec) + size_t(nrows) * sizeof(int32_t);
 }
-
-template <bool STAGED>
+// STAGE: 0 = walk global memory, 2 = records and row counts staged in
+// shared memory (1 = records only was measured: no gain, r02l)
+template <int STAGE>
 __global__ void spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch,
                             int64_t chunk, const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine,
                             FeatState* __restrict__ st);
@@ -757,27 +758,31 @@ void ensure_walk_smem_attr() {
     SOB_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(mu);
     if (dev < 64 && (done >> dev) & 1) return;
-    SOB_CUDA(cudaFuncSetAttribute(spread_walk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWalkSmem)));
+    SOB_CUDA(cudaFuncSetAttribute(spread_walk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWalkSmem)));
     if (dev < 64) done |= uint64_t(1) << dev;
 }
 
-template <bool STAGED>
+template <int STAGE>
 __global__ void __launch_bounds__(kWalkThreads)
     spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
                 const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
-    if (STAGED) {
+    if (STAGE > 0) {
         extern __shared__ __align__(16) unsigned char wsm[];
         MonoRec* srec = reinterpret_cast<MonoRec*>(wsm);
         MonoRec* sfine = srec + nch;
-        int32_t* src = reinterpret_cast<int32_t*>(sfine + nch * kSubs);
         for (int64_t i = threadIdx.x; i < nch; i += kWalkThreads) srec[i] = rec[i];
         for (int64_t i = threadIdx.x; i < nch * kSubs; i += kWalkThreads) sfine[i] = fine[i];
-        const int4* rc4 = reinterpret_cast<const int4*>(rc);
-        int4* src4 = reinterpret_cast<int4*>(src);
-        for (int64_t i = threadIdx.x; i < nrows / 4; i += kWalkThreads) src4[i] = rc4[i];
-        for (int64_t i = (nrows / 4) * 4 + threadIdx.x; i < nrows; i += kWalkThreads) src[i] = rc[i];
+        const int32_t* walk_rc = rc;
+        if (STAGE == 2) {
+            int32_t* src = reinterpret_cast<int32_t*>(sfine + nch * kSubs);
+            const int4* rc4 = reinterpret_cast<const int4*>(rc);
+            int4* src4 = reinterpret_cast<int4*>(src);
+            for (int64_t i = threadIdx.x; i < nrows / 4; i += kWalkThreads) src4[i] = rc4[i];
+            for (int64_t i = (nrows / 4) * 4 + threadIdx.x; i < nrows; i += kWalkThreads) src[i] = rc[i];
+            walk_rc = src;
+        }
         __syncthreads();
-        if (threadIdx.x < 32) walk_and_finalize(src, nrows, ncols, nch, chunk, srec, sfine, st);
+        if (threadIdx.x < 32) walk_and_finalize(walk_rc, nrows, ncols, nch, chunk, srec, sfine, st);
     } else {
         if (threadIdx.x < 32) walk_and_finalize(rc, nrows, ncols, nch, chunk, rec, fine, st);
     }
@@ -808,6 +813,19 @@ FeatWorkspace::FeatWorkspace(const so_matrix& m, cudaStream_t s) {
     rec.alloc(nch * (1 + kSubs) * int64_t(sizeof(MonoRec)), s);  // chunk + sub-chunk records
 }
 
+FeatWorkspace::~FeatWorkspace() {
+    if (aux) cudaStreamDestroy(aux);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+}
+
+void FeatWorkspace::enable_fork() {
+    if (aux) return;
+    SOB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    SOB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    SOB_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+}
+
 void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s, FeatWorkspace* ws_in) {
     const int64_t n = m.nrows, nc = m.ncols;
     const int64_t thr = true_diag_threshold(ratio, n, nc);  // features.cpp:146-147
@@ -834,7 +852,14 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         // 126 -> 43 us, 302 -> 239 us); the row-lockstep sweep for the rest
         // (banded/stencil keys repeat across rows and its slot cache wins;
         // config 3's 4M-row R-MAT: 0.87 vs 0.93 ms entry-parallel)
-        const bool entry = ceil_div(n, 32) < int64_t(current_ctx().num_sms) * 16 || (c.nlong > 0 && n < (1 << 21));
+        static const int force_entry = [] {  // diagnostic knob (A/B): SOB_FEAT_ENTRY=1 / 0 forces a sweep
+            const char* e = std::getenv("SOB_FEAT_ENTRY");
+            return e ? std::atoi(e) : -1;
+        }();
+        const bool entry = force_entry >= 0 ? force_entry == 1
+                           : ws.sweep >= 0  ? ws.sweep == 1
+                                            : (ceil_div(n, 32) < int64_t(current_ctx().num_sms) * 16 ||
+                                               (c.nlong > 0 && n < (1 << 21)));
         if (entry && c.nblk > 0) {
             const int gb = grid_for(c.nblk * kB, kB, 4);
             // a row of more than kBigRowPieces pieces exists only if the pieces
@@ -927,25 +952,38 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     DBuf<double>& csum = ws.csum;
     DBuf<double>& P = ws.P;
     MonoRec* rec = reinterpret_cast<MonoRec*>(ws.rec.get());
+    // N_D / N_TD over the bins only feed the finalize at the end of the
+    // spread walk: with a forked workspace (the tune graph) they run on a
+    // second branch beside feat_rows -> spread_prefix -> spread_mono
+    const bool fork = ws.aux != nullptr;
+    cudaStream_t sb = fork ? ws.aux : s;
+    if (fork) {
+        SOB_CUDA(cudaEventRecord(ws.fork_ev, s));
+        SOB_CUDA(cudaStreamWaitEvent(sb, ws.fork_ev, 0));
+    }
+    if (dense_bins) {
+        feat_bins<int32_t><<<grid_for(nbins, 256), 256, 0, sb>>>(bins.get(), nbins, thr, st);
+        SOB_LAUNCH("feat_bins");
+    } else if (m.dia.ndiags) {
+        feat_bins<unsigned long long><<<grid_for(m.dia.ndiags, 256), 256, 0, sb>>>(dcount.get(), m.dia.ndiags, thr,
+                                                                                    st);
+        SOB_LAUNCH("feat_bins");
+    }
+    if (fork) SOB_CUDA(cudaEventRecord(ws.join_ev, sb));
     feat_rows<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get());
     SOB_LAUNCH("feat_rows");
-    if (dense_bins) {
-        feat_bins<int32_t><<<grid_for(nbins, 256), 256, 0, s>>>(bins.get(), nbins, thr, st);
-    } else if (m.dia.ndiags) {
-        feat_bins<unsigned long long><<<grid_for(m.dia.ndiags, 256), 256, 0, s>>>(dcount.get(), m.dia.ndiags, thr, st);
-    }
-    SOB_LAUNCH("feat_bins");
     spread_prefix<<<1, 512, 0, s>>>(csum.get(), nch, P.get());
     SOB_LAUNCH("spread_prefix");
     MonoRec* fine = rec + nch;
     spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get(), P.get(), rec, fine);
     SOB_LAUNCH("spread_mono");
+    if (fork) SOB_CUDA(cudaStreamWaitEvent(s, ws.join_ev, 0));  // the walk's finalize reads N_D / N_TD
     const size_t wsm = walk_smem_bytes(n, nch);
     if (wsm <= kWalkSmem) {
         ensure_walk_smem_attr();  // normally done by the workspace, before any capture
-        spread_walk<true><<<1, kWalkThreads, wsm, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+        spread_walk<2><<<1, kWalkThreads, wsm, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
     } else {
-        spread_walk<false><<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+        spread_walk<0><<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
     }
     SOB_LAUNCH("spread_walk");
 }

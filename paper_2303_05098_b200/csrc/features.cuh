@@ -24,7 +24,18 @@ struct FeatWorkspace {
     DBuf<unsigned long long> dcount;
     DBuf<double> csum, P;
     DBuf<unsigned char> rec;
+    // optional second branch (enable_fork, before a stream capture): the
+    // diagonal-bin reduction runs beside the spread chain instead of before it
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // CSR-part sweep: -1 = size heuristic, 0 = row-lockstep, 1 = entry-parallel
+    // (the tune plan times both once and keeps the faster, capi.cu)
+    int sweep = -1;
     FeatWorkspace(const so_matrix& m, cudaStream_t s);
+    ~FeatWorkspace();
+    FeatWorkspace(const FeatWorkspace&) = delete;
+    FeatWorkspace& operator=(const FeatWorkspace&) = delete;
+    void enable_fork();
 };
 
 // Enqueue the whole feature pipeline on stream s; the finalized vector lands in
