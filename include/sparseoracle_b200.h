@@ -107,8 +107,10 @@ typedef struct so_tune_outcome {
     int32_t source;        /* TunerKind: 1 decision_tree, 2 random_forest */
     int32_t switched;      /* chosen != active format                  */
     int32_t fallback_csr;  /* predicted format infeasible              */
-    double feature_time_seconds; /* T_FE  (device time, cudaEvent)     */
-    double predict_time_seconds; /* T_PRED (device time, cudaEvent)    */
+    double feature_time_seconds; /* T_FE  (device time: %globaltimer at
+                                    the first feature kernel's start ->
+                                    after the finalize)                  */
+    double predict_time_seconds; /* T_PRED (device time: finalize -> vote) */
     so_feature_vector features;  /* what the model saw                 */
     double wall_time_seconds;    /* host wall clock of the whole call
                                     (graph launch -> outcome on the host) */

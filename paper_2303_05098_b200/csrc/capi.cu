@@ -6,6 +6,7 @@
 // layout, and the per-device context.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -32,7 +33,7 @@ struct TunePlan {
     FeatState* st = nullptr;
     so_tune_outcome* out = nullptr;      // pinned, mapped: the predict kernel writes it over the link
     so_tune_outcome* out_dev = nullptr;  // device view of `out`
-    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;  // plan build: timing the two CSR sweeps
     // private stream the graph is captured and replayed on: a capture on the
     // shared context stream would swallow other threads' work (and the
     // replay would re-run it); nothing but this plan ever uses it
@@ -52,7 +53,6 @@ void destroy_tune_plan(TunePlan* p) {
     if (p->out) cudaFreeHost(p->out);
     if (p->e0) cudaEventDestroy(p->e0);
     if (p->e1) cudaEventDestroy(p->e1);
-    if (p->e2) cudaEventDestroy(p->e2);
     p->ws.reset();
     if (p->ps) cudaStreamDestroy(p->ps);
     delete p;
@@ -1092,7 +1092,6 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&np->out_dev), np->out, 0));
             SOB_CUDA(cudaEventCreate(&np->e0));
             SOB_CUDA(cudaEventCreate(&np->e1));
-            SOB_CUDA(cudaEventCreate(&np->e2));
             np->ws.reset(new FeatWorkspace(*m, s));
             np->ws->enable_fork();  // the graph gets the bins branch beside the spread chain
             SOB_CUDA(cudaStreamSynchronize(s));
@@ -1118,16 +1117,14 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
                 np->ws->sweep = best[1] < best[0] ? 1 : 0;
             }
             cudaGraph_t g = nullptr;
-            // one graph: features, predict + feasibility, with event-record
-            // nodes around each so T_FE / T_PRED are device intervals of the
-            // graph itself (no host submission gap inside them)
+            // one graph: features, predict + feasibility; T_FE / T_PRED are
+            // device intervals taken by the kernels themselves (%globaltimer
+            // stamps: first feature kernel -> finalize -> vote), so the graph
+            // carries no event nodes and the host no event queries
             SOB_CUDA(cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal));
             try {
-                SOB_CUDA(cudaEventRecordWithFlags(np->e0, ps, cudaEventRecordExternal));
                 enqueue_features(*m, ratio, np->st, ps, np->ws.get());
-                SOB_CUDA(cudaEventRecordWithFlags(np->e1, ps, cudaEventRecordExternal));
                 enqueue_tune_predict(*f, np->st, cfg, m->format, np->out_dev, ps);
-                SOB_CUDA(cudaEventRecordWithFlags(np->e2, ps, cudaEventRecordExternal));
             } catch (...) {
                 cudaStreamEndCapture(ps, &g);
                 if (g) cudaGraphDestroy(g);
@@ -1142,15 +1139,23 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
         // every call that produces or changes a matrix synchronises before it
         // returns (make(), conversions), so the matrix arrays are complete:
         // the replay needs no ordering against the context stream
+        static const bool trace = std::getenv("SOB_TUNE_TRACE") != nullptr;  // diagnostic knob: host phases
+        const auto t_plan = std::chrono::steady_clock::now();
         SOB_CUDA(cudaGraphLaunch(plan->exec, plan->ps));
+        const auto t_launch = std::chrono::steady_clock::now();
         SOB_CUDA(cudaStreamSynchronize(plan->ps));
-        so_tune_outcome h = *plan->out;  // written by the predict kernel (mapped host memory)
-        float fe = 0.f, pr = 0.f;
-        SOB_CUDA(cudaEventElapsedTime(&fe, plan->e0, plan->e1));
-        SOB_CUDA(cudaEventElapsedTime(&pr, plan->e1, plan->e2));
-        h.feature_time_seconds = double(fe) * 1e-3;
-        h.predict_time_seconds = double(pr) * 1e-3;
-        h.wall_time_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_entry).count();
+        const auto t_sync = std::chrono::steady_clock::now();
+        so_tune_outcome h = *plan->out;  // written by the predict kernel (mapped host memory), times included
+        const double fe = h.feature_time_seconds * 1e3, pr = h.predict_time_seconds * 1e3;
+        const auto t_end = std::chrono::steady_clock::now();
+        h.wall_time_seconds = std::chrono::duration<double>(t_end - t_entry).count();
+        if (trace) {
+            auto us = [&](std::chrono::steady_clock::time_point t) {
+                return std::chrono::duration<double, std::micro>(t - t_entry).count();
+            };
+            std::fprintf(stderr, "[tune] plan %.1f launch %.1f sync %.1f end %.1f us; fe %.1f pred %.1f us\n",
+                         us(t_plan), us(t_launch), us(t_sync), us(t_end), fe * 1e3, pr * 1e3);
+        }
         *out = h;
     });
 }

@@ -727,6 +727,9 @@ __device__ __forceinline__ void walk_and_finalize(const int32_t* __restrict__ rc
         f.nnz_row_spread = S / double(nrows);
         f.ndiags = int64_t(st->nd);
         f.ntrue_diags = int64_t(st->ntd);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        st->t_end = t;
     }
 }
 
@@ -789,6 +792,9 @@ __global__ void __launch_bounds__(kWalkThreads)
 }
 
 __global__ void feat_init(FeatState* st) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    st->t_begin = t;
     st->visits = 0;
     st->structure = 0;
     st->max_row = 0;

@@ -15,6 +15,9 @@ struct FeatState {
     double S;                      // exact sequential sum of squared deviations
     unsigned ticket;               // dynamic row-group counter of the CSR sweep
     so_feature_vector out;         // finalized vector
+    // %globaltimer (ns, 32 ns ticks on B200) at the start of the first feature
+    // kernel and after the finalize: the tuner's T_FE without event nodes
+    unsigned long long t_begin, t_end;
 };
 
 // Scratch of the feature pipeline for one matrix (reusable across calls, e.g.

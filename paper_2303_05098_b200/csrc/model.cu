@@ -219,6 +219,12 @@ __global__ void __launch_bounds__(kTB) tune_predict_kernel(ForestView f, const F
         out->switched = chosen != active;
         out->fallback_csr = fallback;
         out->features = fv;
+        // T_FE: first feature kernel's start -> finalize; T_PRED: finalize ->
+        // the vote (includes the launch gap between the two kernels)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        out->feature_time_seconds = double(st->t_end - st->t_begin) * 1e-9;
+        out->predict_time_seconds = double(t - st->t_end) * 1e-9;
     }
 }
 
