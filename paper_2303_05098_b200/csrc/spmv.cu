@@ -1031,7 +1031,21 @@ FollowStage g_follow[64];
 bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
                    const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
                    FollowToken& tok) {
-    static const bool off = std::getenv("SOB_NO_FOLLOW") != nullptr;  // diagnostic knob (A/B)
+    // SOB_NO_FOLLOW: diagnostic knob (A/B).  Under an injected CUDA tool
+    // (ncu / nsys: NV_NSIGHT_INJECTION_*, compute-sanitizer:
+    // NV_SANITIZER_INJECTION_*, or CUDA_INJECTION64_PATH) kernels may be
+    // serialised against the copy the kernel follows -- every call would wait
+    // for the timeout -- so the zero-copy kernel runs instead.
+    // SOB_FOLLOW_UNDER_TOOLS=1 keeps it (the sanitizer driver: a timed-out
+    // call falls back and stays correct).
+    static const bool off = [] {
+        if (std::getenv("SOB_NO_FOLLOW")) return true;
+        if (std::getenv("SOB_FOLLOW_UNDER_TOOLS")) return false;
+        for (const char* v : {"CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                              "NV_SANITIZER_INJECTION_TRANSPORT_TYPE", "NV_TPS_LAUNCH_TOKEN"})
+            if (std::getenv(v)) return true;
+        return false;
+    }();
     if (off) return false;
     if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
     if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
@@ -1071,8 +1085,8 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
     const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
     const int64_t per = rows_per_chunk > 0 ? rows_per_chunk / kZcRows : nblk;  // blocks per launch
-    // 2 s plus 1 ns per byte of x (a slowly staged pageable x still arrives)
-    const unsigned long long timeout = 2000ull * 1000 * 1000 + 8ull * uint64_t(nc);
+    // 250 ms plus 1 ns per byte of x (a slowly staged pageable x still arrives)
+    const unsigned long long timeout = 250ull * 1000 * 1000 + 8ull * uint64_t(nc);
     for (int64_t b0 = 0, j = 0; b0 < nblk; b0 += per, ++j) {
         const int64_t b1 = std::min(nblk, b0 + per);
         const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));

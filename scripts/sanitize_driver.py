@@ -23,6 +23,11 @@ import os
 import sys
 import tempfile
 
+# the pinned-buffer case exercises the follow-the-copy kernel even under the
+# sanitizer (which may serialise it against the copy: the call then times out
+# and falls back -- slower, still correct)
+os.environ.setdefault("SOB_FOLLOW_UNDER_TOOLS", "1")
+
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
