@@ -735,3 +735,29 @@ def test_pageable_host_spmv_staging(so, O, shape):
         want = m.spmv(z)
         m.spmv_into(z, z)
         assert np.array_equal(z, want)
+
+
+def test_cpu_baseline_bytes_match_device_accounting(so, O):
+    """scripts/cpu_baseline.py credits the reference CPU path with the same
+    algorithmic bytes as the device roofline: its numpy
+    formula over the reference's own converted arrays must equal
+    so_spmv_bytes of the device matrix, format by format."""
+    import importlib.util
+    import os
+    from paper_2303_05098_b200 import synth
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "cpu_baseline.py")
+    spec = importlib.util.spec_from_file_location("_cpu_baseline", path)
+    cb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(cb)
+    shapes = {"band": synth.banded(20_000, 5, seed=3), "lap": synth.laplacian_2d(120, seed=1),
+              "rmat": synth.rmat(13, 8, seed=5), "hyb": synth.hyb_skewed(30_000, 8, 40, 50, seed=6)}
+    for name, csr in shapes.items():
+        base = O.RefMatrix.raw_coo(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
+        d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+        for f in range(6):
+            try:
+                ref = base.from_coo(f)
+            except O.RefError:
+                continue
+            assert cb.algorithmic_bytes(ref.export()) == d.convert(f).spmv_bytes, (name, f)
