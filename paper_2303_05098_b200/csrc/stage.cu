@@ -396,7 +396,11 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
         }
         worker(pool.size());  // then help with the y copies
     });
-    if (err) std::rethrow_exception(err);
+    if (err) {  // the copy stream may still read the staging buffers: drain both before they are released
+        cudaStreamSynchronize(s);
+        cudaStreamSynchronize(ctx(dev).copy_in);
+        std::rethrow_exception(err);
+    }
     if (yerr) {
         cudaStreamSynchronize(s);
         std::rethrow_exception(yerr);
