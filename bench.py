@@ -159,45 +159,90 @@ def cpu_model():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region.
+
+    NVML (pynvml, microseconds per query) polled every ~0.5 ms from a thread,
+    so even a few-millisecond timed region gets samples inside it; the first
+    sample is taken before start() returns.  Falls back to nvidia-smi (tens
+    of ms per query) when NVML is unavailable.  The NVML device is the CUDA
+    device's PCI bus id (CUDA and NVML ordinals differ under
+    CUDA_VISIBLE_DEVICES)."""
+
+    NAMES = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+             ("sw_power_cap", 0x4))
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, sm_max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        self.source = "nvidia-smi"
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            try:
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = (pynvml, h)
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        pynvml, h = self._nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.samples.append((float(sm), float(mx), int(rs)))
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        if out:
+            f = [v.strip() for v in out.split(",")]
+            if f[0].replace(".", "").isdigit() and f[1].replace(".", "").isdigit():
+                mask = sum(bit for (_, bit), v in zip(self.NAMES, f[2:]) if v.lower().startswith("active"))
+                self.samples.append((float(f[0]), float(f[1]), mask))
+
+    def _sample(self):
+        try:
+            self._sample_nvml() if self._nvml else self._sample_smi()
+        except Exception:
+            pass
 
     def start(self):
+        self._sample()  # one sample before the timed region starts
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+            self._sample()
+            self._stop.wait(0.0005 if self._nvml else 0.2)
 
     def stop(self):
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > i + 2 and s[i + 2].lower().startswith("active")})
+        self._sample()  # and one right after
+        sm = [v[0] for v in self.samples]
+        mx = [v[1] for v in self.samples]
+        reasons = sorted({name for v in self.samples for name, bit in self.NAMES if v[2] & bit})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": self.source}
 
 
 def dist_setup():
