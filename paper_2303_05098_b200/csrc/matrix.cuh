@@ -165,11 +165,10 @@ bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped,
 // launch), calling after_chunk(j) after launch j (e.g. to record an event) --
 // then calls upload(dx) to enqueue the caller's H2D copies of x into dx on
 // `copy`, then the copy-complete flag and the sentinel refill.  After s is
-// synchronised, follow_finish unlocks and returns false when the copy never
-// arrived (y invalid).
+// synchronised (on any thread), follow_finish returns false when the copy
+// never arrived (y invalid).
 struct FollowToken {
-    std::unique_lock<std::mutex> lk;
-    unsigned* timed_out = nullptr;
+    unsigned* timed_out = nullptr;  // this call's timeout word (mapped)
 };
 bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
                    const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,

@@ -1015,14 +1015,21 @@ namespace {
 // Per-device state of the follow path: the sentinel-filled device copy of x
 // (grow-only), the copy-complete flag, the pinned word copied into it, the
 // mapped timeout word, and the event after which the copy may refill x.
+// The mutex covers only the enqueueing (follow_launch returns with it
+// released, so the pageable path may finish a call on another thread);
+// calls on the same device are ordered through the events: a call's upload
+// AND kernel wait for the previous call's sentinel refill.  Each call gets
+// its own timeout word (a ring of kFollowSlots mapped words).
+constexpr int kFollowSlots = 64;
 struct FollowStage {
     std::mutex mu;
     double* dx = nullptr;
     int64_t cap = 0;
     unsigned* flag = nullptr;
     unsigned* one_host = nullptr;
-    unsigned* timed_out = nullptr;  // pinned + mapped
+    unsigned* timed_out = nullptr;  // [kFollowSlots], pinned + mapped
     unsigned* timed_out_dev = nullptr;
+    unsigned next_slot = 0;
     cudaEvent_t refilled = nullptr, copied = nullptr;
 };
 FollowStage g_follow[64];
@@ -1055,22 +1062,26 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
     const int64_t nc = m.ncols;
     FollowStage& f = g_follow[m.device];
-    tok.lk = std::unique_lock<std::mutex>(f.mu);
+    std::lock_guard<std::mutex> lk(f.mu);
     if (!f.flag) {
         SOB_CUDA(cudaMalloc(reinterpret_cast<void**>(&f.flag), sizeof(unsigned)));
         SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.one_host), sizeof(unsigned), cudaHostAllocPortable));
         *f.one_host = 1;
-        SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.timed_out), sizeof(unsigned),
+        SOB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.timed_out), kFollowSlots * sizeof(unsigned),
                                cudaHostAllocMapped | cudaHostAllocPortable));
-        *f.timed_out = 0;
+        for (int i = 0; i < kFollowSlots; ++i) f.timed_out[i] = 0;
         SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&f.timed_out_dev), f.timed_out, 0));
         SOB_CUDA(cudaEventCreateWithFlags(&f.refilled, cudaEventDisableTiming));
         SOB_CUDA(cudaEventCreateWithFlags(&f.copied, cudaEventDisableTiming));
     }
-    tok.timed_out = f.timed_out;
+    const unsigned slot = f.next_slot++ % kFollowSlots;
+    f.timed_out[slot] = 0;
+    tok.timed_out = f.timed_out + slot;
     const int grid_fill = current_ctx().num_sms * 4;
+    // everything of the previous call (its kernel, copy and refill, possibly
+    // on another stream) precedes this call's use -- or release -- of dx
+    if (f.dx) SOB_CUDA(cudaStreamWaitEvent(s, f.refilled, 0));
     if (f.cap < nc) {
-        // the previous buffer may still be read by an earlier call's kernel: order its release on s
         if (f.dx) SOB_CUDA(cudaFreeAsync(f.dx, s));
         f.dx = nullptr;
         f.cap = 0;
@@ -1080,7 +1091,7 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
         SOB_LAUNCH("follow_fill");
         SOB_CUDA(cudaEventRecord(f.refilled, s));
     }
-    // uploads may start once the device copy holds sentinels again
+    // the upload starts once the device copy holds sentinels again
     SOB_CUDA(cudaStreamWaitEvent(copy, f.refilled, 0));
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
     const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
@@ -1092,7 +1103,7 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
         const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));
         dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags),
                                                       m.dia.offsets.get(), m.dia.values.get(), f.dx, y_mapped, f.flag,
-                                                      int(omin), int(omax), f.timed_out_dev, timeout, int(b0),
+                                                      int(omin), int(omax), f.timed_out_dev + slot, timeout, int(b0),
                                                       int(b1));
         SOB_LAUNCH("dia_follow_kernel");
         if (after_chunk) (*after_chunk)(j);
@@ -1112,10 +1123,8 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
 bool follow_finish(FollowToken& tok) {
     bool ok = true;
     if (tok.timed_out && *reinterpret_cast<volatile unsigned*>(tok.timed_out)) {
-        *tok.timed_out = 0;
         ok = false;
     }
-    if (tok.lk.owns_lock()) tok.lk.unlock();
     return ok;
 }
 

@@ -761,3 +761,53 @@ def test_cpu_baseline_bytes_match_device_accounting(so, O):
             except O.RefError:
                 continue
             assert cb.algorithmic_bytes(ref.export()) == d.convert(f).spmv_bytes, (name, f)
+
+
+def test_follow_path_concurrent_callers(so, O):
+    """Pinned and pageable spmv(m, x) from several host threads at once on two
+    narrow-window DIA matrices (the follow-the-copy path shares one device
+    copy of x per device: calls are ordered through its refill event, each
+    with its own timeout word): every result equals the device multiply."""
+    import threading
+
+    import torch
+    from paper_2303_05098_b200 import synth
+
+    mats = []
+    for n, half in ((600_000, 3), (700_000, 6)):
+        csr = synth.banded(n, half, seed=n)
+        d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val).convert(so.DIA)
+        mats.append((d, csr.ncols))
+    errors = []
+
+    def worker(t):
+        try:
+            rng = np.random.default_rng(100 + t)
+            d, nc = mats[t % 2]
+            pinned = t % 3 != 2
+            for _ in range(6):
+                xv = rng.uniform(-1, 1, nc)
+                if pinned:
+                    xt = torch.from_numpy(xv).pin_memory()
+                    yt = torch.empty(d.nrows, dtype=torch.float64).pin_memory()
+                    d.spmv_into(xt.numpy(), yt.numpy())
+                    got = yt.numpy().copy()
+                else:
+                    got = d.spmv(xv)
+                xd = torch.tensor(xv, device="cuda")
+                yd = torch.empty(d.nrows, dtype=torch.float64, device="cuda")
+                torch.cuda.synchronize()
+                d.spmv_device(xd.data_ptr(), yd.data_ptr())
+                torch.cuda.synchronize()
+                ref = yd.cpu().numpy()
+                if not np.array_equal(got, ref):
+                    errors.append((t, "mismatch"))
+        except Exception as e:  # noqa: BLE001
+            errors.append((t, repr(e)))
+
+    ths = [threading.Thread(target=worker, args=(t,)) for t in range(6)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join(timeout=300)
+    assert not errors, errors
