@@ -38,6 +38,33 @@ void count_launch();
 
 void set_error(const std::string& m);
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// launch_pdl may be scheduled while its predecessor on the stream is still
+// running; pdl_enter() -- the first statement of every such kernel -- waits
+// for the predecessor's completion and memory (griddepcontrol.wait) and lets
+// the NEXT kernel be scheduled as soon as all of this kernel's CTAs have
+// started (griddepcontrol.launch_dependents).  A no-op for kernels launched
+// without the attribute.  Used for the feature / tune chain, where the
+// kernels are short and the launch latency between them is a large share.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 // NVTX range over a C-ABI call (convert / features / predict / tune / SpMV /
 // dist iterate), visible in nsys / ncu --nvtx timelines; header-only NVTX v3,
 // a no-op unless a tool is attached (SURVEY §5 tracing).

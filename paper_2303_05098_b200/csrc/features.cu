@@ -116,6 +116,7 @@ template <bool ACCUM_RC>
 __global__ void __launch_bounds__(kB)
     feat_csr_entries(const int32_t* __restrict__ blk, int64_t nblk, const int64_t* __restrict__ rp,
                      FeatCsrOp<ACCUM_RC> op, int64_t big_row) {
+    pdl_enter();
     __shared__ int64_t srp[kRowsPerBlock + 1];
     op.begin();
     for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(kB)
 __global__ void __launch_bounds__(kB)
     feat_coo(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
              int32_t* __restrict__ rc, int32_t* __restrict__ bins, FeatState* __restrict__ st) {
+    pdl_enter();
     __shared__ SmemHash h;
     hash_init(h);
     __syncthreads();
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(kB)
 __global__ void __launch_bounds__(kB)
     feat_ell(int64_t nrows, int width, const int32_t* __restrict__ ecol, int32_t* __restrict__ rc,
              int32_t* __restrict__ bins, FeatState* __restrict__ st) {
+    pdl_enter();
     __shared__ SmemHash h;
     hash_init(h);
     __syncthreads();
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(kB)
     feat_dia(int64_t nrows, int64_t ncols, int nd, const int64_t* __restrict__ off,
              const double* __restrict__ vals, int32_t* __restrict__ rc,
              unsigned long long* __restrict__ dcount, FeatState* __restrict__ st) {
+    pdl_enter();
     __shared__ unsigned long long sdc[kMaxSmemDiag];
     __shared__ int64_t soff[kMaxSmemDiag];
     const int nsm = nd < kMaxSmemDiag ? nd : kMaxSmemDiag;
@@ -261,6 +265,7 @@ __global__ void __launch_bounds__(kB)
 // HDC: fold the DIA part's per-diagonal counts into the dense bins.
 __global__ void dcount_to_bins(const unsigned long long* __restrict__ dcount, const int64_t* __restrict__ off,
                                int nd, int64_t nrows, int32_t* __restrict__ bins) {
+    pdl_enter();
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d < nd && dcount[d]) atomicAdd(bins + (off[d] + nrows - 1), int32_t(dcount[d]));
 }
@@ -275,6 +280,7 @@ __device__ __forceinline__ double sq_dev(int32_t c, double avg) {
 __global__ void __launch_bounds__(kB)
     feat_rows(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, FeatState* __restrict__ st,
               double* __restrict__ csum) {
+    pdl_enter();
     const double avg = double(st->visits) / double(nrows);
     const int64_t base = int64_t(blockIdx.x) * chunk;
     int mx = 0, mn = INT32_MAX;
@@ -316,6 +322,7 @@ __global__ void __launch_bounds__(kB)
 // counts >= 1 -> N_D, counts >= thr -> N_TD (features.cpp:146-151)
 template <typename T>
 __global__ void feat_bins(const T* __restrict__ bins, int64_t nbins, int64_t thr, FeatState* __restrict__ st) {
+    pdl_enter();
     unsigned long long nd = 0, ntd = 0;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nbins; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t c = int64_t(bins[i]);
@@ -451,6 +458,7 @@ struct MonoRec {
 // exclusive prefix of the chunk sums (approximate S at chunk starts)
 __global__ void __launch_bounds__(512) spread_prefix(const double* __restrict__ csum, int64_t nch,
                                                        double* __restrict__ P) {
+    pdl_enter();
     __shared__ double wt[33];
     double carry = 0.0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -577,6 +585,7 @@ __global__ void __launch_bounds__(kB)
     spread_mono(const int32_t* __restrict__ rc, int64_t nrows, int64_t chunk, const FeatState* __restrict__ st,
                 const double* __restrict__ csum, const double* __restrict__ P, MonoRec* __restrict__ rec,
                 MonoRec* __restrict__ fine) {
+    pdl_enter();
     const int64_t c = blockIdx.x;
     const double avg = double(st->visits) / double(nrows);
     mono_chunk(c, rc, nrows, chunk, avg, csum[c], P[c], rec, fine);
@@ -769,6 +778,7 @@ template <int STAGE>
 __global__ void __launch_bounds__(kWalkThreads)
     spread_walk(const int32_t* __restrict__ rc, int64_t nrows, int64_t ncols, int64_t nch, int64_t chunk,
                 const MonoRec* __restrict__ rec, const MonoRec* __restrict__ fine, FeatState* __restrict__ st) {
+    pdl_enter();
     if (STAGE > 0) {
         extern __shared__ __align__(16) unsigned char wsm[];
         MonoRec* srec = reinterpret_cast<MonoRec*>(wsm);
@@ -791,7 +801,17 @@ __global__ void __launch_bounds__(kWalkThreads)
     }
 }
 
-__global__ void feat_init(FeatState* st) {
+// The state, and the scratch every sweep accumulates into (dense diagonal
+// bins, DIA diagonal counts, COO row counts), zeroed in one launch (the
+// chain stays kernel -> kernel for programmatic dependent launch).
+__global__ void feat_init(FeatState* st, int32_t* bins, int64_t nbins, unsigned long long* dcount, int64_t nd,
+                          int32_t* rc, int64_t nrc) {
+    pdl_enter();
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nbins; i += stride) bins[i] = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nd; i += stride) dcount[i] = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nrc; i += stride) rc[i] = 0;
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     st->t_begin = t;
@@ -835,9 +855,6 @@ void FeatWorkspace::enable_fork() {
 void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStream_t s, FeatWorkspace* ws_in) {
     const int64_t n = m.nrows, nc = m.ncols;
     const int64_t thr = true_diag_threshold(ratio, n, nc);  // features.cpp:146-147
-    feat_init<<<1, 1, 0, s>>>(st);
-    SOB_LAUNCH("feat_init");
-
     std::unique_ptr<FeatWorkspace> own;
     if (!ws_in) own.reset(new FeatWorkspace(m, s));
     FeatWorkspace& ws = ws_in ? *ws_in : *own;
@@ -845,9 +862,14 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
     const bool dense_bins = m.format != SO_DIA;
     const int64_t nbins = n + nc;
     DBuf<int32_t>& bins = ws.bins;
-    if (dense_bins) SOB_CUDA(cudaMemsetAsync(bins.get(), 0, bins.bytes(), s));
     DBuf<unsigned long long>& dcount = ws.dcount;
-    if (dcount.n) SOB_CUDA(cudaMemsetAsync(dcount.get(), 0, dcount.bytes(), s));
+    {
+        const int64_t zb = dense_bins ? bins.n : 0, zr = m.format == SO_COO ? rc.n : 0;
+        const int64_t most = std::max<int64_t>({zb, dcount.n, zr, 1});
+        launch_pdl(feat_init, dim3(unsigned(grid_for(most, 256, 4))), dim3(256), 0, s, st, bins.get(), zb,
+                   dcount.get(), dcount.n, rc.get(), zr);
+        SOB_LAUNCH("feat_init");
+    }
     const int grid_rows = grid_for(n, kB, 4);
 
     auto scan_csr = [&](bool accum) {
@@ -875,16 +897,16 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
             const int64_t big_row = big ? kBigRowPieces * kPiece : INT64_MAX;
             if (accum) {
                 FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-                feat_csr_entries<true><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
+                launch_pdl(feat_csr_entries<true>, dim3(gb), dim3(kB), 0, s, c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
             } else {
                 FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-                feat_csr_entries<false><<<gb, kB, 0, s>>>(c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
+                launch_pdl(feat_csr_entries<false>, dim3(gb), dim3(kB), 0, s, c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
             }
             SOB_LAUNCH("feat_csr_entries");
             if (big) {
                 FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-                piece_sweep<FeatCsrOp<false>><<<unsigned(c.npieces), 256, 0, s>>>(
-                    c.piece_k.get(), c.long_row.get(), c.long_piece.get(), c.nlong, op, kBigRowPieces);
+                launch_pdl(piece_sweep<FeatCsrOp<false>>, dim3(unsigned(c.npieces)), dim3(256), 0, s, c.piece_k.get(),
+                           c.long_row.get(), c.long_piece.get(), c.nlong, op, kBigRowPieces);
                 SOB_LAUNCH("feat_csr_pieces");
             }
             return;
@@ -895,38 +917,40 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         unsigned* ticket = c.nlong > 0 ? &st->ticket : nullptr;  // skewed rows: dynamic groups
         if (accum) {
             FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep_cols<FeatCsrOp<true>><<<g, 256, 0, s>>>(c.row_ptr.get(), c.col.get(), n, op, skip, ticket);
+            launch_pdl(row_sweep_cols<FeatCsrOp<true>>, dim3(g), dim3(256), 0, s, c.row_ptr.get(), c.col.get(), n, op, skip,
+                       ticket);
         } else {
             FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            row_sweep_cols<FeatCsrOp<false>><<<g, 256, 0, s>>>(c.row_ptr.get(), c.col.get(), n, op, skip, ticket);
+            launch_pdl(row_sweep_cols<FeatCsrOp<false>>, dim3(g), dim3(256), 0, s, c.row_ptr.get(), c.col.get(), n, op, skip,
+                       ticket);
         }
         SOB_LAUNCH("feat_csr");
         if (c.nlong > 0) {
             FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
-            piece_sweep<FeatCsrOp<false>><<<unsigned(c.npieces), 256, 0, s>>>(c.piece_k.get(), c.long_row.get(),
-                                                                              c.long_piece.get(), c.nlong, op);
+            launch_pdl(piece_sweep<FeatCsrOp<false>>, dim3(unsigned(c.npieces)), dim3(256), 0, s, c.piece_k.get(),
+                       c.long_row.get(), c.long_piece.get(), c.nlong, op, int64_t(0));
             SOB_LAUNCH("feat_csr_pieces");
         }
     };
     auto scan_dia = [&]() {
-        feat_dia<<<grid_rows, kB, 0, s>>>(n, nc, int(m.dia.ndiags), m.dia.offsets.get(), m.dia.values.get(),
-                                          rc.get(), dcount.get(), st);
+        launch_pdl(feat_dia, dim3(grid_rows), dim3(kB), 0, s, n, nc, int(m.dia.ndiags), m.dia.offsets.get(),
+                   m.dia.values.get(), rc.get(), dcount.get(), st);
         SOB_LAUNCH("feat_dia");
     };
     auto scan_ell = [&]() {
-        feat_ell<<<grid_rows, kB, 0, s>>>(n, int(m.ell.width), m.ell.col.get(), rc.get(), bins.get(), st);
+        launch_pdl(feat_ell, dim3(grid_rows), dim3(kB), 0, s, n, int(m.ell.width), m.ell.col.get(), rc.get(),
+                   bins.get(), st);
         SOB_LAUNCH("feat_ell");
     };
     auto scan_coo = [&]() {
         if (m.coo.nnz == 0) return;
-        feat_coo<<<grid_for(m.coo.nnz, kB, 4), kB, 0, s>>>(m.coo.nnz, n, m.coo.row.get(), m.coo.col.get(),
-                                                            rc.get(), bins.get(), st);
+        launch_pdl(feat_coo, dim3(grid_for(m.coo.nnz, kB, 4)), dim3(kB), 0, s, m.coo.nnz, n, m.coo.row.get(),
+                   m.coo.col.get(), rc.get(), bins.get(), st);
         SOB_LAUNCH("feat_coo");
     };
 
     switch (m.format) {
-        case SO_COO:
-            SOB_CUDA(cudaMemsetAsync(rc.get(), 0, rc.bytes(), s));
+        case SO_COO:  // rc zeroed by feat_init
             scan_coo();
             break;
         case SO_CSR:
@@ -945,8 +969,8 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         case SO_HDC:
             scan_dia();
             if (m.dia.ndiags) {
-                dcount_to_bins<<<unsigned(ceil_div(m.dia.ndiags, 256)), 256, 0, s>>>(
-                    dcount.get(), m.dia.offsets.get(), int(m.dia.ndiags), n, bins.get());
+                launch_pdl(dcount_to_bins, dim3(unsigned(ceil_div(m.dia.ndiags, 256))), dim3(256), 0, s,
+                           dcount.get(), m.dia.offsets.get(), int(m.dia.ndiags), n, bins.get());
                 SOB_LAUNCH("dcount_to_bins");
             }
             scan_csr(true);
@@ -968,28 +992,29 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         SOB_CUDA(cudaStreamWaitEvent(sb, ws.fork_ev, 0));
     }
     if (dense_bins) {
-        feat_bins<int32_t><<<grid_for(nbins, 256), 256, 0, sb>>>(bins.get(), nbins, thr, st);
+        launch_pdl(feat_bins<int32_t>, dim3(grid_for(nbins, 256)), dim3(256), 0, sb, bins.get(), nbins, thr, st);
         SOB_LAUNCH("feat_bins");
     } else if (m.dia.ndiags) {
-        feat_bins<unsigned long long><<<grid_for(m.dia.ndiags, 256), 256, 0, sb>>>(dcount.get(), m.dia.ndiags, thr,
-                                                                                    st);
+        launch_pdl(feat_bins<unsigned long long>, dim3(grid_for(m.dia.ndiags, 256)), dim3(256), 0, sb, dcount.get(),
+                   m.dia.ndiags, thr, st);
         SOB_LAUNCH("feat_bins");
     }
     if (fork) SOB_CUDA(cudaEventRecord(ws.join_ev, sb));
-    feat_rows<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get());
+    launch_pdl(feat_rows, dim3(unsigned(nch)), dim3(kB), 0, s, rc.get(), n, chunk, st, csum.get());
     SOB_LAUNCH("feat_rows");
-    spread_prefix<<<1, 512, 0, s>>>(csum.get(), nch, P.get());
+    launch_pdl(spread_prefix, dim3(1), dim3(512), 0, s, csum.get(), nch, P.get());
     SOB_LAUNCH("spread_prefix");
     MonoRec* fine = rec + nch;
-    spread_mono<<<unsigned(nch), kB, 0, s>>>(rc.get(), n, chunk, st, csum.get(), P.get(), rec, fine);
+    launch_pdl(spread_mono, dim3(unsigned(nch)), dim3(kB), 0, s, rc.get(), n, chunk, st, csum.get(), P.get(), rec,
+               fine);
     SOB_LAUNCH("spread_mono");
     if (fork) SOB_CUDA(cudaStreamWaitEvent(s, ws.join_ev, 0));  // the walk's finalize reads N_D / N_TD
     const size_t wsm = walk_smem_bytes(n, nch);
     if (wsm <= kWalkSmem) {
         ensure_walk_smem_attr();  // normally done by the workspace, before any capture
-        spread_walk<2><<<1, kWalkThreads, wsm, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+        launch_pdl(spread_walk<2>, dim3(1), dim3(kWalkThreads), wsm, s, rc.get(), n, nc, nch, chunk, rec, fine, st);
     } else {
-        spread_walk<0><<<1, 32, 0, s>>>(rc.get(), n, nc, nch, chunk, rec, fine, st);
+        launch_pdl(spread_walk<0>, dim3(1), dim3(32), 0, s, rc.get(), n, nc, nch, chunk, rec, fine, st);
     }
     SOB_LAUNCH("spread_walk");
 }

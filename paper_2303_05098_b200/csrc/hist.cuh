@@ -235,6 +235,7 @@ __device__ __forceinline__ int64_t next_group(unsigned* ticket) {
 template <class Op>
 __global__ void __launch_bounds__(256) row_sweep(const int64_t* __restrict__ rp, int64_t nrows, Op op,
                                                  int64_t skip_above = INT64_MAX, unsigned* ticket = nullptr) {
+    pdl_enter();
     op.begin();
     const int lane = int(threadIdx.x & 31u);
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / 32);
@@ -271,6 +272,7 @@ template <class Op>
 __global__ void __launch_bounds__(256) row_sweep_cols(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                       int64_t nrows, Op op, int64_t skip_above = INT64_MAX,
                                                       unsigned* ticket = nullptr) {
+    pdl_enter();
     constexpr int U = 8;
     op.begin();
     const int lane = int(threadIdx.x & 31u);
@@ -340,6 +342,7 @@ template <class Op>
 __global__ void __launch_bounds__(256) piece_sweep(const int64_t* __restrict__ pk, const int32_t* __restrict__ lrow,
                                                    const int64_t* __restrict__ lpiece, int64_t nlong, Op op,
                                                    int64_t min_pieces = 0) {
+    pdl_enter();
     const int64_t k0 = pk[2 * blockIdx.x], k1 = pk[2 * blockIdx.x + 1];
     // row of this piece: the long row whose piece range holds blockIdx.x
     int64_t lo = 0, hi = nlong;

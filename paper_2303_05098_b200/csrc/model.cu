@@ -200,6 +200,7 @@ __device__ bool d_feasible(int target, const so_feature_vector& f, const CapCfg&
 
 __global__ void __launch_bounds__(kTB) tune_predict_kernel(ForestView f, const FeatState* __restrict__ st, CapCfg cfg,
                                                            int active, so_tune_outcome* __restrict__ out) {
+    pdl_enter();
     __shared__ double row[10];
     if (threadIdx.x == 0) to_row(st->out, row);
     __syncthreads();
@@ -364,7 +365,7 @@ void predict_rows_blocked(const so_forest& f, const double* rows_dev, int64_t n,
 void enqueue_tune_predict(const so_forest& f, const FeatState* st, const so_conversion_config& cfg, int active,
                           so_tune_outcome* out_dev, cudaStream_t s) {
     CapCfg c{cfg.kh_override, cfg.max_padding_factor, cfg.max_padded_entries};
-    tune_predict_kernel<<<1, kTB, 0, s>>>(view(f), st, c, active, out_dev);
+    launch_pdl(tune_predict_kernel, dim3(1), dim3(kTB), 0, s, view(f), st, c, active, out_dev);
     SOB_LAUNCH("tune_predict_kernel");
 }
 
