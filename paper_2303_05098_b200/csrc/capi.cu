@@ -1099,22 +1099,33 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
             // which CSR sweep suits this matrix depends on how its diagonal
             // keys repeat (banded/stencil rows: the lockstep sweep's slot
             // cache; scattered keys: the entry-parallel sweep, e.g. a 172K-row
-            // uniform matrix 88 -> 80 us): time both once, keep the faster
+            // uniform matrix 88 -> 80 us, or straight global atomics): time
+            // the three once, keep the fastest
             if ((m->format == SO_CSR || m->format == SO_HDC) && m->csr.nblk > 0 && m->nrows > 0 &&
                 !std::getenv("SOB_FEAT_ENTRY")) {
-                float best[2] = {1e30f, 1e30f};
+                float best[3] = {1e30f, 1e30f, 1e30f};
+                auto time_mode = [&](int mode) {
+                    np->ws->sweep = mode;
+                    SOB_CUDA(cudaEventRecord(np->e0, ps));
+                    enqueue_features(*m, ratio, np->st, ps, np->ws.get());
+                    SOB_CUDA(cudaEventRecord(np->e1, ps));
+                    SOB_CUDA(cudaEventSynchronize(np->e1));
+                    float ms = 0.f;
+                    SOB_CUDA(cudaEventElapsedTime(&ms, np->e0, np->e1));
+                    best[mode] = std::min(best[mode], ms);
+                };
+                time_mode(0);
+                // straight global atomics only pay off when keys barely repeat
+                // (R-MAT: ~9 entries per diagonal); on banded / stencil rows
+                // every entry of a diagonal would hit one address (config 2:
+                // 36 ms), so that mode is not even timed there
+                so_feature_vector fv{};
+                SOB_CUDA(cudaMemcpy(&fv, &np->st->out, sizeof(fv), cudaMemcpyDeviceToHost));
+                const bool try_direct = fv.ndiags > 0 && fv.nnz <= 64 * fv.ndiags;
                 for (int rep = 0; rep < 2; ++rep)
-                    for (int mode = 0; mode < 2; ++mode) {
-                        np->ws->sweep = mode;
-                        SOB_CUDA(cudaEventRecord(np->e0, ps));
-                        enqueue_features(*m, ratio, np->st, ps, np->ws.get());
-                        SOB_CUDA(cudaEventRecord(np->e1, ps));
-                        SOB_CUDA(cudaEventSynchronize(np->e1));
-                        float ms = 0.f;
-                        SOB_CUDA(cudaEventElapsedTime(&ms, np->e0, np->e1));
-                        best[mode] = std::min(best[mode], ms);
-                    }
-                np->ws->sweep = best[1] < best[0] ? 1 : 0;
+                    for (int mode = 0; mode < 3; ++mode)
+                        if (mode != 2 || try_direct) time_mode(mode);
+                np->ws->sweep = int(std::min_element(best, best + 3) - best);
             }
             cudaGraph_t g = nullptr;
             // one graph: features, predict + feasibility; T_FE / T_PRED are

@@ -75,9 +75,19 @@ struct FeatCsrOp {
     __device__ void piece(int r, int64_t k, bool valid) {
         if (valid) atomicAdd(bins + (int64_t(col[k]) - r + nrows - 1), 1);
     }
-    __device__ bool scattered() const { return __shfl_sync(0xffffffffu, h->used >= kHashSlots / 2, 0); }
+    // all_direct (sweep mode 2, the tune plan's choice for matrices whose
+    // keys barely repeat): every entry is a global atomic, no hash probing
+    bool all_direct;
+    __device__ bool scattered() const {
+        return all_direct || __shfl_sync(0xffffffffu, h->used >= kHashSlots / 2, 0);
+    }
     __device__ void direct(int r, int32_t c, bool valid) {
-        if (valid) hash_insert_one(*h, bins, int32_t(int64_t(c) - r + nrows - 1), 1);
+        if (!valid) return;
+        const int32_t key = int32_t(int64_t(c) - r + nrows - 1);
+        if (all_direct)
+            atomicAdd(bins + key, 1);
+        else
+            hash_insert_one(*h, bins, key, 1);
     }
     SlotCache cache;
     static constexpr bool kHasEntry8 = true;
@@ -880,7 +890,7 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         // 126 -> 43 us, 302 -> 239 us); the row-lockstep sweep for the rest
         // (banded/stencil keys repeat across rows and its slot cache wins;
         // config 3's 4M-row R-MAT: 0.87 vs 0.93 ms entry-parallel)
-        static const int force_entry = [] {  // diagnostic knob (A/B): SOB_FEAT_ENTRY=1 / 0 forces a sweep
+        static const int force_entry = [] {  // diagnostic knob (A/B): SOB_FEAT_ENTRY=0/1/2 forces a sweep
             const char* e = std::getenv("SOB_FEAT_ENTRY");
             return e ? std::atoi(e) : -1;
         }();
@@ -896,15 +906,15 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
             const bool big = !no_big && c.nlong > 0 && c.npieces - c.nlong >= kBigRowPieces;
             const int64_t big_row = big ? kBigRowPieces * kPiece : INT64_MAX;
             if (accum) {
-                FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+                FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0, false};
                 launch_pdl(feat_csr_entries<true>, dim3(gb), dim3(kB), 0, s, c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
             } else {
-                FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+                FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0, false};
                 launch_pdl(feat_csr_entries<false>, dim3(gb), dim3(kB), 0, s, c.blk.get(), c.nblk, c.row_ptr.get(), op, big_row);
             }
             SOB_LAUNCH("feat_csr_entries");
             if (big) {
-                FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+                FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0, false};
                 launch_pdl(piece_sweep<FeatCsrOp<false>>, dim3(unsigned(c.npieces)), dim3(256), 0, s, c.piece_k.get(),
                            c.long_row.get(), c.long_piece.get(), c.nlong, op, kBigRowPieces);
                 SOB_LAUNCH("feat_csr_pieces");
@@ -915,18 +925,20 @@ void enqueue_features(const so_matrix& m, double ratio, FeatState* st, cudaStrea
         // long rows (SpMV pieces) are swept piece-parallel instead of by one warp
         const int64_t skip = c.nlong > 0 ? int64_t(c.grp_cap) : INT64_MAX;
         unsigned* ticket = c.nlong > 0 ? &st->ticket : nullptr;  // skewed rows: dynamic groups
+        // sweep mode 2: every entry straight to the global bins (no hash)
+        const bool all_direct = force_entry == 2 || (force_entry < 0 && ws.sweep == 2);
         if (accum) {
-            FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            FeatCsrOp<true> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0, all_direct};
             launch_pdl(row_sweep_cols<FeatCsrOp<true>>, dim3(g), dim3(256), 0, s, c.row_ptr.get(), c.col.get(), n, op, skip,
                        ticket);
         } else {
-            FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0, all_direct};
             launch_pdl(row_sweep_cols<FeatCsrOp<false>>, dim3(g), dim3(256), 0, s, c.row_ptr.get(), c.col.get(), n, op, skip,
                        ticket);
         }
         SOB_LAUNCH("feat_csr");
         if (c.nlong > 0) {
-            FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0};
+            FeatCsrOp<false> op{c.col.get(), n, rc.get(), bins.get(), st, nullptr, 0, false};
             launch_pdl(piece_sweep<FeatCsrOp<false>>, dim3(unsigned(c.npieces)), dim3(256), 0, s, c.piece_k.get(),
                        c.long_row.get(), c.long_piece.get(), c.nlong, op, int64_t(0));
             SOB_LAUNCH("feat_csr_pieces");

@@ -31,8 +31,9 @@ struct FeatWorkspace {
     // diagonal-bin reduction runs beside the spread chain instead of before it
     cudaStream_t aux = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    // CSR-part sweep: -1 = size heuristic, 0 = row-lockstep, 1 = entry-parallel
-    // (the tune plan times both once and keeps the faster, capi.cu)
+    // CSR-part sweep: -1 = size heuristic, 0 = row-lockstep, 1 = entry-parallel,
+    // 2 = row-lockstep with every key a global atomic (no hash); the tune
+    // plan times them once and keeps the fastest (capi.cu)
     int sweep = -1;
     FeatWorkspace(const so_matrix& m, cudaStream_t s);
     ~FeatWorkspace();
