@@ -702,6 +702,7 @@ def summarise_config4(rows, elapsed, world):
         "accuracy": round(float((ch == lab).mean()), 4),
         "accuracy_twins_collapsed": round(float((ch_c == lab_c).mean()), 4),
         "balanced_accuracy_twins_collapsed": round(float(np.mean(recalls)), 4),
+        "within_2pct_of_optimal": round(float((t_ch <= 1.02 * t_opt).mean()), 4),
         "within_5pct_of_optimal": round(float((t_ch <= 1.05 * t_opt).mean()), 4),
         "tuning_cost_csr_spmv_equiv_device": q(cost),
         "tuning_cost_csr_spmv_equiv_wall": q(cost_w),
