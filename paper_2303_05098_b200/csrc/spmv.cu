@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(kZcRows, 1)
 // completion flags need a system fence per block: 0.70 -> 1.17 ms on config
 // 2; system-scope atomics 4.4 ms, scripts/cezc_probe.cu).
 constexpr unsigned kFollowSent = 0x7FF5A5A5u;
+constexpr int64_t kFollowSpan = 16384;  // x window of a block: (1024 + span) doubles <= 136 KB of shared memory
 
 __global__ void follow_fill(unsigned* __restrict__ p, int64_t n32, unsigned* __restrict__ flag) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n32; i += int64_t(gridDim.x) * blockDim.x)
@@ -1058,7 +1059,9 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
         return false;
     const int64_t omin = m.dia_omin, omax = m.dia_omax;
-    if (omax - omin > kZcSpan) return false;
+    // x comes from device memory here (no read amplification over the link):
+    // any window that fits a CTA's shared memory with its 1024 rows
+    if (omax - omin > kFollowSpan) return false;
     if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
     const int64_t nc = m.ncols;
     FollowStage& f = g_follow[m.device];
@@ -1094,6 +1097,16 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     // the upload starts once the device copy holds sentinels again
     SOB_CUDA(cudaStreamWaitEvent(copy, f.refilled, 0));
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
+    if (smem > 48 * 1024) {  // wide windows (2-D stencils): opt in to > 48 KB, once per device
+        static std::mutex attr_mu;
+        static uint64_t attr_done = 0;
+        std::lock_guard<std::mutex> alk(attr_mu);
+        if (m.device >= 64 || !((attr_done >> m.device) & 1)) {
+            SOB_CUDA(cudaFuncSetAttribute(dia_follow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(sizeof(double) * size_t(kZcRows + kFollowSpan + 2))));
+            if (m.device < 64) attr_done |= uint64_t(1) << m.device;
+        }
+    }
     const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
     const int64_t per = rows_per_chunk > 0 ? rows_per_chunk / kZcRows : nblk;  // blocks per launch
     // 250 ms plus 1 ns per byte of x (a slowly staged pageable x still arrives)

@@ -406,21 +406,23 @@ def test_hdc_with_long_rows(so, O):
         assert max_rel(m.spmv(x), O.oc_spmv(want, x)) <= SPMV_TOL, f
 
 
-@pytest.mark.parametrize("shape", ["band13", "band13_unaligned", "wide"])
+@pytest.mark.parametrize("shape", ["band13", "band13_unaligned", "wide", "verywide"])
 def test_pipelined_host_spmv_pinned(so, O, shape):
-    """spmv(m, x) with pinned host buffers on a DIA-window matrix: narrow
-    windows run the zero-copy kernel (x read and y written over the host
-    link; 16-byte and 8-byte aligned x), wide ones the row-chunk copy
-    pipeline (x windows up / chunks / y chunks down on two copy streams).
-    Both bit-identical to the oracle and to the one-shot path."""
+    """spmv(m, x) with pinned host buffers on a DIA-window matrix: windows up
+    to 16384 wide run the follow-the-copy kernel (one x upload, y written over
+    the host link; 16-byte and 8-byte aligned x, the wide case with > 48 KB
+    of shared memory per CTA), wider ones the row-chunk copy pipeline (x
+    windows up / chunks / y chunks down on two copy streams).  Both
+    bit-identical to the oracle and to the one-shot path."""
     import torch
     from paper_2303_05098_b200 import synth
 
-    if shape == "wide":  # offsets -3000, -1, 0, 2, 3000: window span 6000 > the zero-copy limit
+    if shape in ("wide", "verywide"):  # window span 6000 / 40000
         n = 700_000
+        h = 3000 if shape == "wide" else 20000
         rng = np.random.default_rng(3)
         rows, cols = [], []
-        for off in (-3000, -1, 0, 2, 3000):
+        for off in (-h, -1, 0, 2, h):
             r = np.arange(max(0, -off), min(n, n - off))
             rows.append(r)
             cols.append(r + off)
@@ -439,7 +441,7 @@ def test_pipelined_host_spmv_pinned(so, O, shape):
     xn, yn = xt.numpy()[skew:], yt.numpy()[skew:]
     xn[:] = np.random.default_rng(11).uniform(-1, 1, ncols)
     for f in (so.DIA, so.HDC):
-        m = d.from_coo(f) if shape == "wide" else d.convert(f)
+        m = d.from_coo(f) if shape in ("wide", "verywide") else d.convert(f)
         want = O.oc_spmv(O.oc_convert(coo, f), xn)
         for _ in range(2):
             yn[:] = np.nan
