@@ -136,6 +136,16 @@ so_matrix* clone_matrix(const so_matrix& m, cudaStream_t s);
 bool coo_is_canonical(const so_matrix& coo, cudaStream_t s);
 so_matrix* coo_from_triplets_device(int64_t nrows, int64_t ncols, int64_t n, const int64_t* row_h,
                                     const int64_t* col_h, const double* val_h, cudaStream_t s);
+// the same over consecutive host segments (concatenated in order on the
+// device: Matrix Market slices parsed by different threads)
+struct TripletSegment {
+    const int64_t* row;
+    const int64_t* col;
+    const double* val;
+    int64_t n;
+};
+so_matrix* coo_from_triplet_segments(int64_t nrows, int64_t ncols, const TripletSegment* segs, int nseg,
+                                     cudaStream_t s);
 bool csr_rows_canonical(const so_matrix& csr, cudaStream_t s);
 
 // --- Matrix Market I/O (ingest.cu) ---

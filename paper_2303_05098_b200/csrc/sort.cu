@@ -106,18 +106,33 @@ __global__ void run_reduce(const uint64_t* __restrict__ key, const double* __res
 
 so_matrix* coo_from_triplets_device(int64_t nrows, int64_t ncols, int64_t n, const int64_t* row_h,
                                     const int64_t* col_h, const double* val_h, cudaStream_t s) {
+    const TripletSegment seg{row_h, col_h, val_h, n};
+    return coo_from_triplet_segments(nrows, ncols, &seg, n > 0 ? 1 : 0, s);
+}
+
+so_matrix* coo_from_triplet_segments(int64_t nrows, int64_t ncols, const TripletSegment* segs, int nseg,
+                                     cudaStream_t s) {
     auto* m = new so_matrix();
     std::unique_ptr<so_matrix> guard(m);
     SOB_CUDA(cudaGetDevice(&m->device));
     m->format = SO_COO;
     m->nrows = nrows;
     m->ncols = ncols;
+    int64_t n = 0;
+    for (int i = 0; i < nseg; ++i) n += segs[i].n;
     if (n == 0) return guard.release();
     DBuf<int64_t> r(n, s), c(n, s);
     DBuf<double> v(n, s), v2(n, s);
-    SOB_CUDA(cudaMemcpyAsync(r.get(), row_h, sizeof(int64_t) * size_t(n), cudaMemcpyHostToDevice, s));
-    SOB_CUDA(cudaMemcpyAsync(c.get(), col_h, sizeof(int64_t) * size_t(n), cudaMemcpyHostToDevice, s));
-    SOB_CUDA(cudaMemcpyAsync(v.get(), val_h, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, s));
+    // the segments in order, straight into the device arrays (no host concatenation)
+    int64_t at = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const TripletSegment& g = segs[i];
+        if (g.n == 0) continue;
+        SOB_CUDA(cudaMemcpyAsync(r.get() + at, g.row, sizeof(int64_t) * size_t(g.n), cudaMemcpyHostToDevice, s));
+        SOB_CUDA(cudaMemcpyAsync(c.get() + at, g.col, sizeof(int64_t) * size_t(g.n), cudaMemcpyHostToDevice, s));
+        SOB_CUDA(cudaMemcpyAsync(v.get() + at, g.val, sizeof(double) * size_t(g.n), cudaMemcpyHostToDevice, s));
+        at += g.n;
+    }
     DBuf<uint64_t> k(n, s), k2(n, s);
     DBuf<int> bad(1, s);
     SOB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
