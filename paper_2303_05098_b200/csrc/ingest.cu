@@ -322,35 +322,66 @@ so_matrix* read_matrix_market(const std::string& path, cudaStream_t s) {
 }
 
 // ingest.cpp:210-224: banner, "rows cols nnz", 1-based entries with the
-// shortest round-trip decimal (format_double = std::to_chars).
+// shortest round-trip decimal (format_double = std::to_chars).  The entries
+// are formatted by all host threads (contiguous ranges), then written at
+// their byte offsets with pwrite: the same bytes as one sequential writer.
 void write_matrix_market(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row, const int64_t* col,
                          const double* val, const std::string& path) {
-    std::FILE* f = std::fopen(path.c_str(), "wb");
-    if (!f) fail(SO_ERROR, "cannot open " + path + " for writing");
-    std::string out;
-    out.reserve(size_t(std::min<int64_t>(nnz, 1 << 20)) * 32 + 128);
-    out += "%%MatrixMarket matrix coordinate real general\n";
-    out += std::to_string(nrows) + " " + std::to_string(ncols) + " " + std::to_string(nnz) + "\n";
-    char num[64];
-    bool ok = true;
-    for (int64_t k = 0; k < nnz; ++k) {
-        auto r1 = std::to_chars(num, num + sizeof(num), row[k] + 1);
-        out.append(num, r1.ptr);
-        out.push_back(' ');
-        auto r2 = std::to_chars(num, num + sizeof(num), col[k] + 1);
-        out.append(num, r2.ptr);
-        out.push_back(' ');
-        auto r3 = std::to_chars(num, num + sizeof(num), val[k]);
-        out.append(num, r3.ptr);
-        out.push_back('\n');
-        if (out.size() > (size_t(1) << 24)) {
-            ok = ok && std::fwrite(out.data(), 1, out.size(), f) == out.size();
-            out.clear();
+    std::string head = "%%MatrixMarket matrix coordinate real general\n";
+    head += std::to_string(nrows) + " " + std::to_string(ncols) + " " + std::to_string(nnz) + "\n";
+    const int nt = int(std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), nnz >> 16)));
+    std::vector<std::string> part(static_cast<size_t>(nt));
+    auto format = [&](int t) {
+        const int64_t a = nnz * t / nt, e = nnz * (t + 1) / nt;
+        std::string& out = part[size_t(t)];
+        out.reserve(size_t(e - a) * 32);
+        char num[64];
+        for (int64_t k = a; k < e; ++k) {
+            auto r1 = std::to_chars(num, num + sizeof(num), row[k] + 1);
+            out.append(num, r1.ptr);
+            out.push_back(' ');
+            auto r2 = std::to_chars(num, num + sizeof(num), col[k] + 1);
+            out.append(num, r2.ptr);
+            out.push_back(' ');
+            auto r3 = std::to_chars(num, num + sizeof(num), val[k]);
+            out.append(num, r3.ptr);
+            out.push_back('\n');
         }
+    };
+    {
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(format, t);
+        format(0);
+        for (auto& th : pool) th.join();
     }
-    ok = ok && std::fwrite(out.data(), 1, out.size(), f) == out.size();
-    ok = (std::fclose(f) == 0) && ok;
-    if (!ok) fail(SO_ERROR, "write failed for " + path);
+    std::vector<off_t> at(static_cast<size_t>(nt) + 1);
+    at[0] = off_t(head.size());
+    for (int t = 0; t < nt; ++t) at[size_t(t) + 1] = at[size_t(t)] + off_t(part[size_t(t)].size());
+    const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) fail(SO_ERROR, "cannot open " + path + " for writing");
+    std::atomic<bool> bad{false};
+    auto put = [&](const char* data, size_t n, off_t off) {
+        while (n > 0) {
+            const ssize_t w = ::pwrite(fd, data, n, off);
+            if (w <= 0) {
+                bad = true;
+                return;
+            }
+            data += w;
+            n -= size_t(w);
+            off += off_t(w);
+        }
+    };
+    put(head.data(), head.size(), 0);
+    {
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t)
+            pool.emplace_back([&, t] { put(part[size_t(t)].data(), part[size_t(t)].size(), at[size_t(t)]); });
+        put(part[0].data(), part[0].size(), at[0]);
+        for (auto& th : pool) th.join();
+    }
+    if (::close(fd) != 0) bad = true;
+    if (bad) fail(SO_ERROR, "write failed for " + path);
 }
 
 }  // namespace sob

@@ -59,6 +59,15 @@ def main():
             res["read_matrix_market"][name] = {"file_mb": round(size / 1e6, 1), "nnz": int(coo["val"].size),
                                                "reference_s": round(t_ref, 3), "b200_s": round(t_ours, 4),
                                                "speedup": round(t_ref / t_ours, 1), "identical": bool(same)}
+            # write_matrix_market: the reference's writer vs ours (same bytes)
+            p2 = os.path.join(d, "w.mtx")
+            _, tw_ref = timed(lambda: O.ref_write_matrix_market(path, coo))
+            _, tw_ours = timed(lambda: ours.write_matrix_market(p2), reps=3)
+            with open(path, "rb") as fa, open(p2, "rb") as fb:
+                same_w = fa.read() == fb.read()
+            res.setdefault("write_matrix_market", {})[name] = {
+                "reference_s": round(tw_ref, 3), "b200_s": round(tw_ours, 4), "speedup": round(tw_ref / tw_ours, 1),
+                "byte_identical": bool(same_w)}
             print(name, res["read_matrix_market"][name], file=sys.stderr, flush=True)
     csr = synth.rmat(22, 16, seed=42)
     r, c, v = csr.coo_rows(), csr.col.astype(np.int64), csr.val
