@@ -876,8 +876,12 @@ so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) 
             return;
         }
         // pageable buffers (the reference API's std::vector): staged through
-        // pinned memory by host threads, overlapped with the device work
-        if (m->nrows > 0 && spmv_pageable(*m, x, y, s)) return;
+        // pinned memory by host threads, overlapped with the device work;
+        // pinned buffers the follow path declined go straight to the copy
+        // engines (the staging copies would only add host traffic)
+        static const bool pinned_staged = std::getenv("SOB_PINNED_STAGED") != nullptr;  // diagnostic knob (A/B)
+        const bool both_pinned = !pinned_staged && is_pinned(x) && is_pinned(y);
+        if (m->nrows > 0 && !both_pinned && spmv_pageable(*m, x, y, s)) return;
         DBuf<double> dx, dy(m->nrows, s);
         h2d(dx, x, xlen, s);
         spmv_device(*m, dx.get(), dy.get(), s);
