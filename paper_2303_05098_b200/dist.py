@@ -275,8 +275,11 @@ class _NcclIterator:
         if out is not self.xa:
             self.xa, self.xb = self.xb, self.xa
 
+    def owned(self):
+        return self.xa[self.s.own_lo:self.s.own_hi]
+
     def checksum(self):
-        return owned_checksum(self.xa[self.s.own_lo:self.s.own_hi], self.s)
+        return owned_checksum(self.owned(), self.s)
 
     def timeouts(self):
         return 0
