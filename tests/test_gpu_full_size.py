@@ -76,8 +76,20 @@ def _full(so, O, csr, exact_formats=(1, 2, 3, 5)):
             y_csr = y_ref
         fv = m.extract_features(0.2)
         assert np.array_equal(np.array(fv.to_row()), want_f), (f, fv.to_row(), want_f)
+        if f == 1:
+            # the tune plan's own sweep choice (config 3: every key a global
+            # atomic; config 2: the lockstep slot cache) gives the same vector
+            o = so.tune_ml(m, so.DeviceForest(_stump_forest(so)))
+            assert o.features.to_row() == want_f.tolist(), (f, o.features.to_row(), want_f)
         del m, want
     return y_csr
+
+
+def _stump_forest(so):
+    # NNZ <= 4 -> CSR else COO (test_tuners.cpp:142-153); only the features matter here
+    return so.FlatForest(0, np.array([0, 3]), np.array([2, -1, -1], np.int32), np.array([4.0, 0, 0]),
+                         np.array([1, -1, -1], np.int32), np.array([2, -1, -1], np.int32),
+                         np.array([-1, 1, 0], np.int32))
 
 
 def test_config2_banded_full_size(so, O):
