@@ -6,6 +6,7 @@
 // layout, and the per-device context.
 #include <algorithm>
 #include <chrono>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -1124,7 +1125,8 @@ so_status so_tune_ml(const so_matrix* m, const so_forest* f, double ratio, const
                 // every entry of a diagonal would hit one address (config 2:
                 // 36 ms), so that mode is not even timed there
                 so_feature_vector fv{};
-                SOB_CUDA(cudaMemcpy(&fv, &np->st->out, sizeof(fv), cudaMemcpyDeviceToHost));
+                SOB_CUDA(cudaMemcpy(&fv, reinterpret_cast<const char*>(np->st) + offsetof(FeatState, out), sizeof(fv),
+                                    cudaMemcpyDeviceToHost));
                 const bool try_direct = fv.ndiags > 0 && fv.nnz <= 64 * fv.ndiags;
                 for (int rep = 0; rep < 2; ++rep)
                     for (int mode = 0; mode < 3; ++mode)
