@@ -882,6 +882,13 @@ so_status so_spmv(const so_matrix* m, const double* x, int64_t xlen, double* y) 
         // engines (the staging copies would only add host traffic)
         static const bool pinned_staged = std::getenv("SOB_PINNED_STAGED") != nullptr;  // diagnostic knob (A/B)
         const bool both_pinned = !pinned_staged && is_pinned(x) && is_pinned(y);
+        if (both_pinned && m->nrows >= 2 * kPipeRows) {
+            // CSR: the kernels follow one upload of x and store y into mapped host memory
+            const auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+            const bool overlap = xa < ya + sizeof(double) * size_t(m->nrows) && ya < xa + sizeof(double) * size_t(m->ncols);
+            double* ym = static_cast<double*>(const_cast<void*>(mapped_ptr(y)));
+            if (!overlap && ym && spmv_csr_follow(*m, x, ym, s, ctx(m->device).copy_in)) return;
+        }
         if (m->nrows > 0 && !both_pinned && spmv_pageable(*m, x, y, s)) return;
         DBuf<double> dx, dy(m->nrows, s);
         h2d(dx, x, xlen, s);

@@ -169,6 +169,11 @@ int64_t zero_copy_rows_per_block();
 // never arrived: y must be recomputed)
 bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
                      cudaStream_t copy);
+// pinned host x (one upload on `copy`) and mapped host y on a CSR matrix (or
+// HDC without a DIA part): the CSR kernels follow the upload (spmv.cu);
+// synchronous; false = not eligible or the copy never arrived
+bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
+                     cudaStream_t copy);
 // The same, in two halves (pageable staging, stage.cu): follow_launch locks
 // the device's follow stage, launches the kernel -- one launch per y chunk of
 // rows_per_chunk rows (a multiple of zero_copy_rows_per_block(); 0 = one

@@ -156,6 +156,54 @@ __device__ __forceinline__ void csr_rows_sum(const double* prod, bool pad, int r
     }
 }
 
+// ---- following a host->device copy of x (pinned spmv(m, x), FOLLOW) ------
+// The device copy of x holds a NaN sentinel (both 32-bit halves
+// kFollowSent) until the copy engine overwrites it; a kernel launched with
+// FOLLOW reads x from L2 (never a stale L1 line) and waits on an element that
+// still holds a sentinel half until it lands -- or until the flag copied
+// after x says the copy is complete (an x element that happens to equal the
+// sentinel).  A copy that never arrives ends the wait after `timeout_ns` and
+// marks the call (`timed_out`): the caller recomputes on another path.
+constexpr unsigned kFollowSent = 0x7FF5A5A5u;
+
+struct FollowCtx {
+    const unsigned* flag;
+    unsigned* timed_out;
+    unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ bool follow_ready(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    return unsigned(b) != kFollowSent && unsigned(b >> 32) != kFollowSent;
+}
+
+__device__ __noinline__ double follow_wait(const double* p, FollowCtx f) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        unsigned fl;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(fl) : "l"(f.flag) : "memory");
+        const double v = __ldcg(p);
+        if (fl != 0 || follow_ready(v)) return v;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > f.timeout_ns) {
+            atomicExch_system(f.timed_out, 1u);
+            return v;
+        }
+        __nanosleep(256);
+    }
+}
+
+// x[c] for the SpMV kernels: the read-only cached load, or (FOLLOW) an L2
+// load that waits for the copy front
+template <bool FOLLOW>
+__device__ __forceinline__ double ldx(const double* __restrict__ x, int64_t c, const FollowCtx& f) {
+    if (!FOLLOW) return __ldg(x + c);
+    const double v = __ldcg(x + c);
+    return follow_ready(v) ? v : follow_wait(x + c, f);
+}
+
 // Low 32 bits of row_ptr[r]: a group spans < 2^31 entries, so its rows'
 // local bounds int(rp[r] - k0) only need the low words (32-bit loads).
 __device__ __forceinline__ unsigned rp_lo(const int64_t* __restrict__ rp, int64_t r) {
@@ -173,12 +221,12 @@ __device__ __forceinline__ unsigned rp_lo(const int64_t* __restrict__ rp, int64_
 // loaded in a stage is used in the same stage, so every load's latency hides
 // behind the work of the stage (ncu on R-MAT: the previous order stalled on
 // the next group's row bounds right after issuing them).
-template <int IT, bool ACCUM, bool PAD, bool COOP, int RPL>
+template <int IT, bool ACCUM, bool PAD, bool COOP, int RPL, bool FOLLOW = false>
 __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
     csr_warp_kernel(const int32_t* __restrict__ grp, const int64_t* __restrict__ grp_k, int64_t ngrp,
                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                    int64_t nrows) {
+                    int64_t nrows, FollowCtx fctx) {
     constexpr int kCap = 32 * IT;
     __shared__ double sp[8][kCap + (PAD ? kCap / 16 : 0)];  // + the padded layout's slots
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -224,7 +272,7 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
 #pragma unroll
             for (int u = 0; u < IT; ++u) {
                 const int e = u * 32 + lane;
-                if (e < cnt) prod[pad ? e + (e >> 4) : e] = fmul(v[u], __ldg(x + c[u]));
+                if (e < cnt) prod[pad ? e + (e >> 4) : e] = fmul(v[u], ldx<FOLLOW>(x, c[u], fctx));
             }
         }
         __syncwarp();
@@ -291,9 +339,11 @@ __global__ void __launch_bounds__(256, (IT > 8 ? 3 : 4))
 // row -- one warp per long row, lane-strided partial sums joined by a fixed
 // butterfly, so a row of 10^8 entries (5*10^4 pieces) is not one thread's
 // serial chain (deterministic, within the 1e-12 contract).
+template <bool FOLLOW>
 __global__ void __launch_bounds__(kStreamBlock)
     csr_long_pieces(const int64_t* __restrict__ pk, const int32_t* __restrict__ col,
-                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ part) {
+                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ part,
+                    FollowCtx fctx) {
     __shared__ double scratch[kStreamBlock / 32];
     const int64_t k0 = pk[2 * blockIdx.x], k1 = pk[2 * blockIdx.x + 1];
     constexpr int U = kPiece / kStreamBlock;
@@ -309,7 +359,7 @@ __global__ void __launch_bounds__(kStreamBlock)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int64_t k = k0 + u * kStreamBlock + threadIdx.x;
-        if (k < k1) s = fadd(s, fmul(v[u], __ldg(x + c[u])));
+        if (k < k1) s = fadd(s, fmul(v[u], ldx<FOLLOW>(x, c[u], fctx)));
     }
     const double t = block_sum_det<kStreamBlock>(s, scratch);
     if (threadIdx.x == 0) part[blockIdx.x] = t;
@@ -422,18 +472,12 @@ __global__ void __launch_bounds__(kZcRows, 1)
 // that an event after each tells host threads the chunk has landed (per-block
 // completion flags need a system fence per block: 0.70 -> 1.17 ms on config
 // 2; system-scope atomics 4.4 ms, scripts/cezc_probe.cu).
-constexpr unsigned kFollowSent = 0x7FF5A5A5u;
 constexpr int64_t kFollowSpan = 16384;  // x window of a block: (1024 + span) doubles <= 136 KB of shared memory
 
 __global__ void follow_fill(unsigned* __restrict__ p, int64_t n32, unsigned* __restrict__ flag) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n32; i += int64_t(gridDim.x) * blockDim.x)
         p[i] = kFollowSent;
     if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 0;
-}
-
-__device__ __forceinline__ bool follow_ready(double v) {
-    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-    return unsigned(b) != kFollowSent && unsigned(b >> 32) != kFollowSent;
 }
 
 __global__ void __launch_bounds__(kZcRows, 1)
@@ -900,55 +944,69 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
 }
 
 template <int IT, bool PAD, bool COOP, int RPL>
-void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
+                      const FollowCtx* follow) {
     const CsrPart& c = m.csr;
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
-    if (accum)
+    const FollowCtx none{nullptr, nullptr, 0};
+    if (follow)  // pinned spmv(m, x) following the upload of x (never accumulating)
+        csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
+            c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
+    else if (accum)
         csr_warp_kernel<IT, true, PAD, COOP, RPL><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
                                                                        c.row_ptr.get(), c.col.get(), c.val.get(),
-                                                                       x, y, m.nrows);
+                                                                       x, y, m.nrows, none);
     else
         csr_warp_kernel<IT, false, PAD, COOP, RPL><<<grid, 256, 0, s>>>(c.grp.get(), c.grp_k.get(), c.ngrp,
                                                                         c.row_ptr.get(), c.col.get(), c.val.get(),
-                                                                        x, y, m.nrows);
+                                                                        x, y, m.nrows, none);
     SOB_LAUNCH("csr_warp_kernel");
 }
 
 template <int IT, bool PAD, bool COOP>
-void launch_csr_warp3(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+void launch_csr_warp3(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
+                      const FollowCtx* follow) {
     if (m.csr.grp_rpl > 1)
-        launch_csr_warp4<IT, PAD, COOP, kGroupRowsMax / 32>(m, accum, x, y, s);
+        launch_csr_warp4<IT, PAD, COOP, kGroupRowsMax / 32>(m, accum, x, y, s, follow);
     else
-        launch_csr_warp4<IT, PAD, COOP, 1>(m, accum, x, y, s);
+        launch_csr_warp4<IT, PAD, COOP, 1>(m, accum, x, y, s, follow);
 }
 
 template <int IT, bool PAD>
-void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
+                     const FollowCtx* follow) {
     static const bool no_coop = std::getenv("SOB_NO_CSR_COOP") != nullptr;  // diagnostic knob (A/B)
     if (m.csr.ncoop > 0 && !no_coop)
-        launch_csr_warp3<IT, PAD, true>(m, accum, x, y, s);
+        launch_csr_warp3<IT, PAD, true>(m, accum, x, y, s, follow);
     else
-        launch_csr_warp3<IT, PAD, false>(m, accum, x, y, s);
+        launch_csr_warp3<IT, PAD, false>(m, accum, x, y, s, follow);
 }
 
-// accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x
-void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s) {
+// accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x;
+// follow: x is still being uploaded (FOLLOW kernels, never accumulating)
+void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
+                       const FollowCtx* follow = nullptr) {
     const CsrPart& c = m.csr;
     if (c.ngrp == 0) return;
     // flags are set (npad > 0) only when >= 1/64 of the groups prefer the
     // padded layout (convert.cu); otherwise grp_k is plain
     const bool pad = c.npad > 0;
     if (c.grp_cap == 32 * kGroupItemsShort)
-        pad ? launch_csr_warp<kGroupItemsShort, true>(m, accum, x, y, s)
-            : launch_csr_warp<kGroupItemsShort, false>(m, accum, x, y, s);
+        pad ? launch_csr_warp<kGroupItemsShort, true>(m, accum, x, y, s, follow)
+            : launch_csr_warp<kGroupItemsShort, false>(m, accum, x, y, s, follow);
     else
-        pad ? launch_csr_warp<kGroupItemsLong, true>(m, accum, x, y, s)
-            : launch_csr_warp<kGroupItemsLong, false>(m, accum, x, y, s);
+        pad ? launch_csr_warp<kGroupItemsLong, true>(m, accum, x, y, s, follow)
+            : launch_csr_warp<kGroupItemsLong, false>(m, accum, x, y, s, follow);
     if (c.nlong > 0) {
         DBuf<double> part(c.npieces, s);
-        csr_long_pieces<<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(), c.val.get(), x,
-                                                                     part.get());
+        const FollowCtx none{nullptr, nullptr, 0};
+        if (follow)
+            csr_long_pieces<true><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(),
+                                                                                c.val.get(), x, part.get(), *follow);
+        else
+            csr_long_pieces<false><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(),
+                                                                                 c.val.get(), x, part.get(), none);
         SOB_LAUNCH("csr_long_pieces");
         const unsigned g = unsigned(ceil_div(c.nlong * 32, 128));  // one warp per long row
         if (accum)
@@ -1036,16 +1094,13 @@ struct FollowStage {
 FollowStage g_follow[64];
 }  // namespace
 
-bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
-                   const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
-                   FollowToken& tok) {
-    // SOB_NO_FOLLOW: diagnostic knob (A/B).  Under an injected CUDA tool
-    // (ncu / nsys: NV_NSIGHT_INJECTION_*, compute-sanitizer:
-    // NV_SANITIZER_INJECTION_*, or CUDA_INJECTION64_PATH) kernels may be
-    // serialised against the copy the kernel follows -- every call would wait
-    // for the timeout -- so the zero-copy kernel runs instead.
-    // SOB_FOLLOW_UNDER_TOOLS=1 keeps it (the sanitizer driver: a timed-out
-    // call falls back and stays correct).
+// SOB_NO_FOLLOW: diagnostic knob (A/B).  Under an injected CUDA tool (ncu /
+// nsys: NV_NSIGHT_INJECTION_*, compute-sanitizer: NV_SANITIZER_INJECTION_*,
+// or CUDA_INJECTION64_PATH) kernels may be serialised against the copy they
+// follow -- every call would wait for the timeout -- so the follow paths are
+// off.  SOB_FOLLOW_UNDER_TOOLS=1 keeps them (the sanitizer driver: a
+// timed-out call falls back and stays correct).
+bool follow_disabled() {
     static const bool off = [] {
         if (std::getenv("SOB_NO_FOLLOW")) return true;
         if (std::getenv("SOB_FOLLOW_UNDER_TOOLS")) return false;
@@ -1054,17 +1109,18 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
             if (std::getenv(v)) return true;
         return false;
     }();
-    if (off) return false;
-    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
-    if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
-        return false;
-    const int64_t omin = m.dia_omin, omax = m.dia_omax;
-    // x comes from device memory here (no read amplification over the link):
-    // any window that fits a CTA's shared memory with its 1024 rows
-    if (omax - omin > kFollowSpan) return false;
-    if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
-    const int64_t nc = m.ncols;
-    FollowStage& f = g_follow[m.device];
+    return off;
+}
+
+// The shared part of every follow path: the device's sentinel-filled copy of
+// x (allocated / refilled as needed, ordered after the previous call), this
+// call's timeout word, the caller's kernels (launched before the upload so
+// they trail it), the upload, the copy-complete flag and the refill for the
+// next call.
+void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
+                const std::function<void(const double* dx, const FollowCtx& f)>& kernels,
+                const std::function<void(double*)>& upload, FollowToken& tok) {
+    FollowStage& f = g_follow[device];
     std::lock_guard<std::mutex> lk(f.mu);
     if (!f.flag) {
         SOB_CUDA(cudaMalloc(reinterpret_cast<void**>(&f.flag), sizeof(unsigned)));
@@ -1081,7 +1137,7 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     f.timed_out[slot] = 0;
     tok.timed_out = f.timed_out + slot;
     const int grid_fill = current_ctx().num_sms * 4;
-    // everything of the previous call (its kernel, copy and refill, possibly
+    // everything of the previous call (its kernels, copy and refill, possibly
     // on another stream) precedes this call's use -- or release -- of dx
     if (f.dx) SOB_CUDA(cudaStreamWaitEvent(s, f.refilled, 0));
     if (f.cap < nc) {
@@ -1096,6 +1152,33 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     }
     // the upload starts once the device copy holds sentinels again
     SOB_CUDA(cudaStreamWaitEvent(copy, f.refilled, 0));
+    // 250 ms plus 1 ns per byte of x (a slowly staged pageable x still arrives)
+    const FollowCtx fc{f.flag, f.timed_out_dev + slot, 250ull * 1000 * 1000 + 8ull * uint64_t(nc)};
+    kernels(f.dx, fc);
+    upload(f.dx);  // the caller's H2D copies of x into f.dx on `copy`
+    SOB_CUDA(cudaMemcpyAsync(f.flag, f.one_host, sizeof(unsigned), cudaMemcpyHostToDevice, copy));
+    SOB_CUDA(cudaEventRecord(f.copied, copy));
+    // refill the sentinels for the next call once the copy has finished (x
+    // columns no row reads are not waited for by the kernels)
+    SOB_CUDA(cudaStreamWaitEvent(s, f.copied, 0));
+    follow_fill<<<grid_fill, 256, 0, s>>>(reinterpret_cast<unsigned*>(f.dx), 2 * nc, f.flag);
+    SOB_LAUNCH("follow_fill");
+    SOB_CUDA(cudaEventRecord(f.refilled, s));
+}
+
+bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
+                   const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
+                   FollowToken& tok) {
+    if (follow_disabled()) return false;
+    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
+    if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
+        return false;
+    const int64_t omin = m.dia_omin, omax = m.dia_omax;
+    // x comes from device memory here (no read amplification over the link):
+    // any window that fits a CTA's shared memory with its 1024 rows
+    if (omax - omin > kFollowSpan) return false;
+    if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
+    const int64_t nc = m.ncols;
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
     if (smem > 48 * 1024) {  // wide windows (2-D stencils): opt in to > 48 KB, once per device
         static std::mutex attr_mu;
@@ -1109,27 +1192,44 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     }
     const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
     const int64_t per = rows_per_chunk > 0 ? rows_per_chunk / kZcRows : nblk;  // blocks per launch
-    // 250 ms plus 1 ns per byte of x (a slowly staged pageable x still arrives)
-    const unsigned long long timeout = 250ull * 1000 * 1000 + 8ull * uint64_t(nc);
-    for (int64_t b0 = 0, j = 0; b0 < nblk; b0 += per, ++j) {
-        const int64_t b1 = std::min(nblk, b0 + per);
-        const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));
-        dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags),
-                                                      m.dia.offsets.get(), m.dia.values.get(), f.dx, y_mapped, f.flag,
-                                                      int(omin), int(omax), f.timed_out_dev + slot, timeout, int(b0),
-                                                      int(b1));
-        SOB_LAUNCH("dia_follow_kernel");
-        if (after_chunk) (*after_chunk)(j);
+    follow_run(m.device, nc, s, copy, [&](const double* dx, const FollowCtx& fc) {
+        for (int64_t b0 = 0, j = 0; b0 < nblk; b0 += per, ++j) {
+            const int64_t b1 = std::min(nblk, b0 + per);
+            const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));
+            dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags),
+                                                          m.dia.offsets.get(), m.dia.values.get(), dx, y_mapped,
+                                                          fc.flag, int(omin), int(omax), fc.timed_out,
+                                                          fc.timeout_ns, int(b0), int(b1));
+            SOB_LAUNCH("dia_follow_kernel");
+            if (after_chunk) (*after_chunk)(j);
+        }
+    }, upload, tok);
+    return true;
+}
+
+// Pinned spmv(m, x) on a CSR matrix (or HDC without a DIA part): the CSR
+// kernels launched with FOLLOW trail ONE upload of x (each x gather waits for
+// its element) and store y straight into mapped host memory, so y goes down
+// while x still comes up.  The persistent warp kernel walks its groups in
+// address order (group g, g + grid, ...), so on banded / stencil rows the
+// kernel follows the copy front; scattered columns just wait longer.
+bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
+                     cudaStream_t copy) {
+    static const bool off = std::getenv("SOB_NO_CSR_FOLLOW") != nullptr;  // diagnostic knob (A/B)
+    if (off || follow_disabled()) return false;
+    if (!(m.format == SO_CSR || (m.format == SO_HDC && m.dia.ndiags == 0)) || m.csr.nnz == 0) return false;
+    const int64_t nc = m.ncols;
+    FollowToken tok;
+    follow_run(m.device, nc, s, copy, [&](const double* dx, const FollowCtx& fc) {
+        launch_csr_stream(m, false, dx, y_mapped, s, &fc);
+    }, [&](double* dx) {
+        SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
+    }, tok);
+    SOB_CUDA(cudaStreamSynchronize(s));
+    if (!follow_finish(tok)) {  // the copy never showed up: recompute elsewhere
+        SOB_CUDA(cudaStreamSynchronize(copy));
+        return false;
     }
-    upload(f.dx);  // the caller's H2D copies of x into f.dx on `copy`
-    SOB_CUDA(cudaMemcpyAsync(f.flag, f.one_host, sizeof(unsigned), cudaMemcpyHostToDevice, copy));
-    SOB_CUDA(cudaEventRecord(f.copied, copy));
-    // refill the sentinels for the next call once the copy has finished (x
-    // columns past the last row's window are not waited for by the kernel)
-    SOB_CUDA(cudaStreamWaitEvent(s, f.copied, 0));
-    follow_fill<<<grid_fill, 256, 0, s>>>(reinterpret_cast<unsigned*>(f.dx), 2 * nc, f.flag);
-    SOB_LAUNCH("follow_fill");
-    SOB_CUDA(cudaEventRecord(f.refilled, s));
     return true;
 }
 

@@ -451,8 +451,9 @@ def test_pipelined_host_spmv_pinned(so, O, shape):
 
 
 def test_follow_copy_path_edge_cases(so, O):
-    """Pinned spmv(m, x) on a narrow DIA window runs dia_follow_kernel behind
-    ONE copy-engine upload of x (spmv.cu): the device copy of x holds a NaN
+    """Pinned spmv(m, x) on a DIA window runs dia_follow_kernel, on CSR the
+    CSR kernels' FOLLOW variant, behind ONE copy-engine upload of x
+    (spmv.cu): the device copy of x holds a NaN
     sentinel until the copy lands.  Cases: x elements whose bits ARE the
     sentinel (the kernel must finish on the copy-complete flag), x with one
     sentinel half-word, a matrix with more columns than its rows' window
@@ -476,18 +477,19 @@ def test_follow_copy_path_edge_cases(so, O):
         xt = torch.empty(ncols, dtype=torch.float64).pin_memory()
         yt = torch.empty(nrows, dtype=torch.float64).pin_memory()
         xn, yn = xt.numpy(), yt.numpy()
-        m = d.from_coo(so.DIA)
-        want_m = O.oc_convert(coo, so.DIA)
-        for trial in range(4):
-            xn[:] = rng.uniform(-1, 1, ncols)
-            if trial == 1:
-                xn[::997] = sent  # a NaN with the sentinel's bits: NaN rows in y, on the flag path
-            if trial == 2:
-                xn[5::1013] = half
-            want = O.oc_spmv(want_m, xn)
-            yn[:] = 0.0
-            m.spmv_into(xn, yn)
-            assert np.array_equal(yn, want, equal_nan=True), (nrows, ncols, trial)
+        for fmt in (so.DIA, so.CSR):  # the DIA follow kernel and the CSR kernels' FOLLOW variant
+            m = d.from_coo(fmt)
+            want_m = O.oc_convert(coo, fmt)
+            for trial in range(4):
+                xn[:] = rng.uniform(-1, 1, ncols)
+                if trial == 1:
+                    xn[::997] = sent  # a NaN with the sentinel's bits: NaN rows in y, on the flag path
+                if trial == 2:
+                    xn[5::1013] = half
+                want = O.oc_spmv(want_m, xn)
+                yn[:] = 0.0
+                m.spmv_into(xn, yn)
+                assert np.array_equal(yn, want, equal_nan=True), (fmt, nrows, ncols, trial)
 
 
 def test_stencil27_generator_and_row_slices(so, O):
