@@ -212,13 +212,15 @@ def main():
     # SOB_NO_FOLLOW=1, the zero-copy kernel) on a narrow DIA window
     # (>= 2^19 rows: smaller calls take the one-shot path)
     band = synth.banded(600_000, 4, seed=9)
-    dm = P.DeviceMatrix.csr(band.nrows, band.ncols, band.row_ptr, band.col, band.val).convert(P.DIA)
+    bcsr = P.DeviceMatrix.csr(band.nrows, band.ncols, band.row_ptr, band.col, band.val)
     hx, hy = pinned(band.ncols), pinned(band.nrows)
     if hx is not None and hy is not None:
         hx[:] = rng.uniform(-1, 1, band.ncols)
-        for _ in range(2):
-            dm.spmv_into(hx, hy)
-            assert np.array_equal(hy, dm.spmv(np.array(hx))), "pinned spmv differs from the one-shot path"
+        for fmt in (P.DIA, P.CSR, P.COO):  # DIA / CSR follow kernels, the pinned one-shot path
+            dm = bcsr.convert(fmt)
+            for _ in range(2):
+                dm.spmv_into(hx, hy)
+                assert np.array_equal(hy, dm.spmv(np.array(hx))), "pinned spmv differs from the one-shot path"
     # large enough for the global-memory spread walk and the lockstep sweep
     big2 = synth.uniform_random(60_000, 5, seed=8)
     P.DeviceMatrix.csr(big2.nrows, big2.ncols, big2.row_ptr, big2.col, big2.val).extract_features(0.2)
