@@ -123,6 +123,7 @@ def main():
             row["chosen"] = int(o.chosen)
             row["t_fe"] = float(np.median([q.feature_time_seconds for q in outs]))
             row["t_pred"] = float(np.median([q.predict_time_seconds for q in outs]))
+            row["t_wall"] = float(np.median([q.wall_time_seconds for q in outs]))
         row["_ref"] = row_ref
         rows.append(row)
         del base

@@ -39,6 +39,14 @@ def main(path, reps=1000):
         "oracle_speedup_vs_csr_geomean": float(np.exp(np.log(t_csr / t_opt).mean())),
         "t_fe_ms_median": float(np.median(tfe) * 1e3), "t_pred_ms_median": float(np.median(tpr) * 1e3),
     }
+    if rows and "t_wall" in rows[0] and rows[0]["t_wall"]:  # host wall clock of the tune_ml call
+        tw = np.array([float(r["t_wall"]) for r in rows])
+        cw = tw / t_csr
+        qw = np.quantile(cw, [0, 0.25, 0.5, 0.75, 1])
+        out["tuning_cost_csr_spmv_equiv_wall"] = {"mean": float(cw.mean()), "min": qw[0], "q1": qw[1],
+                                                  "median": qw[2], "q3": qw[3], "max": qw[4],
+                                                  "frac_below_10": float((cw < 10).mean())}
+        out["tuning_cost_csr_spmv_equiv"]["frac_below_10"] = float((cost < 10).mean())
     print(json.dumps(out, indent=1))
     return out
 
