@@ -599,11 +599,11 @@ __global__ void wait_flag_kernel(const unsigned long long* flag, unsigned long l
 // Column-major ELL, one thread per row; slots are consumed in order and the
 // row stops at the first sentinel (spmv.cpp:59-71).  Column indices for
 // kU slots are fetched together; values/x only for live slots.
-template <bool ACCUM>
+template <bool ACCUM, bool FOLLOW = false>
 __global__ void __launch_bounds__(256)
     ell_kernel(int64_t nrows, int width, const int32_t* __restrict__ col,
                const double* __restrict__ val, const double* __restrict__ x,
-               double* __restrict__ y) {
+               double* __restrict__ y, FollowCtx fctx) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nrows) return;
     constexpr int kU = 4;
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(256)
         double p[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-            p[u] = live[u] ? fmul(ld_stream(val + int64_t(k0 + u) * nrows + i), __ldg(x + c[u])) : 0.0;
+            p[u] = live[u] ? fmul(ld_stream(val + int64_t(k0 + u) * nrows + i), ldx<FOLLOW>(x, c[u], fctx)) : 0.0;
 #pragma unroll
         for (int u = 0; u < kU; ++u)
             if (live[u]) s = fadd(s, p[u]);
@@ -1036,9 +1036,14 @@ void launch_dia(const so_matrix& m, const double* x, double* y, cudaStream_t s, 
 }
 
 template <bool ACCUM>
-void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s) {
-    ell_kernel<ACCUM><<<unsigned(ceil_div(m.nrows, 256)), 256, 0, s>>>(
-        m.nrows, int(m.ell.width), m.ell.col.get(), m.ell.val.get(), x, y);
+void launch_ell(const so_matrix& m, const double* x, double* y, cudaStream_t s, const FollowCtx* follow = nullptr) {
+    const unsigned grid = unsigned(ceil_div(m.nrows, 256));
+    if (follow)  // rows in block order trail the upload of x (never accumulating)
+        ell_kernel<false, true><<<grid, 256, 0, s>>>(m.nrows, int(m.ell.width), m.ell.col.get(), m.ell.val.get(), x, y,
+                                                     *follow);
+    else
+        ell_kernel<ACCUM><<<grid, 256, 0, s>>>(m.nrows, int(m.ell.width), m.ell.col.get(), m.ell.val.get(), x, y,
+                                               FollowCtx{nullptr, nullptr, 0});
     SOB_LAUNCH("ell_kernel");
 }
 
@@ -1207,21 +1212,28 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     return true;
 }
 
-// Pinned spmv(m, x) on a CSR matrix (or HDC without a DIA part): the CSR
-// kernels launched with FOLLOW trail ONE upload of x (each x gather waits for
-// its element) and store y straight into mapped host memory, so y goes down
-// while x still comes up.  The persistent warp kernel walks its groups in
-// address order (group g, g + grid, ...), so on banded / stencil rows the
-// kernel follows the copy front; scattered columns just wait longer.
+// Pinned spmv(m, x) on a CSR matrix (or HDC without a DIA part) or an ELL
+// matrix (or HYB without a COO part): the kernels launched with FOLLOW trail
+// ONE upload of x (each x gather waits for its element) and store y straight
+// into mapped host memory, so y goes down while x still comes up.  The
+// persistent CSR warp kernel walks its groups in address order (group g,
+// g + grid, ...) and the ELL grid runs its row blocks in order, so on banded
+// / stencil rows the kernels follow the copy front; scattered columns just
+// wait longer.
 bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
                      cudaStream_t copy) {
     static const bool off = std::getenv("SOB_NO_CSR_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     if (off || follow_disabled()) return false;
-    if (!(m.format == SO_CSR || (m.format == SO_HDC && m.dia.ndiags == 0)) || m.csr.nnz == 0) return false;
+    const bool csr = (m.format == SO_CSR || (m.format == SO_HDC && m.dia.ndiags == 0)) && m.csr.nnz > 0;
+    const bool ell = (m.format == SO_ELL || (m.format == SO_HYB && m.coo.nnz == 0)) && m.ell.width > 0;
+    if (!csr && !ell) return false;
     const int64_t nc = m.ncols;
     FollowToken tok;
     follow_run(m.device, nc, s, copy, [&](const double* dx, const FollowCtx& fc) {
-        launch_csr_stream(m, false, dx, y_mapped, s, &fc);
+        if (csr)
+            launch_csr_stream(m, false, dx, y_mapped, s, &fc);
+        else
+            launch_ell<false>(m, dx, y_mapped, s, &fc);
     }, [&](double* dx) {
         SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
     }, tok);

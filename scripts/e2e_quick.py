@@ -4,7 +4,7 @@ import paper_2303_05098_b200 as P
 from paper_2303_05098_b200 import synth
 csr = synth.banded(4_000_000, 13, seed=2)
 base = P.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
-for f in (2, 1, 0):
+for f in (2, 1, 0, 3):
     m = base.convert(f)
     nb = m.spmv_bytes
     x = np.ones(csr.ncols); y = np.empty(csr.nrows)

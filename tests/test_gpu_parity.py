@@ -477,7 +477,7 @@ def test_follow_copy_path_edge_cases(so, O):
         xt = torch.empty(ncols, dtype=torch.float64).pin_memory()
         yt = torch.empty(nrows, dtype=torch.float64).pin_memory()
         xn, yn = xt.numpy(), yt.numpy()
-        for fmt in (so.DIA, so.CSR):  # the DIA follow kernel and the CSR kernels' FOLLOW variant
+        for fmt in (so.DIA, so.CSR, so.ELL):  # the DIA follow kernel and the CSR / ELL kernels. FOLLOW variants
             m = d.from_coo(fmt)
             want_m = O.oc_convert(coo, fmt)
             for trial in range(4):
