@@ -216,7 +216,7 @@ def main():
     hx, hy = pinned(band.ncols), pinned(band.nrows)
     if hx is not None and hy is not None:
         hx[:] = rng.uniform(-1, 1, band.ncols)
-        for fmt in (P.DIA, P.CSR, P.COO):  # DIA / CSR follow kernels, the pinned one-shot path
+        for fmt in (P.DIA, P.CSR, P.ELL, P.COO):  # DIA / CSR / ELL follow kernels, the pinned one-shot path
             dm = bcsr.convert(fmt)
             for _ in range(2):
                 dm.spmv_into(hx, hy)
