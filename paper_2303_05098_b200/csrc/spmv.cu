@@ -1220,23 +1220,32 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
 // g + grid, ...) and the ELL grid runs its row blocks in order, so on banded
 // / stencil rows the kernels follow the copy front; scattered columns just
 // wait longer.
-bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
-                     cudaStream_t copy) {
+bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy,
+                        const std::function<void()>* after_kernels, const std::function<void(double*)>& upload,
+                        FollowToken& tok) {
     static const bool off = std::getenv("SOB_NO_CSR_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     if (off || follow_disabled()) return false;
     const bool csr = (m.format == SO_CSR || (m.format == SO_HDC && m.dia.ndiags == 0)) && m.csr.nnz > 0;
     const bool ell = (m.format == SO_ELL || (m.format == SO_HYB && m.coo.nnz == 0)) && m.ell.width > 0;
     if (!csr && !ell) return false;
-    const int64_t nc = m.ncols;
-    FollowToken tok;
-    follow_run(m.device, nc, s, copy, [&](const double* dx, const FollowCtx& fc) {
+    follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
         if (csr)
             launch_csr_stream(m, false, dx, y_mapped, s, &fc);
         else
             launch_ell<false>(m, dx, y_mapped, s, &fc);
-    }, [&](double* dx) {
-        SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
-    }, tok);
+        if (after_kernels) (*after_kernels)();
+    }, upload, tok);
+    return true;
+}
+
+bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
+                     cudaStream_t copy) {
+    const int64_t nc = m.ncols;
+    FollowToken tok;
+    if (!follow_launch_rows(m, y_mapped, s, copy, nullptr, [&](double* dx) {
+            SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
+        }, tok))
+        return false;
     SOB_CUDA(cudaStreamSynchronize(s));
     if (!follow_finish(tok)) {  // the copy never showed up: recompute elsewhere
         SOB_CUDA(cudaStreamSynchronize(copy));

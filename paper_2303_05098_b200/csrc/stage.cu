@@ -316,6 +316,29 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                     return;
                 }
             }
+            // CSR / ELL: the same with one launch of the FOLLOW kernels; one
+            // event after it gates every y chunk's copy-out
+            if (!dia_only) {
+                cudaStream_t copy = ctx(dev).copy_in;
+                const std::function<void()> after = [&]() {
+                    SOB_CUDA(cudaEventRecord(st.ev[0], s));
+                    for (int64_t j = 1; j < nyc; ++j) SOB_CUDA(cudaEventRecord(st.ev[size_t(j)], s));
+                    for (int64_t j = 0; j < nyc; ++j) ygate[size_t(j)].store(1, std::memory_order_release);
+                };
+                const bool launched = follow_launch_rows(m, Yd, s, copy, &after, [&](double* dx) {
+                    for (int64_t k = 0; k < nxc; ++k) {
+                        wait_x(k);
+                        const int64_t a = k * cx, e = std::min(nc, a + cx);
+                        SOB_CUDA(cudaMemcpyAsync(dx + a, X + a, sizeof(double) * size_t(e - a), cudaMemcpyHostToDevice,
+                                                 copy));
+                    }
+                }, ftok);
+                if (launched) {
+                    follow.store(true, std::memory_order_release);
+                    stamp(t_launched);
+                    return;
+                }
+            }
             // an empty launch range probes eligibility (window <= 256, offsets fit)
             const bool zc = dia_only && spmv_dia_zero_copy(m, Xd, Yd, s, 0, 0);
             if (zc) {
