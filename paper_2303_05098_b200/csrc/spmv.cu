@@ -189,6 +189,9 @@ __device__ __noinline__ double follow_wait(const double* p, FollowCtx f) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (t - t0 > f.timeout_ns) {
             atomicExch_system(f.timed_out, 1u);
+            // every later wait of this call (any kernel) returns at once: the
+            // caller recomputes the call on another path
+            atomicExch(const_cast<unsigned*>(f.flag), 2u);
             return v;
         }
         __nanosleep(256);
@@ -758,11 +761,13 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
     }
 }
 
-template <bool ACCUM>
+// FOLLOW: pinned spmv(m, x) -- each x gather waits for its element of the
+// upload (ldx); the persistent warps walk their chunks in address order.
+template <bool ACCUM, bool FOLLOW = false>
 __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                    CooChunkRec* __restrict__ rec) {
+                    CooChunkRec* __restrict__ rec, FollowCtx fctx) {
     constexpr int IT = kCooItems;
     const int lane = threadIdx.x & 31;
     const int64_t nchunks = (z + kCooChunk - 1) / kCooChunk;
@@ -783,7 +788,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
         const int cnt = int(min(z - base, int64_t(kCooChunk)));
         double p[IT];
 #pragma unroll
-        for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? fmul(v[j], __ldg(x + c[j])) : 0.0;
+        for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? fmul(v[j], ldx<FOLLOW>(x, c[j], fctx)) : 0.0;
         const int prev_row = base > 0 ? row[base - 1] : -1;
         const int next_row = base + cnt < z ? row[base + cnt] : -1;
         int rc[IT];
@@ -923,15 +928,25 @@ __global__ void coo_max_gap(int64_t z, int64_t nrows, const int32_t* __restrict_
 }
 constexpr int64_t kCooGapInline = 4096;  // a lane zero-fills up to ~2 us of rows inline
 
+// chunk records, then the fix-up's control word pair and long-run queue
+int64_t coo_rec_count(const CooPart& coo) { return 2 * ceil_div(coo.nnz, kCooChunk) + 1; }
+
+// `pre`: the record buffer allocated by a follow path before its first launch
 template <bool ACCUM>
-void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s) {
+void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s,
+                const FollowCtx* follow = nullptr, DBuf<CooChunkRec>* pre = nullptr) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
-    // chunk records, then the fix-up's control word pair and long-run queue
     static_assert(sizeof(LongRun) == sizeof(CooChunkRec) && sizeof(CooChunkRec) >= 16, "record layout");
-    DBuf<CooChunkRec> rec(2 * nchunks + 1, s);
+    DBuf<CooChunkRec> own;
+    if (!pre) own.alloc(coo_rec_count(coo), s);
+    DBuf<CooChunkRec>& rec = pre ? *pre : own;
     const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
-    coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x, y,
-                                                rec.get());
+    if (follow)
+        coo_warp_kernel<ACCUM, true><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(),
+                                                          coo.val.get(), x, y, rec.get(), *follow);
+    else
+        coo_warp_kernel<ACCUM><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(), coo.val.get(), x,
+                                                    y, rec.get(), FollowCtx{nullptr, nullptr, 0});
     SOB_LAUNCH("coo_warp_kernel");
     LongRun* runs = reinterpret_cast<LongRun*>(rec.get() + nchunks + 1);
     unsigned long long* ctl = reinterpret_cast<unsigned long long*>(rec.get() + nchunks);
@@ -992,6 +1007,9 @@ void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* 
     // flags are set (npad > 0) only when >= 1/64 of the groups prefer the
     // padded layout (convert.cu); otherwise grp_k is plain
     const bool pad = c.npad > 0;
+    // allocated before any launch: nothing between two kernels that follow
+    // an upload may wait for the device
+    DBuf<double> part(c.nlong > 0 ? c.npieces : 0, s);
     if (c.grp_cap == 32 * kGroupItemsShort)
         pad ? launch_csr_warp<kGroupItemsShort, true>(m, accum, x, y, s, follow)
             : launch_csr_warp<kGroupItemsShort, false>(m, accum, x, y, s, follow);
@@ -999,7 +1017,6 @@ void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* 
         pad ? launch_csr_warp<kGroupItemsLong, true>(m, accum, x, y, s, follow)
             : launch_csr_warp<kGroupItemsLong, false>(m, accum, x, y, s, follow);
     if (c.nlong > 0) {
-        DBuf<double> part(c.npieces, s);
         const FollowCtx none{nullptr, nullptr, 0};
         if (follow)
             csr_long_pieces<true><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(),
@@ -1095,7 +1112,35 @@ struct FollowStage {
     unsigned* timed_out_dev = nullptr;
     unsigned next_slot = 0;
     cudaEvent_t refilled = nullptr, copied = nullptr;
+    bool preloaded = false;
 };
+
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first
+// launch and waits for the device to do so; a follow kernel already running
+// waits for an upload this thread has not queued yet, so a kernel loaded
+// between the follow kernels and the upload stalls the call until the wait
+// times out (HYB with a COO part: 13.9 s on its first call).  Every kernel a
+// follow path launches after its first one is loaded up front, once per
+// device, and its scratch buffers are allocated before its first launch.
+void follow_preload() {
+    const void* fns[] = {
+        reinterpret_cast<const void*>(&csr_long_pieces<true>),
+        reinterpret_cast<const void*>(&csr_long_fixup<false>),
+        reinterpret_cast<const void*>(&coo_warp_kernel<false, true>),
+        reinterpret_cast<const void*>(&coo_warp_kernel<true, true>),
+        reinterpret_cast<const void*>(&coo_fixup<false>),
+        reinterpret_cast<const void*>(&coo_fixup<true>),
+        reinterpret_cast<const void*>(&coo_fixup_long<false>),
+        reinterpret_cast<const void*>(&coo_fixup_long<true>),
+        reinterpret_cast<const void*>(&ell_kernel<false, true>),
+        reinterpret_cast<const void*>(&dia_follow_kernel),
+        reinterpret_cast<const void*>(&follow_fill),
+    };
+    for (const void* fn : fns) {
+        cudaFuncAttributes a;
+        SOB_CUDA(cudaFuncGetAttributes(&a, fn));
+    }
+}
 FollowStage g_follow[64];
 }  // namespace
 
@@ -1137,6 +1182,10 @@ void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
         SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&f.timed_out_dev), f.timed_out, 0));
         SOB_CUDA(cudaEventCreateWithFlags(&f.refilled, cudaEventDisableTiming));
         SOB_CUDA(cudaEventCreateWithFlags(&f.copied, cudaEventDisableTiming));
+    }
+    if (!f.preloaded) {
+        follow_preload();
+        f.preloaded = true;
     }
     const unsigned slot = f.next_slot++ % kFollowSlots;
     f.timed_out[slot] = 0;
@@ -1212,6 +1261,8 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
     return true;
 }
 
+static void coo_profile(const CooPart& coo, int64_t nrows, cudaStream_t s);
+
 // Pinned spmv(m, x) on a CSR matrix (or HDC without a DIA part) or an ELL
 // matrix (or HYB without a COO part): the kernels launched with FOLLOW trail
 // ONE upload of x (each x gather waits for its element) and store y straight
@@ -1219,20 +1270,42 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
 // persistent CSR warp kernel walks its groups in address order (group g,
 // g + grid, ...) and the ELL grid runs its row blocks in order, so on banded
 // / stencil rows the kernels follow the copy front; scattered columns just
-// wait longer.
+// wait longer.  COO (and HYB with a COO part) follow the upload the same way
+// but into device y, copied down after the fix-up: their row sums end at
+// scattered lanes, and 8-byte stores into mapped memory each cost a link
+// transaction (profiles/r02ac_ab_mapped_y.txt).
 bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy,
                         const std::function<void()>* after_kernels, const std::function<void(double*)>& upload,
                         FollowToken& tok) {
     static const bool off = std::getenv("SOB_NO_CSR_FOLLOW") != nullptr;  // diagnostic knob (A/B)
+    static const bool coo_off = std::getenv("SOB_NO_COO_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     if (off || follow_disabled()) return false;
     const bool csr = (m.format == SO_CSR || (m.format == SO_HDC && m.dia.ndiags == 0)) && m.csr.nnz > 0;
     const bool ell = (m.format == SO_ELL || (m.format == SO_HYB && m.coo.nnz == 0)) && m.ell.width > 0;
-    if (!csr && !ell) return false;
+    const bool coo = !coo_off && (m.format == SO_COO || m.format == SO_HYB) && m.coo.nnz > 0;
+    if (!csr && !ell && !coo) return false;
+    if (coo) coo_profile(m.coo, m.nrows, s);  // cached after the first multiply
     follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
-        if (csr)
+        if (csr) {
             launch_csr_stream(m, false, dx, y_mapped, s, &fc);
-        else
+        } else if (ell) {
             launch_ell<false>(m, dx, y_mapped, s, &fc);
+        } else {
+            // both released stream-ordered after the copy below; allocated
+            // before the first launch (see follow_preload)
+            DBuf<double> yd(m.nrows, s);
+            DBuf<CooChunkRec> rec(coo_rec_count(m.coo), s);
+            if (m.format == SO_HYB) {
+                launch_ell<false>(m, dx, yd.get(), s, m.ell.width > 0 ? &fc : nullptr);
+                launch_coo<true>(m.coo, m.nrows, dx, yd.get(), s, &fc, &rec);
+            } else if (m.coo.max_gap < 0 || m.coo.max_gap > kCooGapInline) {  // spmv_device's safe path
+                SOB_CUDA(cudaMemsetAsync(yd.get(), 0, sizeof(double) * size_t(m.nrows), s));
+                launch_coo<true>(m.coo, m.nrows, dx, yd.get(), s, &fc, &rec);
+            } else {
+                launch_coo<false>(m.coo, m.nrows, dx, yd.get(), s, &fc, &rec);
+            }
+            SOB_CUDA(cudaMemcpyAsync(y_mapped, yd.get(), sizeof(double) * size_t(m.nrows), cudaMemcpyDefault, s));
+        }
         if (after_kernels) (*after_kernels)();
     }, upload, tok);
     return true;

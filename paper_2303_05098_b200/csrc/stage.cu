@@ -317,8 +317,13 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                 }
             }
             // CSR / ELL: the same with one launch of the FOLLOW kernels; one
-            // event after it gates every y chunk's copy-out
-            if (!dia_only) {
+            // event after it gates every y chunk's copy-out.  Not with a COO
+            // part: its follow variant writes device y, and one copy of all
+            // of y behind the kernels delays the chunked copy-out (config 2
+            // COO 1.85 -> 1.80 ms, the HYB-shaped matrix COO 1.68 -> 1.81,
+            // HYB 1.62 -> 1.82; profiles/r02ao_coo_follow.txt)
+            const bool coo_part = (m.format == SO_COO || m.format == SO_HYB) && m.coo.nnz > 0;
+            if (!dia_only && !coo_part) {
                 cudaStream_t copy = ctx(dev).copy_in;
                 const std::function<void()> after = [&]() {
                     SOB_CUDA(cudaEventRecord(st.ev[0], s));

@@ -459,7 +459,8 @@ def test_follow_copy_path_edge_cases(so, O):
     sentinel half-word, a matrix with more columns than its rows' window
     reaches (the kernel ends before the copy; the sentinel refill must wait
     for it), and consecutive calls with different x (no stale x from the
-    previous call).  Every result bit-identical to the oracle."""
+    previous call).  Every result bit-identical to the oracle (COO: to the
+    device multiply, the oracle within the bar)."""
     import torch
 
     sent = np.array([0x7FF5A5A57FF5A5A5], dtype=np.uint64).view(np.float64)[0]
@@ -477,7 +478,7 @@ def test_follow_copy_path_edge_cases(so, O):
         xt = torch.empty(ncols, dtype=torch.float64).pin_memory()
         yt = torch.empty(nrows, dtype=torch.float64).pin_memory()
         xn, yn = xt.numpy(), yt.numpy()
-        for fmt in (so.DIA, so.CSR, so.ELL):  # the DIA follow kernel and the CSR / ELL kernels. FOLLOW variants
+        for fmt in (so.DIA, so.CSR, so.ELL, so.COO):  # the DIA follow kernel and the CSR / ELL / COO FOLLOW variants
             m = d.from_coo(fmt)
             want_m = O.oc_convert(coo, fmt)
             for trial in range(4):
@@ -489,7 +490,19 @@ def test_follow_copy_path_edge_cases(so, O):
                 want = O.oc_spmv(want_m, xn)
                 yn[:] = 0.0
                 m.spmv_into(xn, yn)
-                assert np.array_equal(yn, want, equal_nan=True), (fmt, nrows, ncols, trial)
+                if fmt != so.COO:
+                    assert np.array_equal(yn, want, equal_nan=True), (fmt, nrows, ncols, trial)
+                    continue
+                # COO: bit-identical to the device multiply, the oracle within the bar
+                xd = torch.tensor(xn, device="cuda")
+                yd = torch.empty(nrows, dtype=torch.float64, device="cuda")
+                torch.cuda.synchronize()
+                m.spmv_device(xd.data_ptr(), yd.data_ptr())
+                torch.cuda.synchronize()
+                assert np.array_equal(yn, yd.cpu().numpy(), equal_nan=True), (fmt, nrows, ncols, trial)
+                assert np.array_equal(np.isnan(yn), np.isnan(want)), (fmt, nrows, ncols, trial)
+                ok = ~np.isnan(want)
+                assert max_rel(yn[ok], want[ok]) <= SPMV_TOL, (fmt, nrows, ncols, trial)
 
 
 def test_stencil27_generator_and_row_slices(so, O):
@@ -817,18 +830,23 @@ def test_follow_path_concurrent_callers(so, O):
     assert not errors, errors
 
 
-@pytest.mark.parametrize("shape", ["band", "rmat"])
+@pytest.mark.parametrize("shape", ["band", "rmat", "hyb"])
 def test_pinned_host_spmv_all_formats(so, O, shape):
     """Pinned host x/y through spmv(m, x) in every format (DIA: the
-    follow-the-copy kernel; the others: the staged copy-engine path): each
-    result equals the device-resident multiply bit for bit and the oracle
-    within the bar.  (Kernels storing y straight into mapped host memory were
-    measured for the non-DIA formats and rejected: COO 1.9 -> 5.7 ms, CSR
-    unchanged, profiles/r02ac_ab_mapped_y.txt.)"""
+    follow-the-copy kernel; CSR / ELL: their FOLLOW variants storing y into
+    mapped host memory; COO / HYB with a COO part: FOLLOW variants into
+    device y, then one copy down; HDC with both parts: the copy-engine
+    path): each result equals the device-resident multiply bit for bit and
+    the oracle within the bar."""
     import torch
     from paper_2303_05098_b200 import synth
 
-    csr = synth.banded(600_000, 4, seed=4) if shape == "band" else synth.rmat(19, 8, seed=11)
+    if shape == "band":
+        csr = synth.banded(600_000, 4, seed=4)
+    elif shape == "rmat":
+        csr = synth.rmat(19, 8, seed=11)
+    else:  # HYB with a COO part (rows past K_H)
+        csr = synth.hyb_skewed(600_000, 8, 40, 50, seed=6)
     coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
     d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
     xt = torch.empty(csr.ncols, dtype=torch.float64).pin_memory()
@@ -849,3 +867,34 @@ def test_pinned_host_spmv_all_formats(so, O, shape):
         torch.cuda.synchronize()
         assert np.array_equal(yn, yd.cpu().numpy()), (shape, f)
         assert max_rel(yn, O.oc_spmv(O.oc_convert(coo, f), xn)) <= SPMV_TOL, (shape, f)
+
+
+def test_pinned_coo_follow_gappy_rows(so, O):
+    """Pinned spmv(m, x) on a COO matrix whose entries sit in every 10000th
+    row (empty-row runs past kCooGapInline: y = 0 + the accumulating COO
+    kernel, here its FOLLOW variant) and on the same rows in HYB: equal to the
+    device multiply and to the oracle within the bar, over consecutive calls."""
+    import torch
+
+    n = 700_000
+    rng = np.random.default_rng(41)
+    rows = np.repeat(np.arange(5, n, 10_000), 1200)  # HYB: K_H = 1, ELL part within the padding cap
+    cols = rng.integers(0, n, rows.size)
+    coo = O.from_triplets(n, n, rows, cols, rng.uniform(-1, 1, rows.size))
+    d = to_dev(so, coo)
+    xt = torch.empty(n, dtype=torch.float64).pin_memory()
+    yt = torch.empty(n, dtype=torch.float64).pin_memory()
+    xn, yn = xt.numpy(), yt.numpy()
+    for f in (so.COO, so.HYB):
+        m = d.from_coo(f)
+        for trial in range(3):
+            xn[:] = rng.uniform(-1, 1, n)
+            yn[:] = np.nan
+            m.spmv_into(xn, yn)
+            xd = torch.tensor(xn, device="cuda")
+            yd = torch.empty(n, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            m.spmv_device(xd.data_ptr(), yd.data_ptr())
+            torch.cuda.synchronize()
+            assert np.array_equal(yn, yd.cpu().numpy()), (f, trial)
+            assert max_rel(yn, O.oc_spmv(O.oc_convert(coo, f), xn)) <= SPMV_TOL, (f, trial)
