@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(kStreamBlock)
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ part,
                     FollowCtx fctx) {
     __shared__ double scratch[kStreamBlock / 32];
+    pdl_enter();
     const int64_t k0 = pk[2 * blockIdx.x], k1 = pk[2 * blockIdx.x + 1];
     constexpr int U = kPiece / kStreamBlock;
     int c[U];
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(kStreamBlock)
 template <bool ACCUM>
 __global__ void csr_long_fixup(int64_t nlong, const int32_t* __restrict__ lrow, const int64_t* __restrict__ lpiece,
                                const double* __restrict__ part, double* __restrict__ y) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const int64_t l = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (l >= nlong) return;
@@ -655,6 +657,13 @@ __global__ void __launch_bounds__(256)
 // the lane holding the next row's first entry (y written exactly once).
 // ACCUM (HYB COO part, spmv.cpp:95-100): the row sum is added to the ELL
 // result already in y.  Variants measured in scripts/spmv_lab.cu.
+// Fix-up kernels launched with programmatic dependent launch (they wait for
+// the kernel before them with griddepcontrol.wait).  SOB_NO_PDL_FIXUP: A/B.
+bool fixup_pdl() {
+    static const bool on = std::getenv("SOB_NO_PDL_FIXUP") == nullptr;
+    return on;
+}
+
 constexpr int kCooItems = 8;
 constexpr int kCooChunk = 32 * kCooItems;
 constexpr int kCooPerSm = 3;
@@ -773,6 +782,8 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     const int64_t nchunks = (z + kCooChunk - 1) / kCooChunk;
     const int64_t stride = int64_t(gridDim.x) * (blockDim.x >> 5);
     int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    // coo_fixup (launched with PDL) is scheduled early and waits for this grid
+    asm volatile("griddepcontrol.launch_dependents;" :::);
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // coo_fixup's control words (after the records)
         unsigned long long* ctl = reinterpret_cast<unsigned long long*>(rec + nchunks);
         ctl[0] = 0;
@@ -856,6 +867,7 @@ template <bool ACCUM>
 __global__ void __launch_bounds__(256) coo_fixup(int64_t nchunks, const CooChunkRec* __restrict__ rec,
                                                  double* __restrict__ y, LongRun* __restrict__ runs,
                                                  unsigned long long* __restrict__ ctl) {
+    pdl_enter();
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int32_t f = c < nchunks ? rec[c].flags : 0;
     if ((f & kLastOpen) && !(f & kSingle)) {
@@ -898,6 +910,7 @@ template <bool ACCUM>
 __global__ void __launch_bounds__(256) coo_fixup_long(int64_t nchunks, const CooChunkRec* __restrict__ rec,
                                                       double* __restrict__ y, const LongRun* __restrict__ runs,
                                                       const unsigned long long* __restrict__ ctl) {
+    pdl_enter();
     const unsigned long long n = ctl[0];
     for (unsigned long long q = blockIdx.x; q < n; q += gridDim.x) finish_long_runs<ACCUM>(nchunks, rec, y, runs + q, 1);
 }
@@ -950,10 +963,20 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
     SOB_LAUNCH("coo_warp_kernel");
     LongRun* runs = reinterpret_cast<LongRun*>(rec.get() + nchunks + 1);
     unsigned long long* ctl = reinterpret_cast<unsigned long long*>(rec.get() + nchunks);
-    coo_fixup<ACCUM><<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y, runs, ctl);
+    if (fixup_pdl()) {  // scheduled while the chunk kernel runs; waits for it
+        launch_pdl(coo_fixup<ACCUM>, dim3(unsigned(ceil_div(nchunks, 256))), dim3(256), 0, s, nchunks,
+                   static_cast<const CooChunkRec*>(rec.get()), y, runs, ctl);
+    } else {
+        coo_fixup<ACCUM><<<unsigned(ceil_div(nchunks, 256)), 256, 0, s>>>(nchunks, rec.get(), y, runs, ctl);
+    }
     SOB_LAUNCH("coo_fixup");
     if (coo.long_runs != 0) {  // unknown (-1) or present
-        coo_fixup_long<ACCUM><<<current_ctx().num_sms, 256, 0, s>>>(nchunks, rec.get(), y, runs, ctl);
+        if (fixup_pdl())
+            launch_pdl(coo_fixup_long<ACCUM>, dim3(unsigned(current_ctx().num_sms)), dim3(256), 0, s, nchunks,
+                       static_cast<const CooChunkRec*>(rec.get()), y, static_cast<const LongRun*>(runs),
+                       static_cast<const unsigned long long*>(ctl));
+        else
+            coo_fixup_long<ACCUM><<<current_ctx().num_sms, 256, 0, s>>>(nchunks, rec.get(), y, runs, ctl);
         SOB_LAUNCH("coo_fixup_long");
     }
 }
@@ -1018,18 +1041,32 @@ void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* 
             : launch_csr_warp<kGroupItemsLong, false>(m, accum, x, y, s, follow);
     if (c.nlong > 0) {
         const FollowCtx none{nullptr, nullptr, 0};
-        if (follow)
-            csr_long_pieces<true><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(),
-                                                                                c.val.get(), x, part.get(), *follow);
-        else
-            csr_long_pieces<false><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(c.piece_k.get(), c.col.get(),
-                                                                                 c.val.get(), x, part.get(), none);
-        SOB_LAUNCH("csr_long_pieces");
+        const int64_t* pk = c.piece_k.get();
+        const int32_t* col = c.col.get();
+        const double* val = c.val.get();
+        const int32_t* lrow = c.long_row.get();
+        const int64_t* lpiece = c.long_piece.get();
+        const double* cpart = part.get();
         const unsigned g = unsigned(ceil_div(c.nlong * 32, 128));  // one warp per long row
-        if (accum)
-            csr_long_fixup<true><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y);
-        else
-            csr_long_fixup<false><<<g, 128, 0, s>>>(c.nlong, c.long_row.get(), c.long_piece.get(), part.get(), y);
+        if (fixup_pdl()) {  // each waits for the kernel before it (launch latency hidden)
+            launch_pdl(follow ? csr_long_pieces<true> : csr_long_pieces<false>, dim3(unsigned(c.npieces)),
+                       dim3(kStreamBlock), 0, s, pk, col, val, x, part.get(), follow ? *follow : none);
+            SOB_LAUNCH("csr_long_pieces");
+            launch_pdl(accum ? csr_long_fixup<true> : csr_long_fixup<false>, dim3(g), dim3(128), 0, s, c.nlong, lrow,
+                       lpiece, cpart, y);
+        } else {
+            if (follow)
+                csr_long_pieces<true><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(pk, col, val, x, part.get(),
+                                                                                    *follow);
+            else
+                csr_long_pieces<false><<<unsigned(c.npieces), kStreamBlock, 0, s>>>(pk, col, val, x, part.get(),
+                                                                                     none);
+            SOB_LAUNCH("csr_long_pieces");
+            if (accum)
+                csr_long_fixup<true><<<g, 128, 0, s>>>(c.nlong, lrow, lpiece, cpart, y);
+            else
+                csr_long_fixup<false><<<g, 128, 0, s>>>(c.nlong, lrow, lpiece, cpart, y);
+        }
         SOB_LAUNCH("csr_long_fixup");
     }
 }
