@@ -46,6 +46,7 @@ struct CooPart {
     // (each value is meaningful on its own: -1 = unknown = the safe path).
     mutable std::atomic<int64_t> max_gap{-1};  // longest empty-row run
     mutable std::atomic<int> long_runs{-1};    // some row covers > kFixupInline chunks
+    mutable std::atomic<int> short_rows{-1};   // every row <= 32 entries (COO CONT: no records)
 };
 struct CsrPart {
     int64_t nnz = 0;

@@ -698,10 +698,17 @@ __device__ __forceinline__ void coo_load(const int32_t* __restrict__ row, const 
     }
 }
 
-template <bool ACCUM>
+// CONT (every row <= 32 entries, so a row spans at most two chunks and its
+// continuation fits one warp load): no records -- the chunk holding a row's
+// first entry finishes it, reading the row's continuation at the head of the
+// next chunk itself (coo_warp_kernel);
+// the chunk's open row's in-chunk sum is returned in `open_acc` (the lane
+// holding the chunk's last entry) and orphan prefixes are skipped.
+template <bool ACCUM, bool CONT = false>
 __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base, int cnt, int64_t z, int64_t nrows,
                                            const int (&r)[kCooItems], const double (&p)[kCooItems], int prev_row,
-                                           int next_row, double* __restrict__ y, CooChunkRec* __restrict__ rec) {
+                                           int next_row, double* __restrict__ y, CooChunkRec* __restrict__ rec,
+                                           double& open_acc) {
     constexpr int IT = kCooItems;
     constexpr unsigned kFull = 0xffffffffu;
     const int first = lane * IT;
@@ -748,12 +755,17 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
             const int nxt = j + 1 < nmine ? r[j + 1] : (chunk_end ? next_row : nlane_r0);
             const bool orphan = first_cont && rw == first_row;  // began in an earlier chunk
             if (rw != nxt) {
-                if (orphan)
-                    rec[chunk].first_sum = acc;
-                else
+                if (!orphan)
                     y_store<ACCUM>(y + rw, acc);
+                else if (!CONT)
+                    rec[chunk].first_sum = acc;
             }
-            if (chunk_end && j + 1 == nmine) {
+            if (CONT && chunk_end && j + 1 == nmine) {
+                if (rw == nxt) open_acc = acc;
+                if (!ACCUM && base + cnt == z)  // trailing empty rows
+                    for (int64_t q = int64_t(rw) + 1; q < nrows; ++q) y[q] = 0.0;
+            }
+            if (!CONT && chunk_end && j + 1 == nmine) {
                 const bool open = rw == nxt;
                 if (open) {
                     rec[chunk].last_sum = acc;
@@ -772,7 +784,7 @@ __device__ __forceinline__ void coo_finish(int lane, int64_t chunk, int64_t base
 
 // FOLLOW: pinned spmv(m, x) -- each x gather waits for its element of the
 // upload (ldx); the persistent warps walk their chunks in address order.
-template <bool ACCUM, bool FOLLOW = false>
+template <bool ACCUM, bool FOLLOW = false, bool CONT = false>
 __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
@@ -784,7 +796,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     // coo_fixup (launched with PDL) is scheduled early and waits for this grid
     asm volatile("griddepcontrol.launch_dependents;" :::);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // coo_fixup's control words (after the records)
+    if (!CONT && blockIdx.x == 0 && threadIdx.x == 0) {  // coo_fixup's control words (after the records)
         unsigned long long* ctl = reinterpret_cast<unsigned long long*>(rec + nchunks);
         ctl[0] = 0;
         ctl[1] = 0;
@@ -802,6 +814,27 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
         for (int j = 0; j < IT; ++j) p[j] = lane * IT + j < cnt ? fmul(v[j], ldx<FOLLOW>(x, c[j], fctx)) : 0.0;
         const int prev_row = base > 0 ? row[base - 1] : -1;
         const int next_row = base + cnt < z ? row[base + cnt] : -1;
+        // CONT: the head of the next chunk (the open row's continuation, if
+        // any), loaded with this chunk and consumed after its finish
+        int hr = kNoRow, last_row = kNoRow;
+        double hp = 0.0;
+        const int owner = (cnt - 1) / IT;  // lane holding the chunk's last entry
+        if (CONT) {
+            const int64_t k = base + cnt + lane;
+            int hc = 0;
+            double hv = 0.0;
+            if (k < z) {
+                hr = __ldg(row + k);
+                hc = __ldg(col + k);
+                hv = __ldg(val + k);
+            }
+            int tr = kNoRow;
+#pragma unroll
+            for (int j = 0; j < IT; ++j)
+                if (lane * IT + j < cnt) tr = r[j];
+            last_row = __shfl_sync(0xffffffffu, tr, owner);
+            if (hr == last_row) hp = fmul(hv, ldx<FOLLOW>(x, hc, fctx));
+        }
         int rc[IT];
 #pragma unroll
         for (int j = 0; j < IT; ++j) rc[j] = r[j];
@@ -809,7 +842,14 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
         if (nx < nchunks)
             coo_load(row, col, val, nx * kCooChunk + lane * IT, int(min(z - nx * kCooChunk, int64_t(kCooChunk))) - lane * IT,
                      r, c, v);
-        coo_finish<ACCUM>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec);
+        double open_acc = 0.0;
+        coo_finish<ACCUM, CONT>(lane, chunk, base, cnt, z, nrows, rc, p, prev_row, next_row, y, rec, open_acc);
+        if (CONT) {
+            if (next_row == last_row) {  // warp-uniform: the last row continues (< 32 more entries)
+                const double t = warp_sum(hp);  // fixed butterfly: deterministic
+                if (lane == owner) y_store<ACCUM>(y + last_row, fadd(open_acc, t));
+            }
+        }
         if (nx >= nchunks) break;
         chunk = nx;
     }
@@ -924,31 +964,59 @@ __global__ void __launch_bounds__(256) coo_fixup_long(int64_t nchunks, const Coo
 __global__ void coo_max_gap(int64_t z, int64_t nrows, const int32_t* __restrict__ row,
                             unsigned long long* __restrict__ out) {
     // out[0] = longest empty-row run; out[1] |= 1 when some row fully covers
-    // kFixupInline + 1 consecutive chunks (only then can coo_fixup queue a long run)
+    // kFixupInline + 1 consecutive chunks (only then can coo_fixup queue a long
+    // run); out[2] |= 1 when some row holds more than 32 entries
     constexpr int64_t kSpan = int64_t(kFixupInline) * kCooChunk - 1;
     unsigned long long g = 0;
-    bool lng = false;
+    bool lng = false, big = false;
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k <= z; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t prv = k == 0 ? -1 : row[k - 1];
         const int64_t cur = k == z ? nrows : row[k];
         const int64_t gap = cur - prv - 1;
         if (gap > int64_t(g)) g = gap;
         if (k % kCooChunk == 0 && k + kSpan < z && row[k] == row[k + kSpan]) lng = true;
+        if (k + 32 < z && row[k] == row[k + 32]) big = true;
     }
     g = warp_max(g);
     if ((threadIdx.x & 31) == 0 && g) atomicMax(out, g);
     if (__any_sync(0xffffffffu, lng) && (threadIdx.x & 31) == 0) out[1] = 1;
+    if (__any_sync(0xffffffffu, big) && (threadIdx.x & 31) == 0) out[2] = 1;
 }
 constexpr int64_t kCooGapInline = 4096;  // a lane zero-fills up to ~2 us of rows inline
 
 // chunk records, then the fix-up's control word pair and long-run queue
 int64_t coo_rec_count(const CooPart& coo) { return 2 * ceil_div(coo.nnz, kCooChunk) + 1; }
 
+// Every row <= 32 entries (profiled) and a small matrix: the chunk kernel
+// finishes rows crossing into the next chunk itself -- no records, no fix-up
+// kernel (config 1: 28.7 -> 24.9 us).  The head load of the next chunk costs
+// ~0.1 us per million entries (config 2: 375 -> 385 us), the fix-up ~4.5 us
+// flat: break-even near 35 M entries, gated at 16 M
+// (profiles/r02au_coo_cont.txt).  SOB_NO_COO_CONT / SOB_COO_CONT=1: A/B.
+constexpr int64_t kCooContMaxNnz = int64_t(1) << 24;
+bool coo_cont(const CooPart& coo) {
+    static const bool off = std::getenv("SOB_NO_COO_CONT") != nullptr;
+    static const bool always = std::getenv("SOB_COO_CONT") != nullptr;
+    return !off && coo.short_rows.load(std::memory_order_acquire) == 1 && (always || coo.nnz <= kCooContMaxNnz);
+}
+
 // `pre`: the record buffer allocated by a follow path before its first launch
 template <bool ACCUM>
 void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s,
                 const FollowCtx* follow = nullptr, DBuf<CooChunkRec>* pre = nullptr) {
     const int64_t nchunks = ceil_div(coo.nnz, kCooChunk);
+    if (coo_cont(coo)) {
+        const int grid = int(std::min<int64_t>(ceil_div(nchunks, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
+        if (follow)
+            coo_warp_kernel<ACCUM, true, true><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(),
+                                                                    coo.val.get(), x, y, nullptr, *follow);
+        else
+            coo_warp_kernel<ACCUM, false, true><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(),
+                                                                     coo.val.get(), x, y, nullptr,
+                                                                     FollowCtx{nullptr, nullptr, 0});
+        SOB_LAUNCH("coo_warp_kernel");
+        return;
+    }
     static_assert(sizeof(LongRun) == sizeof(CooChunkRec) && sizeof(CooChunkRec) >= 16, "record layout");
     DBuf<CooChunkRec> own;
     if (!pre) own.alloc(coo_rec_count(coo), s);
@@ -1165,6 +1233,8 @@ void follow_preload() {
         reinterpret_cast<const void*>(&csr_long_fixup<false>),
         reinterpret_cast<const void*>(&coo_warp_kernel<false, true>),
         reinterpret_cast<const void*>(&coo_warp_kernel<true, true>),
+        reinterpret_cast<const void*>(&coo_warp_kernel<false, true, true>),
+        reinterpret_cast<const void*>(&coo_warp_kernel<true, true, true>),
         reinterpret_cast<const void*>(&coo_fixup<false>),
         reinterpret_cast<const void*>(&coo_fixup<true>),
         reinterpret_cast<const void*>(&coo_fixup_long<false>),
@@ -1331,7 +1401,7 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
             // both released stream-ordered after the copy below; allocated
             // before the first launch (see follow_preload)
             DBuf<double> yd(m.nrows, s);
-            DBuf<CooChunkRec> rec(coo_rec_count(m.coo), s);
+            DBuf<CooChunkRec> rec(coo_cont(m.coo) ? 0 : coo_rec_count(m.coo), s);
             if (m.format == SO_HYB) {
                 launch_ell<false>(m, dx, yd.get(), s, m.ell.width > 0 ? &fc : nullptr);
                 launch_coo<true>(m.coo, m.nrows, dx, yd.get(), s, &fc, &rec);
@@ -1433,14 +1503,15 @@ static void coo_profile(const CooPart& coo, int64_t nrows, cudaStream_t s) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     SOB_CUDA(cudaStreamIsCapturing(s, &cap));
     if (cap != cudaStreamCaptureStatusNone) return;  // stays unknown: safe paths
-    DBuf<unsigned long long> g(2, s);
-    SOB_CUDA(cudaMemsetAsync(g.get(), 0, 2 * sizeof(unsigned long long), s));
+    DBuf<unsigned long long> g(3, s);
+    SOB_CUDA(cudaMemsetAsync(g.get(), 0, 3 * sizeof(unsigned long long), s));
     coo_max_gap<<<grid_for(coo.nnz + 1, 256, 4), 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), g.get());
     SOB_LAUNCH("coo_max_gap");
-    unsigned long long h[2];
+    unsigned long long h[3];
     SOB_CUDA(cudaMemcpyAsync(h, g.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     SOB_CUDA(cudaStreamSynchronize(s));
     coo.long_runs = h[1] ? 1 : 0;
+    coo.short_rows = h[2] ? 0 : 1;
     coo.max_gap = int64_t(h[0]);
 }
 

@@ -898,3 +898,43 @@ def test_pinned_coo_follow_gappy_rows(so, O):
             torch.cuda.synchronize()
             assert np.array_equal(yn, yd.cpu().numpy()), (f, trial)
             assert max_rel(yn, O.oc_spmv(O.oc_convert(coo, f), xn)) <= SPMV_TOL, (f, trial)
+
+
+def test_coo_cont_and_records_paths(so, O, tmp_path):
+    """COO on a matrix of rows <= 32 entries below kCooContMaxNnz runs the
+    chunk kernel that finishes rows crossing into the next chunk itself
+    (CONT, spmv.cu);
+    the same multiply with records + coo_fixup (SOB_NO_COO_CONT=1, a fresh
+    process) -- both within the bar of the oracle, each deterministic, for
+    COO and HYB (accumulating) and rows crossing chunk boundaries at every
+    offset."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_2303_05098_b200 import synth
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2303_05098_b200 as P\n"
+        "from paper_2303_05098_b200 import synth\n"
+        "csr = synth.hyb_skewed(200_000, 7, 29, 37, seed=5)\n"
+        "d = P.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)\n"
+        "x = np.random.default_rng(8).uniform(-1, 1, csr.ncols)\n"
+        "np.save(sys.argv[1], np.stack([d.convert(f).spmv(x) for f in (0, 4)]))\n" % root)
+    out = {}
+    for name, env in (("cont", {}), ("records", {"SOB_NO_COO_CONT": "1"})):
+        path = str(tmp_path / f"{name}.npy")
+        subprocess.run([sys.executable, "-c", prog, path], check=True, env={**os.environ, **env}, timeout=600)
+        out[name] = np.load(path)
+    csr = synth.hyb_skewed(200_000, 7, 29, 37, seed=5)
+    coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
+    x = np.random.default_rng(8).uniform(-1, 1, csr.ncols)
+    d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+    for i, f in enumerate((0, 4)):
+        want = O.oc_spmv(O.oc_convert(coo, f), x)
+        got = d.convert(f).spmv(x)
+        assert np.array_equal(got, out["cont"][i]), f  # this process runs CONT too
+        for name in ("cont", "records"):
+            assert max_rel(out[name][i], want) <= SPMV_TOL, (name, f)
