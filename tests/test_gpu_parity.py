@@ -782,9 +782,10 @@ def test_cpu_baseline_bytes_match_device_accounting(so, O):
 
 def test_follow_path_concurrent_callers(so, O):
     """Pinned and pageable spmv(m, x) from several host threads at once on two
-    narrow-window DIA matrices (the follow-the-copy path shares one device
-    copy of x per device: calls are ordered through its refill event, each
-    with its own timeout word): every result equals the device multiply."""
+    banded matrices in DIA, CSR, COO and ELL (the follow-the-copy paths share
+    one device copy of x per device: calls are ordered through its refill
+    event, each with its own timeout word): every result equals the device
+    multiply."""
     import threading
 
     import torch
@@ -793,14 +794,15 @@ def test_follow_path_concurrent_callers(so, O):
     mats = []
     for n, half in ((600_000, 3), (700_000, 6)):
         csr = synth.banded(n, half, seed=n)
-        d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val).convert(so.DIA)
-        mats.append((d, csr.ncols))
+        base = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
+        for f in (so.DIA, so.CSR, so.COO, so.ELL):  # every follow kernel family shares the device's staged x
+            mats.append((base.convert(f), csr.ncols))
     errors = []
 
     def worker(t):
         try:
             rng = np.random.default_rng(100 + t)
-            d, nc = mats[t % 2]
+            d, nc = mats[t % len(mats)]
             pinned = t % 3 != 2
             for _ in range(6):
                 xv = rng.uniform(-1, 1, nc)
@@ -822,7 +824,7 @@ def test_follow_path_concurrent_callers(so, O):
         except Exception as e:  # noqa: BLE001
             errors.append((t, repr(e)))
 
-    ths = [threading.Thread(target=worker, args=(t,)) for t in range(6)]
+    ths = [threading.Thread(target=worker, args=(t,)) for t in range(12)]
     for th in ths:
         th.start()
     for th in ths:
