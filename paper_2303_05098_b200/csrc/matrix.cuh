@@ -185,6 +185,8 @@ bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped,
 // never arrived (y invalid).
 struct FollowToken {
     unsigned* timed_out = nullptr;  // this call's timeout word (mapped)
+    cudaEvent_t done = nullptr;     // recorded after the call's kernels (before the sentinel refill)
+    bool upload_first = false;      // in: the upload does not block the host (pinned x): queue it first
 };
 bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
                    const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,

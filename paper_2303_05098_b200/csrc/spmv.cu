@@ -1217,6 +1217,7 @@ struct FollowStage {
     unsigned* timed_out_dev = nullptr;
     unsigned next_slot = 0;
     cudaEvent_t refilled = nullptr, copied = nullptr;
+    cudaEvent_t done[kFollowSlots] = {};  // per call slot: its kernels are complete
     bool preloaded = false;
 };
 
@@ -1289,6 +1290,7 @@ void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
         SOB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&f.timed_out_dev), f.timed_out, 0));
         SOB_CUDA(cudaEventCreateWithFlags(&f.refilled, cudaEventDisableTiming));
         SOB_CUDA(cudaEventCreateWithFlags(&f.copied, cudaEventDisableTiming));
+        for (int i = 0; i < kFollowSlots; ++i) SOB_CUDA(cudaEventCreateWithFlags(&f.done[i], cudaEventDisableTiming));
     }
     if (!f.preloaded) {
         follow_preload();
@@ -1297,6 +1299,7 @@ void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
     const unsigned slot = f.next_slot++ % kFollowSlots;
     f.timed_out[slot] = 0;
     tok.timed_out = f.timed_out + slot;
+    tok.done = f.done[slot];
     const int grid_fill = current_ctx().num_sms * 4;
     // everything of the previous call (its kernels, copy and refill, possibly
     // on another stream) precedes this call's use -- or release -- of dx
@@ -1315,13 +1318,25 @@ void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
     SOB_CUDA(cudaStreamWaitEvent(copy, f.refilled, 0));
     // 250 ms plus 1 ns per byte of x (a slowly staged pageable x still arrives)
     const FollowCtx fc{f.flag, f.timed_out_dev + slot, 250ull * 1000 * 1000 + 8ull * uint64_t(nc)};
-    kernels(f.dx, fc);
-    upload(f.dx);  // the caller's H2D copies of x into f.dx on `copy`
+    // pinned x: the copy is queued first (it starts a kernel launch earlier;
+    // the kernels still trail it).  Staged x: the upload blocks on host
+    // threads, so the kernels go first.  SOB_FOLLOW_KERNEL_FIRST: A/B.
+    static const bool kernel_first = std::getenv("SOB_FOLLOW_KERNEL_FIRST") != nullptr;
+    if (tok.upload_first && !kernel_first) {
+        upload(f.dx);
+        kernels(f.dx, fc);
+    } else {
+        kernels(f.dx, fc);
+        upload(f.dx);  // the caller's H2D copies of x into f.dx on `copy`
+    }
     SOB_CUDA(cudaMemcpyAsync(f.flag, f.one_host, sizeof(unsigned), cudaMemcpyHostToDevice, copy));
     SOB_CUDA(cudaEventRecord(f.copied, copy));
     // refill the sentinels for the next call once the copy has finished (x
     // columns no row reads are not waited for by the kernels)
     SOB_CUDA(cudaStreamWaitEvent(s, f.copied, 0));
+    // the caller waits for this -- kernels and copy done (the caller's x may
+    // be reused once it returns) -- not for the refill below
+    SOB_CUDA(cudaEventRecord(tok.done, s));
     follow_fill<<<grid_fill, 256, 0, s>>>(reinterpret_cast<unsigned*>(f.dx), 2 * nc, f.flag);
     SOB_LAUNCH("follow_fill");
     SOB_CUDA(cudaEventRecord(f.refilled, s));
@@ -1418,15 +1433,26 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
     return true;
 }
 
+// A pinned call returns once its kernels are done (y is in host memory);
+// the sentinel refill queued behind them on `s` is not waited for.
+static void follow_wait_done(const FollowToken& tok, cudaStream_t s) {
+    static const bool stream_sync = std::getenv("SOB_FOLLOW_KERNEL_FIRST") != nullptr;  // A/B (as before)
+    if (stream_sync)
+        SOB_CUDA(cudaStreamSynchronize(s));
+    else
+        SOB_CUDA(cudaEventSynchronize(tok.done));
+}
+
 bool spmv_csr_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
                      cudaStream_t copy) {
     const int64_t nc = m.ncols;
     FollowToken tok;
+    tok.upload_first = true;
     if (!follow_launch_rows(m, y_mapped, s, copy, nullptr, [&](double* dx) {
             SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
         }, tok))
         return false;
-    SOB_CUDA(cudaStreamSynchronize(s));
+    follow_wait_done(tok, s);
     if (!follow_finish(tok)) {  // the copy never showed up: recompute elsewhere
         SOB_CUDA(cudaStreamSynchronize(copy));
         return false;
@@ -1445,12 +1471,13 @@ bool follow_finish(FollowToken& tok) {
 bool spmv_dia_follow(const so_matrix& m, const double* x_host, double* y_mapped, cudaStream_t s,
                      cudaStream_t copy) {
     FollowToken tok;
+    tok.upload_first = true;
     const int64_t nc = m.ncols;
     const bool launched = follow_launch(m, y_mapped, s, copy, 0, nullptr, [&](double* dx) {
         SOB_CUDA(cudaMemcpyAsync(dx, x_host, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, copy));
     }, tok);
     if (!launched) return false;
-    SOB_CUDA(cudaStreamSynchronize(s));
+    follow_wait_done(tok, s);
     if (!follow_finish(tok)) {  // the copy never showed up: recompute elsewhere
         SOB_CUDA(cudaStreamSynchronize(copy));
         return false;
