@@ -191,11 +191,14 @@ struct FollowToken {
 bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
                    const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
                    FollowToken& tok);
-// the same for CSR / ELL (one launch of the FOLLOW kernels, then
-// after_kernels(), e.g. an event gating every y chunk's copy-out)
+// the same for CSR / ELL / COO / HYB (one launch of the FOLLOW kernels, then
+// after_kernels(y_dev), e.g. an event gating every y chunk's copy-out).
+// y_dev == nullptr: the kernels stored y into y_mapped; otherwise y is in
+// device memory (COO parts) and after_kernels queues its copy into y_mapped
+// on `s` (without a callback: one copy of all of y)
 bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy,
-                        const std::function<void()>* after_kernels, const std::function<void(double*)>& upload,
-                        FollowToken& tok);
+                        const std::function<void(const double* y_dev)>* after_kernels,
+                        const std::function<void(double*)>& upload, FollowToken& tok);
 bool follow_finish(FollowToken& tok);
 // min/max DIA offset of a DIA-window matrix (read once, cached on the matrix)
 void ensure_dia_window(const so_matrix& m, cudaStream_t s);

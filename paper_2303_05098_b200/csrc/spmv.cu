@@ -1397,8 +1397,8 @@ static void coo_profile(const CooPart& coo, int64_t nrows, cudaStream_t s);
 // scattered lanes, and 8-byte stores into mapped memory each cost a link
 // transaction (profiles/r02ac_ab_mapped_y.txt).
 bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy,
-                        const std::function<void()>* after_kernels, const std::function<void(double*)>& upload,
-                        FollowToken& tok) {
+                        const std::function<void(const double* y_dev)>* after_kernels,
+                        const std::function<void(double*)>& upload, FollowToken& tok) {
     static const bool off = std::getenv("SOB_NO_CSR_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     static const bool coo_off = std::getenv("SOB_NO_COO_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     if (off || follow_disabled()) return false;
@@ -1410,8 +1410,10 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
     follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
         if (csr) {
             launch_csr_stream(m, false, dx, y_mapped, s, &fc);
+            if (after_kernels) (*after_kernels)(nullptr);
         } else if (ell) {
             launch_ell<false>(m, dx, y_mapped, s, &fc);
+            if (after_kernels) (*after_kernels)(nullptr);
         } else {
             // both released stream-ordered after the copy below; allocated
             // before the first launch (see follow_preload)
@@ -1426,9 +1428,11 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
             } else {
                 launch_coo<false>(m.coo, m.nrows, dx, yd.get(), s, &fc, &rec);
             }
-            SOB_CUDA(cudaMemcpyAsync(y_mapped, yd.get(), sizeof(double) * size_t(m.nrows), cudaMemcpyDefault, s));
+            if (after_kernels)
+                (*after_kernels)(yd.get());
+            else
+                SOB_CUDA(cudaMemcpyAsync(y_mapped, yd.get(), sizeof(double) * size_t(m.nrows), cudaMemcpyDefault, s));
         }
-        if (after_kernels) (*after_kernels)();
     }, upload, tok);
     return true;
 }

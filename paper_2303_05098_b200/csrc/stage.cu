@@ -316,19 +316,29 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
                     return;
                 }
             }
-            // CSR / ELL: the same with one launch of the FOLLOW kernels; one
-            // event after it gates every y chunk's copy-out.  Not with a COO
-            // part: its follow variant writes device y, and one copy of all
-            // of y behind the kernels delays the chunked copy-out (config 2
+            // CSR / ELL / COO / HYB: the same with one launch of the FOLLOW
+            // kernels.  CSR / ELL store y into Yd: one event after them gates
+            // every y chunk's copy-out.  COO parts leave y in device memory:
+            // it comes down chunk by chunk, an event after each chunk's copy
+            // (one copy of all of y was slower than the staged path: config 2
             // COO 1.85 -> 1.80 ms, the HYB-shaped matrix COO 1.68 -> 1.81,
             // HYB 1.62 -> 1.82; profiles/r02ao_coo_follow.txt)
+            static const bool coo_staged = std::getenv("SOB_PAGEABLE_COO_STAGED") != nullptr;  // A/B knob
             const bool coo_part = (m.format == SO_COO || m.format == SO_HYB) && m.coo.nnz > 0;
-            if (!dia_only && !coo_part) {
+            if (!dia_only && !(coo_part && coo_staged)) {
                 cudaStream_t copy = ctx(dev).copy_in;
-                const std::function<void()> after = [&]() {
-                    SOB_CUDA(cudaEventRecord(st.ev[0], s));
-                    for (int64_t j = 1; j < nyc; ++j) SOB_CUDA(cudaEventRecord(st.ev[size_t(j)], s));
-                    for (int64_t j = 0; j < nyc; ++j) ygate[size_t(j)].store(1, std::memory_order_release);
+                const std::function<void(const double*)> after = [&](const double* ydev) {
+                    for (int64_t j = 0; j < nyc; ++j) {
+                        if (ydev) {
+                            const int64_t a = j * cy, e = std::min(n, a + cy);
+                            SOB_CUDA(cudaMemcpyAsync(Yd + a, ydev + a, sizeof(double) * size_t(e - a),
+                                                     cudaMemcpyDefault, s));
+                        }
+                        SOB_CUDA(cudaEventRecord(st.ev[size_t(j)], s));
+                        if (ydev) ygate[size_t(j)].store(1, std::memory_order_release);
+                    }
+                    if (!ydev)
+                        for (int64_t j = 0; j < nyc; ++j) ygate[size_t(j)].store(1, std::memory_order_release);
                 };
                 const bool launched = follow_launch_rows(m, Yd, s, copy, &after, [&](double* dx) {
                     for (int64_t k = 0; k < nxc; ++k) {
