@@ -1056,7 +1056,10 @@ void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
     const FollowCtx none{nullptr, nullptr, 0};
-    if (follow)  // pinned spmv(m, x) following the upload of x (never accumulating)
+    if (follow && accum)  // HDC's CSR part after its DIA part, following the upload of x
+        csr_warp_kernel<IT, true, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
+            c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
+    else if (follow)  // host-buffer spmv(m, x) following the upload of x
         csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
             c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
     else if (accum)
@@ -1090,9 +1093,11 @@ void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y,
 }
 
 // accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x;
-// follow: x is still being uploaded (FOLLOW kernels, never accumulating)
+// follow: x is still being uploaded (FOLLOW kernels)
+// `pre_part`: the long-row pieces buffer, allocated by a follow path before
+// its first launch
 void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
-                       const FollowCtx* follow = nullptr) {
+                       const FollowCtx* follow = nullptr, DBuf<double>* pre_part = nullptr) {
     const CsrPart& c = m.csr;
     if (c.ngrp == 0) return;
     // flags are set (npad > 0) only when >= 1/64 of the groups prefer the
@@ -1100,7 +1105,8 @@ void launch_csr_stream(const so_matrix& m, bool accum, const double* x, double* 
     const bool pad = c.npad > 0;
     // allocated before any launch: nothing between two kernels that follow
     // an upload may wait for the device
-    DBuf<double> part(c.nlong > 0 ? c.npieces : 0, s);
+    DBuf<double> own_part(pre_part || c.nlong == 0 ? 0 : c.npieces, s);
+    DBuf<double>& part = pre_part ? *pre_part : own_part;
     if (c.grp_cap == 32 * kGroupItemsShort)
         pad ? launch_csr_warp<kGroupItemsShort, true>(m, accum, x, y, s, follow)
             : launch_csr_warp<kGroupItemsShort, false>(m, accum, x, y, s, follow);
@@ -1228,8 +1234,29 @@ struct FollowStage {
 // times out (HYB with a COO part: 13.9 s on its first call).  Every kernel a
 // follow path launches after its first one is loaded up front, once per
 // device, and its scratch buffers are allocated before its first launch.
+template <int IT, bool PAD, bool COOP, int RPL>
+void preload_csr_accum_follow() {
+    cudaFuncAttributes a;
+    SOB_CUDA(cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&csr_warp_kernel<IT, true, PAD, COOP, RPL, true>)));
+}
+template <int IT>
+void preload_csr_accum_follow_all() {
+    preload_csr_accum_follow<IT, false, false, 1>();
+    preload_csr_accum_follow<IT, false, true, 1>();
+    preload_csr_accum_follow<IT, true, false, 1>();
+    preload_csr_accum_follow<IT, true, true, 1>();
+    preload_csr_accum_follow<IT, false, false, kGroupRowsMax / 32>();
+    preload_csr_accum_follow<IT, false, true, kGroupRowsMax / 32>();
+    preload_csr_accum_follow<IT, true, false, kGroupRowsMax / 32>();
+    preload_csr_accum_follow<IT, true, true, kGroupRowsMax / 32>();
+}
+
 void follow_preload() {
+    // HDC with both parts: the CSR kernels (accumulating) run after the DIA one
+    preload_csr_accum_follow_all<kGroupItemsShort>();
+    preload_csr_accum_follow_all<kGroupItemsLong>();
     const void* fns[] = {
+        reinterpret_cast<const void*>(&csr_long_fixup<true>),
         reinterpret_cast<const void*>(&csr_long_pieces<true>),
         reinterpret_cast<const void*>(&csr_long_fixup<false>),
         reinterpret_cast<const void*>(&coo_warp_kernel<false, true>),
@@ -1342,21 +1369,32 @@ void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
     SOB_CUDA(cudaEventRecord(f.refilled, s));
 }
 
-bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
-                   const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
-                   FollowToken& tok) {
-    if (follow_disabled()) return false;
-    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
+// The DIA part's window fits the follow kernel (offsets known, staged in
+// shared memory, x window of a 1024-row block <= kFollowSpan).
+bool dia_follow_ok(const so_matrix& m) {
     if (!m.dia_window_known.load(std::memory_order_acquire) || m.dia.ndiags == 0 || m.dia.ndiags > kDiaSmem)
         return false;
-    const int64_t omin = m.dia_omin, omax = m.dia_omax;
     // x comes from device memory here (no read amplification over the link):
     // any window that fits a CTA's shared memory with its 1024 rows
-    if (omax - omin > kFollowSpan) return false;
-    if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
-    const int64_t nc = m.ncols;
+    return m.dia_omax - m.dia_omin <= kFollowSpan;
+}
+
+// dia_follow_kernel over row blocks [b0, b1) (persistent: <= one CTA per SM)
+void launch_dia_follow(const so_matrix& m, const double* dx, double* y, cudaStream_t s, const FollowCtx& fc,
+                       int64_t b0, int64_t b1) {
+    const int64_t omin = m.dia_omin, omax = m.dia_omax;
     const size_t smem = sizeof(double) * size_t(kZcRows + (omax - omin) + 2);
-    if (smem > 48 * 1024) {  // wide windows (2-D stencils): opt in to > 48 KB, once per device
+    const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));
+    dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(m.ncols), int(m.dia.ndiags), m.dia.offsets.get(),
+                                                  m.dia.values.get(), dx, y, fc.flag, int(omin), int(omax),
+                                                  fc.timed_out, fc.timeout_ns, int(b0), int(b1));
+    SOB_LAUNCH("dia_follow_kernel");
+}
+
+// wide windows (2-D stencils): opt in to > 48 KB of shared memory, once per device
+void dia_follow_smem_attr(const so_matrix& m) {
+    const size_t smem = sizeof(double) * size_t(kZcRows + (m.dia_omax - m.dia_omin) + 2);
+    if (smem > 48 * 1024) {
         static std::mutex attr_mu;
         static uint64_t attr_done = 0;
         std::lock_guard<std::mutex> alk(attr_mu);
@@ -1366,17 +1404,22 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
             if (m.device < 64) attr_done |= uint64_t(1) << m.device;
         }
     }
+}
+
+bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStream_t copy, int64_t rows_per_chunk,
+                   const std::function<void(int64_t)>* after_chunk, const std::function<void(double*)>& upload,
+                   FollowToken& tok) {
+    if (follow_disabled()) return false;
+    if (m.format != SO_DIA && !(m.format == SO_HDC && m.csr.nnz == 0)) return false;
+    if (!dia_follow_ok(m)) return false;
+    if (rows_per_chunk < 0 || rows_per_chunk % kZcRows) return false;
+    const int64_t nc = m.ncols;
+    dia_follow_smem_attr(m);
     const int64_t nblk = ceil_div(m.nrows, int64_t(kZcRows));
     const int64_t per = rows_per_chunk > 0 ? rows_per_chunk / kZcRows : nblk;  // blocks per launch
     follow_run(m.device, nc, s, copy, [&](const double* dx, const FollowCtx& fc) {
         for (int64_t b0 = 0, j = 0; b0 < nblk; b0 += per, ++j) {
-            const int64_t b1 = std::min(nblk, b0 + per);
-            const unsigned grid = unsigned(std::min<int64_t>(b1 - b0, current_ctx().num_sms));
-            dia_follow_kernel<<<grid, kZcRows, smem, s>>>(int(m.nrows), int(nc), int(m.dia.ndiags),
-                                                          m.dia.offsets.get(), m.dia.values.get(), dx, y_mapped,
-                                                          fc.flag, int(omin), int(omax), fc.timed_out,
-                                                          fc.timeout_ns, int(b0), int(b1));
-            SOB_LAUNCH("dia_follow_kernel");
+            launch_dia_follow(m, dx, y_mapped, s, fc, b0, std::min(nblk, b0 + per));
             if (after_chunk) (*after_chunk)(j);
         }
     }, upload, tok);
@@ -1401,11 +1444,20 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
                         const std::function<void(double*)>& upload, FollowToken& tok) {
     static const bool off = std::getenv("SOB_NO_CSR_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     static const bool coo_off = std::getenv("SOB_NO_COO_FOLLOW") != nullptr;  // diagnostic knob (A/B)
+    static const bool hdc_off = std::getenv("SOB_NO_HDC_FOLLOW") != nullptr;  // diagnostic knob (A/B)
     if (off || follow_disabled()) return false;
     const bool csr = (m.format == SO_CSR || (m.format == SO_HDC && m.dia.ndiags == 0)) && m.csr.nnz > 0;
     const bool ell = (m.format == SO_ELL || (m.format == SO_HYB && m.coo.nnz == 0)) && m.ell.width > 0;
     const bool coo = !coo_off && (m.format == SO_COO || m.format == SO_HYB) && m.coo.nnz > 0;
-    if (!csr && !ell && !coo) return false;
+    // HDC with both parts: the DIA follow kernel, then the CSR part
+    // accumulating (spmv_device's order), into device y
+    bool hdc2 = !hdc_off && m.format == SO_HDC && m.dia.ndiags > 0 && m.csr.nnz > 0;
+    if (hdc2) {
+        ensure_dia_window(m, s);  // cached after the first call
+        hdc2 = dia_follow_ok(m);
+        if (hdc2) dia_follow_smem_attr(m);
+    }
+    if (!csr && !ell && !coo && !hdc2) return false;
     if (coo) coo_profile(m.coo, m.nrows, s);  // cached after the first multiply
     follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
         if (csr) {
@@ -1414,6 +1466,17 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
         } else if (ell) {
             launch_ell<false>(m, dx, y_mapped, s, &fc);
             if (after_kernels) (*after_kernels)(nullptr);
+        } else if (hdc2) {
+            // released stream-ordered after the copy below; allocated before
+            // the first launch (see follow_preload)
+            DBuf<double> yd(m.nrows, s);
+            DBuf<double> part(m.csr.nlong > 0 ? m.csr.npieces : 0, s);
+            launch_dia_follow(m, dx, yd.get(), s, fc, 0, ceil_div(m.nrows, int64_t(kZcRows)));
+            launch_csr_stream(m, true, dx, yd.get(), s, &fc, &part);
+            if (after_kernels)
+                (*after_kernels)(yd.get());
+            else
+                SOB_CUDA(cudaMemcpyAsync(y_mapped, yd.get(), sizeof(double) * size_t(m.nrows), cudaMemcpyDefault, s));
         } else {
             // both released stream-ordered after the copy below; allocated
             // before the first launch (see follow_preload)

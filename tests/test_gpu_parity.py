@@ -702,7 +702,7 @@ def test_arrow_matrix_features(so, O, n, dense_len):
         assert max_rel(m.spmv(x), O.oc_spmv(ref, x)) <= SPMV_TOL, f
 
 
-@pytest.mark.parametrize("shape", ["band13", "wide", "rmat"])
+@pytest.mark.parametrize("shape", ["band13", "wide", "rmat", "hyb"])
 def test_pageable_host_spmv_staging(so, O, shape):
     """spmv(m, x) with PAGEABLE host buffers (the reference API's
     std::vector): host threads stage x/y through pinned memory chunk by chunk
@@ -717,8 +717,10 @@ def test_pageable_host_spmv_staging(so, O, shape):
         csr = synth.banded(700_000, 13, seed=2)
     elif shape == "wide":
         csr = synth.laplacian_2d(800, seed=1)  # offsets +-800: window wider than the zero-copy limit
-    else:
+    elif shape == "rmat":
         csr = synth.rmat(18, 8, seed=9)
+    else:  # HYB with a COO part, HDC with both parts
+        csr = synth.hyb_skewed(600_000, 8, 40, 50, seed=6)
     coo = O.coo_dict(csr.nrows, csr.ncols, csr.coo_rows(), csr.col, csr.val)
     d = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val)
     rng = np.random.default_rng(12)
@@ -836,10 +838,9 @@ def test_follow_path_concurrent_callers(so, O):
 def test_pinned_host_spmv_all_formats(so, O, shape):
     """Pinned host x/y through spmv(m, x) in every format (DIA: the
     follow-the-copy kernel; CSR / ELL: their FOLLOW variants storing y into
-    mapped host memory; COO / HYB with a COO part: FOLLOW variants into
-    device y, then one copy down; HDC with both parts: the copy-engine
-    path): each result equals the device-resident multiply bit for bit and
-    the oracle within the bar."""
+    mapped host memory; COO / HYB with a COO part and HDC with both parts:
+    FOLLOW variants into device y, then one copy down): each result equals
+    the device-resident multiply bit for bit and the oracle within the bar."""
     import torch
     from paper_2303_05098_b200 import synth
 
