@@ -110,6 +110,12 @@ struct so_matrix {
     // (published with release on dia_window_known; concurrent fillers write the same values)
     mutable std::atomic<bool> dia_window_known{false};
     mutable std::atomic<int64_t> dia_omin{0}, dia_omax{0};
+    // CSR row-group chunks of the pinned follow path (spmv.cu): group and row
+    // at each chunk boundary, filled on first use (published like the window)
+    static constexpr int kFollowChunks = 8;
+    mutable std::atomic<bool> csr_chunks_known{false};
+    mutable std::atomic<int64_t> csr_chunk_grp[kFollowChunks + 1] = {};
+    mutable std::atomic<int64_t> csr_chunk_row[kFollowChunks + 1] = {};
 
     int64_t nnz() const {
         switch (format) {

@@ -1049,9 +1049,10 @@ void launch_coo(const CooPart& coo, int64_t nrows, const double* x, double* y, c
     }
 }
 
+// [g0, g1): the row groups to run (g1 < 0: all)
 template <int IT, bool PAD, bool COOP, int RPL>
 void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
-                      const FollowCtx* follow) {
+                      const FollowCtx* follow, int64_t g0 = 0, int64_t g1 = -1) {
     const CsrPart& c = m.csr;
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
@@ -1059,7 +1060,12 @@ void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y
     if (follow && accum)  // HDC's CSR part after its DIA part, following the upload of x
         csr_warp_kernel<IT, true, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
             c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
-    else if (follow)  // host-buffer spmv(m, x) following the upload of x
+    else if (follow && g1 >= 0) {  // a chunk of the groups (pinned CSR follow path)
+        const int gridc = int(std::min<int64_t>(ceil_div(g1 - g0, 8), int64_t(current_ctx().num_sms) * per_sm));
+        csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<gridc, 256, 0, s>>>(
+            c.grp.get() + g0, c.grp_k.get() + g0, g1 - g0, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows,
+            *follow);
+    } else if (follow)  // host-buffer spmv(m, x) following the upload of x
         csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
             c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
     else if (accum)
@@ -1075,21 +1081,35 @@ void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y
 
 template <int IT, bool PAD, bool COOP>
 void launch_csr_warp3(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
-                      const FollowCtx* follow) {
+                      const FollowCtx* follow, int64_t g0, int64_t g1) {
     if (m.csr.grp_rpl > 1)
-        launch_csr_warp4<IT, PAD, COOP, kGroupRowsMax / 32>(m, accum, x, y, s, follow);
+        launch_csr_warp4<IT, PAD, COOP, kGroupRowsMax / 32>(m, accum, x, y, s, follow, g0, g1);
     else
-        launch_csr_warp4<IT, PAD, COOP, 1>(m, accum, x, y, s, follow);
+        launch_csr_warp4<IT, PAD, COOP, 1>(m, accum, x, y, s, follow, g0, g1);
 }
 
 template <int IT, bool PAD>
 void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y, cudaStream_t s,
-                     const FollowCtx* follow) {
+                     const FollowCtx* follow, int64_t g0 = 0, int64_t g1 = -1) {
     static const bool no_coop = std::getenv("SOB_NO_CSR_COOP") != nullptr;  // diagnostic knob (A/B)
     if (m.csr.ncoop > 0 && !no_coop)
-        launch_csr_warp3<IT, PAD, true>(m, accum, x, y, s, follow);
+        launch_csr_warp3<IT, PAD, true>(m, accum, x, y, s, follow, g0, g1);
     else
-        launch_csr_warp3<IT, PAD, false>(m, accum, x, y, s, follow);
+        launch_csr_warp3<IT, PAD, false>(m, accum, x, y, s, follow, g0, g1);
+}
+
+// The row-group kernel alone over groups [g0, g1), following the upload
+// (matrices without long rows: the pinned CSR chunk pipeline)
+void launch_csr_groups_follow(const so_matrix& m, const double* x, double* y, cudaStream_t s, const FollowCtx& fc,
+                              int64_t g0, int64_t g1) {
+    const CsrPart& c = m.csr;
+    const bool pad = c.npad > 0;
+    if (c.grp_cap == 32 * kGroupItemsShort)
+        pad ? launch_csr_warp<kGroupItemsShort, true>(m, false, x, y, s, &fc, g0, g1)
+            : launch_csr_warp<kGroupItemsShort, false>(m, false, x, y, s, &fc, g0, g1);
+    else
+        pad ? launch_csr_warp<kGroupItemsLong, true>(m, false, x, y, s, &fc, g0, g1)
+            : launch_csr_warp<kGroupItemsLong, false>(m, false, x, y, s, &fc, g0, g1);
 }
 
 // accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x;
@@ -1224,6 +1244,9 @@ struct FollowStage {
     unsigned next_slot = 0;
     cudaEvent_t refilled = nullptr, copied = nullptr;
     cudaEvent_t done[kFollowSlots] = {};  // per call slot: its kernels are complete
+    // pinned CSR chunk pipeline: chunk k's rows done / every chunk's y copied
+    // (recorded and waited inside one enqueue, under mu)
+    cudaEvent_t chunk_ev[so_matrix::kFollowChunks + 1] = {};
     bool preloaded = false;
 };
 
@@ -1318,6 +1341,7 @@ void follow_run(int device, int64_t nc, cudaStream_t s, cudaStream_t copy,
         SOB_CUDA(cudaEventCreateWithFlags(&f.refilled, cudaEventDisableTiming));
         SOB_CUDA(cudaEventCreateWithFlags(&f.copied, cudaEventDisableTiming));
         for (int i = 0; i < kFollowSlots; ++i) SOB_CUDA(cudaEventCreateWithFlags(&f.done[i], cudaEventDisableTiming));
+        for (auto& e : f.chunk_ev) SOB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     if (!f.preloaded) {
         follow_preload();
@@ -1428,6 +1452,26 @@ bool follow_launch(const so_matrix& m, double* y_mapped, cudaStream_t s, cudaStr
 
 static void coo_profile(const CooPart& coo, int64_t nrows, cudaStream_t s);
 
+// Group / row at each chunk boundary of the pinned CSR pipeline (equal group
+// counts), read once per matrix.  False when the groups do not tile the rows.
+static bool csr_follow_chunks(const so_matrix& m, cudaStream_t s) {
+    constexpr int K = so_matrix::kFollowChunks;
+    if (m.csr_chunks_known.load(std::memory_order_acquire)) return m.csr_chunk_row[K].load() == m.nrows;
+    int64_t gs[K + 1];
+    int32_t rows[K + 1];
+    for (int k = 0; k <= K; ++k) {
+        gs[k] = m.csr.ngrp * k / K;
+        SOB_CUDA(cudaMemcpyAsync(&rows[k], m.csr.grp.get() + gs[k], sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
+    SOB_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k <= K; ++k) {
+        m.csr_chunk_grp[k].store(gs[k], std::memory_order_relaxed);
+        m.csr_chunk_row[k].store(rows[0] == 0 ? rows[k] : -1, std::memory_order_relaxed);
+    }
+    m.csr_chunks_known.store(true, std::memory_order_release);
+    return rows[0] == 0 && rows[K] == m.nrows;
+}
+
 // Pinned spmv(m, x) on a CSR matrix (or HDC without a DIA part) or an ELL
 // matrix (or HYB without a COO part): the kernels launched with FOLLOW trail
 // ONE upload of x (each x gather waits for its element) and store y straight
@@ -1459,8 +1503,32 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
     }
     if (!csr && !ell && !coo && !hdc2) return false;
     if (coo) coo_profile(m.coo, m.nrows, s);  // cached after the first multiply
+    // pinned CSR without long rows: kFollowChunks launches over equal group
+    // ranges into device y, each chunk's y copied down on copy_out as soon as
+    // it is done -- the rows kernel's short, partly filled y stores into
+    // mapped memory made the y leg the slow one.  SOB_NO_CSR_CHUNKS: A/B.
+    static const bool no_chunks = std::getenv("SOB_NO_CSR_CHUNKS") != nullptr;
+    const bool chunks = csr && !after_kernels && !no_chunks && m.csr.nlong == 0 &&
+                        m.csr.ngrp >= 64 * so_matrix::kFollowChunks && csr_follow_chunks(m, s);
     follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
-        if (csr) {
+        if (chunks) {
+            constexpr int K = so_matrix::kFollowChunks;
+            FollowStage& st = g_follow[m.device];  // follow_run holds st.mu here
+            cudaStream_t out = current_ctx().copy_out;
+            DBuf<double> yd(m.nrows, s);  // released stream-ordered after the copies
+            for (int k = 0; k < K; ++k) {
+                const int64_t g0 = m.csr_chunk_grp[k].load(), g1 = m.csr_chunk_grp[k + 1].load();
+                const int64_t r0 = m.csr_chunk_row[k].load(), r1 = m.csr_chunk_row[k + 1].load();
+                if (g1 > g0) launch_csr_groups_follow(m, dx, yd.get(), s, fc, g0, g1);
+                SOB_CUDA(cudaEventRecord(st.chunk_ev[k], s));
+                SOB_CUDA(cudaStreamWaitEvent(out, st.chunk_ev[k], 0));
+                if (r1 > r0)
+                    SOB_CUDA(cudaMemcpyAsync(y_mapped + r0, yd.get() + r0, sizeof(double) * size_t(r1 - r0),
+                                             cudaMemcpyDefault, out));
+            }
+            SOB_CUDA(cudaEventRecord(st.chunk_ev[K], out));
+            SOB_CUDA(cudaStreamWaitEvent(s, st.chunk_ev[K], 0));
+        } else if (csr) {
             launch_csr_stream(m, false, dx, y_mapped, s, &fc);
             if (after_kernels) (*after_kernels)(nullptr);
         } else if (ell) {
