@@ -116,6 +116,11 @@ struct so_matrix {
     mutable std::atomic<bool> csr_chunks_known{false};
     mutable std::atomic<int64_t> csr_chunk_grp[kFollowChunks + 1] = {};
     mutable std::atomic<int64_t> csr_chunk_row[kFollowChunks + 1] = {};
+    // COO entry-chunk ranges of the same pipeline: first chunk of each range
+    // and the first row a later range may write
+    mutable std::atomic<bool> coo_chunks_known{false};
+    mutable std::atomic<int64_t> coo_chunk_c[kFollowChunks + 1] = {};
+    mutable std::atomic<int64_t> coo_chunk_row[kFollowChunks + 1] = {};
 
     int64_t nnz() const {
         switch (format) {

@@ -788,12 +788,13 @@ template <bool ACCUM, bool FOLLOW = false, bool CONT = false>
 __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
     coo_warp_kernel(int64_t z, int64_t nrows, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                    CooChunkRec* __restrict__ rec, FollowCtx fctx) {
+                    CooChunkRec* __restrict__ rec, FollowCtx fctx, int64_t c0 = 0, int64_t c1 = INT64_MAX) {
     constexpr int IT = kCooItems;
     const int lane = threadIdx.x & 31;
     const int64_t nchunks = (z + kCooChunk - 1) / kCooChunk;
+    const int64_t cend = min(nchunks, c1);  // [c0, c1): a chunk range (CONT only; the pinned chunk pipeline)
     const int64_t stride = int64_t(gridDim.x) * (blockDim.x >> 5);
-    int64_t chunk = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t chunk = c0 + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     // coo_fixup (launched with PDL) is scheduled early and waits for this grid
     asm volatile("griddepcontrol.launch_dependents;" :::);
     if (!CONT && blockIdx.x == 0 && threadIdx.x == 0) {  // coo_fixup's control words (after the records)
@@ -801,7 +802,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
         ctl[0] = 0;
         ctl[1] = 0;
     }
-    if (chunk >= nchunks) return;
+    if (chunk >= cend) return;
     int r[IT], c[IT];
     double v[IT];
     coo_load(row, col, val, chunk * kCooChunk + lane * IT, int(min(z - chunk * kCooChunk, int64_t(kCooChunk))) - lane * IT,
@@ -839,7 +840,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
 #pragma unroll
         for (int j = 0; j < IT; ++j) rc[j] = r[j];
         const int64_t nx = chunk + stride;
-        if (nx < nchunks)
+        if (nx < cend)
             coo_load(row, col, val, nx * kCooChunk + lane * IT, int(min(z - nx * kCooChunk, int64_t(kCooChunk))) - lane * IT,
                      r, c, v);
         double open_acc = 0.0;
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(256, coo_per_sm(ACCUM))
                 if (lane == owner) y_store<ACCUM>(y + last_row, fadd(open_acc, t));
             }
         }
-        if (nx >= nchunks) break;
+        if (nx >= cend) break;
         chunk = nx;
     }
 }
@@ -1472,6 +1473,42 @@ static bool csr_follow_chunks(const so_matrix& m, cudaStream_t s) {
     return rows[0] == 0 && rows[K] == m.nrows;
 }
 
+// Entry-chunk ranges of the pinned COO pipeline (equal chunk counts) and the
+// row bound after each.  A CONT chunk writes only rows above the previous
+// chunk's last row (its orphan head is skipped, the empty rows before its
+// first row are zeroed by it) up to its own last row (finished with the head
+// of the next chunk), so rows below row[c_k * kCooChunk - 1] + 1 are final
+// once ranges 0..k-1 are done.  Read once per matrix.
+static void coo_follow_chunks(const so_matrix& m, cudaStream_t s) {
+    constexpr int K = so_matrix::kFollowChunks;
+    if (m.coo_chunks_known.load(std::memory_order_acquire)) return;
+    const int64_t nch = ceil_div(m.coo.nnz, int64_t(kCooChunk));
+    int64_t cs[K + 1];
+    int32_t rows[K + 1] = {};
+    for (int k = 0; k <= K; ++k) {
+        cs[k] = nch * k / K;
+        if (k > 0 && k < K)
+            SOB_CUDA(cudaMemcpyAsync(&rows[k], m.coo.row.get() + cs[k] * kCooChunk - 1, sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, s));
+    }
+    SOB_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k <= K; ++k) {
+        m.coo_chunk_c[k].store(cs[k], std::memory_order_relaxed);
+        m.coo_chunk_row[k].store(k == 0 ? 0 : k == K ? m.nrows : int64_t(rows[k]) + 1, std::memory_order_relaxed);
+    }
+    m.coo_chunks_known.store(true, std::memory_order_release);
+}
+
+// The CONT chunk kernel over entry chunks [c0, c1), following the upload
+template <bool ACCUM>
+static void launch_coo_cont_range(const CooPart& coo, int64_t nrows, const double* x, double* y, cudaStream_t s,
+                                  const FollowCtx& fc, int64_t c0, int64_t c1) {
+    const int grid = int(std::min<int64_t>(ceil_div(c1 - c0, 8), int64_t(current_ctx().num_sms) * coo_per_sm(ACCUM)));
+    coo_warp_kernel<ACCUM, true, true><<<grid, 256, 0, s>>>(coo.nnz, nrows, coo.row.get(), coo.col.get(),
+                                                            coo.val.get(), x, y, nullptr, fc, c0, c1);
+    SOB_LAUNCH("coo_warp_kernel");
+}
+
 // Pinned spmv(m, x) on a CSR matrix (or HDC without a DIA part) or an ELL
 // matrix (or HYB without a COO part): the kernels launched with FOLLOW trail
 // ONE upload of x (each x gather waits for its element) and store y straight
@@ -1510,6 +1547,14 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
     static const bool no_chunks = std::getenv("SOB_NO_CSR_CHUNKS") != nullptr;
     const bool chunks = csr && !after_kernels && !no_chunks && m.csr.nlong == 0 &&
                         m.csr.ngrp >= 64 * so_matrix::kFollowChunks && csr_follow_chunks(m, s);
+    // pinned COO of short rows (every row <= 32 entries): the CONT chunk
+    // kernel (no records, no fix-up) over kFollowChunks entry-chunk ranges,
+    // each range's rows copied down as it completes.  SOB_NO_COO_CHUNKS: A/B.
+    static const bool no_coo_chunks = std::getenv("SOB_NO_COO_CHUNKS") != nullptr;
+    const bool coo_chunks = coo && m.format == SO_COO && !after_kernels && !no_coo_chunks &&
+                            m.coo.short_rows.load(std::memory_order_acquire) == 1 &&
+                            ceil_div(m.coo.nnz, int64_t(kCooChunk)) >= 64 * so_matrix::kFollowChunks;
+    if (coo_chunks) coo_follow_chunks(m, s);
     follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
         if (chunks) {
             constexpr int K = so_matrix::kFollowChunks;
@@ -1545,6 +1590,31 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
                 (*after_kernels)(yd.get());
             else
                 SOB_CUDA(cudaMemcpyAsync(y_mapped, yd.get(), sizeof(double) * size_t(m.nrows), cudaMemcpyDefault, s));
+        } else if (coo_chunks) {
+            constexpr int K = so_matrix::kFollowChunks;
+            FollowStage& st = g_follow[m.device];  // follow_run holds st.mu here
+            cudaStream_t out = current_ctx().copy_out;
+            DBuf<double> yd(m.nrows, s);  // released stream-ordered after the copies
+            const int64_t gap = m.coo.max_gap.load(std::memory_order_acquire);
+            const bool zeroed = gap < 0 || gap > kCooGapInline;  // spmv_device's safe path: y zeroed, accumulate
+            if (zeroed) SOB_CUDA(cudaMemsetAsync(yd.get(), 0, sizeof(double) * size_t(m.nrows), s));
+            for (int k = 0; k < K; ++k) {
+                const int64_t c0 = m.coo_chunk_c[k].load(), c1 = m.coo_chunk_c[k + 1].load();
+                const int64_t r0 = m.coo_chunk_row[k].load(), r1 = m.coo_chunk_row[k + 1].load();
+                if (c1 > c0) {
+                    if (zeroed)
+                        launch_coo_cont_range<true>(m.coo, m.nrows, dx, yd.get(), s, fc, c0, c1);
+                    else
+                        launch_coo_cont_range<false>(m.coo, m.nrows, dx, yd.get(), s, fc, c0, c1);
+                }
+                SOB_CUDA(cudaEventRecord(st.chunk_ev[k], s));
+                SOB_CUDA(cudaStreamWaitEvent(out, st.chunk_ev[k], 0));
+                if (r1 > r0)
+                    SOB_CUDA(cudaMemcpyAsync(y_mapped + r0, yd.get() + r0, sizeof(double) * size_t(r1 - r0),
+                                             cudaMemcpyDefault, out));
+            }
+            SOB_CUDA(cudaEventRecord(st.chunk_ev[K], out));
+            SOB_CUDA(cudaStreamWaitEvent(s, st.chunk_ev[K], 0));
         } else {
             // both released stream-ordered after the copy below; allocated
             // before the first launch (see follow_preload)

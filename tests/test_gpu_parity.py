@@ -903,6 +903,47 @@ def test_pinned_coo_follow_gappy_rows(so, O):
             assert max_rel(yn, O.oc_spmv(O.oc_convert(coo, f), xn)) <= SPMV_TOL, (f, trial)
 
 
+@pytest.mark.parametrize("gap", [3_000, 12_000])
+def test_pinned_coo_chunk_pipeline(so, O, gap):
+    """Pinned spmv(m, x) on a COO matrix of short rows (<= 32 entries) runs
+    the CONT chunk kernel over kFollowChunks entry-chunk ranges, each range's
+    rows copied down as it completes (spmv.cu coo_follow_chunks): leading,
+    trailing and interior empty-row runs (below and past kCooGapInline, the
+    latter on the zeroed, accumulating path) land in the right range; equal
+    to the device multiply and to the oracle within the bar, over
+    consecutive calls."""
+    import torch
+
+    n = 500_000
+    rng = np.random.default_rng(gap)
+    keep = np.ones(n, dtype=bool)
+    keep[:1_000] = False          # leading empty rows
+    keep[n - 7_000:] = False      # trailing empty rows
+    for s0 in rng.integers(2_000, n - 20_000, 6):
+        keep[s0:s0 + gap] = False  # interior empty-row runs
+    keep &= rng.random(n) < 0.9
+    live = np.flatnonzero(keep)
+    lens = rng.integers(1, 33, live.size)
+    rows = np.repeat(live, lens)
+    cols = rng.integers(0, n, rows.size)
+    coo = O.from_triplets(n, n, rows, cols, rng.uniform(-1, 1, rows.size))
+    m = to_dev(so, coo).from_coo(so.COO)
+    xt = torch.empty(n, dtype=torch.float64).pin_memory()
+    yt = torch.empty(n, dtype=torch.float64).pin_memory()
+    xn, yn = xt.numpy(), yt.numpy()
+    for trial in range(3):
+        xn[:] = rng.uniform(-1, 1, n)
+        yn[:] = np.nan
+        m.spmv_into(xn, yn)
+        xd = torch.tensor(xn, device="cuda")
+        yd = torch.empty(n, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        m.spmv_device(xd.data_ptr(), yd.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(yn, yd.cpu().numpy()), trial
+        assert max_rel(yn, O.oc_spmv(O.oc_convert(coo, so.COO), xn)) <= SPMV_TOL, trial
+
+
 def test_coo_cont_and_records_paths(so, O, tmp_path):
     """COO on a matrix of rows <= 32 entries below kCooContMaxNnz runs the
     chunk kernel that finishes rows crossing into the next chunk itself
