@@ -1058,15 +1058,20 @@ void launch_csr_warp4(const so_matrix& m, bool accum, const double* x, double* y
     const int per_sm = IT > 8 ? 3 : 4;
     const int grid = int(std::min<int64_t>(ceil_div(c.ngrp, 8), int64_t(current_ctx().num_sms) * per_sm));
     const FollowCtx none{nullptr, nullptr, 0};
-    if (follow && accum)  // HDC's CSR part after its DIA part, following the upload of x
+    if (follow && g1 >= 0) {  // a chunk of the groups (pinned CSR / HDC chunk pipelines)
+        const int gridc = int(std::min<int64_t>(ceil_div(g1 - g0, 8), int64_t(current_ctx().num_sms) * per_sm));
+        if (accum)
+            csr_warp_kernel<IT, true, PAD, COOP, RPL, true><<<gridc, 256, 0, s>>>(
+                c.grp.get() + g0, c.grp_k.get() + g0, g1 - g0, c.row_ptr.get(), c.col.get(), c.val.get(), x, y,
+                m.nrows, *follow);
+        else
+            csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<gridc, 256, 0, s>>>(
+                c.grp.get() + g0, c.grp_k.get() + g0, g1 - g0, c.row_ptr.get(), c.col.get(), c.val.get(), x, y,
+                m.nrows, *follow);
+    } else if (follow && accum)  // HDC's CSR part after its DIA part, following the upload of x
         csr_warp_kernel<IT, true, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
             c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
-    else if (follow && g1 >= 0) {  // a chunk of the groups (pinned CSR follow path)
-        const int gridc = int(std::min<int64_t>(ceil_div(g1 - g0, 8), int64_t(current_ctx().num_sms) * per_sm));
-        csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<gridc, 256, 0, s>>>(
-            c.grp.get() + g0, c.grp_k.get() + g0, g1 - g0, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows,
-            *follow);
-    } else if (follow)  // host-buffer spmv(m, x) following the upload of x
+    else if (follow)  // host-buffer spmv(m, x) following the upload of x
         csr_warp_kernel<IT, false, PAD, COOP, RPL, true><<<grid, 256, 0, s>>>(
             c.grp.get(), c.grp_k.get(), c.ngrp, c.row_ptr.get(), c.col.get(), c.val.get(), x, y, m.nrows, *follow);
     else if (accum)
@@ -1100,17 +1105,18 @@ void launch_csr_warp(const so_matrix& m, bool accum, const double* x, double* y,
 }
 
 // The row-group kernel alone over groups [g0, g1), following the upload
-// (matrices without long rows: the pinned CSR chunk pipeline)
+// (matrices without long rows: the pinned CSR / HDC chunk pipelines;
+// accum: y += A_csr x, HDC's CSR part after its DIA part)
 void launch_csr_groups_follow(const so_matrix& m, const double* x, double* y, cudaStream_t s, const FollowCtx& fc,
-                              int64_t g0, int64_t g1) {
+                              int64_t g0, int64_t g1, bool accum = false) {
     const CsrPart& c = m.csr;
     const bool pad = c.npad > 0;
     if (c.grp_cap == 32 * kGroupItemsShort)
-        pad ? launch_csr_warp<kGroupItemsShort, true>(m, false, x, y, s, &fc, g0, g1)
-            : launch_csr_warp<kGroupItemsShort, false>(m, false, x, y, s, &fc, g0, g1);
+        pad ? launch_csr_warp<kGroupItemsShort, true>(m, accum, x, y, s, &fc, g0, g1)
+            : launch_csr_warp<kGroupItemsShort, false>(m, accum, x, y, s, &fc, g0, g1);
     else
-        pad ? launch_csr_warp<kGroupItemsLong, true>(m, false, x, y, s, &fc, g0, g1)
-            : launch_csr_warp<kGroupItemsLong, false>(m, false, x, y, s, &fc, g0, g1);
+        pad ? launch_csr_warp<kGroupItemsLong, true>(m, accum, x, y, s, &fc, g0, g1)
+            : launch_csr_warp<kGroupItemsLong, false>(m, accum, x, y, s, &fc, g0, g1);
 }
 
 // accum: y += A_csr x (HDC's CSR part after its DIA part), else y = A_csr x;
@@ -1555,6 +1561,11 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
                             m.coo.short_rows.load(std::memory_order_acquire) == 1 &&
                             ceil_div(m.coo.nnz, int64_t(kCooChunk)) >= 64 * so_matrix::kFollowChunks;
     if (coo_chunks) coo_follow_chunks(m, s);
+    // pinned HDC with both parts, no long rows: per CSR chunk, the DIA row
+    // blocks starting in its rows, then its groups accumulating, then its
+    // rows copied down (the same pipeline; SOB_NO_CSR_CHUNKS: A/B)
+    const bool hdc_chunks = hdc2 && !after_kernels && !no_chunks && m.csr.nlong == 0 &&
+                            m.csr.ngrp >= 64 * so_matrix::kFollowChunks && csr_follow_chunks(m, s);
     follow_run(m.device, m.ncols, s, copy, [&](const double* dx, const FollowCtx& fc) {
         if (chunks) {
             constexpr int K = so_matrix::kFollowChunks;
@@ -1579,6 +1590,27 @@ bool follow_launch_rows(const so_matrix& m, double* y_mapped, cudaStream_t s, cu
         } else if (ell) {
             launch_ell<false>(m, dx, y_mapped, s, &fc);
             if (after_kernels) (*after_kernels)(nullptr);
+        } else if (hdc_chunks) {
+            constexpr int K = so_matrix::kFollowChunks;
+            FollowStage& st = g_follow[m.device];  // follow_run holds st.mu here
+            cudaStream_t out = current_ctx().copy_out;
+            DBuf<double> yd(m.nrows, s);  // released stream-ordered after the copies
+            // a DIA block is run with the chunk its first row is in: every
+            // row's block is done before (or with) the chunk accumulating it
+            for (int k = 0; k < K; ++k) {
+                const int64_t g0 = m.csr_chunk_grp[k].load(), g1 = m.csr_chunk_grp[k + 1].load();
+                const int64_t r0 = m.csr_chunk_row[k].load(), r1 = m.csr_chunk_row[k + 1].load();
+                const int64_t b0 = ceil_div(r0, int64_t(kZcRows)), b1 = ceil_div(r1, int64_t(kZcRows));
+                if (b1 > b0) launch_dia_follow(m, dx, yd.get(), s, fc, b0, b1);
+                if (g1 > g0) launch_csr_groups_follow(m, dx, yd.get(), s, fc, g0, g1, true);
+                SOB_CUDA(cudaEventRecord(st.chunk_ev[k], s));
+                SOB_CUDA(cudaStreamWaitEvent(out, st.chunk_ev[k], 0));
+                if (r1 > r0)
+                    SOB_CUDA(cudaMemcpyAsync(y_mapped + r0, yd.get() + r0, sizeof(double) * size_t(r1 - r0),
+                                             cudaMemcpyDefault, out));
+            }
+            SOB_CUDA(cudaEventRecord(st.chunk_ev[K], out));
+            SOB_CUDA(cudaStreamWaitEvent(s, st.chunk_ev[K], 0));
         } else if (hdc2) {
             // released stream-ordered after the copy below; allocated before
             // the first launch (see follow_preload)

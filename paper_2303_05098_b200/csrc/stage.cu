@@ -250,37 +250,42 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
     auto worker = [&](int id) {
         cudaSetDevice(dev);
         if (make_y && id == 0) orchestrate();  // the caller is building y
+        // After a failure the y copies are skipped but every x chunk is
+        // still staged: the orchestrator waits for each (wait_x) before it
+        // can finish, so abandoning one would hang the call (a failed y
+        // allocation raced the x tasks this way).
+        auto y_ready = [&](const Task& k, double*& dst) -> bool {
+            const int j = -k.chunk - 1;
+            if (!(dst = yptr.load(std::memory_order_acquire))) {
+                // y is being built on the caller's thread: sleep, do not
+                // spin (spinning workers take its core and its memory
+                // bandwidth: config 2 zero fill 0.9 -> 2.0 ms)
+                std::unique_lock<std::mutex> lk(ymu);
+                ycv.wait(lk, [&] { return yptr.load(std::memory_order_acquire) || failed.load(); });
+                dst = yptr.load(std::memory_order_acquire);
+                if (!dst) return false;
+            }
+            dst += k.off;
+            while (!ygate[size_t(j)].load(std::memory_order_acquire)) {
+                if (failed.load(std::memory_order_relaxed)) return false;
+                std::this_thread::yield();
+            }
+            while (true) {
+                const cudaError_t q = cudaEventQuery(st.ev[size_t(j)]);
+                if (q == cudaSuccess) return !failed.load(std::memory_order_relaxed);
+                if (q != cudaErrorNotReady) {
+                    failed.store(1);
+                    return false;
+                }
+                std::this_thread::yield();
+            }
+        };
         while (true) {
             const size_t t = next.fetch_add(1);
-            if (t >= tasks.size() || failed.load(std::memory_order_relaxed)) return;
+            if (t >= tasks.size()) return;
             const Task& k = tasks[t];
             double* dst = k.dst;
-            if (k.chunk < 0) {
-                const int j = -k.chunk - 1;
-                if (!(dst = yptr.load(std::memory_order_acquire))) {
-                    // y is being built on the caller's thread: sleep, do not
-                    // spin (spinning workers take its core and its memory
-                    // bandwidth: config 2 zero fill 0.9 -> 2.0 ms)
-                    std::unique_lock<std::mutex> lk(ymu);
-                    ycv.wait(lk, [&] { return yptr.load(std::memory_order_acquire) || failed.load(); });
-                    dst = yptr.load(std::memory_order_acquire);
-                    if (!dst) return;
-                }
-                dst += k.off;
-                while (!ygate[size_t(j)].load(std::memory_order_acquire)) {
-                    if (failed.load(std::memory_order_relaxed)) return;
-                    std::this_thread::yield();
-                }
-                while (true) {
-                    const cudaError_t q = cudaEventQuery(st.ev[size_t(j)]);
-                    if (q == cudaSuccess) break;
-                    if (q != cudaErrorNotReady) {
-                        failed.store(1);
-                        return;
-                    }
-                    std::this_thread::yield();
-                }
-            }
+            if (k.chunk < 0 && (failed.load(std::memory_order_relaxed) || !y_ready(k, dst))) continue;
             copy_host(dst, k.src, k.n, k.chunk >= 0 || !make_y);
             if (k.chunk >= 0) xdone[size_t(k.chunk)].fetch_add(1, std::memory_order_release);
             if (trace && t + 1 == tasks.size()) stamp(t_ycopied);
@@ -439,8 +444,9 @@ bool spmv_pageable(const so_matrix& m, const double* x, double* y, cudaStream_t 
         cudaStreamSynchronize(ctx(dev).copy_in);
         std::rethrow_exception(err);
     }
-    if (yerr) {
+    if (yerr) {  // as above: the staged x may still be going up on the copy stream
         cudaStreamSynchronize(s);
+        cudaStreamSynchronize(ctx(dev).copy_in);
         std::rethrow_exception(yerr);
     }
     if (follow.load()) {

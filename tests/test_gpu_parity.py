@@ -756,6 +756,27 @@ def test_pageable_host_spmv_staging(so, O, shape):
         assert np.array_equal(z, want)
 
 
+@pytest.mark.parametrize("fmt", [0, 1, 2])
+def test_pageable_failed_allocation_never_stalls(so, O, fmt):
+    """spmv_new whose output allocator fails, repeated: the host workers skip
+    the y copies but still stage every x chunk, so the orchestrator waiting
+    for them finishes (abandoning x chunks after the failure hung ~1 call in
+    a few hundred, stage.cu); each call raises OutOfMemory and the next
+    multiply is exact."""
+    from paper_2303_05098_b200 import synth
+
+    csr = synth.laplacian_2d(800, seed=1)
+    m = so.DeviceMatrix.csr(csr.nrows, csr.ncols, csr.row_ptr, csr.col, csr.val).convert(fmt)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, csr.ncols)
+    want = m.spmv(x)
+    for _ in range(300):
+        with pytest.raises(so.OutOfMemory):
+            m.spmv_new(x, fail_alloc=True)
+    assert np.array_equal(m.spmv_new(x), want)
+    assert np.array_equal(m.spmv(x), want)
+
+
 def test_cpu_baseline_bytes_match_device_accounting(so, O):
     """scripts/cpu_baseline.py credits the reference CPU path with the same
     algorithmic bytes as the device roofline: its numpy
